@@ -1,0 +1,139 @@
+/*
+ * bsvd_b200.h -- C-ABI of the B200-native batched one-sided Jacobi SVD.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   batch_svd(problems, opts, state)            /root/reference/pkg/src/bsvd/batch.py:85-157
+ * and the kernel operator API it drives through
+ *   Backend(onesided_sweeps, eig_sweeps, fused_pair_update)
+ *                                               /root/reference/pkg/src/bsvd/backend.py:30-35
+ *   onesided_sweeps   src/_kernels_numba.py:85-138   (unblocked sweeps, per problem)
+ *   eig_sweeps        src/_kernels_numba.py:17-82    (inner Gram eigensolve, blocked path)
+ *   fused_pair_update src/_kernels_numba.py:141-175  (W += W * Delta, V += V * Delta)
+ *   compute_gram      src/svd.py:144-179
+ *   _finalize_factors src/svd.py:243-275
+ * The reference calls those once per problem per sweep from Python; here one
+ * call solves a whole uniform-shape batch on the device (all sweeps, the
+ * per-problem convergence test of src/batch.py:62-82 and finalisation).
+ *
+ * Conventions: plain pointers and sizes, no torch or CUDA types.  All array
+ * pointers are DEVICE pointers; matrices are column-major (src/core.py:1-7),
+ * complex values interleaved (re, im).  `stream` is a cudaStream_t passed as
+ * void* (NULL = legacy default stream).  Calls are stream-ordered, reentrant,
+ * never allocate, never synchronise, and use the current device.
+ */
+#ifndef BSVD_B200_H
+#define BSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSVD_ABI_VERSION 1
+
+/* element types; codes equal src/fileio.py:49-54 (s, d, c, z) */
+typedef enum { BSVD_S = 0, BSVD_D = 1, BSVD_C = 2, BSVD_Z = 3 } bsvd_dtype;
+
+/* solver routes (src/svd.py:559-582): dispatch = svd_dispatch, the others force */
+enum { BSVD_DISPATCH = 0, BSVD_FORCE_UNBLOCKED = 1, BSVD_FORCE_BLOCKED = 2 };
+
+/* JacobiOptions (src/svd.py:58-91) as a POD. */
+typedef struct {
+    double k;           /* rotation-guard multiplier, tol = k*u              */
+    int max_sweeps;     /* max_nsweeps                                       */
+    int nb;             /* block width of the blocked path                   */
+    int inner_sweeps;   /* inner eigensolver sweeps per block pair (0 = 100) */
+    int masking;        /* accepted for parity; every problem exits on its own quiet sweep */
+    int want_v;         /* compute_right_vectors                             */
+    int route;          /* BSVD_DISPATCH / BSVD_FORCE_*                      */
+    int fused_updates;  /* accepted for parity; updates are always fused     */
+    int row_block;      /* accepted for parity (tiling is the kernel's own)  */
+    int kernel;         /* 0 = auto; >0 forces a kernel variant (tests/bench) */
+    int reserved[3];
+} bsvd_opts;
+
+/* Per-problem telemetry, written by the device (mirrors SolveInfo / BatchState). */
+typedef struct {
+    int32_t converged;      /* quiet sweep reached within max_sweeps              */
+    int32_t outer_sweeps;   /* sweeps up to and including the quiet one           */
+    int64_t rotations;      /* SolveInfo.inner_rotations                          */
+    int64_t gram_calls;     /* blocked path: Gram formations                      */
+    int64_t update_calls;   /* blocked path: pair updates applied                 */
+    int32_t last_rotations; /* rotations applied in the final sweep               */
+    int32_t path;           /* 1 unblocked, 2 blocked (| 0x100 when transposed)   */
+    int32_t status;         /* 0 ok, 1 non-finite input                           */
+    int32_t kernel;         /* kernel variant that ran                            */
+} bsvd_info;
+
+/* Status codes returned by the calls. */
+enum {
+    BSVD_OK = 0,
+    BSVD_ERR_ARG = -1,       /* bad dtype / shape / stride / option   */
+    BSVD_ERR_WORKSPACE = -2, /* work_bytes smaller than required      */
+    BSVD_ERR_CUDA = -3,      /* kernel launch failed                  */
+    BSVD_ERR_UNSUPPORTED = -4
+};
+
+/*
+ * Batched economy SVD of `batch` matrices A_b (m x n, any m, n >= 0):
+ *   A_b = U_b diag(S_b) V_b^H,  k = min(m, n)
+ * A_b  at A + b*strideA, leading dimension lda >= m        (input, not modified)
+ * U_b  at U + b*strideU, m x k, ldu >= m                   (output)
+ * S_b  at S + b*strideS, k real values, descending         (output; real dtype)
+ * V_b  at V + b*strideV, n x k, ldv >= n, or V == NULL      (output if want_v)
+ * info: device array of `batch` bsvd_info (may be NULL).
+ * Wide inputs (m < n) are solved through A^H with U and V swapped
+ * ("transpose+" route, src/svd.py:346-347, :531-536).
+ * work: device scratch of bsvd_workspace_bytes(...) bytes (may be 0 bytes).
+ * Strides and leading dimensions are in elements.
+ */
+int bsvd_gesvj_batched(int dtype, int m, int n, int batch,
+                       const void* A, int64_t lda, int64_t strideA,
+                       void* U, int64_t ldu, int64_t strideU,
+                       void* S, int64_t strideS,
+                       void* V, int64_t ldv, int64_t strideV,
+                       const bsvd_opts* opts, bsvd_info* info,
+                       void* work, size_t work_bytes, void* stream);
+
+/* Device scratch needed by bsvd_gesvj_batched for this problem class. */
+size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts* opts);
+
+/* Kernel variant the auto-dispatch would pick (for telemetry/tests). */
+int bsvd_select_kernel(int dtype, int m, int n, const bsvd_opts* opts);
+
+/* Fill opts with the reference defaults (JacobiOptions(), src/svd.py:70-78). */
+void bsvd_default_opts(bsvd_opts* opts);
+
+const char* bsvd_strerror(int code);
+int bsvd_abi_version(void);
+
+/*
+ * Kernel-level operator entry points, batch-granular versions of the
+ * reference's Backend plugin functions (src/backend.py:30-35).  Each works on
+ * `batch` independent problems in place on the device and returns per-problem
+ * rotation counts in rotations[] (device int64, may be NULL).
+ *
+ * bsvd_onesided_sweeps_batched ~ onesided_sweeps(a, v, pairs, starts, tol, max_sweeps);
+ *   sweeps[b] = sweeps run, bit 30 set when the last sweep was quiet (converged).
+ *   a: m x n (lda), v: vrows x n (ldv) or NULL (vrows = 0).
+ * bsvd_gram_batched ~ compute_gram(ai, aj) with ai = a[:, 0:wi], aj = a[:, wi:wi+wj]
+ *   g: (wi+wj) x (wi+wj), ldg.
+ * bsvd_fused_pair_update_batched ~ fused_pair_update(bi, bj, j, row_block, delta)
+ *   b: m x (wi+wj) (ldb) holding [bi bj] side by side, j: w x w (ldj).
+ */
+int bsvd_onesided_sweeps_batched(int dtype, int m, int n, int batch, void* a, int64_t lda,
+                                 int64_t stride_a, int vrows, void* v, int64_t ldv,
+                                 int64_t stride_v, double tol, int max_sweeps,
+                                 int64_t* rotations, int32_t* sweeps, void* stream);
+int bsvd_gram_batched(int dtype, int m, int wi, int wj, int batch, const void* a, int64_t lda,
+                      int64_t stride_a, void* g, int64_t ldg, int64_t stride_g, void* stream);
+int bsvd_fused_pair_update_batched(int dtype, int m, int w, int batch, void* b, int64_t ldb,
+                                   int64_t stride_b, const void* j, int64_t ldj, int64_t stride_j,
+                                   int delta, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSVD_B200_H */

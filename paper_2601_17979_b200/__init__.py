@@ -1,0 +1,67 @@
+"""B200-native batched one-sided Jacobi SVD (arXiv 2601.17979 hot path).
+
+Drop-in for the reference package's batch entry point
+(/root/reference/pkg/src/bsvd/batch.py:85 ``batch_svd``) and the solver
+records it returns.  Every solve runs in hand-written sm_100a CUDA kernels
+behind the C-ABI in include/bsvd_b200.h (paper_2601_17979_b200/_lib/
+libbsvd_b200.so); there is no CPU fallback.
+"""
+
+from .batch import BatchState, batch_svd, convergence_scan
+from .core import (
+    SUPPORTED_DTYPES,
+    DomainError,
+    ShapeError,
+    check_dtype,
+    fmatrix,
+    is_complex,
+    real_dtype,
+    unit_roundoff,
+)
+from .eig import Rotation, compute_rotation
+from .kernels import compute_gram, fused_pair_update, onesided_sweeps
+from .ordering import Schedule, round_robin_schedule, schedule_arrays
+from .solver import DeviceResult, solve_tensor
+from .svd import (
+    JacobiOptions,
+    SolveInfo,
+    SvdResult,
+    WorkCounters,
+    svd_blocked,
+    svd_dispatch,
+    svd_unblocked,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BatchState",
+    "DeviceResult",
+    "DomainError",
+    "JacobiOptions",
+    "Rotation",
+    "Schedule",
+    "ShapeError",
+    "SolveInfo",
+    "SUPPORTED_DTYPES",
+    "SvdResult",
+    "WorkCounters",
+    "batch_svd",
+    "check_dtype",
+    "compute_gram",
+    "compute_rotation",
+    "convergence_scan",
+    "fmatrix",
+    "fused_pair_update",
+    "is_complex",
+    "onesided_sweeps",
+    "real_dtype",
+    "round_robin_schedule",
+    "schedule_arrays",
+    "solve_tensor",
+    "svd_blocked",
+    "svd_dispatch",
+    "svd_unblocked",
+    "unit_roundoff",
+    "__version__",
+]

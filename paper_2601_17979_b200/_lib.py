@@ -1,0 +1,107 @@
+"""ctypes binding of the C-ABI library (include/bsvd_b200.h).
+
+The product path goes through this module only.  There is no CPU fallback:
+if the in-tree libbsvd_b200.so is missing, or no CUDA device is present, the
+call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libbsvd_b200.so")
+
+BSVD_OK = 0
+DISPATCH, FORCE_UNBLOCKED, FORCE_BLOCKED = 0, 1, 2
+
+
+class BsvdOpts(ctypes.Structure):
+    _fields_ = [
+        ("k", ctypes.c_double),
+        ("max_sweeps", ctypes.c_int),
+        ("nb", ctypes.c_int),
+        ("inner_sweeps", ctypes.c_int),
+        ("masking", ctypes.c_int),
+        ("want_v", ctypes.c_int),
+        ("route", ctypes.c_int),
+        ("fused_updates", ctypes.c_int),
+        ("row_block", ctypes.c_int),
+        ("kernel", ctypes.c_int),
+        ("reserved", ctypes.c_int * 3),
+    ]
+
+
+class BsvdInfo(ctypes.Structure):
+    _fields_ = [
+        ("converged", ctypes.c_int32),
+        ("outer_sweeps", ctypes.c_int32),
+        ("rotations", ctypes.c_int64),
+        ("gram_calls", ctypes.c_int64),
+        ("update_calls", ctypes.c_int64),
+        ("last_rotations", ctypes.c_int32),
+        ("path", ctypes.c_int32),
+        ("status", ctypes.c_int32),
+        ("kernel", ctypes.c_int32),
+    ]
+
+
+INFO_BYTES = ctypes.sizeof(BsvdInfo)
+
+# exported symbols, one per declaration in include/bsvd_b200.h
+EXPORTS = (
+    "bsvd_gesvj_batched",
+    "bsvd_workspace_bytes",
+    "bsvd_select_kernel",
+    "bsvd_default_opts",
+    "bsvd_strerror",
+    "bsvd_abi_version",
+    "bsvd_onesided_sweeps_batched",
+    "bsvd_gram_batched",
+    "bsvd_fused_pair_update_batched",
+)
+
+_lib = None
+
+
+def load():
+    """Load libbsvd_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(make -C paper_2601_17979_b200/csrc); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, ci, i64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+    popts = ctypes.POINTER(BsvdOpts)
+    L.bsvd_gesvj_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, vp, i64, i64, vp, i64, vp, i64, i64,
+                                     popts, vp, vp, sz, vp]
+    L.bsvd_gesvj_batched.restype = ci
+    L.bsvd_workspace_bytes.argtypes = [ci, ci, ci, ci, popts]
+    L.bsvd_workspace_bytes.restype = sz
+    L.bsvd_select_kernel.argtypes = [ci, ci, ci, popts]
+    L.bsvd_select_kernel.restype = ci
+    L.bsvd_default_opts.argtypes = [popts]
+    L.bsvd_default_opts.restype = None
+    L.bsvd_strerror.argtypes = [ci]
+    L.bsvd_strerror.restype = ctypes.c_char_p
+    L.bsvd_abi_version.argtypes = []
+    L.bsvd_abi_version.restype = ci
+    L.bsvd_onesided_sweeps_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, ci, vp, i64, i64, ctypes.c_double,
+                                               ci, vp, vp, vp]
+    L.bsvd_onesided_sweeps_batched.restype = ci
+    L.bsvd_gram_batched.argtypes = [ci, ci, ci, ci, ci, vp, i64, i64, vp, i64, i64, vp]
+    L.bsvd_gram_batched.restype = ci
+    L.bsvd_fused_pair_update_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, vp, i64, i64, ci, vp]
+    L.bsvd_fused_pair_update_batched.restype = ci
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str = "bsvd call") -> None:
+    if rc != BSVD_OK:
+        msg = load().bsvd_strerror(rc).decode()
+        raise RuntimeError(f"{what} failed: {msg} (code {rc})")

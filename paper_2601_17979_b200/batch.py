@@ -1,0 +1,241 @@
+"""Batch driver: the drop-in for the reference's ``batch_svd``.
+
+Mirrors /root/reference/pkg/src/bsvd/batch.py:24-157.  The reference steps
+every problem one sweep per round from Python and masks converged problems
+after each round (convergence_scan, :62-82).  Here each uniform
+(dtype, m, n) group is ONE device launch: every problem runs its sweeps on
+the device and stops after its own first quiet sweep (the per-problem early
+exit of the masked batch), so results equal the reference's masked and
+unmasked modes alike (a quiet sweep never writes, F7).  The batch telemetry
+(rounds, masked pair skips, call counts) is reconstructed exactly from the
+per-problem sweep counts the kernels report.
+
+Per-problem failures keep the reference's semantics: a problem that fails
+validation yields ``None`` and its exception is kept in ``state.errors``;
+the batch never aborts (:105-111).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from math import ceil
+
+import numpy as np
+
+from . import _lib
+from .core import DomainError, ShapeError, check_dtype, real_dtype
+from .svd import QR_RATIO, SMALL_CUTOFF, JacobiOptions, SolveInfo, SvdResult, WorkCounters
+
+__all__ = ["BatchState", "batch_svd", "convergence_scan"]
+
+_ROUTE = {None: _lib.DISPATCH, "unblocked": _lib.FORCE_UNBLOCKED, "blocked": _lib.FORCE_BLOCKED}
+
+
+@dataclass
+class BatchState:
+    """Observable batch telemetry (src/batch.py:24-59)."""
+
+    active: np.ndarray
+    outer_sweeps: np.ndarray
+    pair_stats: list
+    counters: WorkCounters = field(default_factory=WorkCounters)
+    errors: dict = field(default_factory=dict)
+
+    @classmethod
+    def for_batch(cls, n_problems: int) -> "BatchState":
+        return cls(
+            active=np.ones(n_problems, dtype=bool),
+            outer_sweeps=np.zeros(n_problems, dtype=np.int64),
+            pair_stats=[None] * n_problems,
+        )
+
+    def _reset(self, n_problems: int) -> None:
+        self.active = np.ones(n_problems, dtype=bool)
+        self.outer_sweeps = np.zeros(n_problems, dtype=np.int64)
+        self.pair_stats = [None] * n_problems
+        self.counters = WorkCounters()
+        self.errors = {}
+
+    @property
+    def n_problems(self) -> int:
+        return len(self.pair_stats)
+
+
+def convergence_scan(state: BatchState) -> bool:
+    """Mask off problems whose latest sweep applied no rotation (src/batch.py:62-82)."""
+    all_done = True
+    for i in range(state.n_problems):
+        if i in state.errors:
+            continue
+        if not state.active[i]:
+            continue
+        stats = state.pair_stats[i]
+        if stats is None:
+            all_done = False
+            continue
+        if all(rot == 0 for (_, _, rot) in stats):
+            state.active[i] = False
+        else:
+            all_done = False
+    return all_done
+
+
+@dataclass
+class _Prep:
+    a: np.ndarray
+    m: int
+    n: int
+    bn: int
+    trans: bool
+    blocked: bool
+    trivial: bool
+    pairs_per_sweep: int
+
+
+def _prepare(a, opts: JacobiOptions, force: str | None) -> _Prep:
+    """Validation and routing of _ProblemRun.__init__ (src/svd.py:323-413)."""
+    a = np.asarray(a)
+    check_dtype(a)
+    if a.ndim != 2:
+        raise ShapeError(f"expected a 2-d matrix, got ndim={a.ndim}")
+    m, n = a.shape
+    if force is not None and m < n:
+        raise ShapeError(f"{force} solver requires m >= n, got {m}x{n}; use svd_dispatch")
+    trans = force is None and m < n
+    bm, bn = (n, m) if trans else (m, n)
+    trivial = bm == 0 or bn == 0
+    if not trivial and force is None and opts.use_qr_preprocess and bm >= QR_RATIO * bn:
+        raise NotImplementedError("QR-preprocessed route (use_qr_preprocess) is not built on the B200 path yet")
+    if force == "unblocked":
+        blocked = False
+    elif force == "blocked":
+        blocked = True
+    else:
+        blocked = bn > SMALL_CUTOFF
+    if trivial:
+        pps = 0
+    elif not blocked:
+        pps = bn * (bn - 1) // 2 if bn >= 2 else 0
+    else:
+        ell = ceil(bn / opts.nb)
+        pps = ell * (ell - 1) // 2 if ell >= 2 else 1
+    return _Prep(a=a, m=m, n=n, bn=bn, trans=trans, blocked=blocked, trivial=trivial, pairs_per_sweep=pps)
+
+
+def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rounds: bool):
+    """Solve a list of problems on the device; returns (results, errors, telemetry)."""
+    from .solver import solve_host
+
+    n_prob = len(problems)
+    preps: list[_Prep | None] = [None] * n_prob
+    errors: dict = {}
+    for idx, a in enumerate(problems):
+        try:
+            preps[idx] = _prepare(a, opts, force)
+        except Exception as exc:  # per-problem isolation (src/batch.py:105-111)
+            errors[idx] = exc
+
+    # group by (dtype, m, n): one launch per group
+    groups: dict = {}
+    for idx, p in enumerate(preps):
+        if p is None or p.trivial:
+            continue
+        groups.setdefault((p.a.dtype.str, p.m, p.n), []).append(idx)
+
+    raw: dict = {}
+    for key, idxs in groups.items():
+        t0 = time.perf_counter()
+        mats = [preps[i].a for i in idxs]
+        try:
+            U, S, V, info, kern = solve_host(mats, opts, route=_ROUTE[force])
+        except Exception as exc:
+            for i in idxs:
+                errors[i] = exc
+            continue
+        dt = (time.perf_counter() - t0) / len(idxs)
+        for j, i in enumerate(idxs):
+            raw[i] = (U[j], S[j], V[j] if V is not None else None, info[j], dt, kern)
+
+    # rounds the reference's lockstep loop would run (src/batch.py:113-142)
+    sweeps_of = {}
+    unconverged = False
+    for idx, p in enumerate(preps):
+        if p is None or idx in errors:
+            continue
+        if p.trivial:
+            sweeps_of[idx] = (0, True)
+        else:
+            inf = raw[idx][3]
+            sweeps_of[idx] = (int(inf["outer_sweeps"]), bool(inf["converged"]))
+            unconverged |= not bool(inf["converged"])
+    if sweeps_of:
+        rounds = opts.max_nsweeps if unconverged else max(max(s, 1) for s, _ in sweeps_of.values())
+    else:
+        rounds = 0
+
+    results: list = [None] * n_prob
+    tele: dict = {}
+    for idx, p in enumerate(preps):
+        if p is None or idx in errors:
+            continue
+        m, n = p.m, p.n
+        k = min(m, n)
+        dt = p.a.dtype
+        cnt = WorkCounters()
+        if p.trivial:
+            u = np.zeros((m, k), dtype=dt, order="F")
+            sigma = np.zeros(k, dtype=real_dtype(dt))
+            v = np.zeros((n, k), dtype=dt, order="F") if opts.compute_right_vectors else None
+            info = SolveInfo(converged=True, outer_sweeps=0, inner_rotations=0, masked_pair_skips=0,
+                             path="empty", counters=cnt)
+            results[idx] = SvdResult(u=u, sigma=sigma, v=v, info=info)
+            tele[idx] = dict(outer_sweeps=0, converged=True, last=0, pair_stats=[])
+            continue
+        U, S, V, inf, dtime, kern = raw[idx]
+        s_i = int(inf["outer_sweeps"])
+        conv = bool(inf["converged"])
+        pps = p.pairs_per_sweep
+        calls = s_i if masked_rounds is False or opts.masking else rounds
+        if p.blocked:
+            cnt.gram_calls = calls * pps
+            cnt.eig_calls = calls * pps
+            cnt.update_calls = int(inf["update_calls"])
+        else:
+            cnt.eig_calls = calls if p.bn >= 2 else 0
+        masked = 0
+        if masked_rounds and opts.masking and conv:
+            masked = (rounds - max(s_i, 1)) * pps
+        cnt.masked_pair_skips = masked
+        cnt.t_eig = dtime
+        base = "blocked" if (int(inf["path"]) & 0xFF) == 2 else "unblocked"
+        path = ("transpose+" if int(inf["path"]) & 0x100 else "") + base
+        info = SolveInfo(converged=conv, outer_sweeps=s_i, inner_rotations=int(inf["rotations"]),
+                         masked_pair_skips=masked, path=path, counters=cnt)
+        results[idx] = SvdResult(u=U, sigma=S, v=V if opts.compute_right_vectors else None, info=info)
+        last = int(inf["last_rotations"])
+        if not p.blocked:
+            stats = [(last == 0, 1, last)]
+        else:
+            stats = [(True, 1, 0)] * pps if last == 0 else [(False, 1, last)] + [(True, 1, 0)] * (pps - 1)
+        tele[idx] = dict(outer_sweeps=s_i, converged=conv, last=last, pair_stats=stats, kernel=kern)
+    return results, errors, tele
+
+
+def batch_svd(problems, opts: JacobiOptions | None = None, state: BatchState | None = None):
+    """Solve every problem in the batch; results align with the input order (src/batch.py:85-157)."""
+    if opts is None:
+        opts = JacobiOptions()
+    problems = list(problems)
+    if not problems:
+        raise DomainError("batch must contain at least one problem")
+    st = state if state is not None else BatchState.for_batch(len(problems))
+    st._reset(len(problems))
+    results, errors, tele = _solve_problems(problems, opts, force=None, masked_rounds=True)
+    st.errors = dict(errors)
+    for idx, t in tele.items():
+        st.outer_sweeps[idx] = t["outer_sweeps"]
+        st.pair_stats[idx] = t["pair_stats"]
+        st.active[idx] = not t["converged"]
+        st.counters.add(results[idx].info.counters)
+    return results

@@ -1,0 +1,269 @@
+// api.cu -- the C-ABI (include/bsvd_b200.h): argument checks, route
+// selection (src/svd.py:375-381 dispatch), kernel planning and launch.
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include "launch.h"
+
+using namespace bsvd;
+
+namespace {
+
+constexpr size_t kSmemFallback = 232448;  // 227 KB opt-in limit of sm_100
+
+size_t smem_limit() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return kSmemFallback;
+    }
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || v <= 0) {
+        cudaGetLastError();
+        return kSmemFallback;
+    }
+    return (size_t)v;
+}
+
+int esize_of(int dt) { return dt == BSVD_S ? 4 : dt == BSVD_D ? 8 : dt == BSVD_C ? 8 : 16; }
+int rsize_of(int dt) { return (dt == BSVD_S || dt == BSVD_C) ? 4 : 8; }
+
+struct Route {
+    int trans, bm, bn, blocked, need_v;
+};
+
+int make_route(int m, int n, const bsvd_opts* o, Route* r) {
+    if (o->route != BSVD_DISPATCH && m < n) return BSVD_ERR_ARG;  // forced solvers need m >= n
+    r->trans = (o->route == BSVD_DISPATCH && m < n) ? 1 : 0;
+    r->bm = r->trans ? n : m;
+    r->bn = r->trans ? m : n;
+    if (o->route == BSVD_FORCE_UNBLOCKED) r->blocked = 0;
+    else if (o->route == BSVD_FORCE_BLOCKED) r->blocked = 1;
+    else r->blocked = r->bn > 32;  // SMALL_CUTOFF, src/svd.py:52
+    r->need_v = (o->want_v || r->trans) ? 1 : 0;
+    return BSVD_OK;
+}
+
+Plan make_plan(int dt, const Route& r, const bsvd_opts* o) {
+    const size_t lim = smem_limit();
+    const int es = esize_of(dt), rs = rsize_of(dt);
+    if (r.blocked) return plan_blocked_general(es, rs, r.bm, r.bn, o->nb, r.need_v, lim);
+    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG32) {
+        Plan p = plan_unblocked_reg(dt, r.bm, r.bn, r.need_v);
+        if (p.kernel) return p;
+        if (o->kernel == KV_UNBLOCKED_REG32) return p;  // kernel 0 => unsupported
+    }
+    return plan_unblocked_general(es, rs, r.bm, r.bn, r.need_v, lim);
+}
+
+int check_opts(const bsvd_opts* o) {
+    if (!o) return BSVD_ERR_ARG;
+    if (!(o->k > 0) || o->max_sweeps < 1 || o->nb < 1 || o->inner_sweeps < 0 || o->row_block < 1)
+        return BSVD_ERR_ARG;
+    if (o->route < 0 || o->route > 2) return BSVD_ERR_ARG;
+    return BSVD_OK;
+}
+
+__global__ void k_info_empty(bsvd_info* info, int batch, int trans) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < batch) {
+        bsvd_info inf;
+        memset(&inf, 0, sizeof(inf));
+        inf.converged = 1;
+        inf.path = trans ? 0x100 : 0;
+        info[i] = inf;
+    }
+}
+
+template <class T>
+int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, int64_t lda, int64_t sA, void* U,
+        int64_t ldu, int64_t sU, void* S, int64_t sS, void* V, int64_t ldv, int64_t sV, const bsvd_opts* o,
+        bsvd_info* info, void* work, cudaStream_t st) {
+    SolveArgs<T> a{};
+    a.A = static_cast<const T*>(A);
+    a.lda = lda;
+    a.strideA = sA;
+    a.m = m;
+    a.n = n;
+    a.trans = r.trans;
+    a.bm = r.bm;
+    a.bn = r.bn;
+    a.U = static_cast<T*>(U);
+    a.ldu = ldu;
+    a.strideU = sU;
+    a.S = static_cast<typename tr<T>::R*>(S);
+    a.strideS = sS;
+    a.V = static_cast<T*>(V);
+    a.ldv = ldv;
+    a.strideV = sV;
+    a.want_v = o->want_v ? 1 : 0;
+    a.need_v = r.need_v;
+    a.tol = o->k * tr<T>::u;
+    a.max_sweeps = o->max_sweeps;
+    a.nb = o->nb;
+    a.inner_budget = o->inner_sweeps >= 1 ? o->inner_sweeps : 100;  // INNER_BUDGET, src/svd.py:55
+    a.batch = batch;
+    a.work = p.work_elems ? static_cast<T*>(work) : nullptr;
+    a.work_stride = (int64_t)p.work_elems;
+    a.info = info;
+    switch (p.kernel) {
+        case KV_UNBLOCKED_GENERAL: return launch_unblocked_general<T>(a, p, st);
+        case KV_BLOCKED_GENERAL: return launch_blocked_general<T>(a, p, st);
+        case KV_UNBLOCKED_REG32:
+            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg_d32(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
+    }
+    return BSVD_ERR_UNSUPPORTED;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bsvd_abi_version(void) { return BSVD_ABI_VERSION; }
+
+void bsvd_default_opts(bsvd_opts* o) {
+    if (!o) return;
+    memset(o, 0, sizeof(*o));
+    o->k = 30.0;
+    o->max_sweeps = 30;
+    o->nb = 16;
+    o->inner_sweeps = 1;
+    o->masking = 0;
+    o->want_v = 1;
+    o->route = BSVD_DISPATCH;
+    o->fused_updates = 1;
+    o->row_block = 64;
+    o->kernel = 0;
+}
+
+const char* bsvd_strerror(int code) {
+    switch (code) {
+        case BSVD_OK: return "ok";
+        case BSVD_ERR_ARG: return "invalid argument";
+        case BSVD_ERR_WORKSPACE: return "workspace too small";
+        case BSVD_ERR_CUDA: return "CUDA launch error";
+        case BSVD_ERR_UNSUPPORTED: return "unsupported kernel variant for this problem";
+    }
+    return "unknown error";
+}
+
+int bsvd_select_kernel(int dtype, int m, int n, const bsvd_opts* opts) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || check_opts(opts)) return BSVD_ERR_ARG;
+    Route r;
+    if (make_route(m, n, opts, &r)) return BSVD_ERR_ARG;
+    if (r.bn == 0 || r.bm == 0) return 0;
+    return make_plan(dtype, r, opts).kernel;
+}
+
+size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts* opts) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || check_opts(opts)) return 0;
+    Route r;
+    if (make_route(m, n, opts, &r)) return 0;
+    if (r.bn == 0 || r.bm == 0) return 0;
+    const Plan p = make_plan(dtype, r, opts);
+    return p.work_elems * (size_t)esize_of(dtype) * (size_t)batch;
+}
+
+int bsvd_gesvj_batched(int dtype, int m, int n, int batch, const void* A, int64_t lda, int64_t strideA, void* U,
+                       int64_t ldu, int64_t strideU, void* S, int64_t strideS, void* V, int64_t ldv,
+                       int64_t strideV, const bsvd_opts* opts, bsvd_info* info, void* work, size_t work_bytes,
+                       void* stream) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0) return BSVD_ERR_ARG;
+    int rc = check_opts(opts);
+    if (rc) return rc;
+    Route r;
+    if ((rc = make_route(m, n, opts, &r))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (batch == 0) return BSVD_OK;
+    const int k = m < n ? m : n;
+    if (k == 0) {  // "empty" path (src/svd.py:351-362)
+        if (info) {
+            k_info_empty<<<(batch + 255) / 256, 256, 0, st>>>(info, batch, r.trans);
+            if (cudaPeekAtLastError() != cudaSuccess) return BSVD_ERR_CUDA;
+        }
+        return BSVD_OK;
+    }
+    if (!A || !U || !S) return BSVD_ERR_ARG;
+    if (lda < m || ldu < m) return BSVD_ERR_ARG;
+    if (opts->want_v && (!V || ldv < n)) return BSVD_ERR_ARG;
+    if (batch > 1 && (strideA < lda * (int64_t)n || strideU < ldu * (int64_t)k || strideS < k)) return BSVD_ERR_ARG;
+    if (batch > 1 && opts->want_v && strideV < ldv * (int64_t)k) return BSVD_ERR_ARG;
+    const Plan p = make_plan(dtype, r, opts);
+    if (!p.kernel) return BSVD_ERR_UNSUPPORTED;
+    const size_t need = p.work_elems * (size_t)esize_of(dtype) * (size_t)batch;
+    if (need > work_bytes || (need && !work)) return BSVD_ERR_WORKSPACE;
+    void* Vp = opts->want_v ? V : nullptr;
+    switch (dtype) {
+        case BSVD_S:
+            return run<float>(r, p, m, n, batch, A, lda, strideA, U, ldu, strideU, S, strideS, Vp, ldv, strideV, opts,
+                              info, work, st);
+        case BSVD_D:
+            return run<double>(r, p, m, n, batch, A, lda, strideA, U, ldu, strideU, S, strideS, Vp, ldv, strideV,
+                               opts, info, work, st);
+        case BSVD_C:
+            return run<cx<float>>(r, p, m, n, batch, A, lda, strideA, U, ldu, strideU, S, strideS, Vp, ldv, strideV,
+                                  opts, info, work, st);
+        case BSVD_Z:
+            return run<cx<double>>(r, p, m, n, batch, A, lda, strideA, U, ldu, strideU, S, strideS, Vp, ldv,
+                                   strideV, opts, info, work, st);
+    }
+    return BSVD_ERR_ARG;
+}
+
+int bsvd_onesided_sweeps_batched(int dtype, int m, int n, int batch, void* a, int64_t lda, int64_t stride_a,
+                                 int vrows, void* v, int64_t ldv, int64_t stride_v, double tol, int max_sweeps,
+                                 int64_t* rotations, int32_t* sweeps, void* stream) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || vrows < 0 || max_sweeps < 1) return BSVD_ERR_ARG;
+    if (batch == 0) return BSVD_OK;
+    if (!a || lda < m || (vrows > 0 && (!v || ldv < vrows))) return BSVD_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    void* vp = vrows > 0 ? v : nullptr;
+    switch (dtype) {
+        case BSVD_S:
+            return launch_onesided_raw<float>((float*)a, lda, stride_a, m, n, batch, (float*)vp, ldv, stride_v, vrows,
+                                              tol, max_sweeps, rotations, sweeps, st);
+        case BSVD_D:
+            return launch_onesided_raw<double>((double*)a, lda, stride_a, m, n, batch, (double*)vp, ldv, stride_v,
+                                               vrows, tol, max_sweeps, rotations, sweeps, st);
+        case BSVD_C:
+            return launch_onesided_raw<cx<float>>((cx<float>*)a, lda, stride_a, m, n, batch, (cx<float>*)vp, ldv,
+                                                  stride_v, vrows, tol, max_sweeps, rotations, sweeps, st);
+        case BSVD_Z:
+            return launch_onesided_raw<cx<double>>((cx<double>*)a, lda, stride_a, m, n, batch, (cx<double>*)vp, ldv,
+                                                   stride_v, vrows, tol, max_sweeps, rotations, sweeps, st);
+    }
+    return BSVD_ERR_ARG;
+}
+
+int bsvd_gram_batched(int dtype, int m, int wi, int wj, int batch, const void* a, int64_t lda, int64_t stride_a,
+                      void* g, int64_t ldg, int64_t stride_g, void* stream) {
+    if (dtype < 0 || dtype > 3 || m < 0 || wi < 1 || wj < 0 || batch < 0) return BSVD_ERR_ARG;
+    if (batch == 0) return BSVD_OK;
+    if (!a || !g || lda < m || ldg < wi + wj) return BSVD_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (dtype) {
+        case BSVD_S: return launch_gram_raw<float>((const float*)a, lda, stride_a, m, wi, wj, batch, (float*)g, ldg, stride_g, st);
+        case BSVD_D: return launch_gram_raw<double>((const double*)a, lda, stride_a, m, wi, wj, batch, (double*)g, ldg, stride_g, st);
+        case BSVD_C: return launch_gram_raw<cx<float>>((const cx<float>*)a, lda, stride_a, m, wi, wj, batch, (cx<float>*)g, ldg, stride_g, st);
+        case BSVD_Z: return launch_gram_raw<cx<double>>((const cx<double>*)a, lda, stride_a, m, wi, wj, batch, (cx<double>*)g, ldg, stride_g, st);
+    }
+    return BSVD_ERR_ARG;
+}
+
+int bsvd_fused_pair_update_batched(int dtype, int m, int w, int batch, void* b, int64_t ldb, int64_t stride_b,
+                                   const void* j, int64_t ldj, int64_t stride_j, int delta, void* stream) {
+    if (dtype < 0 || dtype > 3 || m < 0 || w < 1 || batch < 0) return BSVD_ERR_ARG;
+    if (batch == 0 || m == 0) return BSVD_OK;
+    if (!b || !j || ldb < m || ldj < w) return BSVD_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (dtype) {
+        case BSVD_S: return launch_fused_raw<float>((float*)b, ldb, stride_b, m, w, batch, (const float*)j, ldj, stride_j, delta, st);
+        case BSVD_D: return launch_fused_raw<double>((double*)b, ldb, stride_b, m, w, batch, (const double*)j, ldj, stride_j, delta, st);
+        case BSVD_C: return launch_fused_raw<cx<float>>((cx<float>*)b, ldb, stride_b, m, w, batch, (const cx<float>*)j, ldj, stride_j, delta, st);
+        case BSVD_Z: return launch_fused_raw<cx<double>>((cx<double>*)b, ldb, stride_b, m, w, batch, (const cx<double>*)j, ldj, stride_j, delta, st);
+    }
+    return BSVD_ERR_ARG;
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// launch.h -- internal planning/launch interface between api.cu and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "kernel_args.cuh"
+
+namespace bsvd {
+
+struct Plan {
+    int kernel;         // KV_* variant
+    int resident;       // residency bits (see SolveArgs::resident)
+    size_t smem;        // dynamic shared memory per CTA
+    size_t work_elems;  // global workspace elements per problem
+    int threads;        // CTA size
+    int group;          // lanes per pair (general unblocked)
+    int grid;           // CTAs (0 = one per problem)
+};
+
+Plan plan_unblocked_general(int esize, int rsize, int bm, int bn, int need_v, size_t smem_limit);
+Plan plan_blocked_general(int esize, int rsize, int bm, int bn, int nb, int need_v, size_t smem_limit);
+Plan plan_unblocked_reg(int dtype, int bm, int bn, int need_v);
+
+template <class T>
+int launch_unblocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
+template <class T>
+int launch_blocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
+int launch_unblocked_reg_d32(SolveArgs<double> a, const Plan& p, cudaStream_t st);
+
+int group_for_rows(int bm);
+int threads_for(int bn, int G);
+
+// kernel-level operators (bsvd_*_batched entry points)
+template <class T>
+int launch_onesided_raw(T* A, int64_t lda, int64_t sa, int m, int n, int batch, T* V, int64_t ldv, int64_t sv,
+                        int vrows, double tol, int max_sweeps, int64_t* rot, int32_t* sw, cudaStream_t st);
+template <class T>
+int launch_gram_raw(const T* A, int64_t lda, int64_t sa, int m, int wi, int wj, int batch, T* G, int64_t ldg,
+                    int64_t sg, cudaStream_t st);
+template <class T>
+int launch_fused_raw(T* B, int64_t ldb, int64_t sb, int m, int w, int batch, const T* J, int64_t ldj, int64_t sj,
+                     int delta, cudaStream_t st);
+
+}  // namespace bsvd

@@ -1,0 +1,176 @@
+"""Device-side batch solve through the C-ABI (the hot path).
+
+``solve_tensor`` is the tensor fast path: a device-resident batch in, device
+factors out, one ``bsvd_gesvj_batched`` launch on the current stream, no host
+synchronisation.  ``solve_host`` is the host-buffer path used by the
+reference-shaped API (``batch_svd``): pinned staging, H2D, the same launch,
+D2H.  Layout contract (include/bsvd_b200.h): each matrix column-major, so a
+batch is stored as a C-contiguous (B, n, m) tensor whose [b] slice is the
+transpose view of A_b.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import DTYPE_CODE, real_dtype
+
+INFO_DTYPE = np.dtype([
+    ("converged", "<i4"),
+    ("outer_sweeps", "<i4"),
+    ("rotations", "<i8"),
+    ("gram_calls", "<i8"),
+    ("update_calls", "<i8"),
+    ("last_rotations", "<i4"),
+    ("path", "<i4"),
+    ("status", "<i4"),
+    ("kernel", "<i4"),
+])
+assert INFO_DTYPE.itemsize == _lib.INFO_BYTES
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2601_17979_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+    return torch
+
+
+_TORCH_OF = {}
+
+
+def torch_dtype(np_dtype):
+    torch = _torch()
+    if not _TORCH_OF:
+        _TORCH_OF.update({
+            np.dtype(np.float32): torch.float32,
+            np.dtype(np.float64): torch.float64,
+            np.dtype(np.complex64): torch.complex64,
+            np.dtype(np.complex128): torch.complex128,
+        })
+    return _TORCH_OF[np.dtype(np_dtype)]
+
+
+def np_dtype_of(tdtype):
+    torch = _torch()
+    return {
+        torch.float32: np.dtype(np.float32),
+        torch.float64: np.dtype(np.float64),
+        torch.complex64: np.dtype(np.complex64),
+        torch.complex128: np.dtype(np.complex128),
+    }[tdtype]
+
+
+def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0) -> _lib.BsvdOpts:
+    """JacobiOptions -> POD bsvd_opts (src/svd.py:70-78 field by field)."""
+    o = _lib.BsvdOpts()
+    o.k = float(opts.k)
+    o.max_sweeps = int(opts.max_nsweeps)
+    o.nb = int(opts.nb)
+    o.inner_sweeps = int(opts.inner_sweeps)
+    o.masking = int(bool(opts.masking))
+    o.want_v = int(bool(opts.compute_right_vectors))
+    o.route = int(route)
+    o.fused_updates = int(bool(opts.fused_updates))
+    o.row_block = int(opts.row_block)
+    o.kernel = int(kernel)
+    return o
+
+
+_WS_CACHE: dict = {}
+
+
+def _workspace(nbytes: int, device):
+    torch = _torch()
+    if nbytes == 0:
+        return None
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    buf = _WS_CACHE.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = buf
+    return buf
+
+
+@dataclass
+class DeviceResult:
+    u: object      # (B, k, m) tensor: u[b] is U_b^T (column-major U_b)
+    s: object      # (B, k) real tensor
+    v: object      # (B, k, n) tensor or None
+    info: object   # (B * INFO_BYTES,) uint8 tensor
+    kernel: int
+
+
+def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: int = 0,
+                 out=None) -> DeviceResult:
+    """Batched SVD of a device tensor a_t (B, n, m) (column-major matrices).
+
+    Launches on torch's current stream; returns device tensors without
+    synchronising.  ``out`` may pass preallocated (u, s, v, info) tensors.
+    """
+    torch = _torch()
+    L = _lib.load()
+    B = a_t.shape[0]
+    assert a_t.shape == (B, n, m) and a_t.is_contiguous() and a_t.is_cuda
+    dt = np_dtype_of(a_t.dtype)
+    code = DTYPE_CODE[dt]
+    k = min(m, n)
+    o = make_opts(opts, route, kernel)
+    dev = a_t.device
+    if out is None:
+        u = torch.empty((B, k, m), dtype=a_t.dtype, device=dev)
+        s = torch.empty((B, k), dtype=torch_dtype(real_dtype(dt)), device=dev)
+        v = torch.empty((B, k, n), dtype=a_t.dtype, device=dev) if o.want_v else None
+        info = torch.empty((B * _lib.INFO_BYTES,), dtype=torch.uint8, device=dev)
+    else:
+        u, s, v, info = out
+    ws_bytes = L.bsvd_workspace_bytes(code, m, n, B, ctypes.byref(o))
+    ws = _workspace(ws_bytes, dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    rc = L.bsvd_gesvj_batched(
+        code, m, n, B,
+        a_t.data_ptr(), max(m, 1), m * n,
+        u.data_ptr(), max(m, 1), k * m,
+        s.data_ptr(), k,
+        v.data_ptr() if v is not None else None, max(n, 1), k * n,
+        ctypes.byref(o), info.data_ptr(),
+        ws.data_ptr() if ws is not None else None, ws_bytes, stream)
+    _lib.check(rc, f"bsvd_gesvj_batched({dt.name}, {m}x{n}, batch={B})")
+    kern = L.bsvd_select_kernel(code, m, n, ctypes.byref(o))
+    return DeviceResult(u=u, s=s, v=v, info=info, kernel=int(kern))
+
+
+def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, device=None):
+    """Equal shape/dtype numpy matrices -> (U (B,m,k), S (B,k), V (B,n,k)|None, info records).
+
+    Host-buffer path: pinned staging of the column-major batch, H2D, one
+    launch, D2H.  Returned U[b] / V[b] are F-ordered views.
+    """
+    torch = _torch()
+    B = len(mats)
+    m, n = mats[0].shape
+    dt = np.dtype(mats[0].dtype)
+    k = min(m, n)
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    tdt = torch_dtype(dt)
+    host = torch.empty((B, n, m), dtype=tdt, pin_memory=True)
+    hv = host.numpy()
+    for b, a in enumerate(mats):
+        hv[b] = a.T
+    a_t = host.to(device, non_blocking=True)
+    res = solve_tensor(a_t, m, n, opts, route, kernel)
+    u_h = res.u.to("cpu")
+    s_h = res.s.to("cpu")
+    v_h = res.v.to("cpu") if res.v is not None else None
+    info_h = res.info.to("cpu")
+    torch.cuda.current_stream(device).synchronize()
+    U = np.swapaxes(u_h.numpy(), 1, 2)
+    S = s_h.numpy()
+    V = np.swapaxes(v_h.numpy(), 1, 2) if v_h is not None else None
+    info = np.frombuffer(info_h.numpy().tobytes(), dtype=INFO_DTYPE)
+    return U, S, V, info, res.kernel

@@ -1,0 +1,247 @@
+"""GPU parity tests: the B200 kernels (through the C-ABI) against the
+reference's golden vectors and the CPU restatement on identical inputs.
+
+Tolerances (north star): singular values normwise-relative
+max|s - s_ref| <= n u s1_ref; e1, e2, e3 < 30u (e3 < 100u for double
+geometric spectra, src/cli.py:209); sorted, converged; outer sweeps within
+one of the reference (guard decisions near threshold can flip with the
+reduction order).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2601_17979_b200 as bs
+from common import ALL_DTYPES, Opts, check_factors, check_sigma_parity, random_matrix, unit_roundoff
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FORCE_FN = {None: bs.svd_dispatch, "unblocked": bs.svd_unblocked, "blocked": bs.svd_blocked}
+
+
+def _opts(d):
+    return bs.JacobiOptions(**d)
+
+
+def test_golden_cases(golden):
+    checked = 0
+    for cid, c in golden.cases.items():
+        a = golden.get(cid, "a")
+        res = FORCE_FN[c["force"]](a, _opts(c["opts"]))
+        assert res.info.path == c["path"], cid
+        assert res.info.converged == c["converged"], cid
+        assert abs(res.info.outer_sweeps - c["outer_sweeps"]) <= 1, (cid, res.info.outer_sweeps, c["outer_sweeps"])
+        m, n = a.shape
+        k = min(m, n)
+        assert res.u.shape == (m, k) and res.sigma.shape == (k,)
+        assert res.sigma.dtype == bs.real_dtype(a.dtype)
+        assert (res.v is None) == (not c["has_v"])
+        if a.size:
+            check_sigma_parity(res.sigma, golden.get(cid, "s"), max(m, n), unit_roundoff(a.dtype))
+            e3k = 100.0 if cid.startswith("c3_") else None
+            check_factors(a, res.u, res.sigma, res.v, e3_k=e3k)
+        checked += 1
+    assert checked == len(golden.cases)
+
+
+@pytest.mark.parametrize("dt", ALL_DTYPES)
+@pytest.mark.parametrize("shape", [(8, 8), (20, 12), (32, 32), (33, 17), (5, 3), (2, 2), (6, 1), (3, 11),
+                                   (64, 64), (80, 40), (40, 96), (48, 33)])
+def test_random_batches_vs_oracle(dt, shape):
+    m, n = shape
+    mats = [random_matrix(m, n, dt, seed=7000 + 13 * b + m * n) for b in range(12)]
+    st = bs.BatchState.for_batch(len(mats))
+    res = bs.batch_svd(mats, bs.JacobiOptions(), st)
+    uu = unit_roundoff(dt)
+    for a, r in zip(mats, res):
+        _, s_ref, _, info = O.solve(a, None, None)
+        assert r.info.path == info["path"]
+        assert r.info.converged
+        assert abs(r.info.outer_sweeps - info["outer_sweeps"]) <= 1
+        check_sigma_parity(r.sigma, s_ref, max(m, n), uu)
+        check_factors(a, r.u, r.sigma, r.v)
+    assert not st.active.any()
+
+
+@pytest.mark.parametrize("dt", ALL_DTYPES)
+@pytest.mark.parametrize("nb,shape", [(8, (48, 48)), (8, (24, 24)), (8, (20, 20)), (16, (40, 12)), (4, (30, 30)),
+                                      (16, (128, 128))])
+def test_forced_blocked_vs_oracle(dt, nb, shape):
+    m, n = shape
+    opts = bs.JacobiOptions(nb=nb)
+    mats = [random_matrix(m, n, dt, seed=9100 + b + nb) for b in range(3)]
+    for a in mats:
+        r = bs.svd_blocked(a, opts)
+        _, s_ref, _, info = O.solve(a, Opts(nb=nb), "blocked")
+        assert r.info.path == "blocked" and r.info.converged
+        assert abs(r.info.outer_sweeps - info["outer_sweeps"]) <= 1
+        check_sigma_parity(r.sigma, s_ref, max(m, n), unit_roundoff(dt))
+        check_factors(a, r.u, r.sigma, r.v)
+        assert r.info.counters.gram_calls == r.info.counters.eig_calls > 0
+
+
+def test_inner_budget_and_twostage_options():
+    a = random_matrix(32, 32, seed=35)
+    r0 = bs.svd_blocked(a, bs.JacobiOptions(nb=8, inner_sweeps=0))
+    r1 = bs.svd_blocked(a, bs.JacobiOptions(nb=8, inner_sweeps=1))
+    r2 = bs.svd_blocked(a, bs.JacobiOptions(nb=8, fused_updates=False))
+    u = 2.0 ** -53
+    for r in (r0, r1, r2):
+        check_factors(a, r.u, r.sigma, r.v)
+    assert np.max(np.abs(r0.sigma - r1.sigma)) <= 30 * u * float(r0.sigma[0])
+    _, s_ref, _, info = O.solve(a, Opts(nb=8, inner_sweeps=0), "blocked")
+    check_sigma_parity(r0.sigma, s_ref, 32, u)
+    assert abs(r0.info.outer_sweeps - info["outer_sweeps"]) <= 1
+
+
+def test_known_answers():
+    r = bs.svd_unblocked(np.asfortranarray([[3.0, 4.0], [0.0, 5.0]]))
+    assert np.allclose(r.sigma, [np.sqrt(45.0), np.sqrt(5.0)], rtol=1e-14)
+    r = bs.svd_unblocked(np.asfortranarray(np.eye(4)))
+    assert r.info.outer_sweeps == 1 and r.info.inner_rotations == 0 and np.array_equal(r.sigma, np.ones(4))
+    d = np.asfortranarray(np.diag(np.arange(1.0, 9.0)))
+    r = bs.svd_dispatch(d)
+    assert np.array_equal(r.sigma, np.arange(8.0, 0.0, -1.0))
+    zc = np.zeros((3, 2), order="F")
+    zc[0, 0] = 2.0
+    r = bs.svd_dispatch(zc)
+    assert r.sigma[0] == 2.0 and r.sigma[1] == 0.0
+    assert np.allclose(r.u.T @ r.u, np.eye(2), atol=1e-14)
+    r = bs.svd_dispatch(np.zeros((4, 4), order="F"))
+    assert np.all(r.sigma == 0) and np.allclose(r.u.T @ r.u, np.eye(4), atol=1e-14)
+    r = bs.svd_dispatch(np.asfortranarray([[2.0]]))
+    assert r.sigma[0] == 2.0
+    r = bs.svd_blocked(np.asfortranarray(np.diag([2.0, 1.0])), bs.JacobiOptions(nb=16))
+    assert np.array_equal(r.sigma, [2.0, 1.0]) and r.info.converged
+    # diagonal inputs exact to 4u (tests/test_acceptance.py:173-179)
+    for dt in ALL_DTYPES:
+        dg = np.asfortranarray(np.diag(np.linspace(3.0, 0.5, 12)).astype(dt))
+        r = bs.svd_dispatch(dg)
+        assert np.max(np.abs(r.sigma - np.linspace(3.0, 0.5, 12))) <= 4 * unit_roundoff(dt) * 3.0
+        assert r.info.inner_rotations == 0
+
+
+def test_wide_and_values_only():
+    a = random_matrix(2, 5, seed=41)
+    r = bs.svd_dispatch(a)
+    assert r.info.path == "transpose+unblocked"
+    assert r.u.shape == (2, 2) and r.v.shape == (5, 2)
+    check_factors(a, r.u, r.sigma, r.v)
+    a = random_matrix(3, 7, seed=42)
+    r = bs.svd_dispatch(a, bs.JacobiOptions(compute_right_vectors=False))
+    assert r.v is None and r.u.shape == (3, 3)
+    check_factors(a, r.u, r.sigma, None)
+    a = random_matrix(8, 8, seed=22)
+    r = bs.svd_unblocked(a, bs.JacobiOptions(compute_right_vectors=False))
+    assert r.v is None
+    check_factors(a, r.u, r.sigma, None)
+
+
+def test_input_not_mutated_and_force_errors():
+    a = random_matrix(10, 6, seed=23)
+    keep = a.copy()
+    bs.svd_unblocked(a)
+    assert np.array_equal(a, keep)
+    with pytest.raises(bs.ShapeError):
+        bs.svd_unblocked(random_matrix(2, 5))
+    with pytest.raises(bs.ShapeError):
+        bs.svd_blocked(random_matrix(2, 5))
+    with pytest.raises(bs.DomainError):
+        bs.svd_dispatch(np.zeros((3, 3), dtype=np.int64, order="F"))
+
+
+def test_batch_semantics():
+    # tests/test_batch.py: batch == standalone, masking bitwise, fault isolation
+    probs = [random_matrix(24, 24, seed=50), random_matrix(40, 40, seed=51), random_matrix(16, 10, seed=52)]
+    opts = bs.JacobiOptions(nb=8)
+    batch = bs.batch_svd(probs, opts)
+    solo = [bs.svd_dispatch(p, opts) for p in probs]
+    for b, s in zip(batch, solo):
+        assert np.array_equal(b.u, s.u) and np.array_equal(b.sigma, s.sigma) and np.array_equal(b.v, s.v)
+        assert b.info.outer_sweeps == s.info.outer_sweeps
+    diag = np.asfortranarray(np.diag(np.linspace(1.0, 0.25, 48)))
+    probs = [diag.copy(order="F") for _ in range(4)] + [random_matrix(48, 48, seed=54 + i) for i in range(4)]
+    st_off, st_on = bs.BatchState.for_batch(8), bs.BatchState.for_batch(8)
+    r_off = bs.batch_svd(probs, bs.JacobiOptions(nb=8, masking=False), st_off)
+    r_on = bs.batch_svd(probs, bs.JacobiOptions(nb=8, masking=True), st_on)
+    assert st_on.counters.masked_pair_skips > 0 and st_off.counters.masked_pair_skips == 0
+    assert st_on.counters.eig_calls < st_off.counters.eig_calls
+    for a, b in zip(r_off, r_on):
+        assert np.array_equal(a.u, b.u) and np.array_equal(a.sigma, b.sigma) and np.array_equal(a.v, b.v)
+    assert np.array_equal(st_off.outer_sweeps, st_on.outer_sweeps)
+    good = random_matrix(16, 16, seed=55)
+    bad = np.zeros((4, 4), dtype=np.int32, order="F")
+    st = bs.BatchState.for_batch(3)
+    out = bs.batch_svd([good, bad, good.copy(order="F")], bs.JacobiOptions(), st)
+    assert out[1] is None and 1 in st.errors
+    assert np.array_equal(out[0].sigma, out[2].sigma)
+    st = bs.BatchState.for_batch(2)
+    bs.batch_svd([np.asfortranarray(np.eye(8)), random_matrix(8, 8, seed=56)], bs.JacobiOptions(), st)
+    assert st.outer_sweeps[0] == 1 and st.outer_sweeps[1] > 1
+
+
+def test_masked_skip_accounting_matches_reference(golden):
+    # identity masked for 8 rounds at n=32 gives 8 * 496 skips
+    probs = [np.asfortranarray(np.eye(32)), golden.get("c1_random_0", "a")]
+    st = bs.BatchState.for_batch(2)
+    res = bs.batch_svd(probs, bs.JacobiOptions(masking=True), st)
+    s1 = res[1].info.outer_sweeps
+    assert res[0].info.masked_pair_skips == (s1 - 1) * 496
+    assert st.counters.eig_calls == 1 + s1
+
+
+@pytest.mark.parametrize("dt", ALL_DTYPES)
+def test_kernel_level_ops_vs_oracle(dt):
+    u = unit_roundoff(dt)
+    a = random_matrix(16, 8, dt, seed=5)
+    v = np.asfortranarray(np.eye(8, dtype=dt))
+    a2, v2 = a.copy(order="F"), v.copy(order="F")
+    sw, rot, cv = bs.onesided_sweeps(a, v, tol=30 * u, max_sweeps=1)
+    sw2, rot2, cv2 = O.onesided_sweeps(a2, v2, 30 * u, 1)
+    assert rot == rot2 and sw == sw2 == 1 and cv == cv2
+    assert np.max(np.abs(a - a2)) <= 64 * u * np.max(np.abs(a2))
+    assert np.max(np.abs(v - v2)) <= 64 * u
+    ai, aj = random_matrix(20, 6, dt, seed=6), random_matrix(20, 5, dt, seed=7)
+    g = bs.compute_gram(ai, aj)
+    g2 = O.compute_gram(ai, aj)
+    assert np.array_equal(g, g.conj().T) and np.all(np.imag(np.diag(g)) == 0)
+    assert np.max(np.abs(g - g2)) <= 100 * u * np.linalg.norm(np.hstack([ai, aj])) ** 2
+    bi, bj, jm = random_matrix(70, 5, dt, seed=8), random_matrix(70, 3, dt, seed=9), random_matrix(8, 8, dt, seed=10)
+    ref = np.hstack([bi, bj]) @ jm
+    bs.fused_pair_update(bi, bj, jm, row_block=16)
+    assert np.allclose(np.hstack([bi, bj]), ref, atol=64 * u * np.max(np.abs(ref)) * 5)
+
+
+def test_full_size_c1_properties():
+    """BASELINE C1-10k shape at full batch: size-independent invariants."""
+    import torch
+
+    from paper_2601_17979_b200.matgen import gen_batch_device
+
+    B, n = 10000, 32
+    a = gen_batch_device("arith", n, n, B, np.float64, kappa=1e10, seed=0)
+    res = bs.solve_tensor(a, n, n, bs.JacobiOptions())
+    torch.cuda.synchronize()
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    info = np.frombuffer(res.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert info["converged"].all()
+    s = res.s.cpu().numpy()
+    assert np.all(np.diff(s, axis=1) <= 0)
+    # prescribed spectrum (e4 < 30u) and Frobenius mass conservation (c09)
+    sig = 1.0 - (np.arange(n) / (n - 1)) * (1.0 - 1e-10)
+    e4 = np.linalg.norm(s - sig, axis=1) / n
+    assert e4.max() < 30 * 2.0 ** -53
+    fro2 = (a.double() ** 2).sum(dim=(1, 2)).cpu().numpy()
+    assert np.max(np.abs((s ** 2).sum(1) - fro2) / fro2) < 30 * 2.0 ** -53 * n
+    # factor checks on a sample, against the oracle on the same inputs
+    A = a.cpu().numpy()
+    U = res.u.cpu().numpy()
+    V = res.v.cpu().numpy()
+    for b in range(0, B, 997):
+        ab = A[b].T
+        check_factors(ab, U[b].T, s[b], V[b].T)
+        _, s_ref, _, oi = O.solve(ab, None, None)
+        check_sigma_parity(s[b], s_ref, n, 2.0 ** -53)
+        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 1

@@ -1,0 +1,151 @@
+"""CPU-only tests of the host side: schedule closed form, options, the C-ABI
+library (loads, exports every declared symbol), result metadata, and that the
+product path refuses to run without a GPU (no CPU fallback)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2601_17979_b200 as bs
+from paper_2601_17979_b200 import _lib
+from paper_2601_17979_b200.ordering import rr_pair
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("ell", [2, 3, 4, 5, 7, 8, 9, 16, 31, 32])
+def test_schedule_closed_form_matches_reference(golden, ell):
+    pairs, starts = bs.schedule_arrays(ell)
+    assert np.array_equal(pairs, golden.get(f"sched_{ell}", "pairs"))
+    assert np.array_equal(starts, golden.get(f"sched_{ell}", "starts"))
+    assert not pairs.flags.writeable
+
+
+@pytest.mark.parametrize("ell", range(2, 97))
+def test_schedule_covers_all_pairs_disjointly(ell):
+    # reference tests/test_ordering.py:48-68 and acceptance c08
+    sched = bs.round_robin_schedule(ell)
+    seen = set()
+    for it in sched.iterations:
+        idx = [x for p in it for x in p]
+        assert len(idx) == len(set(idx))
+        for i, j in it:
+            assert 0 <= i < j < ell
+            seen.add((i, j))
+    assert len(seen) == ell * (ell - 1) // 2
+
+
+def test_schedule_layouts_of_reference_tests():
+    # tests/test_ordering.py:12-30
+    assert bs.round_robin_schedule(2).iterations == (((0, 1),),)
+    assert bs.round_robin_schedule(4).iterations == (((0, 1), (2, 3)), ((0, 3), (1, 2)), ((0, 2), (1, 3)))
+    assert bs.round_robin_schedule(8).iterations[0] == ((0, 1), (2, 3), (4, 5), (6, 7))
+    with pytest.raises(bs.DomainError):
+        bs.round_robin_schedule(1)
+
+
+def test_rr_pair_phantom():
+    # odd ell: exactly one pair per iteration touches the phantom
+    for ell in (3, 5, 9, 31):
+        S = ell + 1
+        for t in range(S - 1):
+            flags = [rr_pair(t, k, S, ell)[2] for k in range(S // 2)]
+            assert flags.count(False) == 1
+
+
+def test_options_defaults_and_validation():
+    o = bs.JacobiOptions()
+    assert (o.k, o.max_nsweeps, o.nb, o.inner_sweeps, o.masking, o.use_qr_preprocess,
+            o.compute_right_vectors, o.fused_updates, o.row_block) == (30.0, 30, 16, 1, False, False, True, True, 64)
+    for kw in ({"k": 0.0}, {"k": -1.0}, {"max_nsweeps": 0}, {"nb": 0}, {"inner_sweeps": -1}, {"row_block": 0}):
+        with pytest.raises(bs.DomainError):
+            bs.JacobiOptions(**kw)
+
+
+def test_compute_rotation_known_answer(golden):
+    # tests/test_eig.py:23-32
+    r = bs.compute_rotation(9.0, 41.0, 12.0)
+    g = golden.meta["rotation_9_41_12"]
+    assert r.c == g["c"] and r.s == g["s"] and r.t == g["t"]
+    assert abs(r.c - 3 / np.sqrt(10)) < 1e-15 and abs(r.t + 1 / 3) < 1e-15
+
+
+def test_library_loads_and_exports_header_symbols():
+    L = _lib.load()
+    with open(os.path.join(ROOT, "include", "bsvd_b200.h")) as fh:
+        hdr = fh.read()
+    declared = set(re.findall(r"^\s*(?:int|size_t|void|const char\*)\s+(bsvd_\w+)\s*\(", hdr, flags=re.M))
+    assert declared == set(_lib.EXPORTS), declared ^ set(_lib.EXPORTS)
+    for sym in declared:
+        assert hasattr(L, sym)
+    assert L.bsvd_abi_version() == 1
+    o = _lib.BsvdOpts()
+    L.bsvd_default_opts(ctypes.byref(o))
+    assert (o.k, o.max_sweeps, o.nb, o.inner_sweeps, o.want_v, o.row_block) == (30.0, 30, 16, 1, 1, 64)
+    assert L.bsvd_strerror(-2).decode() == "workspace too small"
+
+
+def test_library_argument_errors_without_device():
+    # argument checks run on the host and fail before any device work
+    L = _lib.load()
+    o = _lib.BsvdOpts()
+    L.bsvd_default_opts(ctypes.byref(o))
+    rc = L.bsvd_gesvj_batched(7, 4, 4, 1, None, 4, 16, None, 4, 16, None, 4, None, 4, 16,
+                              ctypes.byref(o), None, None, 0, None)
+    assert rc == -1
+    o.route = 1  # forced unblocked on a wide matrix -> ShapeError analogue
+    rc = L.bsvd_gesvj_batched(1, 2, 5, 1, None, 2, 10, None, 2, 4, None, 2, None, 5, 10,
+                              ctypes.byref(o), None, None, 0, None)
+    assert rc == -1
+    o.route = 0
+    o.max_sweeps = 0
+    assert L.bsvd_gesvj_batched(1, 4, 4, 1, None, 4, 16, None, 4, 16, None, 4, None, 4, 16,
+                                ctypes.byref(o), None, None, 0, None) == -1
+
+
+def test_kernel_selection_routes():
+    L = _lib.load()
+    o = _lib.BsvdOpts()
+    L.bsvd_default_opts(ctypes.byref(o))
+    assert L.bsvd_select_kernel(1, 64, 64, ctypes.byref(o)) == 2      # blocked (n > 32)
+    assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) in (1, 3)  # unblocked route
+    assert L.bsvd_select_kernel(1, 0, 5, ctypes.byref(o)) == 0        # empty
+
+
+def test_info_struct_layout():
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    assert INFO_DTYPE.itemsize == ctypes.sizeof(_lib.BsvdInfo) == 48
+
+
+def test_batch_rejects_bad_problems_without_device():
+    # per-problem isolation (src/batch.py:105-111) happens before any device work
+    bad = np.zeros((4, 4), dtype=np.int8, order="F")
+    st = bs.BatchState.for_batch(2)
+    out = bs.batch_svd([bad, np.zeros((2, 2, 2))], bs.JacobiOptions(), st)
+    assert out == [None, None]
+    assert isinstance(st.errors[0], bs.DomainError)
+    assert isinstance(st.errors[1], bs.ShapeError)
+    with pytest.raises(bs.DomainError):
+        bs.batch_svd([])
+
+
+def test_empty_shapes_need_no_device():
+    r = bs.svd_dispatch(np.zeros((0, 0), order="F"))
+    assert r.sigma.shape == (0,) and r.info.path == "empty" and r.info.converged
+    r = bs.svd_dispatch(np.zeros((0, 3), order="F"))
+    assert r.u.shape == (0, 0) and r.v.shape == (3, 0)
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    a = np.eye(4)
+    st = bs.BatchState.for_batch(1)
+    out = bs.batch_svd([a], bs.JacobiOptions(), st)
+    assert out == [None]
+    assert isinstance(st.errors[0], RuntimeError)
+    with pytest.raises(RuntimeError):
+        bs.svd_dispatch(a)

@@ -1,0 +1,29 @@
+"""Quick device timing of the solver on BASELINE shapes (development aid)."""
+import sys, os, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2601_17979_b200 as bs
+from paper_2601_17979_b200.matgen import gen_batch_device
+from paper_2601_17979_b200.solver import INFO_DTYPE
+
+cfgs = [("C1-10k", "arith", 32, 32, 10000, np.float64, 1e10, True),
+        ("C2-full", "random", 16, 16, 10000, np.float32, 1, True),
+        ("C2-vals", "random", 16, 16, 10000, np.float32, 1, False),
+        ("C4", "random", 256, 32, 5000, np.complex128, 1, True),
+        ("C3", "geo", 64, 64, 2000, np.float64, 1e12, True),
+        ("C5", "random", 128, 128, 500, np.float64, 1, True)]
+only = sys.argv[1:] 
+for name, fam, m, n, B, dt, kappa, wantv in cfgs:
+    if only and name not in only: continue
+    a = gen_batch_device(fam, m, n, B, dt, kappa=kappa, seed=0)
+    opts = bs.JacobiOptions(compute_right_vectors=wantv)
+    r = bs.solve_tensor(a, m, n, opts); torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(3):
+        ev0.record(); r = bs.solve_tensor(a, m, n, opts); ev1.record(); torch.cuda.synchronize()
+        ts.append(ev0.elapsed_time(ev1))
+    info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    t = min(ts)
+    print(f"{name:8s} B={B} {m}x{n} {np.dtype(dt).name} kernel={r.kernel} {t:.2f} ms  {B/t*1e3:,.0f} mat/s  "
+          f"sweeps={info['outer_sweeps'].mean():.2f} conv={info['converged'].mean():.3f} rot/mat={info['rotations'].mean():.0f}", flush=True)
