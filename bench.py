@@ -1,0 +1,443 @@
+"""Benchmark: batched one-sided Jacobi SVD on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c1-10k]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+A step solves one whole batch (default C1-10k: 10,000 x 32x32 FP64, arith
+spectrum kappa=1e10, full U/S/V) with inputs resident in HBM.  Multi-GPU is
+weak scaling by plain batch splitting: every rank solves its own batch of the
+same size; no collective on the data path.  The L2 (126 MB) is
+flushed with a 512 MiB write between timed steps; each step is timed with
+CUDA events on the launching stream; the job time is the max over ranks.
+
+Also reported on one JSON line: the FP64 (FP32) FMA roofline of the solver
+kernel (algorithmic flops from the reference's own telemetry formula, SURVEY
+8(d), evaluated on the CPU restatement's sweep/rotation counts for the same
+inputs ÷ measured pipe peak), the CPU baseline (oracle/ port on the host
+cores, bounded sample), the end-to-end number through the C-ABI with host
+buffers, clocks sampled during the run, and the launch count.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port, all host threads) on the same config and prints the same line
+with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batched SVD matrices/sec & Gflop/s vs n (FP64/FP32) at 1/2/4/8 B200 vs CPU ref"
+
+CONFIGS = {
+    "c1-10k": dict(desc="C1-10k: 10000 x 32x32 FP64, arith spectrum kappa=1e10, full U/S/V (north-star target)",
+                   family="arith", m=32, n=32, batch=10000, dtype="float64", kappa=1e10, want_v=True, route=None),
+    "c1": dict(desc="C1: 1000 x 32x32 FP64, arith kappa=1e10, full U/S/V", family="arith", m=32, n=32, batch=1000,
+               dtype="float64", kappa=1e10, want_v=True, route=None),
+    "c1r": dict(desc="C1r: 10000 x 32x32 FP64 uniform random, full U/S/V", family="random", m=32, n=32,
+                batch=10000, dtype="float64", kappa=1.0, want_v=True, route=None),
+    "c2-full": dict(desc="C2: 10000 x 16x16 FP32 random, full vectors", family="random", m=16, n=16, batch=10000,
+                    dtype="float32", kappa=1.0, want_v=True, route=None),
+    "c2-vals": dict(desc="C2: 10000 x 16x16 FP32 random, values-only", family="random", m=16, n=16, batch=10000,
+                    dtype="float32", kappa=1.0, want_v=False, route=None),
+    "c3-geo": dict(desc="C3a: 10000 x 64x64 FP64 geometric spectrum kappa=1e12", family="geo", m=64, n=64,
+                   batch=10000, dtype="float64", kappa=1e12, want_v=True, route=None),
+    "c3-rank": dict(desc="C3b: 10000 x 64x64 FP64 rank 48 (geo 1e6 + 16 zeros)", family="rankdef", m=64, n=64,
+                    batch=10000, dtype="float64", kappa=1e6, want_v=True, route=None, rank=48),
+    "c4": dict(desc="C4: 5000 x 256x32 complex128 random (reference dispatch: unblocked)", family="random", m=256,
+               n=32, batch=5000, dtype="complex128", kappa=1.0, want_v=True, route=None),
+    "c4-blocked": dict(desc="C4: 5000 x 256x32 complex128 random, blocked Gram path (svd_blocked)",
+                       family="random", m=256, n=32, batch=5000, dtype="complex128", kappa=1.0, want_v=True,
+                       route="blocked"),
+    "c5": dict(desc="C5: 2000 x 128x128 FP64 random, blocked (ell=8)", family="random", m=128, n=128, batch=2000,
+               dtype="float64", kappa=1.0, want_v=True, route=None),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work, from the reference telemetry formula
+# ---------------------------------------------------------------------------
+def flops_per_problem(info: dict, m: int, n: int, cplx: bool, want_v: bool, nb: int = 16) -> float:
+    bm, bn = max(m, n), min(m, n)
+    f = 0.0
+    if info["path"].endswith("unblocked"):
+        S, R = info["outer_sweeps"], info["inner_rotations"]
+        f = S * bn * (bn - 1) / 2 * 6 * bm + R * 6 * (bm + (bn if want_v else 0))
+    else:
+        w = min(2 * nb, bn)
+        G, R, Up = info["gram_calls"], info["inner_rotations"], info["update_calls"]
+        f = G * w * (w + 1) * bm + R * 12 * w + Up * 2 * w * w * (bm + (bn if want_v else 0))
+    return f * (4.0 if cplx else 1.0)
+
+
+def compulsory_bytes(m, n, es, rs, want_v):
+    k = min(m, n)
+    return 2 * m * n * es + (n * k * es if want_v else 0) + k * rs
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the run)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = str(gpu_index)
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+        except Exception as exc:  # pragma: no cover
+            log("clock sampler unavailable:", exc)
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9 and parts[0] == self.gpu:
+                self.samples.append((time.perf_counter(), parts))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        win = [p for (t, p) in self.samples if t0 - 0.15 <= t <= t1 + 0.15] or [p for (_, p) in self.samples]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(p[1]) for p in win if p[1].replace(".", "").isdigit()]
+        mx = [float(p[2]) for p in win if p[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in win for i in range(4) if p[5 + i].lower().startswith("active")})
+        pw = [float(p[3]) for p in win if p[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(win), "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------
+def oracle_time(a_host3, cfg, nthreads, count):
+    """Time the CPU restatement on exactly `count` problems; returns (count, seconds, infos)."""
+    from oracle import oracle as O
+    from paper_2601_17979_b200 import JacobiOptions
+
+    opts = JacobiOptions(compute_right_vectors=cfg["want_v"])
+    t = time.perf_counter()
+    _, _, _, infos = O.solve_batch(a_host3[:count], opts, cfg["route"], nthreads=nthreads)
+    return count, time.perf_counter() - t, infos
+
+
+def oracle_sample(a_host3, cfg, nthreads, max_seconds=None, min_count=16):
+    """Time the CPU restatement on a prefix sized to ~max_seconds; returns (count, seconds, infos)."""
+    from oracle import oracle as O
+    from paper_2601_17979_b200 import JacobiOptions
+
+    opts = JacobiOptions(compute_right_vectors=cfg["want_v"])
+    B = a_host3.shape[0]
+    count = min(B, max(min_count, nthreads * 2))
+    t = time.perf_counter()
+    _, _, _, infos = O.solve_batch(a_host3[:count], opts, cfg["route"], nthreads=nthreads)
+    dt = time.perf_counter() - t
+    if max_seconds is not None and dt < max_seconds * 0.5 and count < B:
+        count = int(min(B, count * max_seconds / max(dt, 1e-3)))
+        t = time.perf_counter()
+        _, _, _, infos = O.solve_batch(a_host3[:count], opts, cfg["route"], nthreads=nthreads)
+        dt = time.perf_counter() - t
+    return count, dt, infos
+
+
+def host_batch(a_dev):
+    """(B, n, m) device tensor -> (B, m, n) host ndarray (matrices as the user sees them)."""
+    return np.swapaxes(a_dev.cpu().numpy(), 1, 2)
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference algorithm's CPU implementation (oracle port), all host threads."""
+    import torch
+
+    from paper_2601_17979_b200.matgen import gen_batch_device
+
+    nthreads = len(os.sched_getaffinity(0))
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    a_dev = gen_batch_device(cfg["family"], cfg["m"], cfg["n"], cfg["batch"], np.dtype(cfg["dtype"]),
+                             kappa=cfg["kappa"], seed=0, rank=cfg.get("rank"), device=dev)
+    A = host_batch(a_dev)
+    cplx = np.dtype(cfg["dtype"]).kind == "c"
+    # size each step to about 6 s of wall on all threads so K+W steps stay within minutes
+    count, dt, infos = oracle_sample(A, cfg, nthreads, max_seconds=6.0)
+    rates, fl = [], []
+    for s in range(args.warmup + args.steps):
+        c, d, infos = oracle_time(A, cfg, nthreads, count)
+        if s >= args.warmup:
+            rates.append(c / d)
+            fl.append(sum(flops_per_problem(i, cfg["m"], cfg["n"], cplx, cfg["want_v"]) for i in infos) / d)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "matrices/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": count / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_tag(cfg),
+        "data": "synthetic (device-generated, same generator and seed as the b200 arm)",
+        "config": config_block(cfg, args),
+        "gflops": statistics.median(fl) / 1e9,
+        "cpu_baseline": {"value": value, "unit": "matrices/s", "cores": nthreads, "kind": "port",
+                         "sample": f"{count} of {cfg['batch']} problems per step (oracle/ C++ restatement, "
+                                   f"OpenMP over problems, {nthreads} threads)"},
+        "e2e": {"value": value, "unit": "matrices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def dtype_tag(cfg):
+    return {"float64": "f64", "float32": "f32", "complex128": "c128", "complex64": "c64"}[cfg["dtype"]]
+
+
+def config_block(cfg, args):
+    return {"workload": cfg["desc"], "config_id": args.config, "batch_per_gpu": cfg["batch"], "m": cfg["m"],
+            "n": cfg["n"], "dtype": cfg["dtype"], "want_v": cfg["want_v"], "route": cfg["route"] or "dispatch",
+            "parallelism": f"batch split x{args.gpus} (no collective)",
+            "l2": "flushed between timed steps (512 MiB write); inputs device-resident"}
+
+
+def measure_fma_peak(dtype_code):
+    """Best-of-5 FMA-pipe throughput (TFLOP/s) with the library's microbenchmark."""
+    import torch
+
+    from paper_2601_17979_b200 import _lib
+
+    L = _lib.load()
+    blocks, iters = 148 * 16, 2048
+    out = torch.empty(blocks, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    best = 0.0
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(L.bsvd_bench_fma_peak(dtype_code, blocks, iters, out.data_ptr(), st), "fma peak")
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        best = max(best, 2.0 * 128 * 256 * blocks * iters / t / 1e12)
+    return best
+
+
+def load_traffic(config_id):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(config_id)
+    return None
+
+
+def run_b200(args, cfg):
+    import torch
+
+    import paper_2601_17979_b200 as bs
+    from paper_2601_17979_b200 import _lib
+    from paper_2601_17979_b200.matgen import gen_batch_device
+    from paper_2601_17979_b200.solver import INFO_DTYPE, solve_tensor
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dt = np.dtype(cfg["dtype"])
+    cplx = dt.kind == "c"
+    m, n, B = cfg["m"], cfg["n"], cfg["batch"]
+    k = min(m, n)
+    opts = bs.JacobiOptions(compute_right_vectors=cfg["want_v"])
+    route = {None: _lib.DISPATCH, "blocked": _lib.FORCE_BLOCKED, "unblocked": _lib.FORCE_UNBLOCKED}[cfg["route"]]
+    # each rank its own problems (weak scaling): seed offset by rank
+    a = gen_batch_device(cfg["family"], m, n, B, dt, kappa=cfg["kappa"], seed=1000 * rank, rank=cfg.get("rank"),
+                         device=dev)
+    es = dt.itemsize
+    rs = np.dtype(bs.real_dtype(dt)).itemsize
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    u_t = torch.empty((B, k, m), dtype=a.dtype, device=dev)
+    s_t = torch.empty((B, k), dtype=torch.float64 if rs == 8 else torch.float32, device=dev)
+    v_t = torch.empty((B, k, n), dtype=a.dtype, device=dev) if cfg["want_v"] else None
+    info_t = torch.empty((B * _lib.INFO_BYTES,), dtype=torch.uint8, device=dev)
+    out = (u_t, s_t, v_t, info_t)
+
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    phys = dev.index
+    if cvd:
+        ids = [x.strip() for x in cvd.split(",")]
+        if dev.index < len(ids) and ids[dev.index].isdigit():
+            phys = int(ids[dev.index])
+    sampler = ClockSampler(phys)
+    sampler.start()
+    time.sleep(0.3)
+    for _ in range(args.warmup):
+        res = solve_tensor(a, m, n, opts, route, out=out)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.perf_counter()
+    evs = []
+    stream = torch.cuda.current_stream()
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush, outside the timed events
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = solve_tensor(a, m, n, opts, route, out=out)
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall1 = time.perf_counter()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    dev_s = sum(step_ms) / 1e3
+    if dist:
+        tt = torch.tensor([dev_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_s = float(tt.item())
+    info = np.frombuffer(res.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    kernel_id = int(info["kernel"][0])
+
+    # end-to-end through the C-ABI with host (pinned) buffers: H2D + solve + D2H every step
+    a_host = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
+    a_host.copy_(a)
+    u_h = torch.empty(u_t.shape, dtype=u_t.dtype, pin_memory=True)
+    s_h = torch.empty(s_t.shape, dtype=s_t.dtype, pin_memory=True)
+    v_h = torch.empty(v_t.shape, dtype=v_t.dtype, pin_memory=True) if v_t is not None else None
+    i_h = torch.empty(info_t.shape, dtype=info_t.dtype, pin_memory=True)
+    a_in = torch.empty_like(a)
+    e2e_ms = []
+    for it in range(args.warmup + args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        a_in.copy_(a_host, non_blocking=True)
+        solve_tensor(a_in, m, n, opts, route, out=out)
+        u_h.copy_(u_t, non_blocking=True)
+        s_h.copy_(s_t, non_blocking=True)
+        if v_h is not None:
+            v_h.copy_(v_t, non_blocking=True)
+        i_h.copy_(info_t, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e_s = sum(e2e_ms) / 1e3
+    if dist:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    h2d = B * m * n * es
+    d2h = B * m * k * es + B * k * rs + (B * n * k * es if v_t is not None else 0) + B * _lib.INFO_BYTES
+    sampler.stop()
+    clocks = sampler.summary(t_wall0, t_wall1)
+
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # algorithmic flops per problem from the reference telemetry on the same inputs (CPU restatement)
+    nthreads = len(os.sched_getaffinity(0))
+    A = host_batch(a)
+    cpu_line = None
+    if world == 1:
+        cnt, cdt, cinfos = oracle_sample(A, cfg, nthreads, max_seconds=8.0)
+        cpu_line = {"value": cnt / cdt, "unit": "matrices/s", "cores": nthreads, "kind": "port",
+                    "sample": f"first {cnt} of the {B} bench problems, oracle/ C++ restatement "
+                              f"(OpenMP over problems, {nthreads} threads), {cdt:.1f} s wall"}
+    else:
+        cnt, cdt, cinfos = oracle_sample(A, cfg, nthreads, min_count=64)
+    f_mat = float(np.mean([flops_per_problem(i, m, n, cplx, cfg["want_v"]) for i in cinfos]))
+    o_sweeps = float(np.mean([i["outer_sweeps"] for i in cinfos]))
+    peak = measure_fma_peak(0 if rs == 4 else 1)
+    steps_total = args.steps * world
+    value = B * steps_total / dev_s
+    ms_per_step = dev_s / args.steps * 1e3
+    launch_s = (sum(step_ms) / len(step_ms)) / 1e3  # rank-0 average launch duration
+    achieved = f_mat * B / launch_s / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "matrices/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": dtype_tag(cfg),
+        "data": f"synthetic ({cfg['family']} spectrum, device-generated; A = U diag(s) V^H for prescribed spectra)",
+        "config": config_block(cfg, args),
+        "gflops": f_mat * B * steps_total / dev_s / 1e9,
+        "roofline": {"bound": "fp64-fma" if rs == 8 else "fp32-fma", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": load_traffic(args.config),
+                     "peak_source": "measured on this box by bsvd_bench_fma_peak (MEASURED_PEAKS.json has no "
+                                    "FP64/FP32 pipe entry)",
+                     "flops_per_matrix": f_mat, "flops_source": "SURVEY 8(d) formula on the CPU restatement's "
+                     "sweep/rotation counts for the same inputs (bitwise equal to the reference's)",
+                     "hbm_bytes_per_matrix": compulsory_bytes(m, n, es, rs, cfg["want_v"])},
+        "cpu_baseline": cpu_line,
+        "e2e": {"value": B * steps_total / e2e_s, "unit": "matrices/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "path": "bsvd_gesvj_batched with pinned host buffers, H2D+solve+D2H"},
+        "clocks": clocks,
+        "gpu_launches": args.steps,
+        "kernel_variant": kernel_id,
+        "parity": {"converged_frac": float(info["converged"].mean()), "gpu_mean_sweeps": float(
+            info["outer_sweeps"].mean()), "ref_mean_sweeps_sample": o_sweeps},
+        "wall_s_timed_region": t_wall1 - t_wall0,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c1-10k")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

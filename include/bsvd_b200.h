@@ -133,6 +133,14 @@ int bsvd_fused_pair_update_batched(int dtype, int m, int w, int batch, void* b, 
                                    int64_t stride_b, const void* j, int64_t ldj, int64_t stride_j,
                                    int delta, void* stream);
 
+/*
+ * Diagnostics: FMA-pipe peak microbenchmark used as the roofline denominator
+ * (dtype BSVD_D or BSVD_S).  Launches blocks x 256 threads, each running
+ * iters x 128 dependent-free FMAs; out: device scratch of `blocks` elements.
+ * Flops = 2 * 128 * 256 * blocks * iters.
+ */
+int bsvd_bench_fma_peak(int dtype, int blocks, int iters, void* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,7 @@ EXPORTS = (
     "bsvd_onesided_sweeps_batched",
     "bsvd_gram_batched",
     "bsvd_fused_pair_update_batched",
+    "bsvd_bench_fma_peak",
 )
 
 _lib = None
@@ -97,6 +98,8 @@ def load():
     L.bsvd_gram_batched.restype = ci
     L.bsvd_fused_pair_update_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, vp, i64, i64, ci, vp]
     L.bsvd_fused_pair_update_batched.restype = ci
+    L.bsvd_bench_fma_peak.argtypes = [ci, ci, ci, vp, vp]
+    L.bsvd_bench_fma_peak.restype = ci
     _lib = L
     return L
 

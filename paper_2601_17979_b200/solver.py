@@ -45,7 +45,8 @@ _TORCH_OF = {}
 
 
 def torch_dtype(np_dtype):
-    torch = _torch()
+    import torch
+
     if not _TORCH_OF:
         _TORCH_OF.update({
             np.dtype(np.float32): torch.float32,
