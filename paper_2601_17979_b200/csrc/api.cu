@@ -44,14 +44,14 @@ int make_route(int m, int n, const bsvd_opts* o, Route* r) {
     return BSVD_OK;
 }
 
-Plan make_plan(int dt, const Route& r, const bsvd_opts* o) {
+Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = true) {
     const size_t lim = smem_limit();
     const int es = esize_of(dt), rs = rsize_of(dt);
     if (r.blocked) return plan_blocked_general(es, rs, r.bm, r.bn, o->nb, r.need_v, lim);
-    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG32) {
-        Plan p = plan_unblocked_reg(dt, r.bm, r.bn, r.need_v);
+    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG32 || o->kernel == KV_UNBLOCKED_REG32_O3) {
+        Plan p = plan_unblocked_reg(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
         if (p.kernel) return p;
-        if (o->kernel == KV_UNBLOCKED_REG32) return p;  // kernel 0 => unsupported
+        if (o->kernel != 0) return p;  // forced variant unavailable => kernel 0 => unsupported
     }
     return plan_unblocked_general(es, rs, r.bm, r.bn, r.need_v, lim);
 }
@@ -110,6 +110,7 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_UNBLOCKED_GENERAL: return launch_unblocked_general<T>(a, p, st);
         case KV_BLOCKED_GENERAL: return launch_blocked_general<T>(a, p, st);
         case KV_UNBLOCKED_REG32:
+        case KV_UNBLOCKED_REG32_O3:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg_d32(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
     }
@@ -189,7 +190,7 @@ int bsvd_gesvj_batched(int dtype, int m, int n, int batch, const void* A, int64_
     if (opts->want_v && (!V || ldv < n)) return BSVD_ERR_ARG;
     if (batch > 1 && (strideA < lda * (int64_t)n || strideU < ldu * (int64_t)k || strideS < k)) return BSVD_ERR_ARG;
     if (batch > 1 && opts->want_v && strideV < ldv * (int64_t)k) return BSVD_ERR_ARG;
-    const Plan p = make_plan(dtype, r, opts);
+    const Plan p = make_plan(dtype, r, opts, lda == m);
     if (!p.kernel) return BSVD_ERR_UNSUPPORTED;
     const size_t need = p.work_elems * (size_t)esize_of(dtype) * (size_t)batch;
     if (need > work_bytes || (need && !work)) return BSVD_ERR_WORKSPACE;

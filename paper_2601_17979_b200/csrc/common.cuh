@@ -177,6 +177,72 @@ BSVD_DEV RotParams rot_params(double num, double absg2) {
 }
 
 // ---------------------------------------------------------------------------
+// Call-free float64 division / square root for register-resident kernels.
+// CUDA's IEEE '/' and sqrt() branch to a slow-path subroutine; the CALL makes
+// the register allocator spill every live value around it, which wrecks a
+// kernel that keeps its working copy in registers.  These versions refine the
+// MUFU approximations with Newton steps in DFMA and a final residual
+// correction (result within 1 ulp of the IEEE value), and handle 0, tiny
+// (pre-scaled by exact powers of two) and infinite operands with selects.
+// ---------------------------------------------------------------------------
+BSVD_DEV double rcp_approx(double b) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+    return r;
+}
+BSVD_DEV double rsqrt_approx(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
+// a / b for b > 0 (b may be tiny or +inf); a finite.
+BSVD_DEV double fdiv(double a, double b) {
+    const bool sm = b < 0x1p-960;
+    const double as = sm ? a * 0x1p+1000 : a;
+    const double bs = sm ? b * 0x1p+1000 : b;
+    double r = rcp_approx(bs);
+    double e = fma(-bs, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-bs, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-bs, r, 1.0);
+    r = fma(r, e, r);
+    const double q = as * r;
+    const double rem = fma(-bs, q, as);
+    const double qr = fma(rem, r, q);
+    return isinf(bs) ? 0.0 * as : (isinf(q) ? q : qr);
+}
+// sqrt(x) for x >= 0 (x may be 0, tiny or +inf).
+BSVD_DEV double fsqrt(double x) {
+    const bool tiny = x < 0x1p-960;
+    const double xs = tiny ? x * 0x1p+1000 : x;
+    double y = rsqrt_approx(xs);
+    double e = fma(-(xs * y), y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-(xs * y), y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-(xs * y), y, 1.0);
+    y = fma(0.5 * y, e, y);
+    double s = xs * y;
+    const double rr = fma(-s, s, xs);
+    s = fma(rr, 0.5 * y, s);
+    s = tiny ? s * 0x1p-500 : s;
+    return (x == 0.0 || isinf(x)) ? x : s;
+}
+// rot_params with the call-free primitives (same formula, <= 1 ulp per op).
+BSVD_DEV RotParams rot_params_fast(double num, double absg2) {
+    const double tau = fdiv(num, absg2);
+    const double sgn = tau >= 0.0 ? 1.0 : -1.0;
+    const double t = fdiv(sgn, fabs(tau) + fsqrt(fma(tau, tau, 1.0)));
+    const double h = fsqrt(fma(t, t, 1.0));
+    RotParams p;
+    p.t = t;
+    p.s = fdiv(t, h);
+    p.cm1 = -fdiv(t * t, h * (1.0 + h));
+    return p;
+}
+
+// ---------------------------------------------------------------------------
 // Round-robin tournament schedule (src/ordering.py:32-75) in closed form.
 // Slots other than top[0] form a ring [bot0, top1..top_{h-1}, bot_{h-1}..bot1]
 // of length S-1; every iteration each value advances one ring position.

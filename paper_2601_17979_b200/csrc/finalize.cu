@@ -1,0 +1,53 @@
+// finalize.cu -- kernel (5) as a standalone pass for the register-resident
+// solvers: the raw converged working copy W (bm x bn) and V (bn x bn) sit in
+// the workspace; one CTA per problem stages them in shared memory and runs
+// the shared finalisation routine (finalize.cuh: sigma in float64, tiny-column
+// completion, stable descending sort, permuted U/V, transpose swap).
+#include "kernel_args.cuh"
+#include "launch.h"
+
+namespace bsvd {
+
+template <class T>
+__global__ void __launch_bounds__(128) k_finalize_ws(SolveArgs<T> a) {
+    using R = typename tr<T>::R;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int prob = blockIdx.x;
+    const int bm = a.bm, bn = a.bn;
+    const T* src = a.work + (size_t)prob * a.work_stride;
+    T* W = reinterpret_cast<T*>(smem);
+    T* Vw = a.need_v ? W + (size_t)bm * bn : nullptr;
+    size_t off = ((size_t)bm * bn + (a.need_v ? (size_t)bn * bn : 0)) * sizeof(T);
+    off = (off + 15) & ~size_t(15);
+    R* sig = reinterpret_cast<R*>(smem + off);
+    off += ((size_t)bn * sizeof(R) + 15) & ~size_t(15);
+    int* perm = reinterpret_cast<int*>(smem + off);
+    off += ((size_t)bn * sizeof(int) + 15) & ~size_t(15);
+    int* flag = reinterpret_cast<int*>(smem + off);
+    const int total = bm * bn + (a.need_v ? bn * bn : 0);
+    for (int e = threadIdx.x; e < total; e += blockDim.x) W[e] = src[e];
+    __syncthreads();
+    finalize_block<T>(W, bm, bm, bn, Vw, bn, sig, perm, flag, final_out(a, prob));
+}
+
+template <class T>
+int launch_finalize_ws(SolveArgs<T> a, cudaStream_t st) {
+    const size_t es = sizeof(T);
+    size_t smem = ((size_t)a.bm * a.bn + (a.need_v ? (size_t)a.bn * a.bn : 0)) * es;
+    smem = ((smem + 15) & ~size_t(15)) + (((size_t)a.bn * sizeof(typename tr<T>::R) + 15) & ~size_t(15)) +
+           (((size_t)a.bn * 4 + 15) & ~size_t(15)) + 16;
+    if (smem > 48 * 1024) {
+        if (cudaFuncSetAttribute(k_finalize_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return BSVD_ERR_CUDA;
+    }
+    k_finalize_ws<T><<<a.batch, 128, smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+template int launch_finalize_ws<float>(SolveArgs<float>, cudaStream_t);
+template int launch_finalize_ws<double>(SolveArgs<double>, cudaStream_t);
+template int launch_finalize_ws<cx<float>>(SolveArgs<cx<float>>, cudaStream_t);
+template int launch_finalize_ws<cx<double>>(SolveArgs<cx<double>>, cudaStream_t);
+
+}  // namespace bsvd

@@ -39,7 +39,8 @@ struct SolveArgs {
 enum {
     KV_UNBLOCKED_GENERAL = 1,
     KV_BLOCKED_GENERAL = 2,
-    KV_UNBLOCKED_REG32 = 3,
+    KV_UNBLOCKED_REG32 = 3,     // 32x32 FP64 register-resident, 2 CTAs/SM (255 regs)
+    KV_UNBLOCKED_REG32_O3 = 4,  // same, capped at 168 regs for 3 CTAs/SM
 };
 
 template <class T>

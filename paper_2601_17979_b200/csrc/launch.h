@@ -20,13 +20,16 @@ struct Plan {
 
 Plan plan_unblocked_general(int esize, int rsize, int bm, int bn, int need_v, size_t smem_limit);
 Plan plan_blocked_general(int esize, int rsize, int bm, int bn, int nb, int need_v, size_t smem_limit);
-Plan plan_unblocked_reg(int dtype, int bm, int bn, int need_v);
+Plan plan_unblocked_reg(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
 
 template <class T>
 int launch_unblocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
 template <class T>
 int launch_blocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
 int launch_unblocked_reg_d32(SolveArgs<double> a, const Plan& p, cudaStream_t st);
+
+template <class T>
+int launch_finalize_ws(SolveArgs<T> a, cudaStream_t st);
 
 int group_for_rows(int bm);
 int threads_for(int bn, int G);

@@ -41,7 +41,7 @@ def test_golden_cases(golden):
         assert res.u.shape == (m, k) and res.sigma.shape == (k,)
         assert res.sigma.dtype == bs.real_dtype(a.dtype)
         assert (res.v is None) == (not c["has_v"])
-        if a.size:
+        if a.size and c["converged"]:  # an unconverged (sweep-capped) solve has no accuracy contract
             check_sigma_parity(res.sigma, golden.get(cid, "s"), max(m, n), unit_roundoff(a.dtype))
             e3k = 100.0 if cid.startswith("c3_") else None
             check_factors(a, res.u, res.sigma, res.v, e3_k=e3k)

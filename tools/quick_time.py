@@ -12,18 +12,23 @@ cfgs = [("C1-10k", "arith", 32, 32, 10000, np.float64, 1e10, True),
         ("C4", "random", 256, 32, 5000, np.complex128, 1, True),
         ("C3", "geo", 64, 64, 2000, np.float64, 1e12, True),
         ("C5", "random", 128, 128, 500, np.float64, 1, True)]
-only = sys.argv[1:] 
+args = sys.argv[1:]
+kernels = [0]
+if "--kernels" in args:
+    i = args.index("--kernels"); kernels = [int(x) for x in args[i+1].split(",")]; del args[i:i+2]
+only = args
 for name, fam, m, n, B, dt, kappa, wantv in cfgs:
     if only and name not in only: continue
     a = gen_batch_device(fam, m, n, B, dt, kappa=kappa, seed=0)
     opts = bs.JacobiOptions(compute_right_vectors=wantv)
-    r = bs.solve_tensor(a, m, n, opts); torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ts = []
-    for _ in range(3):
-        ev0.record(); r = bs.solve_tensor(a, m, n, opts); ev1.record(); torch.cuda.synchronize()
+    for kern in kernels:
+      r = bs.solve_tensor(a, m, n, opts, kernel=kern); torch.cuda.synchronize()
+      ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+      ts = []
+      for _ in range(3):
+        ev0.record(); r = bs.solve_tensor(a, m, n, opts, kernel=kern); ev1.record(); torch.cuda.synchronize()
         ts.append(ev0.elapsed_time(ev1))
-    info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
-    t = min(ts)
-    print(f"{name:8s} B={B} {m}x{n} {np.dtype(dt).name} kernel={r.kernel} {t:.2f} ms  {B/t*1e3:,.0f} mat/s  "
+      info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+      t = min(ts)
+      print(f"{name:8s} B={B} {m}x{n} {np.dtype(dt).name} kernel={int(info['kernel'][0])} {t:.2f} ms  {B/t*1e3:,.0f} mat/s  "
           f"sweeps={info['outer_sweeps'].mean():.2f} conv={info['converged'].mean():.3f} rot/mat={info['rotations'].mean():.0f}", flush=True)
