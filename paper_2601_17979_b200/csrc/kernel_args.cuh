@@ -39,8 +39,10 @@ struct SolveArgs {
 enum {
     KV_UNBLOCKED_GENERAL = 1,
     KV_BLOCKED_GENERAL = 2,
-    KV_UNBLOCKED_REG32 = 3,     // 32x32 FP64 register-resident, 2 CTAs/SM (255 regs)
-    KV_UNBLOCKED_REG32_O3 = 4,  // same, capped at 168 regs for 3 CTAs/SM
+    KV_UNBLOCKED_REG32 = 3,     // 32x32 FP64 register-resident (168 regs, 12 warps/SM)
+    KV_UNBLOCKED_REG32_O3 = 4,  // same, 255 regs, 8 warps/SM
+    KV_UNBLOCKED_REG32_R2 = 5,  // same, 204 regs, 10 warps/SM
+    KV_UNBLOCKED_REG32_R3 = 6,  // same, 227 regs, 9 warps/SM
 };
 
 template <class T>

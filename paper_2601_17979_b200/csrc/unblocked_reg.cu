@@ -1,43 +1,48 @@
 // unblocked_reg.cu -- kernel (2), register-resident fast path for 32x32 FP64.
 //
 // Same iteration as onesided_sweeps (src/_kernels_numba.py:85-138) on the
-// reference's round-robin schedule (src/ordering.py:32-75), with the working
-// copy held in registers instead of shared memory:
+// reference's round-robin schedule (src/ordering.py:32-75); the working copy
+// lives in registers instead of memory:
 //
-//  * A warp owns TWO problems; half-warp h (16 lanes) owns problem h, and each
-//    lane holds two full rows of W (rows l and l+16, 2 x 32 doubles).  The
-//    16 disjoint column pairs of a schedule iteration sit in fixed register
-//    slots (2k, 2k+1); instead of indexing columns by the schedule, the
-//    columns are MOVED between slots after every iteration along the
-//    tournament ring (bot0 -> top1 -> ... -> top15 -> bot15 -> ... -> bot1 ->
-//    bot0), so every register index is a compile-time constant.  After 31
-//    iterations (one sweep) the slots are back in natural column order.
-//  * The 48 dot products of an iteration (g_ii, g_jj, g_ji for 16 pairs) are
-//    formed per lane over its two rows and reduced over the 16 lanes with a
-//    transposing xor butterfly (45 shuffles instead of 48 x 4): after the last
-//    level lane k of each half holds the full sums of pair k and evaluates the
-//    rotation (guard F4, parameters F5) in float64 exactly like the reference.
-//  * Parameters go through a 4-deep shared-memory ring guarded by mbarriers to
-//    a V warp that holds the two problems' V rows the same way and applies
-//    the identical rotations (warp specialisation: the V update never waits
-//    on the dot-product/parameter chain).
-//  * A problem stops after its first quiet sweep (per-problem convergence on
-//    the device); the warp keeps stepping its partner problem, whose quiet
-//    sweeps are exact no-ops (F7).
-//  * The raw converged W and V go to a workspace; the finalisation kernel
-//    (finalize.cu) forms sigma, normalises, sorts and permutes.
+//  * A warp owns TWO problems; half-warp h (16 lanes) owns problem h and every
+//    lane holds two full rows (rows l and l+16, 2 x 32 doubles).  The 16
+//    disjoint column pairs of a schedule iteration sit in fixed register slots
+//    (2k, 2k+1); instead of indexing columns by the schedule, the columns MOVE
+//    one position along the tournament ring (bot0 -> top1 -> ... -> top15 ->
+//    bot15 -> ... -> bot1 -> bot0) after every iteration, so every register
+//    index is a compile-time constant.  After the 31 iterations of a sweep the
+//    columns are back in natural order.
+//  * Dot products: each lane forms the 48 partials (g_ii, g_jj, g_ji for 16
+//    pairs over its two rows) and transposes them through shared memory; lane
+//    k of each half then sums pair k's 16 partials and evaluates the guard
+//    (F4) and the rotation (F5) in float64 with call-free rcp/rsqrt refinement
+//    (common.cuh), so no ABI call forces the resident rows to spill.
+//  * Phase alternation instead of a V warp: during a sweep the warp holds W
+//    and logs every rotation (c - 1, w s) to an L2-resident log; after the
+//    sweep it parks W in the workspace, pulls V into the same registers,
+//    replays the logged rotations (cp.async double-buffered, throughput-bound
+//    FP64 with plenty of ILP), parks V and resumes W.  Warps in the latency-
+//    bound W phase interleave with warps in the throughput-bound V phase.
+//  * Per-problem convergence: a problem stops after its first quiet sweep
+//    (src/svd.py:427-430); its half keeps stepping with identity rotations
+//    while the partner problem runs (a quiet sweep never writes, F7).
+//  * The data are pre-scaled by an exact power of two (max |a| in [0.5, 1)),
+//    undone on output: rotations are scale-invariant and the scaling is
+//    exact, so the rotation sequence is unchanged; it keeps the squared
+//    column norms far from under/overflow.
+//  * Raw W and V go to the workspace; finalize.cu forms sigma, normalises,
+//    sorts and permutes (kernel 5).
 #include "kernel_args.cuh"
 #include "launch.h"
 
 namespace bsvd {
 namespace reg32 {
 
-constexpr int N = 32;       // columns
-constexpr int H = 16;       // column pairs per iteration
-constexpr int NIT = 31;     // iterations per sweep
-constexpr int RING = 4;     // parameter ring depth (iterations)
-constexpr int WPAIRS = 2;   // (A warp, V warp) pairs per CTA -> 4 problems per CTA
-constexpr int RSTR = 34;    // doubles per row of the dot-product transpose buffer (bank padding)
+constexpr int N = 32;      // columns
+constexpr int H = 16;      // column pairs per iteration
+constexpr int NIT = 31;    // iterations per sweep
+constexpr int RSTR = 34;   // doubles per row of the dot-product transpose buffer (bank padding)
+constexpr int LOG_ELEMS = NIT * H * 2 + 32;  // doubles per problem: rotation log (31 x 16 Par) + masks
 
 // ring position -> register slot (slot 2k = top[k], slot 2k+1 = bot[k])
 __host__ __device__ constexpr int ring_slot(int q) {
@@ -47,30 +52,15 @@ __host__ __device__ constexpr int ring_slot(int q) {
 struct __align__(16) Par {
     double cm1, c;  // x <- x + (cm1 x + c y);  y <- y + (cm1 y - c x)
 };
-struct __align__(16) Slot {
-    Par p[2][H];      // [problem half][pair]
-    unsigned mask;    // rotation bits: pair k of half h at bit 16h + k
-    int stop;
-    int pad[2];
+
+struct WarpSmem {
+    double red[3 * H * RSTR];  // dot-product transpose
+    Par pub[2][H];             // this iteration's rotations, [half][pair]
+    Par stage[2][2][H];        // V replay: double-buffered log rows [buf][half][pair]
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
-    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared.b64 st, [%0];\n\t}" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
 }
 
 // advance every column one ring position (compile-time register moves)
@@ -81,7 +71,7 @@ __device__ __forceinline__ void ring_rotate(double (&x)[N]) {
     x[ring_slot(0)] = t;
 }
 
-// value (column index) at ring position r after t rotations, ell = 32
+// column index at ring position r after t rotations (ell = 32)
 __device__ __forceinline__ int col_at(int r, int t) {
     int q = r - t;
     if (q < 0) q += NIT;
@@ -95,254 +85,350 @@ __device__ __forceinline__ void apply(double& x, double& y, double cm1, double c
     y = ny;
 }
 
-template <bool WANT_V, int MINB>
-__global__ void __launch_bounds__(WANT_V ? 128 : 64, WANT_V ? MINB : 2 * MINB) k_reg32(SolveArgs<double> a) {
-    __shared__ Slot ring[WPAIRS][RING];
-    __shared__ uint64_t full[WPAIRS][RING], empty_[WPAIRS][RING];
-    __shared__ __align__(16) double redbuf[WPAIRS][3 * H * RSTR];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int half = lane >> 4, hl = lane & 15;
-    const int wp = warp % WPAIRS;           // warp pair
-    const bool is_v = warp >= WPAIRS;
-    const int prob = blockIdx.x * (2 * WPAIRS) + wp * 2 + half;
-    const bool live = prob < a.batch;
-    if (threadIdx.x == 0) {
-        for (int w = 0; w < WPAIRS; ++w)
-            for (int s = 0; s < RING; ++s) {
-                mbar_init(&full[w][s], 32);
-                mbar_init(&empty_[w][s], 32);
-            }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const int r0 = hl, r1 = hl + 16;
-    double* wsW = a.work + (size_t)(live ? prob : 0) * a.work_stride;
-    double* wsV = wsW + N * N;
+__device__ __forceinline__ double pow2(int e) {  // 2^e for e in [-1022, 1023]
+    return __longlong_as_double((long long)(1023 + e) << 52);
+}
 
-    if (!is_v) {
-        // ---------------- A warp: dots, rotation parameters, W update ----------------
-        double* red = redbuf[wp];
-        double x0[N], x1[N];
-        const double* Ap = a.A + (size_t)(live ? prob : 0) * a.strideA;
-        int bad = 0;
-        double amax = 0.0;
+// Rotation of pair (i, j) from (d = g_ii - g_jj, g = |g_ji|), reference F5:
+// t = sgn(tau) / (|tau| + sqrt(1 + tau^2)), tau = d / (2g), evaluated as
+// t = sgn(d) 2g / (|d| + sqrt(d^2 + 4 g^2)) on exponent-normalised d, g;
+// c = 1/sqrt(1 + t^2); s = t c; c - 1 = -s^2 / (1 + c)  (= -t^2/(h(1+h))).
+__device__ __forceinline__ void rotation(double d, double g, double& s_out, double& cm1_out) {
+    const double mx = fmax(fabs(d), g);
+    const int e = (int)((__double_as_longlong(mx) >> 52) & 0x7ff) - 1023;
+    const double sc = pow2(-max(-1022, min(1022, e)));
+    const double dn = d * sc, gn = g * sc;  // exact
+    const double q = fma(dn, dn, 4.0 * gn * gn);
+    double r = rsqrt_approx(q);
+    double ee = fma(-(q * r), r, 1.0);
+    r = fma(0.5 * r, ee, r);
+    ee = fma(-(q * r), r, 1.0);
+    r = fma(0.5 * r, ee, r);
+    double sq = q * r;
+    sq = fma(fma(-sq, sq, q), 0.5 * r, sq);
+    const double den = fabs(dn) + sq;
+    double rd = rcp_approx(den);
+    double e2 = fma(-den, rd, 1.0);
+    rd = fma(rd, e2, rd);
+    e2 = fma(-den, rd, 1.0);
+    rd = fma(rd, e2, rd);
+    const double num = 2.0 * gn;
+    double t = num * rd;
+    t = fma(fma(-den, t, num), rd, t);
+    t = d >= 0.0 ? t : -t;  // sgn(0) = +1
+    const double h2 = fma(t, t, 1.0);
+    double c = rsqrt_approx(h2);
+    ee = fma(-(h2 * c), c, 1.0);
+    c = fma(0.5 * c, ee, c);
+    ee = fma(-(h2 * c), c, 1.0);
+    c = fma(0.5 * c, ee, c);
+    ee = fma(-(h2 * c), c, 1.0);
+    c = fma(0.5 * c, ee, c);
+    const double s = t * c;
+    const double op = 1.0 + c;
+    double ro = rcp_approx(op);
+    e2 = fma(-op, ro, 1.0);
+    ro = fma(ro, e2, ro);
+    e2 = fma(-op, ro, 1.0);
+    ro = fma(ro, e2, ro);
+    const double s2 = s * s;
+    double cm = s2 * ro;
+    cm = fma(fma(-op, cm, s2), ro, cm);
+    s_out = s;
+    cm1_out = -cm;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
+}
+
+template <int NW, int MAXREG>
+__global__ void __launch_bounds__(NW * 32) __maxnreg__(MAXREG) k_reg32(SolveArgs<double> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
+    const int half = lane >> 4, hl = lane & 15;
+    const int prob = (blockIdx.x * NW + warp) * 2 + half;
+    const bool live = prob < a.batch;
+    const int r0 = hl, r1 = hl + 16;
+    const size_t pstride = (size_t)a.work_stride;
+    double* wsW = a.work + (size_t)(live ? prob : 0) * pstride;  // W 32x32, V 32x32, then the log
+    double* wsV = wsW + N * N;
+    Par* logp = reinterpret_cast<Par*>(wsW + 2 * N * N);           // [31][16]
+    uint32_t* logm = reinterpret_cast<uint32_t*>(logp + NIT * H);  // [31]
+    const bool want_v = a.need_v != 0;
+
+    double x0[N], x1[N];
+    int bad = 0;
+    double amax = 0.0;
+    {
+        const double* Ap = a.A + (size_t)(live ? prob : 0) * a.strideA;  // plan requires lda == 32
 #pragma unroll
         for (int c = 0; c < N; ++c) {
-            x0[c] = live ? Ap[r0 + c * N] : 0.0;  // plan requires lda == 32
+            x0[c] = live ? Ap[r0 + c * N] : 0.0;
             x1[c] = live ? Ap[r1 + c * N] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
             bad |= !isfinite(x0[c]) | !isfinite(x1[c]);
             amax = fmax(amax, fmax(fabs(x0[c]), fabs(x1[c])));
         }
-        // exact power-of-two pre-scaling to max|a| in [0.5, 1): rotations are
-        // scale invariant and the scaling is exact, so the iteration is the same;
-        // it keeps the call-free div/sqrt operands in range (undone on output)
+    }
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        int ex = (int)((__double_as_longlong(amax) >> 52) & 0x7ff) - 1022;
-        if (!(amax > 0.0) || !isfinite(amax)) ex = 0;
-        ex = max(-1021, min(1022, ex));
-        const double scale = __longlong_as_double((long long)(1023 - ex) << 52);
-        const double unscale = __longlong_as_double((long long)(1023 + ex) << 52);
+    for (int o = 8; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    int ex = (int)((__double_as_longlong(amax) >> 52) & 0x7ff) - 1022;
+    if (!(amax > 0.0) || !isfinite(amax)) ex = 0;
+    ex = max(-1021, min(1021, ex));
+    {
+        const double scale = pow2(-ex);
 #pragma unroll
         for (int c = 0; c < N; ++c) {
             x0[c] *= scale;
             x1[c] *= scale;
         }
-        const double tol = a.tol;
-        int sweeps = 0, last = 0, done = live ? 0 : 1;
-        long long rot_total = 0;
-        uint32_t it = 0;
+    }
+    const double tol = a.tol;
+    int sweeps = 0, last = 0, done = live ? 0 : 1;
+    long long rot_total = 0;
+    bool v_started = false;  // V still identity until the first replay
+
 #pragma unroll 1
-        for (int sw = 0; sw < a.max_sweeps; ++sw) {
-            int my_rot = 0;
+    for (int sw = 0; sw < a.max_sweeps; ++sw) {
+        int my_rot = 0;
+        unsigned any_mask = 0;
+        // ======================= W phase: one sweep =======================
 #pragma unroll 1
-            for (int t = 0; t < NIT; ++t) {
-                // ---- dot products: 16 pairs x 3 values per lane over its two rows,
-                //      transposed through shared memory: lane k of each half then sums
-                //      the 16 partials of pair k (conflict-free LDS.128, 34-double rows)
+        for (int t = 0; t < NIT; ++t) {
 #pragma unroll
-                for (int k = 0; k < H; ++k) {
-                    const double xa0 = x0[2 * k], xb0 = x0[2 * k + 1], xa1 = x1[2 * k], xb1 = x1[2 * k + 1];
-                    red[(3 * k + 0) * RSTR + lane] = fma(xa1, xa1, xa0 * xa0);
-                    red[(3 * k + 1) * RSTR + lane] = fma(xb1, xb1, xb0 * xb0);
-                    red[(3 * k + 2) * RSTR + lane] = fma(xb1, xa1, xb0 * xa0);
-                }
-                __syncwarp();
-                double g[3];
+            for (int k = 0; k < H; ++k) {
+                const double xa0 = x0[2 * k], xb0 = x0[2 * k + 1], xa1 = x1[2 * k], xb1 = x1[2 * k + 1];
+                sm.red[(3 * k + 0) * RSTR + lane] = fma(xa1, xa1, xa0 * xa0);
+                sm.red[(3 * k + 1) * RSTR + lane] = fma(xb1, xb1, xb0 * xb0);
+                sm.red[(3 * k + 2) * RSTR + lane] = fma(xb1, xa1, xb0 * xa0);
+            }
+            __syncwarp();
+            double g[3];
 #pragma unroll
-                for (int e = 0; e < 3; ++e) {
-                    const double2* row = reinterpret_cast<const double2*>(red + (3 * hl + e) * RSTR + 16 * half);
-                    double2 p0 = row[0], p1 = row[1], p2 = row[2], p3 = row[3];
-                    double s0 = p0.x + p0.y, s1 = p1.x + p1.y, s2 = p2.x + p2.y, s3 = p3.x + p3.y;
-                    p0 = row[4]; p1 = row[5]; p2 = row[6]; p3 = row[7];
-                    s0 += p0.x + p0.y;
-                    s1 += p1.x + p1.y;
-                    s2 += p2.x + p2.y;
-                    s3 += p3.x + p3.y;
-                    g[e] = (s0 + s1) + (s2 + s3);
-                }
-                // lane hl now holds pair k = hl: slots (2k, 2k+1) = (top[k], bot[k])
-                const int k = hl;
-                const int ctop = (k == 0) ? 0 : col_at(k, t);
-                const int cbot = col_at(k == 0 ? 0 : 2 * H - 1 - k, t);
-                const bool flip = ctop > cbot;  // reference pair (i, j) = (min, max)
-                const double gii = flip ? g[1] : g[0];
-                const double gjj = flip ? g[0] : g[1];
-                const double gji = g[2];
-                const double absg = fabs(gji);
-                Par par;
-                par.cm1 = 0.0;
-                par.c = 0.0;
-                bool rot = false;
-                if (!(absg <= 0.0) && !(absg < tol * fsqrt(gii * gjj))) {
-                    rot = true;
-                    const double w = copysign(1.0, gji);  // conj(g_ji)/|g_ji| for real data
-                    const RotParams p = rot_params_fast(gii - gjj, 2.0 * absg);
-                    const double ws = w * p.s;
-                    par.cm1 = p.cm1;
-                    // x = top slot, y = bot slot; i = min(top, bot)
-                    par.c = flip ? -ws : ws;
-                }
-                rot = rot && !done;
-                if (!rot) {
-                    par.cm1 = 0.0;
-                    par.c = 0.0;
-                }
-                my_rot += rot ? 1 : 0;
-                const unsigned mask = __ballot_sync(0xffffffffu, rot);
-                // ---- publish to the ring (V warp) ----
-                const uint32_t s = it % RING;
-                if (WANT_V && it >= RING) mbar_wait(&empty_[wp][s], ((it / RING) - 1) & 1);
-                Slot& sl = ring[wp][s];
-                sl.p[half][k] = par;
-                if (lane == 0) {
-                    sl.mask = mask;
-                    sl.stop = 0;
-                }
-                __syncwarp();
-                if (WANT_V) mbar_arrive(&full[wp][s]);
-                // ---- W update: pairs rotating in either half; identity params elsewhere ----
+            for (int e = 0; e < 3; ++e) {
+                const double2* row = reinterpret_cast<const double2*>(sm.red + (3 * hl + e) * RSTR + 16 * half);
+                double2 p0 = row[0], p1 = row[1], p2 = row[2], p3 = row[3];
+                double s0 = p0.x + p0.y, s1 = p1.x + p1.y, s2 = p2.x + p2.y, s3 = p3.x + p3.y;
+                p0 = row[4];
+                p1 = row[5];
+                p2 = row[6];
+                p3 = row[7];
+                s0 += p0.x + p0.y;
+                s1 += p1.x + p1.y;
+                s2 += p2.x + p2.y;
+                s3 += p3.x + p3.y;
+                g[e] = (s0 + s1) + (s2 + s3);
+            }
+            // lane hl holds pair k = hl: slots (2k, 2k+1) = (top[k], bot[k])
+            const int k = hl;
+            const int ctop = (k == 0) ? 0 : col_at(k, t);
+            const int cbot = col_at(k == 0 ? 0 : 2 * H - 1 - k, t);
+            const bool flip = ctop > cbot;  // reference pair (i, j) = (min, max)
+            const double gii = flip ? g[1] : g[0];
+            const double gjj = flip ? g[0] : g[1];
+            const double gji = g[2];
+            const double absg = fabs(gji);
+            Par par;
+            par.cm1 = 0.0;
+            par.c = 0.0;
+            const bool rot = !done && !(absg <= 0.0) && !(absg < tol * fsqrt(gii * gjj));
+            if (rot) {
+                double s, cm1;
+                rotation(gii - gjj, absg, s, cm1);
+                const double ws = gji >= 0.0 ? s : -s;  // conj(g_ji)/|g_ji| * s for real data
+                par.cm1 = cm1;
+                par.c = flip ? -ws : ws;  // x = top slot, y = bot slot; i = min(top, bot)
+            }
+            my_rot += rot ? 1 : 0;
+            const unsigned mask = __ballot_sync(0xffffffffu, rot);
+            any_mask |= mask;
+            sm.pub[half][k] = par;
+            if (want_v) {
+                logp[t * H + k] = par;
+                if (hl == 0) logm[t] = (mask >> (16 * half)) & 0xFFFFu;
+            }
+            __syncwarp();
+            if (mask) {
+                // branch-free: identity rotations (cm1 = c = 0) are exact no-ops
 #pragma unroll
                 for (int q = 0; q < H; ++q) {
-                    if (mask & (0x10001u << q)) {
-                        const Par pq = sl.p[half][q];
+                    const Par pq = sm.pub[half][q];
+                    apply(x0[2 * q], x0[2 * q + 1], pq.cm1, pq.c);
+                    apply(x1[2 * q], x1[2 * q + 1], pq.cm1, pq.c);
+                }
+            }
+            __syncwarp();
+            ring_rotate(x0);
+            ring_rotate(x1);
+        }
+        // ---- sweep end: per-problem rotation count over the half warp ----
+        int tot = my_rot;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (!done) {
+            sweeps = sw + 1;
+            last = tot;
+            rot_total += tot;
+            if (tot == 0) done = 1;
+        }
+        const int partner_done = __shfl_xor_sync(0xffffffffu, done, 16);  // all lanes, unconditionally
+        const bool both_done = done && partner_done;
+        // ======================= V phase: replay the sweep =======================
+        if (want_v && any_mask) {
+#pragma unroll
+            for (int c = 0; c < N; ++c) {  // park W
+                wsW[r0 + c * N] = x0[c];
+                wsW[r1 + c * N] = x1[c];
+            }
+            if (v_started) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    x0[c] = wsV[r0 + c * N];
+                    x1[c] = wsV[r1 + c * N];
+                }
+            } else {  // V = I before the first replay
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    x0[c] = (c == r0) ? 1.0 : 0.0;
+                    x1[c] = (c == r1) ? 1.0 : 0.0;
+                }
+                v_started = true;
+            }
+            __syncwarp();  // this warp's log writes are visible to all its lanes
+            // mask words of this half's problem: lane hl holds iterations hl and hl + 16
+            const uint32_t ma = logm[hl];
+            const uint32_t mb = (hl + 16 < NIT) ? logm[hl + 16] : 0u;
+            cp_async16(&sm.stage[0][half][hl], &logp[hl]);
+            cp_commit();
+#pragma unroll 1
+            for (int t = 0; t < NIT; ++t) {
+                if (t + 1 < NIT) cp_async16(&sm.stage[(t + 1) & 1][half][hl], &logp[(t + 1) * H + hl]);
+                cp_commit();
+                const uint32_t own = __shfl_sync(0xffffffffu, t < 16 ? ma : mb, 16 * half + (t & 15));
+                const uint32_t both = own | __shfl_xor_sync(0xffffffffu, own, 16);
+                cp_wait<1>();
+                __syncwarp();
+                if (both) {
+                    const Par* st = sm.stage[t & 1][half];
+#pragma unroll
+                    for (int q = 0; q < H; ++q) {
+                        const Par pq = st[q];
                         apply(x0[2 * q], x0[2 * q + 1], pq.cm1, pq.c);
                         apply(x1[2 * q], x1[2 * q + 1], pq.cm1, pq.c);
                     }
                 }
-                if (!WANT_V) __syncwarp();  // the slot is rewritten next iteration
+                __syncwarp();
                 ring_rotate(x0);
                 ring_rotate(x1);
-                ++it;
             }
-            // ---- sweep end: per-problem rotation count over the half warp ----
-            int tot = my_rot;
+            cp_wait<0>();
 #pragma unroll
-            for (int o = 8; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-            if (!done) {
-                sweeps = sw + 1;
-                last = tot;
-                rot_total += tot;
-                if (tot == 0) done = 1;
+            for (int c = 0; c < N; ++c) {  // park V, resume W
+                wsV[r0 + c * N] = x0[c];
+                wsV[r1 + c * N] = x1[c];
             }
-            const int other = __shfl_xor_sync(0xffffffffu, done, 16);
-            if (done && other) break;
-        }
-        // stop marker for the V warp
-        if (WANT_V) {
-            const uint32_t s = it % RING;
-            if (it >= RING) mbar_wait(&empty_[wp][s], ((it / RING) - 1) & 1);
-            if (lane == 0) ring[wp][s].stop = 1;
-            __syncwarp();
-            mbar_arrive(&full[wp][s]);
-        }
-        if (live) {
 #pragma unroll
             for (int c = 0; c < N; ++c) {
-                wsW[r0 + c * N] = x0[c] * unscale;
-                wsW[r1 + c * N] = x1[c] * unscale;
-            }
-            const unsigned badm = __ballot_sync(0xffffffffu, bad != 0);
-            if (hl == 0 && a.info) {
-                bsvd_info inf;
-                inf.converged = done;
-                inf.outer_sweeps = sweeps;
-                inf.rotations = rot_total;
-                inf.gram_calls = 0;
-                inf.update_calls = 0;
-                inf.last_rotations = last;
-                inf.path = 1;
-                inf.status = (badm >> (16 * half)) & 0xFFFFu ? 1 : 0;
-                inf.kernel = MINB == 3 ? KV_UNBLOCKED_REG32_O3 : KV_UNBLOCKED_REG32;
-                a.info[prob] = inf;
+                x0[c] = wsW[r0 + c * N];
+                x1[c] = wsW[r1 + c * N];
             }
         }
-    } else if (WANT_V) {
-        // ---------------- V warp: replay the rotations on V ----------------
-        double y0[N], y1[N];
+        if (both_done) break;
+    }
+    if (live) {
+        const double unscale = pow2(ex);
 #pragma unroll
         for (int c = 0; c < N; ++c) {
-            y0[c] = (c == r0) ? 1.0 : 0.0;
-            y1[c] = (c == r1) ? 1.0 : 0.0;
+            wsW[r0 + c * N] = x0[c] * unscale;
+            wsW[r1 + c * N] = x1[c] * unscale;
         }
-#pragma unroll 1
-        for (uint32_t it = 0;; ++it) {
-            const uint32_t s = it % RING;
-            mbar_wait(&full[wp][s], (it / RING) & 1);
-            const Slot& sl = ring[wp][s];
-            if (sl.stop) break;
-            const unsigned mask = sl.mask;
-#pragma unroll
-            for (int q = 0; q < H; ++q) {
-                if (mask & (0x10001u << q)) {
-                    const Par pq = sl.p[half][q];
-                    apply(y0[2 * q], y0[2 * q + 1], pq.cm1, pq.c);
-                    apply(y1[2 * q], y1[2 * q + 1], pq.cm1, pq.c);
-                }
-            }
-            __syncwarp();
-            mbar_arrive(&empty_[wp][s]);
-            ring_rotate(y0);
-            ring_rotate(y1);
-        }
-        if (live) {
+        if (want_v && !v_started) {
 #pragma unroll
             for (int c = 0; c < N; ++c) {
-                wsV[r0 + c * N] = y0[c];
-                wsV[r1 + c * N] = y1[c];
+                wsV[r0 + c * N] = (c == r0) ? 1.0 : 0.0;
+                wsV[r1 + c * N] = (c == r1) ? 1.0 : 0.0;
             }
         }
+    }
+    const unsigned badm = __ballot_sync(0xffffffffu, bad != 0);
+    if (live && hl == 0 && a.info) {
+        bsvd_info inf;
+        inf.converged = done;
+        inf.outer_sweeps = sweeps;
+        inf.rotations = rot_total;
+        inf.gram_calls = 0;
+        inf.update_calls = 0;
+        inf.last_rotations = last;
+        inf.path = 1;
+        inf.status = ((badm >> (16 * half)) & 0xFFFFu) ? 1 : 0;
+        inf.kernel = a.kernel;
+        a.info[prob] = inf;
     }
 }
 
 }  // namespace reg32
 
+// register-budget variants: (warps per CTA, min CTAs per SM) -> registers per thread
+//   KV_UNBLOCKED_REG32    (4, 3): 168 regs, 12 warps/SM (default)
+//   KV_UNBLOCKED_REG32_R2 (2, 5): 204 regs, 10 warps/SM
+//   KV_UNBLOCKED_REG32_R3 (1, 9): 227 regs,  9 warps/SM
+//   KV_UNBLOCKED_REG32_O3 (4, 2): 255 regs,  8 warps/SM
+static int variant_nw(int kv) {
+    switch (kv) {
+        case KV_UNBLOCKED_REG32_R2: return 2;
+        case KV_UNBLOCKED_REG32_R3: return 1;
+        default: return 4;
+    }
+}
+
 Plan plan_unblocked_reg(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant) {
     Plan p{};
     if (dtype == BSVD_D && bm == 32 && bn == 32 && lda_ok) {
-        p.kernel = variant == KV_UNBLOCKED_REG32_O3 ? KV_UNBLOCKED_REG32_O3 : KV_UNBLOCKED_REG32;
-        p.threads = need_v ? 128 : 64;
-        p.smem = 0;
-        p.work_elems = 2 * 32 * 32;
+        const bool known = variant == KV_UNBLOCKED_REG32 || variant == KV_UNBLOCKED_REG32_O3 ||
+                           variant == KV_UNBLOCKED_REG32_R2 || variant == KV_UNBLOCKED_REG32_R3;
+        p.kernel = known ? variant : KV_UNBLOCKED_REG32;
+        p.threads = variant_nw(p.kernel) * 32;
+        p.smem = variant_nw(p.kernel) * sizeof(reg32::WarpSmem);
+        p.work_elems = 2 * 32 * 32 + reg32::LOG_ELEMS;
         p.grid = 0;
         p.resident = 0;
+        (void)need_v;
     }
     return p;
 }
 
+template <int NW, int MAXREG>
+static int launch_variant(SolveArgs<double> a, cudaStream_t st) {
+    const int per_cta = 2 * NW;
+    const int grid = (a.batch + per_cta - 1) / per_cta;
+    const size_t smem = NW * sizeof(reg32::WarpSmem);
+    auto k = reg32::k_reg32<NW, MAXREG>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<grid, NW * 32, smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
 int launch_unblocked_reg_d32(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
     a.kernel = p.kernel;
-    a.work_stride = 2 * 32 * 32;
-    const int per_cta = 2 * reg32::WPAIRS;
-    const int grid = (a.batch + per_cta - 1) / per_cta;
-    if (p.kernel == KV_UNBLOCKED_REG32_O3) {
-        if (a.need_v) reg32::k_reg32<true, 3><<<grid, 128, 0, st>>>(a);
-        else reg32::k_reg32<false, 3><<<grid, 64, 0, st>>>(a);
-    } else {
-        if (a.need_v) reg32::k_reg32<true, 2><<<grid, 128, 0, st>>>(a);
-        else reg32::k_reg32<false, 2><<<grid, 64, 0, st>>>(a);
+    a.work_stride = (int64_t)p.work_elems;
+    int rc;
+    switch (p.kernel) {
+        case KV_UNBLOCKED_REG32_O3: rc = launch_variant<4, 255>(a, st); break;
+        case KV_UNBLOCKED_REG32_R2: rc = launch_variant<2, 200>(a, st); break;
+        case KV_UNBLOCKED_REG32_R3: rc = launch_variant<1, 224>(a, st); break;
+        default: rc = launch_variant<4, 168>(a, st); break;
     }
-    if (cudaPeekAtLastError() != cudaSuccess) return BSVD_ERR_CUDA;
+    if (rc) return rc;
     return launch_finalize_ws<double>(a, st);
 }
 

@@ -83,8 +83,8 @@ def e3(v) -> float:
     return one_norm(np.eye(r, dtype=v.dtype) - v.conj().T @ v) / n if n else 0.0
 
 
-def check_sigma_parity(s, s_ref, n, u, c=1.0):
-    """max |s - s_ref| <= c * n * u * s1_ref (normwise-relative)."""
+def check_sigma_parity(s, s_ref, n, u, c=2.0):
+    """max |s - s_ref| <= c * n * u * s1_ref (normwise-relative), c = 2."""
     s = np.asarray(s, dtype=np.float64)
     s_ref = np.asarray(s_ref, dtype=np.float64)
     assert s.shape == s_ref.shape
