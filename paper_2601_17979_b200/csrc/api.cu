@@ -48,7 +48,7 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
     const size_t lim = smem_limit();
     const int es = esize_of(dt), rs = rsize_of(dt);
     if (r.blocked) return plan_blocked_general(es, rs, r.bm, r.bn, o->nb, r.need_v, lim);
-    if (o->kernel == 0 || (o->kernel >= KV_UNBLOCKED_REG32 && o->kernel <= KV_UNBLOCKED_REG32_R3)) {
+    if (o->kernel == 0 || (o->kernel >= KV_UNBLOCKED_REG32 && o->kernel <= KV_UNBLOCKED_REG32_F2)) {
         Plan p = plan_unblocked_reg(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
         if (p.kernel) return p;
         if (o->kernel != 0) return p;  // forced variant unavailable => kernel 0 => unsupported
@@ -106,6 +106,7 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
     a.work = p.work_elems ? static_cast<T*>(work) : nullptr;
     a.work_stride = (int64_t)p.work_elems;
     a.info = info;
+    a.reserved_stagger = o->reserved[0];
     switch (p.kernel) {
         case KV_UNBLOCKED_GENERAL: return launch_unblocked_general<T>(a, p, st);
         case KV_BLOCKED_GENERAL: return launch_blocked_general<T>(a, p, st);
@@ -113,6 +114,7 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_UNBLOCKED_REG32_O3:
         case KV_UNBLOCKED_REG32_R2:
         case KV_UNBLOCKED_REG32_R3:
+        case KV_UNBLOCKED_REG32_F2:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg_d32(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
     }

@@ -32,6 +32,7 @@ struct SolveArgs {
     int resident;        // bit0: W in smem, bit1: V in smem, bit2: scratch in smem
     int group;           // lanes per column pair (general unblocked kernel)
     int kernel;          // variant id for telemetry
+    int reserved_stagger;  // experimental: per-warp start stagger (ns)
     bsvd_info* info;
 };
 
@@ -43,6 +44,7 @@ enum {
     KV_UNBLOCKED_REG32_O3 = 4,  // same, 255 regs, 8 warps/SM
     KV_UNBLOCKED_REG32_R2 = 5,  // same, 204 regs, 10 warps/SM
     KV_UNBLOCKED_REG32_R3 = 6,  // same, 227 regs, 9 warps/SM
+    KV_UNBLOCKED_REG32_F2 = 7,  // 168 regs, two-FMA rotation update (opt-in)
 };
 
 template <class T>

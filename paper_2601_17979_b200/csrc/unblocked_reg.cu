@@ -78,11 +78,25 @@ __device__ __forceinline__ int col_at(int r, int t) {
     return q == 0 ? 1 : (q <= H - 1 ? 2 * q : 2 * (2 * H - 1 - q) + 1);
 }
 
+// Reference form (F5): x + (cm1 x + c y), one full-scale rounding.
 __device__ __forceinline__ void apply(double& x, double& y, double cm1, double c) {
     const double nx = x + fma(cm1, x, c * y);
     const double ny = y + fma(cm1, y, -(c * x));
     x = nx;
     y = ny;
+}
+// Two-FMA form: (x + c y) + cm1 x with the shrink term fused (no rounded c = 1
+// + cm1 ever formed, so the small-angle bias F5 guards against cannot arise);
+// two full-scale roundings instead of one.  Opt-in (KV_UNBLOCKED_REG32_F2).
+__device__ __forceinline__ void apply2(double& x, double& y, double cm1, double c) {
+    const double tx = fma(c, y, x);
+    const double ty = fma(-c, x, y);
+    x = fma(cm1, x, tx);
+    y = fma(cm1, y, ty);
+}
+template <bool F2>
+__device__ __forceinline__ void applyv(double& x, double& y, double cm1, double c) {
+    if constexpr (F2) apply2(x, y, cm1, c); else apply(x, y, cm1, c);
 }
 
 __device__ __forceinline__ double pow2(int e) {  // 2^e for e in [-1022, 1023]
@@ -147,7 +161,7 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
 }
 
-template <int NW, int MAXREG>
+template <int NW, int MAXREG, bool F2>
 __global__ void __launch_bounds__(NW * 32) __maxnreg__(MAXREG) k_reg32(SolveArgs<double> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -192,6 +206,7 @@ __global__ void __launch_bounds__(NW * 32) __maxnreg__(MAXREG) k_reg32(SolveArgs
             x1[c] *= scale;
         }
     }
+    if (a.reserved_stagger > 0) __nanosleep((unsigned)((warp % 3) * a.reserved_stagger));
     const double tol = a.tol;
     int sweeps = 0, last = 0, done = live ? 0 : 1;
     long long rot_total = 0;
@@ -262,8 +277,8 @@ __global__ void __launch_bounds__(NW * 32) __maxnreg__(MAXREG) k_reg32(SolveArgs
 #pragma unroll
                 for (int q = 0; q < H; ++q) {
                     const Par pq = sm.pub[half][q];
-                    apply(x0[2 * q], x0[2 * q + 1], pq.cm1, pq.c);
-                    apply(x1[2 * q], x1[2 * q + 1], pq.cm1, pq.c);
+                    applyv<F2>(x0[2 * q], x0[2 * q + 1], pq.cm1, pq.c);
+                    applyv<F2>(x1[2 * q], x1[2 * q + 1], pq.cm1, pq.c);
                 }
             }
             __syncwarp();
@@ -322,8 +337,8 @@ __global__ void __launch_bounds__(NW * 32) __maxnreg__(MAXREG) k_reg32(SolveArgs
 #pragma unroll
                     for (int q = 0; q < H; ++q) {
                         const Par pq = st[q];
-                        apply(x0[2 * q], x0[2 * q + 1], pq.cm1, pq.c);
-                        apply(x1[2 * q], x1[2 * q + 1], pq.cm1, pq.c);
+                        applyv<F2>(x0[2 * q], x0[2 * q + 1], pq.cm1, pq.c);
+                        applyv<F2>(x1[2 * q], x1[2 * q + 1], pq.cm1, pq.c);
                     }
                 }
                 __syncwarp();
@@ -394,7 +409,8 @@ Plan plan_unblocked_reg(int dtype, int bm, int bn, int need_v, bool lda_ok, int 
     Plan p{};
     if (dtype == BSVD_D && bm == 32 && bn == 32 && lda_ok) {
         const bool known = variant == KV_UNBLOCKED_REG32 || variant == KV_UNBLOCKED_REG32_O3 ||
-                           variant == KV_UNBLOCKED_REG32_R2 || variant == KV_UNBLOCKED_REG32_R3;
+                           variant == KV_UNBLOCKED_REG32_R2 || variant == KV_UNBLOCKED_REG32_R3 ||
+                           variant == KV_UNBLOCKED_REG32_F2;
         p.kernel = known ? variant : KV_UNBLOCKED_REG32;
         p.threads = variant_nw(p.kernel) * 32;
         p.smem = variant_nw(p.kernel) * sizeof(reg32::WarpSmem);
@@ -406,12 +422,12 @@ Plan plan_unblocked_reg(int dtype, int bm, int bn, int need_v, bool lda_ok, int 
     return p;
 }
 
-template <int NW, int MAXREG>
+template <int NW, int MAXREG, bool F2 = false>
 static int launch_variant(SolveArgs<double> a, cudaStream_t st) {
     const int per_cta = 2 * NW;
     const int grid = (a.batch + per_cta - 1) / per_cta;
     const size_t smem = NW * sizeof(reg32::WarpSmem);
-    auto k = reg32::k_reg32<NW, MAXREG>;
+    auto k = reg32::k_reg32<NW, MAXREG, F2>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<grid, NW * 32, smem, st>>>(a);
@@ -426,6 +442,7 @@ int launch_unblocked_reg_d32(SolveArgs<double> a, const Plan& p, cudaStream_t st
         case KV_UNBLOCKED_REG32_O3: rc = launch_variant<4, 255>(a, st); break;
         case KV_UNBLOCKED_REG32_R2: rc = launch_variant<2, 200>(a, st); break;
         case KV_UNBLOCKED_REG32_R3: rc = launch_variant<1, 224>(a, st); break;
+        case KV_UNBLOCKED_REG32_F2: rc = launch_variant<4, 168, true>(a, st); break;
         default: rc = launch_variant<4, 168>(a, st); break;
     }
     if (rc) return rc;

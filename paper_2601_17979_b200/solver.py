@@ -67,7 +67,7 @@ def np_dtype_of(tdtype):
     }[tdtype]
 
 
-def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0) -> _lib.BsvdOpts:
+def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0, stagger: int = 0) -> _lib.BsvdOpts:
     """JacobiOptions -> POD bsvd_opts (src/svd.py:70-78 field by field)."""
     o = _lib.BsvdOpts()
     o.k = float(opts.k)
@@ -80,6 +80,7 @@ def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0) -> _lib.BsvdOpt
     o.fused_updates = int(bool(opts.fused_updates))
     o.row_block = int(opts.row_block)
     o.kernel = int(kernel)
+    o.reserved[0] = int(stagger)
     return o
 
 
@@ -108,7 +109,7 @@ class DeviceResult:
 
 
 def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: int = 0,
-                 out=None) -> DeviceResult:
+                 out=None, stagger: int = 0) -> DeviceResult:
     """Batched SVD of a device tensor a_t (B, n, m) (column-major matrices).
 
     Launches on torch's current stream; returns device tensors without
@@ -121,7 +122,7 @@ def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: 
     dt = np_dtype_of(a_t.dtype)
     code = DTYPE_CODE[dt]
     k = min(m, n)
-    o = make_opts(opts, route, kernel)
+    o = make_opts(opts, route, kernel, stagger)
     dev = a_t.device
     if out is None:
         u = torch.empty((B, k, m), dtype=a_t.dtype, device=dev)
