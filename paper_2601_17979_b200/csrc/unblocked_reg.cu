@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(NW * 32) __maxnreg__(MAXREG) k_reg32(SolveArgs
             const unsigned mask = __ballot_sync(0xffffffffu, rot);
             any_mask |= mask;
             sm.pub[half][k] = par;
-            if (want_v) {
+            if (want_v && live) {  // a dead half aliases problem 0's workspace: never write
                 logp[t * H + k] = par;
                 if (hl == 0) logm[t] = (mask >> (16 * half)) & 0xFFFFu;
             }
@@ -299,10 +299,12 @@ __global__ void __launch_bounds__(NW * 32) __maxnreg__(MAXREG) k_reg32(SolveArgs
         const bool both_done = done && partner_done;
         // ======================= V phase: replay the sweep =======================
         if (want_v && any_mask) {
+            if (live) {
 #pragma unroll
-            for (int c = 0; c < N; ++c) {  // park W
-                wsW[r0 + c * N] = x0[c];
-                wsW[r1 + c * N] = x1[c];
+                for (int c = 0; c < N; ++c) {  // park W
+                    wsW[r0 + c * N] = x0[c];
+                    wsW[r1 + c * N] = x1[c];
+                }
             }
             if (v_started) {
 #pragma unroll
@@ -346,11 +348,14 @@ __global__ void __launch_bounds__(NW * 32) __maxnreg__(MAXREG) k_reg32(SolveArgs
                 ring_rotate(x1);
             }
             cp_wait<0>();
+            if (live) {
 #pragma unroll
-            for (int c = 0; c < N; ++c) {  // park V, resume W
-                wsV[r0 + c * N] = x0[c];
-                wsV[r1 + c * N] = x1[c];
+                for (int c = 0; c < N; ++c) {  // park V
+                    wsV[r0 + c * N] = x0[c];
+                    wsV[r1 + c * N] = x1[c];
+                }
             }
+            __syncwarp();
 #pragma unroll
             for (int c = 0; c < N; ++c) {
                 x0[c] = wsW[r0 + c * N];
