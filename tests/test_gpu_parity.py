@@ -251,3 +251,36 @@ def test_full_size_c1_properties():
         _, s_ref, _, oi = O.solve(ab, None, None)
         check_sigma_parity(s[b], s_ref, n, 2.0 ** -53)
         assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 2
+
+
+@pytest.mark.parametrize("batch", [1, 3, 7, 9, 17])
+def test_reg32_partial_ctas(batch):
+    """32x32 f64 batches that leave dead half-warps / warps in the last CTA."""
+    mats = [random_matrix(32, 32, np.float64, seed=300 + 7 * b + batch) for b in range(batch)]
+    res = bs.batch_svd(mats, bs.JacobiOptions())
+    for a, r in zip(mats, res):
+        _, s_ref, _, info = O.solve(a, None, None)
+        assert r.info.converged and abs(r.info.outer_sweeps - info["outer_sweeps"]) <= 2
+        check_sigma_parity(r.sigma, s_ref, 32, 2.0 ** -53)
+        check_factors(a, r.u, r.sigma, r.v)
+
+
+@pytest.mark.parametrize("kernel", [1, 3, 4, 5, 6, 7])
+def test_c1_kernel_variants_agree(kernel):
+    """Every 32x32 FP64 kernel variant meets the parity contract on the same inputs."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    B = 64
+    A = np.stack([random_matrix(32, 32, np.float64, seed=500 + b) for b in range(B)])
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, 32, 32, bs.JacobiOptions(), kernel=kernel)
+    torch.cuda.synchronize()
+    info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (info["kernel"] == kernel).all() and info["converged"].all()
+    U, S, V = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy(), np.swapaxes(r.v.cpu().numpy(), 1, 2)
+    for b in range(0, B, 9):
+        _, s_ref, _, oi = O.solve(A[b], None, None)
+        check_sigma_parity(S[b], s_ref, 32, 2.0 ** -53, c=4.0 if kernel == 7 else 2.0)
+        check_factors(A[b], U[b], S[b], V[b])
