@@ -47,7 +47,14 @@ int make_route(int m, int n, const bsvd_opts* o, Route* r) {
 Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = true) {
     const size_t lim = smem_limit();
     const int es = esize_of(dt), rs = rsize_of(dt);
-    if (r.blocked) return plan_blocked_general(es, rs, r.bm, r.bn, o->nb, r.need_v, lim);
+    if (r.blocked) {
+        if (o->kernel == 0 || o->kernel == KV_BLOCKED_DMMA) {
+            Plan p = plan_blocked_dmma(dt, r.bm, r.bn, o->nb, r.need_v, contiguous && !r.trans, lim);
+            if (p.kernel) return p;
+            if (o->kernel != 0) return p;
+        }
+        return plan_blocked_general(es, rs, r.bm, r.bn, o->nb, r.need_v, lim);
+    }
     if (o->kernel == 0 || (o->kernel >= KV_UNBLOCKED_REG32 && o->kernel <= KV_UNBLOCKED_REG32_F2)) {
         Plan p = plan_unblocked_reg(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
         if (p.kernel) return p;
@@ -110,6 +117,9 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
     switch (p.kernel) {
         case KV_UNBLOCKED_GENERAL: return launch_unblocked_general<T>(a, p, st);
         case KV_BLOCKED_GENERAL: return launch_blocked_general<T>(a, p, st);
+        case KV_BLOCKED_DMMA:
+            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_blocked_dmma(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG32:
         case KV_UNBLOCKED_REG32_O3:
         case KV_UNBLOCKED_REG32_R2:

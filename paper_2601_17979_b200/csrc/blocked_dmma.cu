@@ -1,0 +1,402 @@
+// blocked_dmma.cu -- kernel (3), blocked one-sided Jacobi on FP64 tensor cores.
+//
+// Restates _sweep_blocked (src/svd.py:481-522) for real float64, nb = 16
+// (w = 2 nb = 32), n a multiple of 16: per block pair (i, j) of the
+// round-robin schedule over ell = n/16 blocks (src/ordering.py:32-75)
+//   compute_gram  G = [Wi Wj]^T [Wi Wj]            (src/svd.py:144-179)
+//   _eig_delta    inner sweep(s) of two-sided Jacobi on G with
+//                 Delta = P - I accumulation        (src/eig.py:151-174,
+//                                                    src/_kernels_numba.py:17-82)
+//   fused update  [Wi Wj] += [Wi Wj] Delta, V too   (src/_kernels_numba.py:141-175)
+// and a sweep whose pairs all had zero inner rotations ends the problem.
+//
+// B200 mapping (one CTA of 256 threads per problem):
+//  * W (and V when it fits) resident in shared memory for the whole solve,
+//    column-major with a padded leading dimension (bank spread of DMMA
+//    fragment loads); V of larger problems stays in global memory (L2).
+//  * The ell/2 block pairs of a schedule iteration are disjoint (F9) and run
+//    concurrently, one warp group per pair (named barriers per group).
+//  * Gram and update are DMMA m8n8k4 tiles (mma.sync ... f64: SASS DMMA.8x8x4,
+//    the FP64 tensor pipe): the Gram as the 10 upper 8x8 tiles of X^T X over
+//    the m rows, mirrored exactly; the update as 8-row blocks x 4 column tiles
+//    with the accumulator initialised to the block itself (the "+W" of
+//    W + W Delta fused into the MMA, one rounding per element chain).
+//  * The inner eigensolve keeps G and Delta in shared memory: the 16 disjoint
+//    rotations of an inner iteration get their parameters from 16 lanes
+//    (call-free rotation_tsc), then the group updates every 2x2 block of G
+//    (rotation p on its rows, then q on its columns -- the reference's order
+//    for p < q -- mirror written exactly) and the Delta columns.
+//  * Data are pre-scaled by an exact power of two (undone before finalize).
+#include "kernel_args.cuh"
+#include "launch.h"
+#include "rotation.cuh"
+
+namespace bsvd {
+namespace bdmma {
+
+constexpr int NT = 256;   // threads per CTA
+constexpr int NWARP = NT / 32;
+constexpr int WB = 32;    // Gram width 2 nb
+constexpr int HB = 16;    // inner pairs per iteration
+constexpr int GLD = 36;   // leading dimension of G / Delta in smem
+
+struct InnerPar {
+    double cm1, ws;  // real: wsc == ws
+    int i, j, rot, pad;
+};
+
+struct GroupSmem {
+    double G[WB * GLD];
+    double D[WB * GLD];
+    double d[WB];
+    InnerPar prm[HB];
+    int irot;      // inner rotations of the current inner sweep
+    int pad[3];
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// x <- x + (cm1 x + b y), y <- y + (cm1 y - a x)   (rot_pair with real ws/wsc)
+__device__ __forceinline__ void rot2(double& x, double& y, double cm1, double a, double b) {
+    const double nx = x + fma(cm1, x, b * y);
+    const double ny = y + fma(cm1, y, -(a * x));
+    x = nx;
+    y = ny;
+}
+
+__global__ void __launch_bounds__(NT, 1) k_blocked_dmma(SolveArgs<double> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int prob = blockIdx.x;
+    const int bm = a.bm, bn = a.bn;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3;  // MMA fragment coordinates
+    const int ldW = bm + 4, ldV = bn + 4;
+    const bool v_smem = (a.resident & 2) != 0;
+    const int ell = bn / 16;
+    const int Sb = ell + (ell & 1), hb = Sb / 2, nib = Sb - 1;
+    int ngp = 1;
+    while (ngp < hb && ngp < NWARP) ngp <<= 1;  // groups (power of two)
+    const int wg = NWARP / ngp;                  // warps per group
+    const int grp = warp / wg, wig = warp % wg;
+    const int gthreads = wg * 32, gtid = tid - grp * gthreads;
+
+    size_t off = 0;
+    double* W = reinterpret_cast<double*>(smem);
+    off += (size_t)bn * ldW * sizeof(double);
+    double* Vw = nullptr;
+    int ldv_w = ldV;
+    if (a.need_v) {
+        if (v_smem) {
+            Vw = reinterpret_cast<double*>(smem + off);
+            off += (size_t)bn * ldV * sizeof(double);
+        } else {
+            Vw = a.work + (size_t)prob * a.work_stride;
+            ldv_w = bn;
+        }
+    }
+    off = (off + 15) & ~size_t(15);
+    GroupSmem* gs = reinterpret_cast<GroupSmem*>(smem + off);
+    off += (size_t)ngp * sizeof(GroupSmem);
+    off = (off + 15) & ~size_t(15);
+    double* sig = reinterpret_cast<double*>(smem + off);
+    off += (size_t)bn * sizeof(double);
+    int* perm = reinterpret_cast<int*>(smem + off);
+    off += ((size_t)bn * sizeof(int) + 15) & ~size_t(15);
+    int* misc = reinterpret_cast<int*>(smem + off);  // [0] sweep rot, [1] flag, [2] bad, [3] gram, [4] upd
+    unsigned long long* amax_bits = reinterpret_cast<unsigned long long*>(misc + 6);
+    if (tid < 6) misc[tid] = 0;
+    if (tid == 0) *amax_bits = 0ull;
+    __syncthreads();
+
+    // ---- load W (kernel (1)), V = I, pre-scale by an exact power of two ----
+    {
+        const double* Ap = a.A + (size_t)prob * a.strideA;
+        int bad = 0;
+        double amax = 0.0;
+        for (int e = tid; e < bm * bn; e += NT) {
+            const int r = e % bm, c = e / bm;
+            const double x = Ap[r + (size_t)c * a.lda];
+            bad |= !isfinite(x);
+            amax = fmax(amax, fabs(x));
+            W[r + c * ldW] = x;
+        }
+        if (bad) atomicOr(&misc[2], 1);
+        // non-negative doubles order like their bit patterns
+        atomicMax(amax_bits, (unsigned long long)__double_as_longlong(amax));
+        if (Vw)
+            for (int e = tid; e < bn * bn; e += NT) {
+                const int r = e % bn, c = e / bn;
+                Vw[r + c * ldv_w] = (r == c) ? 1.0 : 0.0;
+            }
+    }
+    __syncthreads();
+    const int ex = prescale_exponent(__longlong_as_double((long long)*amax_bits));
+    {
+        const double sc = pow2(-ex);
+        for (int e = tid; e < bm * bn; e += NT) W[e % bm + (e / bm) * ldW] *= sc;
+    }
+    __syncthreads();
+
+    const double tol = a.tol;
+    GroupSmem& S = gs[grp];
+    const int bar_id = 1 + grp;
+    int sweeps = 0, last = 0;
+    bool conv = false;
+    long long rot_total = 0;
+
+    for (int sw = 0; sw < a.max_sweeps; ++sw) {
+        for (int tb = 0; tb < nib; ++tb) {
+            for (int slot = grp; slot < hb; slot += ngp) {
+                int bi, bj;
+                if (!rr_pair(tb, slot, Sb, ell, bi, bj)) continue;  // phantom (odd ell): group idles
+                const int i0 = bi * 16, j0 = bj * 16;
+                auto wcol = [&](int x) -> double* { return W + (size_t)(x < 16 ? i0 + x : j0 + x - 16) * ldW; };
+                // ---- 1. Gram on DMMA: 10 upper 8x8 tiles of X^T X ----
+                for (int ti = wig; ti < 10; ti += wg) {
+                    const int P = ti < 4 ? 0 : (ti < 7 ? 1 : (ti < 9 ? 2 : 3));
+                    const int Q = ti < 4 ? ti : (ti < 7 ? ti - 3 : (ti < 9 ? ti - 5 : 3));
+                    const double* xp = wcol(8 * P + g8);
+                    const double* xq = wcol(8 * Q + g8);
+                    double c0 = 0.0, c1 = 0.0;
+                    for (int k = 0; k < bm; k += 4) dmma(c0, c1, xp[k + t4], xq[k + t4]);
+                    // D[g8][2 t4 + e] = G[8P + g8][8Q + 2 t4 + e]
+                    const int r = 8 * P + g8;
+                    const int cA = 8 * Q + 2 * t4;
+                    const double cv[2] = {c0, c1};
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int c = cA + e;
+                        if (r == c) {
+                            S.d[r] = cv[e];
+                            S.G[r + c * GLD] = 0.0;
+                        } else {
+                            S.G[r + c * GLD] = cv[e];
+                            S.G[c + r * GLD] = cv[e];  // exact mirror
+                        }
+                    }
+                }
+                for (int e = gtid; e < WB * WB; e += gthreads) S.D[(e & 31) + (e >> 5) * GLD] = 0.0;
+                if (gtid == 0) S.irot = 0;
+                group_bar(bar_id, gthreads);
+                // ---- 2. inner eigensolve (inner_budget sweeps, early exit) ----
+                long long pair_rot = 0;
+                for (int isw = 0; isw < a.inner_budget; ++isw) {
+                    for (int tw = 0; tw < WB - 1; ++tw) {
+                        if (gtid < HB) {
+                            int i, j;
+                            rr_pair(tw, gtid, WB, WB, i, j);
+                            InnerPar pr;
+                            pr.i = i;
+                            pr.j = j;
+                            pr.rot = 0;
+                            pr.cm1 = 0.0;
+                            pr.ws = 0.0;
+                            const double gij = S.G[i + j * GLD];
+                            const double absg = fabs(gij);
+                            if (!(absg <= 0.0) && !(absg < tol * fsqrt(fabs(S.d[i]) * fabs(S.d[j])))) {
+                                double t, s, cm1;
+                                rotation_tsc(S.d[i] - S.d[j], absg, t, s, cm1);
+                                pr.rot = 1;
+                                pr.cm1 = cm1;
+                                pr.ws = gij >= 0.0 ? s : -s;  // w s, w = g_ij / |g_ij|
+                                const double td = t * absg;
+                                S.d[i] += td;
+                                S.d[j] -= td;
+                                atomicAdd(&S.irot, 1);
+                            }
+                            S.prm[gtid] = pr;
+                        }
+                        group_bar(bar_id, gthreads);
+                        // G <- J^T G J over 2x2 blocks p <= q; Delta columns
+                        for (int e = gtid; e < HB * HB; e += gthreads) {
+                            const int p = e >> 4, q = e & 15;
+                            if (p > q) continue;
+                            const InnerPar P = S.prm[p];
+                            if (p == q) {
+                                if (P.rot) {
+                                    S.G[P.i + P.j * GLD] = 0.0;
+                                    S.G[P.j + P.i * GLD] = 0.0;
+                                }
+                                continue;
+                            }
+                            const InnerPar Q = S.prm[q];
+                            if (!P.rot && !Q.rot) continue;
+                            double x00 = S.G[P.i + Q.i * GLD], x01 = S.G[P.i + Q.j * GLD];
+                            double x10 = S.G[P.j + Q.i * GLD], x11 = S.G[P.j + Q.j * GLD];
+                            if (P.rot) {  // rows i_p, j_p: g_iq + (cm1 g_iq + ws g_jq), g_jq + (cm1 g_jq - wsc g_iq)
+                                rot2(x00, x10, P.cm1, P.ws, P.ws);
+                                rot2(x01, x11, P.cm1, P.ws, P.ws);
+                            }
+                            if (Q.rot) {  // columns i_q, j_q
+                                rot2(x00, x01, Q.cm1, Q.ws, Q.ws);
+                                rot2(x10, x11, Q.cm1, Q.ws, Q.ws);
+                            }
+                            S.G[P.i + Q.i * GLD] = x00;
+                            S.G[Q.i + P.i * GLD] = x00;
+                            S.G[P.i + Q.j * GLD] = x01;
+                            S.G[Q.j + P.i * GLD] = x01;
+                            S.G[P.j + Q.i * GLD] = x10;
+                            S.G[Q.i + P.j * GLD] = x10;
+                            S.G[P.j + Q.j * GLD] = x11;
+                            S.G[Q.j + P.j * GLD] = x11;
+                        }
+                        for (int e = gtid; e < WB * HB; e += gthreads) {
+                            const int r = e & 31, p = e >> 5;
+                            const InnerPar P = S.prm[p];
+                            if (!P.rot) continue;
+                            double xi = S.D[r + P.i * GLD], xj = S.D[r + P.j * GLD];
+                            rot2(xi, xj, P.cm1, P.ws, P.ws);  // Delta_:i + (cm1 Delta_:i + wsc Delta_:j) ...
+                            if (r == P.i) {
+                                xi += P.cm1;  // identity contribution
+                                xj -= P.ws;
+                            }
+                            if (r == P.j) {
+                                xi += P.ws;
+                                xj += P.cm1;
+                            }
+                            S.D[r + P.i * GLD] = xi;
+                            S.D[r + P.j * GLD] = xj;
+                        }
+                        group_bar(bar_id, gthreads);
+                    }
+                    const int irot = S.irot;
+                    group_bar(bar_id, gthreads);
+                    if (gtid == 0) S.irot = 0;
+                    __syncwarp();  // the reset precedes this warp's next atomicAdd
+                    pair_rot += irot;
+                    if (irot == 0) break;
+                }
+                if (gtid == 0) {
+                    atomicAdd(&misc[3], 1);
+                    if (pair_rot) {
+                        atomicAdd(&misc[0], (int)min(pair_rot, (long long)0x3fffffff));
+                        atomicAdd(&misc[4], 1);
+                    }
+                }
+                if (pair_rot) {
+                    // ---- 3. fused update on DMMA: [Bi Bj] += [Bi Bj] Delta (W, then V) ----
+                    for (int pass = 0; pass < (Vw ? 2 : 1); ++pass) {
+                        double* B = pass == 0 ? W : Vw;
+                        const int rows = pass == 0 ? bm : bn;
+                        const int ld = pass == 0 ? ldW : ldv_w;
+                        auto bcol = [&](int x) -> double* {
+                            return B + (size_t)(x < 16 ? i0 + x : j0 + x - 16) * ld;
+                        };
+                        for (int rb = wig; rb < rows / 8; rb += wg) {
+                            const int r0 = rb * 8;
+                            double c[4][2];
+#pragma unroll
+                            for (int C = 0; C < 4; ++C) {
+                                c[C][0] = bcol(8 * C + 2 * t4)[r0 + g8];
+                                c[C][1] = bcol(8 * C + 2 * t4 + 1)[r0 + g8];
+                            }
+                            double af[8];
+#pragma unroll
+                            for (int ks = 0; ks < 8; ++ks) af[ks] = bcol(4 * ks + t4)[r0 + g8];
+#pragma unroll
+                            for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+                                for (int C = 0; C < 4; ++C)
+                                    dmma(c[C][0], c[C][1], af[ks], S.D[(4 * ks + t4) + (8 * C + g8) * GLD]);
+#pragma unroll
+                            for (int C = 0; C < 4; ++C) {
+                                bcol(8 * C + 2 * t4)[r0 + g8] = c[C][0];
+                                bcol(8 * C + 2 * t4 + 1)[r0 + g8] = c[C][1];
+                            }
+                        }
+                    }
+                }
+                group_bar(bar_id, gthreads);  // G / Delta reused by this group's next slot
+            }
+            __syncthreads();  // every pair of this schedule iteration is updated
+        }
+        const int srot = misc[0];
+        __syncthreads();
+        if (tid == 0) misc[0] = 0;
+        sweeps = sw + 1;
+        last = srot;
+        if (srot == 0) {
+            conv = true;
+            break;
+        }
+        rot_total += srot;
+    }
+    // ---- unscale and finalise (kernel 5) ----
+    {
+        const double us = pow2(ex);
+        for (int e = tid; e < bm * bn; e += NT) W[e % bm + (e / bm) * ldW] *= us;
+    }
+    __syncthreads();
+    finalize_block<double>(W, ldW, bm, bn, Vw, ldv_w, sig, perm, &misc[1], final_out(a, prob));
+    if (tid == 0 && a.info) {
+        bsvd_info inf;
+        inf.converged = conv ? 1 : 0;
+        inf.outer_sweeps = sweeps;
+        inf.rotations = rot_total;
+        inf.gram_calls = misc[3];
+        inf.update_calls = misc[4];
+        inf.last_rotations = last;
+        inf.path = 2;
+        inf.status = misc[2] ? 1 : 0;
+        inf.kernel = KV_BLOCKED_DMMA;
+        a.info[prob] = inf;
+    }
+}
+
+size_t smem_bytes(int bm, int bn, bool v_smem) {
+    const int ell = bn / 16;
+    const int hb = (ell + (ell & 1)) / 2;
+    int ngp = 1;
+    while (ngp < hb && ngp < NWARP) ngp <<= 1;
+    size_t off = (size_t)bn * (bm + 4) * 8;
+    if (v_smem) off += (size_t)bn * (bn + 4) * 8;
+    off = (off + 15) & ~size_t(15);
+    off += (size_t)ngp * sizeof(GroupSmem);
+    off = (off + 15) & ~size_t(15);
+    off += (size_t)bn * 8 + (((size_t)bn * 4 + 15) & ~size_t(15)) + 64;
+    return off;
+}
+
+}  // namespace bdmma
+
+Plan plan_blocked_dmma(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, size_t smem_limit) {
+    Plan p{};
+    if (dtype != BSVD_D || nb != 16 || bn % 16 != 0 || bn < 32 || bm % 8 != 0 || !contiguous) return p;
+    const size_t with_v = bdmma::smem_bytes(bm, bn, need_v != 0);
+    const size_t without_v = bdmma::smem_bytes(bm, bn, false);
+    if (need_v && with_v <= smem_limit) {
+        p.resident = 3;
+        p.smem = with_v;
+        p.work_elems = 0;
+    } else if (without_v <= smem_limit) {
+        p.resident = 1;
+        p.smem = without_v;
+        p.work_elems = need_v ? (size_t)bn * bn : 0;
+    } else {
+        return p;
+    }
+    p.kernel = KV_BLOCKED_DMMA;
+    p.threads = bdmma::NT;
+    return p;
+}
+
+int launch_blocked_dmma(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
+    a.resident = p.resident;
+    a.kernel = KV_BLOCKED_DMMA;
+    a.work_stride = (int64_t)p.work_elems;
+    if (cudaFuncSetAttribute(bdmma::k_blocked_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) !=
+        cudaSuccess)
+        return BSVD_ERR_CUDA;
+    bdmma::k_blocked_dmma<<<a.batch, bdmma::NT, p.smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+}  // namespace bsvd

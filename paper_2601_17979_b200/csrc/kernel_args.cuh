@@ -45,6 +45,7 @@ enum {
     KV_UNBLOCKED_REG32_R2 = 5,  // same, 204 regs, 10 warps/SM
     KV_UNBLOCKED_REG32_R3 = 6,  // same, 227 regs, 9 warps/SM
     KV_UNBLOCKED_REG32_F2 = 7,  // 168 regs, two-FMA rotation update (opt-in)
+    KV_BLOCKED_DMMA = 8,        // blocked FP64, nb = 16, Gram/update on DMMA tensor cores
 };
 
 template <class T>

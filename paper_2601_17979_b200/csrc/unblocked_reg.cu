@@ -34,6 +34,7 @@
 //    sorts and permutes (kernel 5).
 #include "kernel_args.cuh"
 #include "launch.h"
+#include "rotation.cuh"
 
 namespace bsvd {
 namespace reg32 {
@@ -99,57 +100,9 @@ __device__ __forceinline__ void applyv(double& x, double& y, double cm1, double 
     if constexpr (F2) apply2(x, y, cm1, c); else apply(x, y, cm1, c);
 }
 
-__device__ __forceinline__ double pow2(int e) {  // 2^e for e in [-1022, 1023]
-    return __longlong_as_double((long long)(1023 + e) << 52);
-}
-
-// Rotation of pair (i, j) from (d = g_ii - g_jj, g = |g_ji|), reference F5:
-// t = sgn(tau) / (|tau| + sqrt(1 + tau^2)), tau = d / (2g), evaluated as
-// t = sgn(d) 2g / (|d| + sqrt(d^2 + 4 g^2)) on exponent-normalised d, g;
-// c = 1/sqrt(1 + t^2); s = t c; c - 1 = -s^2 / (1 + c)  (= -t^2/(h(1+h))).
 __device__ __forceinline__ void rotation(double d, double g, double& s_out, double& cm1_out) {
-    const double mx = fmax(fabs(d), g);
-    const int e = (int)((__double_as_longlong(mx) >> 52) & 0x7ff) - 1023;
-    const double sc = pow2(-max(-1022, min(1022, e)));
-    const double dn = d * sc, gn = g * sc;  // exact
-    const double q = fma(dn, dn, 4.0 * gn * gn);
-    double r = rsqrt_approx(q);
-    double ee = fma(-(q * r), r, 1.0);
-    r = fma(0.5 * r, ee, r);
-    ee = fma(-(q * r), r, 1.0);
-    r = fma(0.5 * r, ee, r);
-    double sq = q * r;
-    sq = fma(fma(-sq, sq, q), 0.5 * r, sq);
-    const double den = fabs(dn) + sq;
-    double rd = rcp_approx(den);
-    double e2 = fma(-den, rd, 1.0);
-    rd = fma(rd, e2, rd);
-    e2 = fma(-den, rd, 1.0);
-    rd = fma(rd, e2, rd);
-    const double num = 2.0 * gn;
-    double t = num * rd;
-    t = fma(fma(-den, t, num), rd, t);
-    t = d >= 0.0 ? t : -t;  // sgn(0) = +1
-    const double h2 = fma(t, t, 1.0);
-    double c = rsqrt_approx(h2);
-    ee = fma(-(h2 * c), c, 1.0);
-    c = fma(0.5 * c, ee, c);
-    ee = fma(-(h2 * c), c, 1.0);
-    c = fma(0.5 * c, ee, c);
-    ee = fma(-(h2 * c), c, 1.0);
-    c = fma(0.5 * c, ee, c);
-    const double s = t * c;
-    const double op = 1.0 + c;
-    double ro = rcp_approx(op);
-    e2 = fma(-op, ro, 1.0);
-    ro = fma(ro, e2, ro);
-    e2 = fma(-op, ro, 1.0);
-    ro = fma(ro, e2, ro);
-    const double s2 = s * s;
-    double cm = s2 * ro;
-    cm = fma(fma(-op, cm, s2), ro, cm);
-    s_out = s;
-    cm1_out = -cm;
+    double t;
+    rotation_tsc(d, g, t, s_out, cm1_out);
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -195,9 +148,7 @@ __global__ void __launch_bounds__(NW * 32) __maxnreg__(MAXREG) k_reg32(SolveArgs
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    int ex = (int)((__double_as_longlong(amax) >> 52) & 0x7ff) - 1022;
-    if (!(amax > 0.0) || !isfinite(amax)) ex = 0;
-    ex = max(-1021, min(1021, ex));
+    const int ex = prescale_exponent(amax);
     {
         const double scale = pow2(-ex);
 #pragma unroll

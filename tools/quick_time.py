@@ -11,7 +11,9 @@ cfgs = [("C1-10k", "arith", 32, 32, 10000, np.float64, 1e10, True),
         ("C2-vals", "random", 16, 16, 10000, np.float32, 1, False),
         ("C4", "random", 256, 32, 5000, np.complex128, 1, True),
         ("C3", "geo", 64, 64, 2000, np.float64, 1e12, True),
-        ("C5", "random", 128, 128, 500, np.float64, 1, True)]
+        ("C5", "random", 128, 128, 500, np.float64, 1, True),
+        ("C3-10k", "geo", 64, 64, 10000, np.float64, 1e12, True),
+        ("C5-2k", "random", 128, 128, 2000, np.float64, 1, True)]
 args = sys.argv[1:]
 kernels = [0]
 if "--kernels" in args:
