@@ -49,9 +49,9 @@ struct GroupSmem {
     double G[WB * GLD];
     double D[WB * GLD];
     double d[WB];
-    InnerPar prm[HB];
-    int irot;      // inner rotations of the current inner sweep
-    int pad[3];
+    InnerPar prm[2][HB];  // rotation parameters, double-buffered by iteration parity
+    int cnt[2];           // inner rotations per inner sweep (by sweep parity)
+    int pad[2];
 };
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -72,7 +72,33 @@ __device__ __forceinline__ void rot2(double& x, double& y, double cm1, double a,
     y = ny;
 }
 
-__global__ void __launch_bounds__(NT, 1) k_blocked_dmma(SolveArgs<double> a) {
+// Rotation of inner pair (i, j) from g = G[i][j] (reference eig_sweeps guard and
+// formulas, src/_kernels_numba.py:35-60): zeroes the pivot and updates d when it rotates.
+__device__ __forceinline__ void inner_params(GroupSmem& S, int i, int j, double g, double tol, InnerPar& pr,
+                                             int* cnt) {
+    pr.i = i;
+    pr.j = j;
+    pr.rot = 0;
+    pr.cm1 = 0.0;
+    pr.ws = 0.0;
+    const double absg = fabs(g);
+    const double di = S.d[i], dj = S.d[j];
+    if (!(absg <= 0.0) && !(absg < tol * fsqrt(fabs(di) * fabs(dj)))) {
+        double t, s, cm1;
+        rotation_tsc(di - dj, absg, t, s, cm1);
+        pr.rot = 1;
+        pr.cm1 = cm1;
+        pr.ws = g >= 0.0 ? s : -s;  // w s, w = g_ij / |g_ij|
+        const double td = t * absg;
+        S.d[i] = di + td;
+        S.d[j] = dj - td;
+        S.G[i + j * GLD] = 0.0;  // g_ij = g_ji = 0 after the rotation
+        S.G[j + i * GLD] = 0.0;
+        atomicAdd(cnt, 1);
+    }
+}
+
+__global__ void __launch_bounds__(NT, 2) k_blocked_dmma(SolveArgs<double> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int prob = blockIdx.x;
     const int bm = a.bm, bn = a.bn;
@@ -184,73 +210,92 @@ __global__ void __launch_bounds__(NT, 1) k_blocked_dmma(SolveArgs<double> a) {
                     }
                 }
                 for (int e = gtid; e < WB * WB; e += gthreads) S.D[(e & 31) + (e >> 5) * GLD] = 0.0;
-                if (gtid == 0) S.irot = 0;
+                if (gtid == 0) {
+                    S.cnt[0] = 0;
+                    S.cnt[1] = 0;
+                }
                 group_bar(bar_id, gthreads);
                 // ---- 2. inner eigensolve (inner_budget sweeps, early exit) ----
+                // One barrier per inner iteration.  The ring of the tournament makes
+                // pair k' of iteration t+1 draw its two columns from pairs (k'-1, k'+1)
+                // of iteration t (k' = 0: (0,1), k' = 15: (14,15)), so the thread that
+                // owns 2x2 block (k'-1, k'+1) computes pair k''s rotation right after
+                // updating that block.  Rotation parameters are double-buffered by
+                // iteration parity.  A parameter evaluation past the last counted
+                // sweep only touches G and d, which are discarded (Delta is what
+                // leaves the eigensolve), so speculating one iteration ahead is exact.
                 long long pair_rot = 0;
-                for (int isw = 0; isw < a.inner_budget; ++isw) {
-                    for (int tw = 0; tw < WB - 1; ++tw) {
-                        if (gtid < HB) {
-                            int i, j;
-                            rr_pair(tw, gtid, WB, WB, i, j);
-                            InnerPar pr;
-                            pr.i = i;
-                            pr.j = j;
-                            pr.rot = 0;
-                            pr.cm1 = 0.0;
-                            pr.ws = 0.0;
-                            const double gij = S.G[i + j * GLD];
-                            const double absg = fabs(gij);
-                            if (!(absg <= 0.0) && !(absg < tol * fsqrt(fabs(S.d[i]) * fabs(S.d[j])))) {
-                                double t, s, cm1;
-                                rotation_tsc(S.d[i] - S.d[j], absg, t, s, cm1);
-                                pr.rot = 1;
-                                pr.cm1 = cm1;
-                                pr.ws = gij >= 0.0 ? s : -s;  // w s, w = g_ij / |g_ij|
-                                const double td = t * absg;
-                                S.d[i] += td;
-                                S.d[j] -= td;
-                                atomicAdd(&S.irot, 1);
-                            }
-                            S.prm[gtid] = pr;
+                if (gtid < HB) {
+                    int i, j;
+                    rr_pair(0, gtid, WB, WB, i, j);
+                    InnerPar pr;
+                    inner_params(S, i, j, S.G[i + j * GLD], tol, pr, &S.cnt[0]);
+                    S.prm[0][gtid] = pr;
+                }
+                group_bar(bar_id, gthreads);
+                // the (<= 2) off-diagonal blocks this thread owns, fixed for the eig
+                int bp[2] = {-1, -1}, bq[2] = {-1, -1};
+                {
+                    int nown = 0;
+                    for (int blk = gtid; blk < 120 && nown < 2; blk += gthreads) {
+                        int P = 0, rem = blk;
+                        while (rem >= 15 - P) {
+                            rem -= 15 - P;
+                            ++P;
                         }
-                        group_bar(bar_id, gthreads);
-                        // G <- J^T G J over 2x2 blocks p <= q; Delta columns
-                        for (int e = gtid; e < HB * HB; e += gthreads) {
-                            const int p = e >> 4, q = e & 15;
-                            if (p > q) continue;
-                            const InnerPar P = S.prm[p];
-                            if (p == q) {
-                                if (P.rot) {
-                                    S.G[P.i + P.j * GLD] = 0.0;
-                                    S.G[P.j + P.i * GLD] = 0.0;
-                                }
-                                continue;
+                        bp[nown] = P;
+                        bq[nown] = P + 1 + rem;
+                        ++nown;
+                    }
+                }
+                int it = 0;
+                for (int isw = 0; isw < a.inner_budget; ++isw) {
+                    for (int tw = 0; tw < WB - 1; ++tw, ++it) {
+                        const InnerPar* cur = S.prm[it & 1];
+                        InnerPar* nxt = S.prm[(it + 1) & 1];
+                        const int tn = (tw + 1 == WB - 1) ? 0 : tw + 1;       // next iteration in the ring
+                        int* ncnt = &S.cnt[(tw + 1 == WB - 1 ? isw + 1 : isw) & 1];
+#pragma unroll
+                        for (int ob = 0; ob < 2; ++ob) {
+                            const int P = bp[ob], Q = bq[ob];
+                            if (P < 0) continue;
+                            const int nk = (P == 0 && Q == 1) ? 0 : (P == 14 && Q == 15) ? 15 : (Q == P + 2 ? P + 1 : -1);
+                            const InnerPar Pp = cur[P], Qp = cur[Q];
+                            if (!Pp.rot && !Qp.rot && nk < 0) continue;
+                            double x00 = S.G[Pp.i + Qp.i * GLD], x01 = S.G[Pp.i + Qp.j * GLD];
+                            double x10 = S.G[Pp.j + Qp.i * GLD], x11 = S.G[Pp.j + Qp.j * GLD];
+                            if (Pp.rot) {  // rows i_p, j_p: g_iq + (cm1 g_iq + ws g_jq), g_jq + (cm1 g_jq - wsc g_iq)
+                                rot2(x00, x10, Pp.cm1, Pp.ws, Pp.ws);
+                                rot2(x01, x11, Pp.cm1, Pp.ws, Pp.ws);
                             }
-                            const InnerPar Q = S.prm[q];
-                            if (!P.rot && !Q.rot) continue;
-                            double x00 = S.G[P.i + Q.i * GLD], x01 = S.G[P.i + Q.j * GLD];
-                            double x10 = S.G[P.j + Q.i * GLD], x11 = S.G[P.j + Q.j * GLD];
-                            if (P.rot) {  // rows i_p, j_p: g_iq + (cm1 g_iq + ws g_jq), g_jq + (cm1 g_jq - wsc g_iq)
-                                rot2(x00, x10, P.cm1, P.ws, P.ws);
-                                rot2(x01, x11, P.cm1, P.ws, P.ws);
+                            if (Qp.rot) {  // columns i_q, j_q
+                                rot2(x00, x01, Qp.cm1, Qp.ws, Qp.ws);
+                                rot2(x10, x11, Qp.cm1, Qp.ws, Qp.ws);
                             }
-                            if (Q.rot) {  // columns i_q, j_q
-                                rot2(x00, x01, Q.cm1, Q.ws, Q.ws);
-                                rot2(x10, x11, Q.cm1, Q.ws, Q.ws);
+                            if (Pp.rot || Qp.rot) {
+                                S.G[Pp.i + Qp.i * GLD] = x00;
+                                S.G[Qp.i + Pp.i * GLD] = x00;
+                                S.G[Pp.i + Qp.j * GLD] = x01;
+                                S.G[Qp.j + Pp.i * GLD] = x01;
+                                S.G[Pp.j + Qp.i * GLD] = x10;
+                                S.G[Qp.i + Pp.j * GLD] = x10;
+                                S.G[Pp.j + Qp.j * GLD] = x11;
+                                S.G[Qp.j + Pp.j * GLD] = x11;
                             }
-                            S.G[P.i + Q.i * GLD] = x00;
-                            S.G[Q.i + P.i * GLD] = x00;
-                            S.G[P.i + Q.j * GLD] = x01;
-                            S.G[Q.j + P.i * GLD] = x01;
-                            S.G[P.j + Q.i * GLD] = x10;
-                            S.G[Q.i + P.j * GLD] = x10;
-                            S.G[P.j + Q.j * GLD] = x11;
-                            S.G[Q.j + P.j * GLD] = x11;
+                            if (nk >= 0) {
+                                int i, j;
+                                rr_pair(tn, nk, WB, WB, i, j);
+                                const bool ri = (i == Pp.i) || (i == Pp.j);  // i in the block's rows?
+                                const int rr = ri ? i : j, cc = ri ? j : i;
+                                const double g = (rr == Pp.i) ? ((cc == Qp.i) ? x00 : x01) : ((cc == Qp.i) ? x10 : x11);
+                                InnerPar pr;
+                                inner_params(S, i, j, g, tol, pr, ncnt);
+                                nxt[nk] = pr;
+                            }
                         }
                         for (int e = gtid; e < WB * HB; e += gthreads) {
                             const int r = e & 31, p = e >> 5;
-                            const InnerPar P = S.prm[p];
+                            const InnerPar P = cur[p];
                             if (!P.rot) continue;
                             double xi = S.D[r + P.i * GLD], xj = S.D[r + P.j * GLD];
                             rot2(xi, xj, P.cm1, P.ws, P.ws);  // Delta_:i + (cm1 Delta_:i + wsc Delta_:j) ...
@@ -265,15 +310,15 @@ __global__ void __launch_bounds__(NT, 1) k_blocked_dmma(SolveArgs<double> a) {
                             S.D[r + P.i * GLD] = xi;
                             S.D[r + P.j * GLD] = xj;
                         }
+                        // counter of sweep isw+1 (= isw-1): every thread read it before phase (isw, 0)'s barrier
+                        if (tw == 1 && gtid == 0) S.cnt[(isw + 1) & 1] = 0;
                         group_bar(bar_id, gthreads);
                     }
-                    const int irot = S.irot;
-                    group_bar(bar_id, gthreads);
-                    if (gtid == 0) S.irot = 0;
-                    __syncwarp();  // the reset precedes this warp's next atomicAdd
+                    const int irot = S.cnt[isw & 1];
                     pair_rot += irot;
                     if (irot == 0) break;
                 }
+                group_bar(bar_id, gthreads);  // every thread has read the counters before they are reused
                 if (gtid == 0) {
                     atomicAdd(&misc[3], 1);
                     if (pair_rot) {
@@ -346,7 +391,7 @@ __global__ void __launch_bounds__(NT, 1) k_blocked_dmma(SolveArgs<double> a) {
         inf.last_rotations = last;
         inf.path = 2;
         inf.status = misc[2] ? 1 : 0;
-        inf.kernel = KV_BLOCKED_DMMA;
+        inf.kernel = a.kernel;
         a.info[prob] = inf;
     }
 }
@@ -367,12 +412,14 @@ size_t smem_bytes(int bm, int bn, bool v_smem) {
 
 }  // namespace bdmma
 
-Plan plan_blocked_dmma(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, size_t smem_limit) {
+Plan plan_blocked_dmma(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, size_t smem_limit,
+                       int variant) {
     Plan p{};
     if (dtype != BSVD_D || nb != 16 || bn % 16 != 0 || bn < 32 || bm % 8 != 0 || !contiguous) return p;
     const size_t with_v = bdmma::smem_bytes(bm, bn, need_v != 0);
     const size_t without_v = bdmma::smem_bytes(bm, bn, false);
-    if (need_v && with_v <= smem_limit) {
+    const bool v_global = variant == KV_BLOCKED_DMMA_VG;  // V in L2: more CTAs per SM
+    if (need_v && !v_global && with_v <= smem_limit) {
         p.resident = 3;
         p.smem = with_v;
         p.work_elems = 0;
@@ -383,18 +430,21 @@ Plan plan_blocked_dmma(int dtype, int bm, int bn, int nb, int need_v, bool conti
     } else {
         return p;
     }
-    p.kernel = KV_BLOCKED_DMMA;
+    p.kernel = v_global ? KV_BLOCKED_DMMA_VG : KV_BLOCKED_DMMA;
     p.threads = bdmma::NT;
     return p;
 }
 
 int launch_blocked_dmma(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
     a.resident = p.resident;
-    a.kernel = KV_BLOCKED_DMMA;
+    a.kernel = p.kernel;
     a.work_stride = (int64_t)p.work_elems;
     if (cudaFuncSetAttribute(bdmma::k_blocked_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) !=
         cudaSuccess)
         return BSVD_ERR_CUDA;
+    // the occupancy of this kernel is shared-memory bound: ask for the largest carveout
+    cudaFuncSetAttribute(bdmma::k_blocked_dmma, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     bdmma::k_blocked_dmma<<<a.batch, bdmma::NT, p.smem, st>>>(a);
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }

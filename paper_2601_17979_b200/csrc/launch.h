@@ -21,7 +21,8 @@ struct Plan {
 Plan plan_unblocked_general(int esize, int rsize, int bm, int bn, int need_v, size_t smem_limit);
 Plan plan_blocked_general(int esize, int rsize, int bm, int bn, int nb, int need_v, size_t smem_limit);
 Plan plan_unblocked_reg(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
-Plan plan_blocked_dmma(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, size_t smem_limit);
+Plan plan_blocked_dmma(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, size_t smem_limit,
+                       int variant);
 int launch_blocked_dmma(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 
 template <class T>
