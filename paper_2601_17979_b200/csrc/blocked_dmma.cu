@@ -38,7 +38,7 @@ constexpr int NT = 256;   // threads per CTA
 constexpr int NWARP = NT / 32;
 constexpr int WB = 32;    // Gram width 2 nb
 constexpr int HB = 16;    // inner pairs per iteration
-constexpr int GLD = 36;   // leading dimension of G / Delta in smem
+constexpr int GLD = 34;   // leading dimension of G / Delta in smem (16-byte column shift: conflict-free LDS.128)
 
 struct InnerPar {
     double cm1, ws;  // real: wsc == ws
@@ -96,6 +96,140 @@ __device__ __forceinline__ void inner_params(GroupSmem& S, int i, int j, double 
         S.G[j + i * GLD] = 0.0;
         atomicAdd(cnt, 1);
     }
+}
+
+// One group's inner eigensolve on G (zero diagonal) / d, accumulating Delta
+// (initialised to 0).  Returns the inner rotations of the counted sweeps.
+//
+// One barrier per inner iteration.  The ring of the tournament makes pair k'
+// of iteration t+1 draw its two columns from pairs (k'-1, k'+1) of iteration t
+// (k' = 0: (0,1), k' = 15: (14,15)), so the thread owning 2x2 block
+// (k'-1, k'+1) evaluates pair k''s rotation right after updating that block;
+// parameters are double-buffered by iteration parity.  An evaluation past the
+// last counted sweep only touches G and d, which are discarded (Delta is what
+// leaves the eigensolve), so speculating one iteration ahead is exact.
+// Delta columns: thread -> (pair p = gtid % 16, a contiguous chunk of rows),
+// 16-byte shared-memory accesses, parameters loaded once per iteration.
+template <int GT>
+__device__ __noinline__ long long inner_eig(GroupSmem& S, int gtid, int bar_id, int budget, double tol) {
+    constexpr int NCH = GT / 16;        // row chunks per pair
+    constexpr int RPC = WB / NCH;       // rows per chunk (16, 8, 4 or 2)
+    constexpr int NOWN = (120 + GT - 1) / GT;
+    if (gtid < HB) {
+        int i, j;
+        rr_pair(0, gtid, WB, WB, i, j);
+        InnerPar pr;
+        inner_params(S, i, j, S.G[i + j * GLD], tol, pr, &S.cnt[0]);
+        S.prm[0][gtid] = pr;
+    }
+    group_bar(bar_id, GT);
+    int bp[NOWN], bq[NOWN];
+#pragma unroll
+    for (int o = 0; o < NOWN; ++o) {
+        const int blk = gtid + o * GT;
+        bp[o] = -1;
+        bq[o] = -1;
+        if (blk < 120) {
+            int P = 0, rem = blk;
+            while (rem >= 15 - P) {
+                rem -= 15 - P;
+                ++P;
+            }
+            bp[o] = P;
+            bq[o] = P + 1 + rem;
+        }
+    }
+    const int dp = gtid & 15, r0 = (gtid >> 4) * RPC;  // Delta task
+    long long pair_rot = 0;
+    int it = 0;
+    for (int isw = 0; isw < budget; ++isw) {
+        for (int tw = 0; tw < WB - 1; ++tw, ++it) {
+            const InnerPar* cur = S.prm[it & 1];
+            InnerPar* nxt = S.prm[(it + 1) & 1];
+            const int tn = (tw + 1 == WB - 1) ? 0 : tw + 1;  // next iteration in the ring
+            int* ncnt = &S.cnt[(tw + 1 == WB - 1 ? isw + 1 : isw) & 1];
+#pragma unroll
+            for (int ob = 0; ob < NOWN; ++ob) {
+                const int P = bp[ob], Q = bq[ob];
+                if (P < 0) continue;
+                const int nk = (P == 0 && Q == 1) ? 0 : (P == 14 && Q == 15) ? 15 : (Q == P + 2 ? P + 1 : -1);
+                const InnerPar Pp = cur[P], Qp = cur[Q];
+                if (!Pp.rot && !Qp.rot && nk < 0) continue;
+                double x00 = S.G[Pp.i + Qp.i * GLD], x01 = S.G[Pp.i + Qp.j * GLD];
+                double x10 = S.G[Pp.j + Qp.i * GLD], x11 = S.G[Pp.j + Qp.j * GLD];
+                if (Pp.rot) {  // rows i_p, j_p: g_iq + (cm1 g_iq + ws g_jq), g_jq + (cm1 g_jq - wsc g_iq)
+                    rot2(x00, x10, Pp.cm1, Pp.ws, Pp.ws);
+                    rot2(x01, x11, Pp.cm1, Pp.ws, Pp.ws);
+                }
+                if (Qp.rot) {  // columns i_q, j_q
+                    rot2(x00, x01, Qp.cm1, Qp.ws, Qp.ws);
+                    rot2(x10, x11, Qp.cm1, Qp.ws, Qp.ws);
+                }
+                if (Pp.rot || Qp.rot) {
+                    S.G[Pp.i + Qp.i * GLD] = x00;
+                    S.G[Qp.i + Pp.i * GLD] = x00;
+                    S.G[Pp.i + Qp.j * GLD] = x01;
+                    S.G[Qp.j + Pp.i * GLD] = x01;
+                    S.G[Pp.j + Qp.i * GLD] = x10;
+                    S.G[Qp.i + Pp.j * GLD] = x10;
+                    S.G[Pp.j + Qp.j * GLD] = x11;
+                    S.G[Qp.j + Pp.j * GLD] = x11;
+                }
+                if (nk >= 0) {
+                    int i, j;
+                    rr_pair(tn, nk, WB, WB, i, j);
+                    const bool ri = (i == Pp.i) || (i == Pp.j);  // i among the block's rows?
+                    const int rr = ri ? i : j, cc = ri ? j : i;
+                    const double g = (rr == Pp.i) ? ((cc == Qp.i) ? x00 : x01) : ((cc == Qp.i) ? x10 : x11);
+                    InnerPar pr;
+                    inner_params(S, i, j, g, tol, pr, ncnt);
+                    nxt[nk] = pr;
+                }
+            }
+            {
+                const InnerPar Pd = cur[dp];
+                if (Pd.rot) {
+                    double* ci = &S.D[r0 + Pd.i * GLD];
+                    double* cj = &S.D[r0 + Pd.j * GLD];
+                    double xi[RPC], xj[RPC];
+#pragma unroll
+                    for (int v = 0; v < RPC; v += 2) {
+                        const double2 a2 = *reinterpret_cast<const double2*>(ci + v);
+                        const double2 b2 = *reinterpret_cast<const double2*>(cj + v);
+                        xi[v] = a2.x;
+                        xi[v + 1] = a2.y;
+                        xj[v] = b2.x;
+                        xj[v + 1] = b2.y;
+                    }
+#pragma unroll
+                    for (int v = 0; v < RPC; ++v) {
+                        rot2(xi[v], xj[v], Pd.cm1, Pd.ws, Pd.ws);  // Delta_:i + (cm1 Delta_:i + wsc Delta_:j) ...
+                        const int r = r0 + v;
+                        if (r == Pd.i) {  // identity contribution of P = I + Delta
+                            xi[v] += Pd.cm1;
+                            xj[v] -= Pd.ws;
+                        }
+                        if (r == Pd.j) {
+                            xi[v] += Pd.ws;
+                            xj[v] += Pd.cm1;
+                        }
+                    }
+#pragma unroll
+                    for (int v = 0; v < RPC; v += 2) {
+                        *reinterpret_cast<double2*>(ci + v) = make_double2(xi[v], xi[v + 1]);
+                        *reinterpret_cast<double2*>(cj + v) = make_double2(xj[v], xj[v + 1]);
+                    }
+                }
+            }
+            // counter of sweep isw+1 (= isw-1): every thread read it before phase (isw, 0)'s barrier
+            if (tw == 1 && gtid == 0) S.cnt[(isw + 1) & 1] = 0;
+            group_bar(bar_id, GT);
+        }
+        const int irot = S.cnt[isw & 1];
+        pair_rot += irot;
+        if (irot == 0) break;
+    }
+    return pair_rot;
 }
 
 __global__ void __launch_bounds__(NT, 2) k_blocked_dmma(SolveArgs<double> a) {
@@ -216,107 +350,12 @@ __global__ void __launch_bounds__(NT, 2) k_blocked_dmma(SolveArgs<double> a) {
                 }
                 group_bar(bar_id, gthreads);
                 // ---- 2. inner eigensolve (inner_budget sweeps, early exit) ----
-                // One barrier per inner iteration.  The ring of the tournament makes
-                // pair k' of iteration t+1 draw its two columns from pairs (k'-1, k'+1)
-                // of iteration t (k' = 0: (0,1), k' = 15: (14,15)), so the thread that
-                // owns 2x2 block (k'-1, k'+1) computes pair k''s rotation right after
-                // updating that block.  Rotation parameters are double-buffered by
-                // iteration parity.  A parameter evaluation past the last counted
-                // sweep only touches G and d, which are discarded (Delta is what
-                // leaves the eigensolve), so speculating one iteration ahead is exact.
                 long long pair_rot = 0;
-                if (gtid < HB) {
-                    int i, j;
-                    rr_pair(0, gtid, WB, WB, i, j);
-                    InnerPar pr;
-                    inner_params(S, i, j, S.G[i + j * GLD], tol, pr, &S.cnt[0]);
-                    S.prm[0][gtid] = pr;
-                }
-                group_bar(bar_id, gthreads);
-                // the (<= 2) off-diagonal blocks this thread owns, fixed for the eig
-                int bp[2] = {-1, -1}, bq[2] = {-1, -1};
-                {
-                    int nown = 0;
-                    for (int blk = gtid; blk < 120 && nown < 2; blk += gthreads) {
-                        int P = 0, rem = blk;
-                        while (rem >= 15 - P) {
-                            rem -= 15 - P;
-                            ++P;
-                        }
-                        bp[nown] = P;
-                        bq[nown] = P + 1 + rem;
-                        ++nown;
-                    }
-                }
-                int it = 0;
-                for (int isw = 0; isw < a.inner_budget; ++isw) {
-                    for (int tw = 0; tw < WB - 1; ++tw, ++it) {
-                        const InnerPar* cur = S.prm[it & 1];
-                        InnerPar* nxt = S.prm[(it + 1) & 1];
-                        const int tn = (tw + 1 == WB - 1) ? 0 : tw + 1;       // next iteration in the ring
-                        int* ncnt = &S.cnt[(tw + 1 == WB - 1 ? isw + 1 : isw) & 1];
-#pragma unroll
-                        for (int ob = 0; ob < 2; ++ob) {
-                            const int P = bp[ob], Q = bq[ob];
-                            if (P < 0) continue;
-                            const int nk = (P == 0 && Q == 1) ? 0 : (P == 14 && Q == 15) ? 15 : (Q == P + 2 ? P + 1 : -1);
-                            const InnerPar Pp = cur[P], Qp = cur[Q];
-                            if (!Pp.rot && !Qp.rot && nk < 0) continue;
-                            double x00 = S.G[Pp.i + Qp.i * GLD], x01 = S.G[Pp.i + Qp.j * GLD];
-                            double x10 = S.G[Pp.j + Qp.i * GLD], x11 = S.G[Pp.j + Qp.j * GLD];
-                            if (Pp.rot) {  // rows i_p, j_p: g_iq + (cm1 g_iq + ws g_jq), g_jq + (cm1 g_jq - wsc g_iq)
-                                rot2(x00, x10, Pp.cm1, Pp.ws, Pp.ws);
-                                rot2(x01, x11, Pp.cm1, Pp.ws, Pp.ws);
-                            }
-                            if (Qp.rot) {  // columns i_q, j_q
-                                rot2(x00, x01, Qp.cm1, Qp.ws, Qp.ws);
-                                rot2(x10, x11, Qp.cm1, Qp.ws, Qp.ws);
-                            }
-                            if (Pp.rot || Qp.rot) {
-                                S.G[Pp.i + Qp.i * GLD] = x00;
-                                S.G[Qp.i + Pp.i * GLD] = x00;
-                                S.G[Pp.i + Qp.j * GLD] = x01;
-                                S.G[Qp.j + Pp.i * GLD] = x01;
-                                S.G[Pp.j + Qp.i * GLD] = x10;
-                                S.G[Qp.i + Pp.j * GLD] = x10;
-                                S.G[Pp.j + Qp.j * GLD] = x11;
-                                S.G[Qp.j + Pp.j * GLD] = x11;
-                            }
-                            if (nk >= 0) {
-                                int i, j;
-                                rr_pair(tn, nk, WB, WB, i, j);
-                                const bool ri = (i == Pp.i) || (i == Pp.j);  // i in the block's rows?
-                                const int rr = ri ? i : j, cc = ri ? j : i;
-                                const double g = (rr == Pp.i) ? ((cc == Qp.i) ? x00 : x01) : ((cc == Qp.i) ? x10 : x11);
-                                InnerPar pr;
-                                inner_params(S, i, j, g, tol, pr, ncnt);
-                                nxt[nk] = pr;
-                            }
-                        }
-                        for (int e = gtid; e < WB * HB; e += gthreads) {
-                            const int r = e & 31, p = e >> 5;
-                            const InnerPar P = cur[p];
-                            if (!P.rot) continue;
-                            double xi = S.D[r + P.i * GLD], xj = S.D[r + P.j * GLD];
-                            rot2(xi, xj, P.cm1, P.ws, P.ws);  // Delta_:i + (cm1 Delta_:i + wsc Delta_:j) ...
-                            if (r == P.i) {
-                                xi += P.cm1;  // identity contribution
-                                xj -= P.ws;
-                            }
-                            if (r == P.j) {
-                                xi += P.ws;
-                                xj += P.cm1;
-                            }
-                            S.D[r + P.i * GLD] = xi;
-                            S.D[r + P.j * GLD] = xj;
-                        }
-                        // counter of sweep isw+1 (= isw-1): every thread read it before phase (isw, 0)'s barrier
-                        if (tw == 1 && gtid == 0) S.cnt[(isw + 1) & 1] = 0;
-                        group_bar(bar_id, gthreads);
-                    }
-                    const int irot = S.cnt[isw & 1];
-                    pair_rot += irot;
-                    if (irot == 0) break;
+                switch (gthreads) {
+                    case 256: pair_rot = inner_eig<256>(S, gtid, bar_id, a.inner_budget, tol); break;
+                    case 128: pair_rot = inner_eig<128>(S, gtid, bar_id, a.inner_budget, tol); break;
+                    case 64: pair_rot = inner_eig<64>(S, gtid, bar_id, a.inner_budget, tol); break;
+                    default: pair_rot = inner_eig<32>(S, gtid, bar_id, a.inner_budget, tol); break;
                 }
                 group_bar(bar_id, gthreads);  // every thread has read the counters before they are reused
                 if (gtid == 0) {
