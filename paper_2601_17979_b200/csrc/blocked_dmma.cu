@@ -34,8 +34,6 @@
 namespace bsvd {
 namespace bdmma {
 
-constexpr int NT = 256;   // threads per CTA
-constexpr int NWARP = NT / 32;
 constexpr int WB = 32;    // Gram width 2 nb
 constexpr int HB = 16;    // inner pairs per iteration
 constexpr int GLD = 34;   // leading dimension of G / Delta in smem (16-byte column shift: conflict-free LDS.128)
@@ -232,7 +230,9 @@ __device__ __noinline__ long long inner_eig(GroupSmem& S, int gtid, int bar_id, 
     return pair_rot;
 }
 
-__global__ void __launch_bounds__(NT, 2) k_blocked_dmma(SolveArgs<double> a) {
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_blocked_dmma(SolveArgs<double> a) {
+    constexpr int NWARP = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     const int prob = blockIdx.x;
     const int bm = a.bm, bn = a.bn;
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(NT, 2) k_blocked_dmma(SolveArgs<double> a) {
     const int ell = bn / 16;
     const int Sb = ell + (ell & 1), hb = Sb / 2, nib = Sb - 1;
     int ngp = 1;
-    while (ngp < hb && ngp < NWARP) ngp <<= 1;  // groups (power of two)
+    while (ngp < hb && ngp < NWARP && ngp < 8) ngp <<= 1;  // groups (power of two; named barriers 1..8)
     const int wg = NWARP / ngp;                  // warps per group
     const int grp = warp / wg, wig = warp % wg;
     const int gthreads = wg * 32, gtid = tid - grp * gthreads;
@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(NT, 2) k_blocked_dmma(SolveArgs<double> a) {
                 // ---- 2. inner eigensolve (inner_budget sweeps, early exit) ----
                 long long pair_rot = 0;
                 switch (gthreads) {
+                    case 512: pair_rot = inner_eig<512>(S, gtid, bar_id, a.inner_budget, tol); break;
                     case 256: pair_rot = inner_eig<256>(S, gtid, bar_id, a.inner_budget, tol); break;
                     case 128: pair_rot = inner_eig<128>(S, gtid, bar_id, a.inner_budget, tol); break;
                     case 64: pair_rot = inner_eig<64>(S, gtid, bar_id, a.inner_budget, tol); break;
@@ -435,11 +436,11 @@ __global__ void __launch_bounds__(NT, 2) k_blocked_dmma(SolveArgs<double> a) {
     }
 }
 
-size_t smem_bytes(int bm, int bn, bool v_smem) {
+size_t smem_bytes(int bm, int bn, bool v_smem, int nwarp) {
     const int ell = bn / 16;
     const int hb = (ell + (ell & 1)) / 2;
     int ngp = 1;
-    while (ngp < hb && ngp < NWARP) ngp <<= 1;
+    while (ngp < hb && ngp < nwarp && ngp < 8) ngp <<= 1;
     size_t off = (size_t)bn * (bm + 4) * 8;
     if (v_smem) off += (size_t)bn * (bn + 4) * 8;
     off = (off + 15) & ~size_t(15);
@@ -451,13 +452,23 @@ size_t smem_bytes(int bm, int bn, bool v_smem) {
 
 }  // namespace bdmma
 
+// variants: KV_BLOCKED_DMMA    256 threads, <=128 regs, V in smem when it fits
+//           KV_BLOCKED_DMMA_VG 256 threads, <= 85 regs (3 CTAs/SM), V in L2
+//           KV_BLOCKED_DMMA_512 512 threads (16 warps for one-CTA-per-SM problems), V in smem if it fits
 Plan plan_blocked_dmma(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, size_t smem_limit,
                        int variant) {
     Plan p{};
     if (dtype != BSVD_D || nb != 16 || bn % 16 != 0 || bn < 32 || bm % 8 != 0 || !contiguous) return p;
-    const size_t with_v = bdmma::smem_bytes(bm, bn, need_v != 0);
-    const size_t without_v = bdmma::smem_bytes(bm, bn, false);
-    const bool v_global = variant == KV_BLOCKED_DMMA_VG;  // V in L2: more CTAs per SM
+    int kv = variant;
+    if (kv != KV_BLOCKED_DMMA && kv != KV_BLOCKED_DMMA_VG && kv != KV_BLOCKED_DMMA_512) {
+        // auto: 64x64-class problems run 3 CTAs/SM with V in L2; larger ones take 16 warps in one CTA
+        kv = (bdmma::smem_bytes(bm, bn, false, 8) * 3 <= (size_t)228 * 1024) ? KV_BLOCKED_DMMA_VG
+                                                                              : KV_BLOCKED_DMMA_512;
+    }
+    const int nwarp = kv == KV_BLOCKED_DMMA_512 ? 16 : 8;
+    const size_t with_v = bdmma::smem_bytes(bm, bn, need_v != 0, nwarp);
+    const size_t without_v = bdmma::smem_bytes(bm, bn, false, nwarp);
+    const bool v_global = kv == KV_BLOCKED_DMMA_VG;
     if (need_v && !v_global && with_v <= smem_limit) {
         p.resident = 3;
         p.smem = with_v;
@@ -469,23 +480,31 @@ Plan plan_blocked_dmma(int dtype, int bm, int bn, int nb, int need_v, bool conti
     } else {
         return p;
     }
-    p.kernel = v_global ? KV_BLOCKED_DMMA_VG : KV_BLOCKED_DMMA;
-    p.threads = bdmma::NT;
+    p.kernel = kv;
+    p.threads = nwarp * 32;
     return p;
+}
+
+template <int NT, int MINB>
+static int launch_bd(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
+    auto k = bdmma::k_blocked_dmma<NT, MINB>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    // the occupancy of this kernel is shared-memory bound: ask for the largest carveout
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    k<<<a.batch, NT, p.smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 
 int launch_blocked_dmma(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
     a.resident = p.resident;
     a.kernel = p.kernel;
     a.work_stride = (int64_t)p.work_elems;
-    if (cudaFuncSetAttribute(bdmma::k_blocked_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) !=
-        cudaSuccess)
-        return BSVD_ERR_CUDA;
-    // the occupancy of this kernel is shared-memory bound: ask for the largest carveout
-    cudaFuncSetAttribute(bdmma::k_blocked_dmma, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    bdmma::k_blocked_dmma<<<a.batch, bdmma::NT, p.smem, st>>>(a);
-    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+    switch (p.kernel) {
+        case KV_BLOCKED_DMMA_VG: return launch_bd<256, 3>(a, p, st);
+        case KV_BLOCKED_DMMA_512: return launch_bd<512, 1>(a, p, st);
+        default: return launch_bd<256, 2>(a, p, st);
+    }
 }
 
 }  // namespace bsvd

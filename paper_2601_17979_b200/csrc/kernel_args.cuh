@@ -46,7 +46,8 @@ enum {
     KV_UNBLOCKED_REG32_R3 = 6,  // same, 227 regs, 9 warps/SM
     KV_UNBLOCKED_REG32_F2 = 7,  // 168 regs, two-FMA rotation update (opt-in)
     KV_BLOCKED_DMMA = 8,        // blocked FP64, nb = 16, Gram/update on DMMA tensor cores
-    KV_BLOCKED_DMMA_VG = 9,     // same, V kept in global memory (L2) for occupancy
+    KV_BLOCKED_DMMA_VG = 9,     // same, V kept in global memory (L2), 3 CTAs/SM
+    KV_BLOCKED_DMMA_512 = 10,   // same, 512-thread CTAs (16 warps) for one-CTA-per-SM sizes
 };
 
 template <class T>
