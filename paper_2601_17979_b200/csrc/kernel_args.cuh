@@ -48,6 +48,7 @@ enum {
     KV_BLOCKED_DMMA = 8,        // blocked FP64, nb = 16, Gram/update on DMMA tensor cores
     KV_BLOCKED_DMMA_VG = 9,     // same, V kept in global memory (L2), 3 CTAs/SM
     KV_BLOCKED_DMMA_512 = 10,   // same, 512-thread CTAs (16 warps) for one-CTA-per-SM sizes
+    KV_UNBLOCKED_REG16F = 11,   // 16x16 FP32 register-resident, 4 problems per warp
 };
 
 template <class T>

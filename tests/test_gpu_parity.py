@@ -50,7 +50,7 @@ def test_golden_cases(golden):
 
 
 @pytest.mark.parametrize("dt", ALL_DTYPES)
-@pytest.mark.parametrize("shape", [(8, 8), (20, 12), (32, 32), (33, 17), (5, 3), (2, 2), (6, 1), (3, 11),
+@pytest.mark.parametrize("shape", [(8, 8), (16, 16), (20, 12), (32, 32), (33, 17), (5, 3), (2, 2), (6, 1), (3, 11),
                                    (64, 64), (80, 40), (40, 96), (48, 33)])
 def test_random_batches_vs_oracle(dt, shape):
     m, n = shape
@@ -284,3 +284,27 @@ def test_c1_kernel_variants_agree(kernel):
         _, s_ref, _, oi = O.solve(A[b], None, None)
         check_sigma_parity(S[b], s_ref, 32, 2.0 ** -53, c=4.0 if kernel == 7 else 2.0)
         check_factors(A[b], U[b], S[b], V[b])
+
+
+@pytest.mark.parametrize("want_v", [True, False])
+def test_c2_fp32_register_kernel(want_v):
+    """BASELINE C2 shape (16x16 FP32, values-only and full) through the FP32 register kernel."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    B = 203  # not a multiple of the 16 problems per CTA
+    A = np.stack([random_matrix(16, 16, np.float32, seed=800 + b) for b in range(B)])
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, 16, 16, bs.JacobiOptions(compute_right_vectors=want_v))
+    torch.cuda.synchronize()
+    info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (info["kernel"] == 11).all() and info["converged"].all()
+    U, S = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy()
+    V = np.swapaxes(r.v.cpu().numpy(), 1, 2) if want_v else None
+    u = 2.0 ** -24
+    for b in range(0, B, 7):
+        _, s_ref, _, oi = O.solve(A[b], Opts(compute_right_vectors=want_v), None)
+        check_sigma_parity(S[b], s_ref, 16, u)
+        check_factors(A[b], U[b], S[b], V[b] if want_v else None)
+        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 2
