@@ -61,6 +61,15 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         if (p.kernel) return p;
         if (o->kernel != 0) return p;
     }
+    if (is_reg32e(o->kernel)) return plan_unblocked_reg32e(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
+    if (is_reg32b(o->kernel)) {
+        Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
+        return p;  // forced variant unavailable => kernel 0 => unsupported
+    }
+    if (o->kernel == 0) {  // default for 32x32 FP64: the second-generation register kernel
+        Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, 0);
+        if (p.kernel) return p;
+    }
     if (o->kernel == 0 || (o->kernel >= KV_UNBLOCKED_REG32 && o->kernel <= KV_UNBLOCKED_REG32_F2)) {
         Plan p = plan_unblocked_reg(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
         if (p.kernel) return p;
@@ -130,6 +139,19 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_BLOCKED_DMMA_VG:
         case KV_BLOCKED_DMMA_512:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_blocked_dmma(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
+        case KV_UNBLOCKED_REG32B:
+        case KV_UNBLOCKED_REG32B + 1:
+        case KV_UNBLOCKED_REG32B + 2:
+        case KV_UNBLOCKED_REG32B + 3:
+        case KV_UNBLOCKED_REG32B_LAST:
+            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32b(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
+        case KV_UNBLOCKED_REG32E:
+        case KV_UNBLOCKED_REG32E + 1:
+        case KV_UNBLOCKED_REG32E + 2:
+        case KV_UNBLOCKED_REG32E_LAST:
+            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32e(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG32:
         case KV_UNBLOCKED_REG32_O3:

@@ -30,6 +30,12 @@ int launch_unblocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
 template <class T>
 int launch_blocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
 int launch_unblocked_reg_d32(SolveArgs<double> a, const Plan& p, cudaStream_t st);
+bool is_reg32b(int kv);
+Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
+int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st);
+bool is_reg32e(int kv);
+Plan plan_unblocked_reg32e(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
+int launch_unblocked_reg32e(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 Plan plan_unblocked_reg16(int dtype, int bm, int bn, int need_v, bool lda_ok);
 int launch_unblocked_reg16(SolveArgs<float> a, const Plan& p, cudaStream_t st);
 

@@ -1,0 +1,558 @@
+// unblocked_reg32b.cu -- kernel (2), second-generation register-resident
+// 32x32 FP64 path (the north-star C1 shape).
+//
+// Same iteration as onesided_sweeps (src/_kernels_numba.py:85-138) on the
+// reference's round-robin schedule (src/ordering.py:32-75), re-organised for
+// FP64-pipe throughput.  Layout is that of unblocked_reg.cu (a warp owns two
+// problems; half-warp h owns problem h; lane hl holds rows hl and hl + 16 of
+// all 32 columns in registers; the 16 pairs of an iteration sit in fixed
+// register slots), with four changes:
+//
+//  * U-fold unrolled ring.  The tournament moves every column one ring
+//    position per iteration.  Unrolling U iterations makes the slot of each
+//    pair a compile-time function of the offset inside the group, so the
+//    registers move once per group (by pi^U, one 31-cycle = 32 moves) instead
+//    of once per iteration.
+//  * Maintained column norms.  g_ii and g_jj are carried per column (in
+//    shared memory, indexed by column id) and updated exactly like the
+//    reference's two-sided eigen-update d_i += t|g|, d_j -= t|g|
+//    (src/_kernels_numba.py:60-62); only g_ji is a fresh dot product.  The
+//    norms are recomputed from the data in the first iteration of every sweep
+//    and in any iteration that follows a >4x shrink of a norm (cancellation
+//    guard, as LAPACK xGESVJ does).  A quiet sweep therefore decides
+//    convergence on freshly computed norms, like the reference.
+//  * Two-FMA rotation update x' = fma(cm1, x, fma(ws, y, x)): c - 1 is still
+//    carried separately (F5), one FP64 instruction per flop of the update.
+//  * Short-latency rotation parameters (rotation_half, rotation.cuh).
+//
+// Deviations are numerical only (same schedule, same guard, same rotation
+// formula up to rounding); tools/acc_cmp.py and tests/test_gpu_parity.py hold
+// the kernel to the parity contract.  V is replayed from a per-sweep rotation
+// log exactly as in unblocked_reg.cu; finalize.cu forms sigma, U, the order.
+#include "kernel_args.cuh"
+#include "launch.h"
+#include "rotation.cuh"
+
+namespace bsvd {
+namespace r32b {
+
+constexpr int N = 32;      // columns
+constexpr int H = 16;      // column pairs per iteration
+constexpr int NIT = 31;    // iterations per sweep (ring length)
+constexpr int RSTR = 34;   // doubles per row of the dot-product transpose buffer (bank padding)
+constexpr int LOG_ELEMS = NIT * H * 2 + 32;  // doubles per problem: rotation log (31 x 16 Par) + masks
+
+__host__ __device__ constexpr int ring_slot(int q) {  // ring position -> register slot at t = 0
+    return q == 0 ? 1 : (q <= H - 1 ? 2 * q : 2 * (2 * H - 1 - q) + 1);
+}
+__host__ __device__ constexpr int md(int a) { return ((a % NIT) + NIT) % NIT; }
+// register slot of pair k's top / bottom column at offset u inside an unrolled group
+__host__ __device__ constexpr int TS(int k, int u) { return k == 0 ? 0 : ring_slot(md(k - u)); }
+__host__ __device__ constexpr int BS(int k, int u) { return ring_slot(md((k == 0 ? 0 : NIT - k) - u)); }
+
+struct __align__(16) Par {
+    double cm1, c;  // x <- x + (cm1 x + c y);  y <- y + (cm1 y - c x)
+};
+
+struct WarpSmem {
+    double red[3 * H * RSTR];  // dot-product transpose
+    Par pub[2][H];             // this iteration's rotations, [half][pair]
+    Par stage[2][2][H];        // V replay: double-buffered log rows [buf][half][pair]
+    double nrm[2][N];          // maintained squared column norms [half][column]
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
+}
+
+// move every column SH ring positions forward (compile-time register moves)
+template <int SH>
+__device__ __forceinline__ void ring_shift(double (&x)[N]) {
+    if constexpr (md(SH) != 0) {
+        double y[NIT];
+#pragma unroll
+        for (int q = 0; q < NIT; ++q) y[q] = x[ring_slot(q)];
+#pragma unroll
+        for (int q = 0; q < NIT; ++q) x[ring_slot(q)] = y[md(q - SH)];
+    }
+}
+
+__device__ __forceinline__ void apply2(double& x, double& y, double cm1, double c) {
+    const double tx = fma(c, y, x);
+    const double ty = fma(-c, x, y);
+    x = fma(cm1, x, tx);
+    y = fma(cm1, y, ty);
+}
+
+__device__ __forceinline__ double sum16(const double* p) {  // 16 consecutive doubles, fixed tree
+    const double2* r = reinterpret_cast<const double2*>(p);
+    const double2 p0 = r[0], p1 = r[1], p2 = r[2], p3 = r[3], p4 = r[4], p5 = r[5], p6 = r[6], p7 = r[7];
+    const double s0 = (p0.x + p0.y) + (p1.x + p1.y), s1 = (p2.x + p2.y) + (p3.x + p3.y);
+    const double s2 = (p4.x + p4.y) + (p5.x + p5.y), s3 = (p6.x + p6.y) + (p7.x + p7.y);
+    return (s0 + s1) + (s2 + s3);
+}
+
+// partial dot products of this lane's two rows for the 16 pairs at offset u
+template <int u, bool FULL>
+__device__ __forceinline__ void partials(const double (&x0)[N], const double (&x1)[N], double* red, int lane) {
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+        const double a0 = x0[TS(k, u)], b0 = x0[BS(k, u)], a1 = x1[TS(k, u)], b1 = x1[BS(k, u)];
+        if constexpr (FULL) {
+            red[(3 * k + 0) * RSTR + lane] = fma(a1, a1, a0 * a0);
+            red[(3 * k + 1) * RSTR + lane] = fma(b1, b1, b0 * b0);
+            red[(3 * k + 2) * RSTR + lane] = fma(b1, a1, b0 * a0);
+        } else {
+            red[k * RSTR + lane] = fma(b1, a1, b0 * a0);
+        }
+    }
+}
+
+// Development probes (tools/microbench/wchain.cu defines R32_PROBE_ON): clock
+// deltas between stage boundaries of the W iteration, warp 0 of block 0.
+#ifdef R32_PROBE_ON
+__device__ unsigned long long g_r32_probe[8];
+#define R32P(i, v) r32_probe(i, v, st)
+#else
+#define R32P(i, v)
+#endif
+
+struct IterState {
+    long long tl;       // last probe clock (R32_PROBE_ON only)
+    int my_rot;         // rotations of this lane's pair in the sweep
+    uint32_t itbits;    // bit t: some pair of either problem rotated in iteration t
+    bool full;          // this iteration recomputes the norms from the data
+};
+
+#ifdef R32_PROBE_ON
+__device__ __forceinline__ void r32_probe(int i, double v, IterState& st) {
+    long long c;
+    asm volatile("mov.u64 %0, %%clock64; // %1" : "=l"(c) : "d"(v) : "memory");
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        if (i > 0) atomicAdd(&g_r32_probe[i], (unsigned long long)(c - st.tl));
+        else atomicAdd(&g_r32_probe[0], 1ull);
+    }
+    st.tl = c;
+}
+#endif
+
+// Column ids of pair k at iteration t, packed ct | cb << 8 | flip << 16
+// (built once per CTA in shared memory; reference orientation i < j).
+__host__ __device__ inline uint32_t pair_code(int t, int k) {
+    int qt = k - t, qb = (k == 0 ? 0 : NIT - k) - t;
+    qt += qt < 0 ? NIT : 0;
+    qb += qb < 0 ? NIT : 0;
+    const int ct = (k == 0) ? 0 : ring_slot(qt);
+    const int cb = ring_slot(qb);
+    return (uint32_t)ct | ((uint32_t)cb << 8) | ((ct > cb) ? (1u << 16) : 0u);
+}
+
+__device__ __forceinline__ double xor_sign(double x, bool neg) {
+    return __longlong_as_double(__double_as_longlong(x) ^ ((long long)neg << 63));
+}
+
+// |d|, g -> s = sin(th) >= 0, c - 1, |t| (rotation_half without the signs).
+// Fast path without rescaling (the data are pre-scaled to max |a| in
+// [0.5, 1), so d^2 + 4 g^2 only underflows for pairs of columns below
+// 2^-250); the exact rescale is a rare fix-up after the fact.
+__device__ __forceinline__ void rot_abs_core(double dabs, double g, double& s, double& cm1, double& tabs) {
+    const double q = fma(4.0 * g, g, dabs * dabs);
+    const double ir = rsqrt_cubic(q);
+    const double gi = g * ir;
+    const double c2 = fma(0.5 * dabs, ir, 0.5);
+    const double ic = rsqrt_cubic(c2);
+    const double c = c2 * ic;
+    s = gi * ic;
+    cm1 = -(s * s) * rcp_cubic(1.0 + c);
+    tabs = s * ic;
+}
+__device__ __forceinline__ void rot_abs(double dabs, double g, double& s, double& cm1, double& tabs) {
+    rot_abs_core(dabs, g, s, cm1, tabs);
+    if (fmax(dabs, g) < 0x1p-500) rot_abs_core(dabs * 0x1p+600, g * 0x1p+600, s, cm1, tabs);
+}
+
+// g_ji partial product of next pair k (offset u) from this lane's two rows
+template <int u>
+__device__ __forceinline__ void cross_partial(const double (&x0)[N], const double (&x1)[N], double* red, int lane,
+                                              int k) {
+    red[k * RSTR + lane] = fma(x1[BS(k, u)], x1[TS(k, u)], x0[BS(k, u)] * x0[TS(k, u)]);
+}
+// squared-norm partials of next pairs' top / bottom columns (full iterations), rows H + 2k, H + 2k + 1
+template <int u>
+__device__ __forceinline__ void norm_partials(const double (&x0)[N], const double (&x1)[N], double* red, int lane) {
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+        const double a0 = x0[TS(k, u)], b0 = x0[BS(k, u)], a1 = x1[TS(k, u)], b1 = x1[BS(k, u)];
+        red[(H + 2 * k) * RSTR + lane] = fma(a1, a1, a0 * a0);
+        red[(H + 2 * k + 1) * RSTR + lane] = fma(b1, b1, b0 * b0);
+    }
+}
+// partials of the iteration at offset u (sweep start: always full)
+template <int u>
+__device__ __forceinline__ void all_partials(const double (&x0)[N], const double (&x1)[N], double* red, int lane,
+                                             bool full) {
+#pragma unroll
+    for (int k = 0; k < H; ++k) cross_partial<u>(x0, x1, red, lane, k);
+    if (full) norm_partials<u>(x0, x1, red, lane);
+}
+
+// One W iteration at offset u of the unrolled group; t = global iteration
+// (0..30).  On entry red[] holds this iteration's partial products; the
+// update is fused with the partials of iteration t + 1 (offset u + 1 in the
+// pre-shift register naming: next pair k = columns of this iteration's pairs
+// k - 1 and k + 1), so they are ready when the next reduction starts.
+template <int u>
+__device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab, int t,
+                                       int lane, int half, int hl, bool done, double tol, double tol2,
+                                       Par* logl, IterState& st) {
+    R32P(0, x0[TS(0, u)]);
+    const uint32_t code = ctab[t * H + hl];
+    __syncwarp();
+    // ---- lane hl owns pair k = hl of its half's problem ----
+    const int k = hl;
+    const int ct = code & 0xff, cb = (code >> 8) & 0xff;
+    const bool flip = (code >> 16) != 0;
+    double gt, gb;
+    if (st.full) {
+        gt = sum16(sm.red + (H + 2 * k) * RSTR + 16 * half);
+        gb = sum16(sm.red + (H + 2 * k + 1) * RSTR + 16 * half);
+    } else {
+        gt = sm.nrm[half][ct];
+        gb = sm.nrm[half][cb];
+    }
+    const double g = sum16(sm.red + k * RSTR + 16 * half);
+    const double absg = fabs(g);
+    R32P(1, g);
+    // guard (F4): rotate unless |g| <= 0 or |g| < tol sqrt(gii gjj); squared
+    // comparison, exact-sqrt fallback where g^2 could underflow
+    const double p = gt * gb;
+    bool rot = !(absg * absg < tol2 * p);
+    if (absg < 0x1p-400 && absg > 0.0) rot = !(absg < tol * fsqrt(p));
+    rot = rot && !done && absg > 0.0;
+    const double d = gt - gb;
+    double s, cm1, tabs;
+    rot_abs(fabs(d), absg, s, cm1, tabs);
+    // sign of tau in slot orientation: sgn(d), and for d == 0 the reference's
+    // sgn(0) = +1 taken in (i, j) orientation
+    const bool eneg = d < 0.0 || (d == 0.0 && flip);
+    Par par;
+    par.cm1 = rot ? cm1 : 0.0;
+    par.c = rot ? xor_sign(s, (g < 0.0) != eneg) : 0.0;  // x = top slot, y = bot slot
+    R32P(2, par.cm1);
+    sm.pub[half][k] = par;
+    const unsigned mask = __ballot_sync(0xffffffffu, rot);
+    if (logl) logl[t * H] = par;
+    __syncwarp();
+    R32P(6, sm.pub[half][0].c);
+    const double dtg = rot ? xor_sign(tabs * absg, eneg) : 0.0;
+    const double nt = gt + dtg, nb = gb - dtg;
+    sm.nrm[half][ct] = nt;
+    sm.nrm[half][cb] = nb;
+    const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
+    st.my_rot += rot ? 1 : 0;
+    st.full = __ballot_sync(0xffffffffu, shrink) != 0u;
+    st.itbits |= (mask != 0u ? 1u : 0u) << t;
+    constexpr int un = u + 1;  // offset of iteration t + 1 (pre-shift naming)
+    if (mask) {
+        Par pq[H];  // all rotations first: the loop below interleaves stores to red[]
+#pragma unroll
+        for (int q = 0; q < H; ++q) pq[q] = sm.pub[half][q];
+        apply2(x0[TS(0, u)], x0[BS(0, u)], pq[0].cm1, pq[0].c);
+        apply2(x1[TS(0, u)], x1[BS(0, u)], pq[0].cm1, pq[0].c);
+#pragma unroll
+        for (int q = 1; q < H; ++q) {
+            apply2(x0[TS(q, u)], x0[BS(q, u)], pq[q].cm1, pq[q].c);
+            apply2(x1[TS(q, u)], x1[BS(q, u)], pq[q].cm1, pq[q].c);
+            cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs this iteration's pairs q - 2 and q
+        }
+        cross_partial<un>(x0, x1, sm.red, lane, H - 1);
+    } else {
+#pragma unroll
+        for (int q = 0; q < H; ++q) cross_partial<un>(x0, x1, sm.red, lane, q);
+    }
+    if (st.full) norm_partials<un>(x0, x1, sm.red, lane);
+    R32P(3, x1[BS(H - 1, u)]);
+}
+
+// One V replay iteration at offset u (log row t is staged in sm.stage[t & 1]).
+template <int u>
+__device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int t, int half, int hl,
+                                       const Par* logl, uint32_t itbits) {
+    if (t + 1 < NIT) cp_async16(&sm.stage[(t + 1) & 1][half][hl], logl + (t + 1) * H);
+    cp_commit();
+    cp_wait<1>();
+    __syncwarp();
+    if ((itbits >> t) & 1u) {
+        const Par* stp = sm.stage[t & 1][half];
+        Par pr[H];  // all rotations first, then 128 independent FMAs
+#pragma unroll
+        for (int q = 0; q < H; ++q) pr[q] = stp[q];
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            const Par pq = pr[q];
+            apply2(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
+            apply2(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
+        }
+    }
+    __syncwarp();
+}
+
+template <int U>
+__device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab,
+                                        int lane, int half, int hl, bool done, double tol, double tol2, Par* logl,
+                                        IterState& st) {
+    constexpr int NG = (NIT + U - 1) / U;
+    constexpr int R = NIT - (NG - 1) * U;  // iterations in the last group
+    all_partials<0>(x0, x1, sm.red, lane, true);  // first iteration of a sweep: fresh norms
+#pragma unroll 1
+    for (int gi = 0; gi < NG; ++gi) {
+        const int t0 = gi * U;
+        const bool last = gi == NG - 1;
+        w_iter<0>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
+        if constexpr (U >= 2) {
+            if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
+            w_iter<1 % U>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
+        }
+        if constexpr (U >= 3) {
+            if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
+            w_iter<2 % U>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
+        }
+        if constexpr (U >= 4) {
+            if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
+            w_iter<3 % U>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
+        }
+        ring_shift<U>(x0);
+        ring_shift<U>(x1);
+    }
+}
+
+template <int U>
+__device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int half, int hl,
+                                        const Par* logl, uint32_t itbits) {
+    constexpr int NG = (NIT + U - 1) / U;
+    constexpr int R = NIT - (NG - 1) * U;
+#pragma unroll 1
+    for (int gi = 0; gi < NG; ++gi) {
+        const int t0 = gi * U;
+        const bool last = gi == NG - 1;
+        v_iter<0>(x0, x1, sm, t0, half, hl, logl, itbits);
+        if constexpr (U >= 2) {
+            if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
+            v_iter<1 % U>(x0, x1, sm, t0 + 1, half, hl, logl, itbits);
+        }
+        if constexpr (U >= 3) {
+            if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
+            v_iter<2 % U>(x0, x1, sm, t0 + 2, half, hl, logl, itbits);
+        }
+        if constexpr (U >= 4) {
+            if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
+            v_iter<3 % U>(x0, x1, sm, t0 + 3, half, hl, logl, itbits);
+        }
+        ring_shift<U>(x0);
+        ring_shift<U>(x1);
+    }
+}
+
+template <int NW, int MINB, int U, int UV = U>
+__global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
+    const int half = lane >> 4, hl = lane & 15;
+    const int prob = (blockIdx.x * NW + warp) * 2 + half;
+    const bool live = prob < a.batch;
+    const int r0 = hl, r1 = hl + 16;
+    const size_t pstride = (size_t)a.work_stride;
+    double* wsW = a.work + (size_t)(live ? prob : 0) * pstride;  // W 32x32, V 32x32, then the log
+    double* wsV = wsW + N * N;
+    Par* logp = reinterpret_cast<Par*>(wsW + 2 * N * N);           // [31][16]
+    const bool want_v = a.need_v != 0;
+    // this lane's column of the rotation log; a dead half never writes (it
+    // aliases problem 0's workspace) but may read
+    Par* logl = want_v ? logp + hl : nullptr;
+    Par* logw = live ? logl : nullptr;
+    uint32_t* ctab = reinterpret_cast<uint32_t*>(smem_raw + NW * sizeof(WarpSmem));
+    for (int e = threadIdx.x; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
+    __syncthreads();
+
+    double x0[N], x1[N];
+    int bad = 0;
+    double amax = 0.0;
+    {
+        const double* Ap = a.A + (size_t)(live ? prob : 0) * a.strideA;  // plan requires lda == 32
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            x0[c] = live ? Ap[r0 + c * N] : 0.0;
+            x1[c] = live ? Ap[r1 + c * N] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            bad |= !isfinite(x0[c]) | !isfinite(x1[c]);
+            amax = fmax(amax, fmax(fabs(x0[c]), fabs(x1[c])));
+        }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const int ex = prescale_exponent(amax);
+    {
+        const double scale = pow2(-ex);
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            x0[c] *= scale;
+            x1[c] *= scale;
+        }
+    }
+    const double tol = a.tol, tol2 = a.tol * a.tol;
+    int sweeps = 0, last = 0, done = live ? 0 : 1;
+    long long rot_total = 0;
+    bool v_started = false;  // V still identity until the first replay
+
+#pragma unroll 1
+    for (int sw = 0; sw < a.max_sweeps; ++sw) {
+        IterState st;
+        st.my_rot = 0;
+        st.itbits = 0;
+        st.full = true;  // fresh norms at the start of every sweep
+        w_sweep<U>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, logw, st);
+        // ---- sweep end: per-problem rotation count over the half warp ----
+        int tot = st.my_rot;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (!done) {
+            sweeps = sw + 1;
+            last = tot;
+            rot_total += tot;
+            if (tot == 0) done = 1;
+        }
+        const int partner_done = __shfl_xor_sync(0xffffffffu, done, 16);
+        const bool both_done = done && partner_done;
+        // ======================= V phase: replay the sweep =======================
+        if (want_v && st.itbits) {
+            if (live) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {  // park W
+                    wsW[r0 + c * N] = x0[c];
+                    wsW[r1 + c * N] = x1[c];
+                }
+            }
+            if (v_started) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    x0[c] = wsV[r0 + c * N];
+                    x1[c] = wsV[r1 + c * N];
+                }
+            } else {  // V = I before the first replay
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    x0[c] = (c == r0) ? 1.0 : 0.0;
+                    x1[c] = (c == r1) ? 1.0 : 0.0;
+                }
+                v_started = true;
+            }
+            __syncwarp();  // this warp's log writes are visible to all its lanes
+            cp_async16(&sm.stage[0][half][hl], logl);
+            cp_commit();
+            v_sweep<UV>(x0, x1, sm, half, hl, logl, st.itbits);
+            cp_wait<0>();
+            if (live) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {  // park V
+                    wsV[r0 + c * N] = x0[c];
+                    wsV[r1 + c * N] = x1[c];
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                x0[c] = wsW[r0 + c * N];
+                x1[c] = wsW[r1 + c * N];
+            }
+        }
+        if (both_done) break;
+    }
+    if (live) {
+        const double unscale = pow2(ex);
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            wsW[r0 + c * N] = x0[c] * unscale;
+            wsW[r1 + c * N] = x1[c] * unscale;
+        }
+        if (want_v && !v_started) {
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                wsV[r0 + c * N] = (c == r0) ? 1.0 : 0.0;
+                wsV[r1 + c * N] = (c == r1) ? 1.0 : 0.0;
+            }
+        }
+    }
+    const unsigned badm = __ballot_sync(0xffffffffu, bad != 0);
+    if (live && hl == 0 && a.info) {
+        bsvd_info inf;
+        inf.converged = done;
+        inf.outer_sweeps = sweeps;
+        inf.rotations = rot_total;
+        inf.gram_calls = 0;
+        inf.update_calls = 0;
+        inf.last_rotations = last;
+        inf.path = 1;
+        inf.status = ((badm >> (16 * half)) & 0xFFFFu) ? 1 : 0;
+        inf.kernel = a.kernel;
+        a.info[prob] = inf;
+    }
+}
+
+}  // namespace r32b
+
+// variants: (warps per CTA, min CTAs per SM, unroll, per-pair skip)
+bool is_reg32b(int kv) { return kv >= KV_UNBLOCKED_REG32B && kv <= KV_UNBLOCKED_REG32B_LAST; }
+
+Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant) {
+    Plan p{};
+    if (dtype == BSVD_D && bm == 32 && bn == 32 && lda_ok) {
+        p.kernel = is_reg32b(variant) ? variant : KV_UNBLOCKED_REG32B;
+        p.threads = 128;
+        p.smem = 4 * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
+        p.work_elems = 2 * 32 * 32 + r32b::LOG_ELEMS;
+        p.grid = 0;
+        p.resident = 0;
+        (void)need_v;
+    }
+    return p;
+}
+
+template <int NW, int MINB, int U, int UV = U>
+static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
+    const int per_cta = 2 * NW;
+    const int grid = (a.batch + per_cta - 1) / per_cta;
+    const size_t smem = NW * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
+    auto k = r32b::k_reg32b<NW, MINB, U, UV>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<grid, NW * 32, smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
+    a.kernel = p.kernel;
+    a.work_stride = (int64_t)p.work_elems;
+    int rc;
+    switch (p.kernel) {
+        case KV_UNBLOCKED_REG32B + 1: rc = launch_r32b<4, 3, 2, 2>(a, st); break;  // 168 regs, 12 warps/SM
+        case KV_UNBLOCKED_REG32B + 2: rc = launch_r32b<4, 2, 2, 4>(a, st); break;  // V unroll 4
+        case KV_UNBLOCKED_REG32B + 3: rc = launch_r32b<1, 11, 2, 2>(a, st); break; // one-warp CTAs
+        case KV_UNBLOCKED_REG32B + 4: rc = launch_r32b<4, 3, 2, 4>(a, st); break;
+        default: rc = launch_r32b<4, 2, 2, 2>(a, st); break;                       // 255 regs, 8 warps/SM
+    }
+    if (rc) return rc;
+    return launch_finalize_ws<double>(a, st);
+}
+
+}  // namespace bsvd

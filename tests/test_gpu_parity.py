@@ -265,7 +265,7 @@ def test_reg32_partial_ctas(batch):
         check_factors(a, r.u, r.sigma, r.v)
 
 
-@pytest.mark.parametrize("kernel", [1, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("kernel", [1, 3, 4, 5, 6, 7, 12, 13, 14, 15, 16, 26, 27, 28, 29])
 def test_c1_kernel_variants_agree(kernel):
     """Every 32x32 FP64 kernel variant meets the parity contract on the same inputs."""
     import torch

@@ -113,7 +113,7 @@ def test_kernel_selection_routes():
     assert L.bsvd_select_kernel(1, 64, 64, ctypes.byref(o)) in (8, 9, 10)  # blocked FP64 on DMMA (n > 32)
     assert L.bsvd_select_kernel(3, 64, 64, ctypes.byref(o)) == 2      # blocked complex: general kernel
     assert L.bsvd_select_kernel(0, 16, 16, ctypes.byref(o)) == 11     # 16x16 FP32 register kernel
-    assert L.bsvd_select_kernel(1, 32, 32, ctypes.byref(o)) == 3      # 32x32 FP64 register kernel
+    assert L.bsvd_select_kernel(1, 32, 32, ctypes.byref(o)) == 12     # 32x32 FP64 register kernel (2nd gen)
     assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) in (1, 3)  # unblocked route
     assert L.bsvd_select_kernel(1, 0, 5, ctypes.byref(o)) == 0        # empty
 
