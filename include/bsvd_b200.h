@@ -97,6 +97,29 @@ int bsvd_gesvj_batched(int dtype, int m, int n, int batch,
                        const bsvd_opts* opts, bsvd_info* info,
                        void* work, size_t work_bytes, void* stream);
 
+/*
+ * Host-buffer variant: the same solve with A, U, S, V and info in HOST memory
+ * (pinned for full PCIe bandwidth; dense packing required: lda = m,
+ * strideA = m*n, ldu = m, strideU = m*k, strideS = k, ldv = n, strideV = n*k).
+ * The batch is cut into chunks of `chunk` problems that are pipelined over
+ * the caller's `nstreams` streams (H2D of one chunk, the solve of another and
+ * the D2H of a third overlap); work is ordered after prior work on
+ * streams[0], and streams[0] is ordered after all of it on return, so the call
+ * behaves like one stream-ordered operation on streams[0].  `work` is DEVICE
+ * scratch of bsvd_host_workspace_bytes(...) bytes (staging for nstreams
+ * chunks plus their solver workspace).  Asynchronous: synchronise streams[0]
+ * before reading the outputs.  Replaces the reference's per-problem host loop
+ * batch_svd -> _ProblemRun (src/batch.py:85-157) for host-resident batches.
+ */
+int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch,
+                            const void* A, void* U, void* S, void* V,
+                            const bsvd_opts* opts, bsvd_info* info,
+                            int chunk, void* work, size_t work_bytes,
+                            void* const* streams, int nstreams);
+
+/* Device scratch needed by bsvd_gesvj_batched_host for (chunk, nstreams). */
+size_t bsvd_host_workspace_bytes(int dtype, int m, int n, int chunk, int nstreams, const bsvd_opts* opts);
+
 /* Device scratch needed by bsvd_gesvj_batched for this problem class. */
 size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts* opts);
 

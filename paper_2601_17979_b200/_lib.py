@@ -52,7 +52,9 @@ INFO_BYTES = ctypes.sizeof(BsvdInfo)
 # exported symbols, one per declaration in include/bsvd_b200.h
 EXPORTS = (
     "bsvd_gesvj_batched",
+    "bsvd_gesvj_batched_host",
     "bsvd_workspace_bytes",
+    "bsvd_host_workspace_bytes",
     "bsvd_select_kernel",
     "bsvd_default_opts",
     "bsvd_strerror",
@@ -81,6 +83,11 @@ def load():
     L.bsvd_gesvj_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, vp, i64, i64, vp, i64, vp, i64, i64,
                                      popts, vp, vp, sz, vp]
     L.bsvd_gesvj_batched.restype = ci
+    L.bsvd_gesvj_batched_host.argtypes = [ci, ci, ci, ci, vp, vp, vp, vp, popts, vp, ci, vp, sz,
+                                          ctypes.POINTER(vp), ci]
+    L.bsvd_gesvj_batched_host.restype = ci
+    L.bsvd_host_workspace_bytes.argtypes = [ci, ci, ci, ci, ci, popts]
+    L.bsvd_host_workspace_bytes.restype = sz
     L.bsvd_workspace_bytes.argtypes = [ci, ci, ci, ci, popts]
     L.bsvd_workspace_bytes.restype = sz
     L.bsvd_select_kernel.argtypes = [ci, ci, ci, popts]

@@ -204,6 +204,98 @@ int bsvd_select_kernel(int dtype, int m, int n, const bsvd_opts* opts) {
     return make_plan(dtype, r, opts).kernel;
 }
 
+namespace {
+// Staging layout of one pipeline slot (device): A | U | V | S | info | solver workspace.
+struct HostSlot {
+    size_t a, u, v, s, info, ws, total;
+};
+HostSlot host_slot(int dtype, int m, int n, int chunk, const bsvd_opts* o) {
+    const size_t es = (size_t)esize_of(dtype), rs = (size_t)rsize_of(dtype);
+    const size_t k = (size_t)(m < n ? m : n);
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    HostSlot h{};
+    h.a = al((size_t)chunk * m * n * es);
+    h.u = al((size_t)chunk * m * k * es);
+    h.v = o->want_v ? al((size_t)chunk * n * k * es) : 0;
+    h.s = al((size_t)chunk * k * rs);
+    h.info = al((size_t)chunk * sizeof(bsvd_info));
+    h.ws = al(bsvd_workspace_bytes(dtype, m, n, chunk, o));
+    h.total = h.a + h.u + h.v + h.s + h.info + h.ws;
+    return h;
+}
+}  // namespace
+
+size_t bsvd_host_workspace_bytes(int dtype, int m, int n, int chunk, int nstreams, const bsvd_opts* opts) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || chunk < 1 || nstreams < 1 || check_opts(opts)) return 0;
+    return host_slot(dtype, m, n, chunk, opts).total * (size_t)nstreams;
+}
+
+int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch, const void* A, void* U, void* S, void* V,
+                            const bsvd_opts* opts, bsvd_info* info, int chunk, void* work, size_t work_bytes,
+                            void* const* streams, int nstreams) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || chunk < 1 || nstreams < 1 || !streams)
+        return BSVD_ERR_ARG;
+    int rc = check_opts(opts);
+    if (rc) return rc;
+    if (batch == 0) return BSVD_OK;
+    const int k = m < n ? m : n;
+    if (k > 0 && (!A || !U || !S || (opts->want_v && !V))) return BSVD_ERR_ARG;
+    const HostSlot hs = host_slot(dtype, m, n, chunk, opts);
+    if (hs.total * (size_t)nstreams > work_bytes || !work) return BSVD_ERR_WORKSPACE;
+    const size_t es = (size_t)esize_of(dtype), rs = (size_t)rsize_of(dtype);
+    cudaStream_t s0 = static_cast<cudaStream_t>(streams[0]);
+    // fork: every stream starts after the work already queued on streams[0]
+    cudaEvent_t fork = nullptr;
+    cudaEvent_t* joins = new cudaEvent_t[nstreams]();
+    if (nstreams > 1) {
+        if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) { delete[] joins; return BSVD_ERR_CUDA; }
+        cudaEventRecord(fork, s0);
+        for (int i = 1; i < nstreams; ++i) cudaStreamWaitEvent(static_cast<cudaStream_t>(streams[i]), fork, 0);
+    }
+    rc = BSVD_OK;
+    const int nchunks = (batch + chunk - 1) / chunk;
+    for (int c = 0; c < nchunks && rc == BSVD_OK; ++c) {
+        const int slot = c % nstreams;
+        cudaStream_t st = static_cast<cudaStream_t>(streams[slot]);
+        const int b0 = c * chunk, cb = (batch - b0) < chunk ? (batch - b0) : chunk;
+        unsigned char* base = static_cast<unsigned char*>(work) + hs.total * (size_t)slot;
+        void* Ad = base;
+        void* Ud = base + hs.a;
+        void* Vd = opts->want_v ? base + hs.a + hs.u : nullptr;
+        void* Sd = base + hs.a + hs.u + hs.v;
+        bsvd_info* Id = reinterpret_cast<bsvd_info*>(base + hs.a + hs.u + hs.v + hs.s);
+        void* Wd = base + hs.a + hs.u + hs.v + hs.s + hs.info;
+        const size_t abytes = (size_t)cb * m * n * es;
+        if (abytes && cudaMemcpyAsync(Ad, static_cast<const unsigned char*>(A) + (size_t)b0 * m * n * es, abytes,
+                                      cudaMemcpyHostToDevice, st) != cudaSuccess) { rc = BSVD_ERR_CUDA; break; }
+        rc = bsvd_gesvj_batched(dtype, m, n, cb, Ad, m > 0 ? m : 1, (int64_t)m * n, Ud, m > 0 ? m : 1,
+                                (int64_t)m * k, Sd, k, Vd, n > 0 ? n : 1, (int64_t)n * k, opts, Id, Wd, hs.ws, st);
+        if (rc) break;
+        const size_t ub = (size_t)cb * m * k * es, vb = (size_t)cb * n * k * es, sb = (size_t)cb * k * rs;
+        bool ok = true;
+        if (ub) ok &= cudaMemcpyAsync(static_cast<unsigned char*>(U) + (size_t)b0 * m * k * es, Ud, ub,
+                                      cudaMemcpyDeviceToHost, st) == cudaSuccess;
+        if (sb) ok &= cudaMemcpyAsync(static_cast<unsigned char*>(S) + (size_t)b0 * k * rs, Sd, sb,
+                                      cudaMemcpyDeviceToHost, st) == cudaSuccess;
+        if (opts->want_v && vb) ok &= cudaMemcpyAsync(static_cast<unsigned char*>(V) + (size_t)b0 * n * k * es, Vd,
+                                                      vb, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+        if (info) ok &= cudaMemcpyAsync(info + b0, Id, (size_t)cb * sizeof(bsvd_info), cudaMemcpyDeviceToHost,
+                                        st) == cudaSuccess;
+        if (!ok) rc = BSVD_ERR_CUDA;
+    }
+    // join: streams[0] waits for the other streams' last chunk
+    for (int i = 1; i < nstreams; ++i) {
+        if (cudaEventCreateWithFlags(&joins[i], cudaEventDisableTiming) != cudaSuccess) { rc = BSVD_ERR_CUDA; continue; }
+        cudaEventRecord(joins[i], static_cast<cudaStream_t>(streams[i]));
+        cudaStreamWaitEvent(s0, joins[i], 0);
+    }
+    for (int i = 1; i < nstreams; ++i)
+        if (joins[i]) cudaEventDestroy(joins[i]);
+    if (fork) cudaEventDestroy(fork);
+    delete[] joins;
+    return rc;
+}
+
 size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts* opts) {
     if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || check_opts(opts)) return 0;
     Route r;

@@ -129,7 +129,9 @@ struct IterState {
     long long tl;       // last probe clock (R32_PROBE_ON only)
     int my_rot;         // rotations of this lane's pair in the sweep
     uint32_t itbits;    // bit t: some pair of either problem rotated in iteration t
-    bool full;          // this iteration recomputes the norms from the data
+    bool full;          // this iteration recomputes the norms of some problem of the warp
+    uint32_t fmask;     // ballot of the lanes whose problem takes the fresh norms (per half: a
+                        // problem's numerics never depend on the problem sharing its warp)
 };
 
 #ifdef R32_PROBE_ON
@@ -221,7 +223,7 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     const int ct = code & 0xff, cb = (code >> 8) & 0xff;
     const bool flip = (code >> 16) != 0;
     double gt, gb;
-    if (st.full) {
+    if (st.full && ((st.fmask >> lane) & 1u)) {
         gt = sum16(sm.red + (H + 2 * k) * RSTR + 16 * half);
         gb = sum16(sm.red + (H + 2 * k + 1) * RSTR + 16 * half);
     } else {
@@ -258,7 +260,11 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     sm.nrm[half][cb] = nb;
     const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
     st.my_rot += rot ? 1 : 0;
-    st.full = __ballot_sync(0xffffffffu, shrink) != 0u;
+    {  // a >4x shrink in a problem makes that problem's next iteration recompute its norms
+        const uint32_t sb = __ballot_sync(0xffffffffu, shrink);
+        st.fmask = ((sb & 0xFFFFu) ? 0xFFFFu : 0u) | ((sb >> 16) ? 0xFFFF0000u : 0u);
+        st.full = sb != 0u;
+    }
     st.itbits |= (mask != 0u ? 1u : 0u) << t;
     constexpr int un = u + 1;  // offset of iteration t + 1 (pre-shift naming)
     if (mask) {
@@ -421,6 +427,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         st.my_rot = 0;
         st.itbits = 0;
         st.full = true;  // fresh norms at the start of every sweep
+        st.fmask = 0xffffffffu;
         w_sweep<U>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, logw, st);
         // ---- sweep end: per-problem rotation count over the half warp ----
         int tot = st.my_rot;

@@ -152,7 +152,8 @@ __device__ __forceinline__ void rot_abs(double dabs, double g, double& s, double
 struct WState {
     int my_rot;     // rotations of this lane's pair in the sweep
     bool any;       // some rotation in this sweep (either problem)
-    bool full;      // this iteration recomputes the norms from the data
+    bool full;      // this iteration recomputes the norms of some problem of the pair
+    uint32_t fmask; // lanes whose problem takes the fresh norms (per half)
     uint32_t g;     // global iteration counter (ring slot / phase)
 };
 
@@ -171,8 +172,10 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], PairSme
         const double ft = sum16(sm.red + (2 * hl) * RSTR + 16 * half);
         const double fb = sum16(sm.red + (2 * hl + 1) * RSTR + 16 * half);
         const uint32_t code = ctab[t * H + hl];
-        sm.nrm[half][code & 0xff] = ft;
-        sm.nrm[half][(code >> 8) & 0xff] = fb;
+        if ((st.fmask >> lane) & 1u) {
+            sm.nrm[half][code & 0xff] = ft;
+            sm.nrm[half][(code >> 8) & 0xff] = fb;
+        }
         __syncwarp();
     }
 #pragma unroll
@@ -207,7 +210,11 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], PairSme
     const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
     st.my_rot += rot ? 1 : 0;
     const unsigned mask = __ballot_sync(0xffffffffu, rot);
-    st.full = __ballot_sync(0xffffffffu, shrink) != 0u;
+    {  // a >4x shrink in a problem makes that problem's next iteration recompute its norms
+        const uint32_t sb = __ballot_sync(0xffffffffu, shrink);
+        st.fmask = ((sb & 0xFFFFu) ? 0xFFFFu : 0u) | ((sb >> 16) ? 0xFFFF0000u : 0u);
+        st.full = sb != 0u;
+    }
     st.any |= mask != 0u;
     const uint32_t s_idx = st.g % RING;
     Slot& slot = sm.ring[s_idx];
@@ -372,6 +379,7 @@ __global__ void __launch_bounds__(2 * NP * 32, MINB) k_reg32e(SolveArgs<double> 
         st.my_rot = 0;
         st.any = false;
         st.full = true;  // fresh norms at the start of every sweep
+        st.fmask = 0xffffffffu;
         if (want_v) w_sweep<UW, true>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, st);
         else w_sweep<UW, false>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, st);
         int tot = st.my_rot;

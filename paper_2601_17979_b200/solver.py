@@ -147,11 +147,58 @@ def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: 
     return DeviceResult(u=u, s=s, v=v, info=info, kernel=int(kern))
 
 
+def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: int = _lib.DISPATCH,
+                       kernel: int = 0, chunk: int = 0, streams=None):
+    """Pipelined host-buffer solve through bsvd_gesvj_batched_host.
+
+    a_h (B, n, m), u_h (B, k, m), s_h (B, k), v_h (B, k, n) | None, info_h
+    (B * INFO_BYTES,) are CPU tensors (pinned for full PCIe bandwidth).  The
+    batch is cut into ``chunk``-problem pieces whose H2D, solve and D2H
+    overlap across ``streams`` (torch streams; default: the current stream
+    plus two side streams).  Asynchronous on streams[0]: synchronise it
+    before reading the outputs.
+    """
+    torch = _torch()
+    L = _lib.load()
+    B = a_h.shape[0]
+    dt = np_dtype_of(a_h.dtype)
+    code = DTYPE_CODE[dt]
+    o = make_opts(opts, route, kernel)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if streams is None:
+        streams = [torch.cuda.current_stream(dev)] + _side_streams(dev, 2)
+    if chunk <= 0:
+        chunk = max(1, -(-B // (2 * len(streams))))
+    ws_bytes = L.bsvd_host_workspace_bytes(code, m, n, chunk, len(streams), ctypes.byref(o))
+    ws = _workspace(ws_bytes, dev)
+    arr = (ctypes.c_void_p * len(streams))(*[st.cuda_stream for st in streams])
+    rc = L.bsvd_gesvj_batched_host(
+        code, m, n, B, a_h.data_ptr(), u_h.data_ptr(), s_h.data_ptr(),
+        v_h.data_ptr() if v_h is not None else None, ctypes.byref(o),
+        info_h.data_ptr() if info_h is not None else None, chunk,
+        ws.data_ptr() if ws is not None else None, ws_bytes, arr, len(streams))
+    _lib.check(rc, f"bsvd_gesvj_batched_host({dt.name}, {m}x{n}, batch={B})")
+    return int(L.bsvd_select_kernel(code, m, n, ctypes.byref(o)))
+
+
+_SIDE: dict = {}
+
+
+def _side_streams(dev, count):
+    torch = _torch()
+    key = str(dev)
+    lst = _SIDE.setdefault(key, [])
+    while len(lst) < count:
+        lst.append(torch.cuda.Stream(dev))
+    return lst[:count]
+
+
 def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, device=None):
     """Equal shape/dtype numpy matrices -> (U (B,m,k), S (B,k), V (B,n,k)|None, info records).
 
-    Host-buffer path: pinned staging of the column-major batch, H2D, one
-    launch, D2H.  Returned U[b] / V[b] are F-ordered views.
+    Host-buffer path: pinned staging of the column-major batch, then the
+    pipelined bsvd_gesvj_batched_host (H2D / solve / D2H overlapped in
+    chunks).  Returned U[b] / V[b] are F-ordered views.
     """
     torch = _torch()
     B = len(mats)
@@ -164,15 +211,15 @@ def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, de
     hv = host.numpy()
     for b, a in enumerate(mats):
         hv[b] = a.T
-    a_t = host.to(device, non_blocking=True)
-    res = solve_tensor(a_t, m, n, opts, route, kernel)
-    u_h = res.u.to("cpu")
-    s_h = res.s.to("cpu")
-    v_h = res.v.to("cpu") if res.v is not None else None
-    info_h = res.info.to("cpu")
-    torch.cuda.current_stream(device).synchronize()
+    u_h = torch.empty((B, k, m), dtype=tdt, pin_memory=True)
+    s_h = torch.empty((B, k), dtype=torch_dtype(real_dtype(dt)), pin_memory=True)
+    v_h = torch.empty((B, k, n), dtype=tdt, pin_memory=True) if opts.compute_right_vectors else None
+    info_h = torch.empty((B * _lib.INFO_BYTES,), dtype=torch.uint8, pin_memory=True)
+    with torch.cuda.device(device):
+        kern = solve_host_buffers(host, u_h, s_h, v_h, info_h, m, n, opts, route, kernel)
+        torch.cuda.current_stream(device).synchronize()
     U = np.swapaxes(u_h.numpy(), 1, 2)
     S = s_h.numpy()
     V = np.swapaxes(v_h.numpy(), 1, 2) if v_h is not None else None
     info = np.frombuffer(info_h.numpy().tobytes(), dtype=INFO_DTYPE)
-    return U, S, V, info, res.kernel
+    return U, S, V, info, kern

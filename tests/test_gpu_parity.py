@@ -308,3 +308,54 @@ def test_c2_fp32_register_kernel(want_v):
         check_sigma_parity(S[b], s_ref, 16, u)
         check_factors(A[b], U[b], S[b], V[b] if want_v else None)
         assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt,m,n,want_v", [(np.float64, 32, 32, True), (np.float32, 16, 16, False),
+                                           (np.complex128, 40, 24, True), (np.float64, 12, 20, True)])
+def test_host_pipeline_matches_device_path(dt, m, n, want_v):
+    """bsvd_gesvj_batched_host (chunked H2D / solve / D2H over 3 streams) == the device call, bitwise."""
+    import torch
+
+    from paper_2601_17979_b200.solver import solve_host_buffers, solve_tensor, torch_dtype
+
+    B = 37  # ragged against the chunk size
+    A = np.stack([random_matrix(m, n, dt, seed=900 + b) for b in range(B)])
+    opts = bs.JacobiOptions(compute_right_vectors=want_v)
+    a_d = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    ref = solve_tensor(a_d, m, n, opts)
+    torch.cuda.synchronize()
+    k = min(m, n)
+    tdt = torch_dtype(dt)
+    a_h = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).pin_memory()
+    u_h = torch.empty((B, k, m), dtype=tdt).pin_memory()
+    s_h = torch.empty((B, k), dtype=ref.s.dtype).pin_memory()
+    v_h = torch.empty((B, k, n), dtype=tdt).pin_memory() if want_v else None
+    i_h = torch.empty((B * 48,), dtype=torch.uint8).pin_memory()
+    solve_host_buffers(a_h, u_h, s_h, v_h, i_h, m, n, opts, chunk=5)
+    torch.cuda.synchronize()
+    assert torch.equal(u_h, ref.u.cpu()) and torch.equal(s_h, ref.s.cpu())
+    if want_v:
+        assert torch.equal(v_h, ref.v.cpu())
+    assert torch.equal(i_h, ref.info.cpu())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", [0, 26])
+def test_problem_results_independent_of_warp_partner(kernel):
+    """Two problems share a warp in the 32x32 register kernels; a problem's bits must not depend on its
+    partner (the reference's batch == standalone guarantee, tests/test_batch.py:19-28)."""
+    import torch
+
+    B = 24
+    A = np.stack([random_matrix(32, 32, np.float64, seed=1200 + b) for b in range(B)])
+    A[3] = np.diag(np.geomspace(1.0, 1e-12, 32)) @ A[3]  # a problem with many >4x norm shrinks
+    perm = np.random.default_rng(5).permutation(B)
+    a0 = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    a1 = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A[perm], 1, 2))).cuda()
+    r0 = bs.solve_tensor(a0, 32, 32, bs.JacobiOptions(), kernel=kernel)
+    r1 = bs.solve_tensor(a1, 32, 32, bs.JacobiOptions(), kernel=kernel)
+    torch.cuda.synchronize()
+    assert torch.equal(r0.u[torch.from_numpy(perm).cuda()], r1.u)
+    assert torch.equal(r0.s[torch.from_numpy(perm).cuda()], r1.s)
+    assert torch.equal(r0.v[torch.from_numpy(perm).cuda()], r1.v)
