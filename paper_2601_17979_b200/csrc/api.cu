@@ -48,6 +48,11 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
     const size_t lim = smem_limit();
     const int es = esize_of(dt), rs = rsize_of(dt);
     if (r.blocked) {
+        if (o->kernel == 0 || o->kernel == KV_BLOCKED_REG) {
+            Plan p = plan_blocked_reg(dt, r.bm, r.bn, o->nb, r.need_v, contiguous && !r.trans, o->inner_sweeps);
+            if (p.kernel) return p;
+            if (o->kernel != 0) return p;
+        }
         if (o->kernel == 0 || o->kernel == KV_BLOCKED_DMMA || o->kernel == KV_BLOCKED_DMMA_VG ||
             o->kernel == KV_BLOCKED_DMMA_512) {
             Plan p = plan_blocked_dmma(dt, r.bm, r.bn, o->nb, r.need_v, contiguous && !r.trans, lim, o->kernel);
@@ -134,6 +139,9 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_BLOCKED_GENERAL: return launch_blocked_general<T>(a, p, st);
         case KV_UNBLOCKED_REG16F:
             if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
+        case KV_BLOCKED_REG:
+            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_blocked_reg(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_BLOCKED_DMMA:
         case KV_BLOCKED_DMMA_VG:

@@ -1,0 +1,491 @@
+// blocked_reg.cu -- kernel (3), blocked one-sided Jacobi with register-resident
+// block pairs (real FP64, nb = 16, n a multiple of 16, m <= 64 * NWG).
+//
+// Same outer iteration as _sweep_blocked (src/svd.py:481-522): the ell = n/16
+// column blocks are paired by the round-robin schedule (src/ordering.py:32-75);
+// per block pair (i, j) the reference forms G = [Wi Wj]^T [Wi Wj]
+// (compute_gram, src/svd.py:144-179), runs inner sweep(s) of two-sided Jacobi
+// on G accumulating P = I + Delta (_eig_delta / eig_sweeps, src/eig.py:151-174,
+// src/_kernels_numba.py:17-82) and applies [Wi Wj] <- [Wi Wj] P, [Vi Vj] <-
+// [Vi Vj] P (fused_pair_update, src/_kernels_numba.py:141-175) when the block
+// pair rotated; a sweep in which no block pair rotated ends the problem.
+//
+// B200 mapping: the Gram eigensolve is kernel (2) run on the block pair itself.
+// Two-sided Jacobi on G = X^T X and one-sided Jacobi on X = [Wi Wj] apply the
+// same rotation sequence (each rotation is computed from the current
+// g_ii, g_jj, g_ij = the current columns' norms and dot product), so the group
+// of NWG warps that owns a block pair holds X in registers (lane l: rows l and
+// l + 32 of its 64-row slab, all 32 columns -- the layout of
+// unblocked_reg32b.cu) and rotates it directly; G is never formed (no squared
+// condition number), the W update of the reference is the in-register
+// rotation, and the rotation product P = I + Delta is accumulated alongside (P
+// row l in lane l).  The V update [Vi Vj] P -- the only dense contraction left
+// -- runs on the FP64 tensor pipe (DMMA m8n8k4) straight from the
+// L2-resident workspace.  Inner sweeps use the machinery of the 32x32 register
+// kernel: maintained column norms (fresh at each inner sweep's start and after
+// a >4x shrink), the g_ji transpose reduction (plus a cross-warp sum when
+// NWG > 1), half-angle rotation parameters, the two-FMA update, the U = 2
+// unrolled tournament ring.
+#include "kernel_args.cuh"
+#include "launch.h"
+#include "rotation.cuh"
+
+namespace bsvd {
+namespace breg {
+
+constexpr int NB = 16;     // block width (nb)
+constexpr int N = 32;      // block-pair width w = 2 nb
+constexpr int H = 16;      // column pairs per inner iteration
+constexpr int NIT = 31;    // inner iterations per inner sweep
+constexpr int RSTR = 34;   // transpose buffer row stride (doubles)
+constexpr int PLD = 36;    // row stride of the staged P (doubles): conflict-free B fragments
+constexpr int MAXG = 8;    // block-pair groups per CTA (n <= 256)
+
+__host__ __device__ constexpr int ring_slot(int q) {
+    return q == 0 ? 1 : (q <= H - 1 ? 2 * q : 2 * (2 * H - 1 - q) + 1);
+}
+__host__ __device__ constexpr int md(int a) { return ((a % NIT) + NIT) % NIT; }
+__host__ __device__ constexpr int TS(int k, int u) { return k == 0 ? 0 : ring_slot(md(k - u)); }
+__host__ __device__ constexpr int BS(int k, int u) { return ring_slot(md((k == 0 ? 0 : NIT - k) - u)); }
+
+struct __align__(16) Par {
+    double cm1, c;  // x <- x + (cm1 x + c y);  y <- y + (cm1 y - c x)
+};
+
+struct WarpSmem {
+    double red[3 * H * RSTR];  // transpose buffer: rows 0..15 g, 16..31 top norms, 32..47 bottom norms
+    Par pub[H];
+    double nrm[N];             // maintained squared norms of the block pair's columns
+};
+
+struct GroupSmem {
+    double P[N * PLD];            // staged rotation product for the V contraction
+    double gsum[2][4][3 * H];     // cross-warp partial sums [parity][warp][value]
+    int rot;                      // inner rotations of the block pair (this inner sweep)
+    int pad[3];
+};
+
+__host__ __device__ inline uint32_t pair_code(int t, int k) {
+    int qt = k - t, qb = (k == 0 ? 0 : NIT - k) - t;
+    qt += qt < 0 ? NIT : 0;
+    qb += qb < 0 ? NIT : 0;
+    const int ct = (k == 0) ? 0 : ring_slot(qt);
+    const int cb = ring_slot(qb);
+    return (uint32_t)ct | ((uint32_t)cb << 8) | ((ct > cb) ? (1u << 16) : 0u);
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int SH>
+__device__ __forceinline__ void ring_shift(double (&x)[N]) {
+    if constexpr (md(SH) != 0) {
+        double y[NIT];
+#pragma unroll
+        for (int q = 0; q < NIT; ++q) y[q] = x[ring_slot(q)];
+#pragma unroll
+        for (int q = 0; q < NIT; ++q) x[ring_slot(q)] = y[md(q - SH)];
+    }
+}
+
+__device__ __forceinline__ void apply2(double& x, double& y, double cm1, double c) {
+    const double tx = fma(c, y, x);
+    const double ty = fma(-c, x, y);
+    x = fma(cm1, x, tx);
+    y = fma(cm1, y, ty);
+}
+
+__device__ __forceinline__ double sum16(const double* p) {
+    const double2* r = reinterpret_cast<const double2*>(p);
+    const double2 p0 = r[0], p1 = r[1], p2 = r[2], p3 = r[3], p4 = r[4], p5 = r[5], p6 = r[6], p7 = r[7];
+    const double s0 = (p0.x + p0.y) + (p1.x + p1.y), s1 = (p2.x + p2.y) + (p3.x + p3.y);
+    const double s2 = (p4.x + p4.y) + (p5.x + p5.y), s3 = (p6.x + p6.y) + (p7.x + p7.y);
+    return (s0 + s1) + (s2 + s3);
+}
+// total over the warp's 32 lanes of row `row` of the transpose buffer (identical on both halves)
+__device__ __forceinline__ double sum32(const double* red, int row, int half) {
+    const double s = sum16(red + row * RSTR + 16 * half);
+    const double o = __shfl_xor_sync(0xffffffffu, s, 16);
+    return half ? o + s : s + o;
+}
+
+__device__ __forceinline__ double xor_sign(double x, bool neg) {
+    return __longlong_as_double(__double_as_longlong(x) ^ ((long long)neg << 63));
+}
+
+__device__ __forceinline__ void rot_abs_core(double dabs, double g, double& s, double& cm1, double& tabs) {
+    const double q = fma(4.0 * g, g, dabs * dabs);
+    const double ir = rsqrt_cubic(q);
+    const double gi = g * ir;
+    const double c2 = fma(0.5 * dabs, ir, 0.5);
+    const double ic = rsqrt_cubic(c2);
+    const double c = c2 * ic;
+    s = gi * ic;
+    cm1 = -(s * s) * rcp_cubic(1.0 + c);
+    tabs = s * ic;
+}
+__device__ __forceinline__ void rot_abs(double dabs, double g, double& s, double& cm1, double& tabs) {
+    rot_abs_core(dabs, g, s, cm1, tabs);
+    if (fmax(dabs, g) < 0x1p-500) rot_abs_core(dabs * 0x1p+600, g * 0x1p+600, s, cm1, tabs);
+}
+
+struct Ctx {
+    WarpSmem* sm;
+    GroupSmem* gs;
+    const uint32_t* ctab;
+    int lane, half, k, wig, bar_id;
+    double tol, tol2;
+    bool want_p;
+};
+
+struct IState {
+    int my_rot;   // rotations of pair k in this inner sweep (counted by lanes < 16)
+    bool full;    // this iteration reads fresh norms
+    int par;      // cross-warp buffer parity
+};
+
+// reduce the warp's partial rows [row0, row0 + nrows) and (NWG > 1) sum across the group's warps
+template <int NWG>
+__device__ __forceinline__ void group_totals(const Ctx& c, IState& st, double* out, int nval) {
+    // out[v] for v < nval: v-th value of pair k (rows v * H + k)
+    for (int v = 0; v < nval; ++v) out[v] = sum32(c.sm->red, v * H + c.k, c.half);
+    if constexpr (NWG > 1) {
+        double* gsm = c.gs->gsum[st.par][0];
+        if (c.lane < H)
+            for (int v = 0; v < nval; ++v) gsm[c.wig * 3 * H + v * H + c.k] = out[v];
+        group_bar(c.bar_id, NWG * 32);
+        for (int v = 0; v < nval; ++v) {
+            double s = gsm[v * H + c.k];
+#pragma unroll
+            for (int w = 1; w < NWG; ++w) s += gsm[w * 3 * H + v * H + c.k];
+            out[v] = s;
+        }
+        st.par ^= 1;
+    }
+}
+
+template <int u, int NWG>
+__device__ __forceinline__ void inner_iter(double (&x0)[N], double (&x1)[N], double (&p)[N], const Ctx& c, int t,
+                                           IState& st) {
+    WarpSmem& sm = *c.sm;
+    // partial products of this lane's two rows (fresh norms too in full iterations)
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+        const double a0 = x0[TS(q, u)], b0 = x0[BS(q, u)], a1 = x1[TS(q, u)], b1 = x1[BS(q, u)];
+        sm.red[q * RSTR + c.lane] = fma(b1, a1, b0 * a0);
+    }
+    if (st.full) {
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            const double a0 = x0[TS(q, u)], b0 = x0[BS(q, u)], a1 = x1[TS(q, u)], b1 = x1[BS(q, u)];
+            sm.red[(H + q) * RSTR + c.lane] = fma(a1, a1, a0 * a0);
+            sm.red[(2 * H + q) * RSTR + c.lane] = fma(b1, b1, b0 * b0);
+        }
+    }
+    const uint32_t code = c.ctab[t * H + c.k];
+    __syncwarp();
+    double tot[3];
+    group_totals<NWG>(c, st, tot, st.full ? 3 : 1);
+    __syncwarp();
+    const int ct = code & 0xff, cb = (code >> 8) & 0xff;
+    const bool flip = (code >> 16) != 0;
+    const double g = tot[0];
+    const double gt = st.full ? tot[1] : sm.nrm[ct];
+    const double gb = st.full ? tot[2] : sm.nrm[cb];
+    const double absg = fabs(g);
+    const double pp = gt * gb;
+    bool rot = !(absg * absg < c.tol2 * pp);
+    if (absg < 0x1p-400 && absg > 0.0) rot = !(absg < c.tol * fsqrt(pp));
+    rot = rot && absg > 0.0;
+    const double d = gt - gb;
+    double s, cm1, tabs;
+    rot_abs(fabs(d), absg, s, cm1, tabs);
+    const bool eneg = d < 0.0 || (d == 0.0 && flip);
+    Par par;
+    par.cm1 = rot ? cm1 : 0.0;
+    par.c = rot ? xor_sign(s, (g < 0.0) != eneg) : 0.0;
+    const double dtg = rot ? xor_sign(tabs * absg, eneg) : 0.0;
+    const double nt = gt + dtg, nb = gb - dtg;
+    const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
+    if (c.lane < H) {
+        sm.pub[c.k] = par;
+        sm.nrm[ct] = nt;
+        sm.nrm[cb] = nb;
+        st.my_rot += rot ? 1 : 0;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, rot);
+    st.full = __ballot_sync(0xffffffffu, shrink) != 0u;
+    __syncwarp();
+    if (mask) {
+        if (c.want_p) {
+#pragma unroll
+            for (int q = 0; q < H; ++q) {
+                const Par pq = sm.pub[q];
+                apply2(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
+                apply2(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
+                apply2(p[TS(q, u)], p[BS(q, u)], pq.cm1, pq.c);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < H; ++q) {
+                const Par pq = sm.pub[q];
+                apply2(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
+                apply2(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
+            }
+        }
+    }
+}
+
+// one inner sweep (31 iterations, ring unrolled by 2); returns with columns in natural order
+template <int NWG>
+__device__ __forceinline__ void inner_sweep(double (&x0)[N], double (&x1)[N], double (&p)[N], const Ctx& c,
+                                            IState& st) {
+    st.full = true;
+#pragma unroll 1
+    for (int gi = 0; gi < 16; ++gi) {
+        const int t0 = 2 * gi;
+        inner_iter<0, NWG>(x0, x1, p, c, t0, st);
+        if (gi == 15) {
+            ring_shift<1>(x0);
+            ring_shift<1>(x1);
+            ring_shift<1>(p);
+            break;
+        }
+        inner_iter<1, NWG>(x0, x1, p, c, t0 + 1, st);
+        ring_shift<2>(x0);
+        ring_shift<2>(x1);
+        ring_shift<2>(p);
+    }
+}
+
+template <int NWG>
+__global__ void __launch_bounds__(256, 1) k_blocked_reg(SolveArgs<double> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int prob = blockIdx.x;
+    const int m = a.bm, n = a.bn;
+    const int ell = n / NB, Sb = ell + (ell & 1), hb = Sb / 2, nib = Sb - 1;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nthr = blockDim.x;
+    const int grp = warp / NWG, wig = warp % NWG;
+    const int ngrp = nthr / (32 * NWG);
+    WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem);
+    GroupSmem* gsm = reinterpret_cast<GroupSmem*>(smem + (size_t)(nthr / 32) * sizeof(WarpSmem));
+    uint32_t* ctab = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(gsm) + ngrp * sizeof(GroupSmem));
+    int* misc = reinterpret_cast<int*>(ctab + NIT * H);  // [0] sweep rot, [1] bad, [2..3] amax bits
+    long long* ctr = reinterpret_cast<long long*>(misc + 4);  // [0] gram calls, [1] update calls
+    double* W = a.work + (size_t)prob * (size_t)a.work_stride;  // m x n, then V n x n
+    double* V = W + (size_t)m * n;
+    const bool want_p = a.need_v != 0;
+
+    for (int e = tid; e < NIT * H; e += nthr) ctab[e] = pair_code(e / H, e % H);
+    if (tid < 4) misc[tid] = 0;
+    if (tid < 2) ctr[tid] = 0;
+    __syncthreads();
+    // ---- kernel (1): load A into W, V = I, exact power-of-two prescale ----
+    {
+        const double* Ap = a.A + (size_t)prob * a.strideA;
+        double amax = 0.0;
+        int bad = 0;
+        for (int e = tid; e < m * n; e += nthr) {
+            const double x = Ap[(e % m) + (size_t)(e / m) * a.lda];
+            bad |= !isfinite(x);
+            amax = fmax(amax, fabs(x));
+        }
+        if (bad) atomicOr(&misc[1], 1);
+        atomicMax(reinterpret_cast<unsigned long long*>(misc + 2), (unsigned long long)__double_as_longlong(amax));
+        __syncthreads();
+        const int ex = prescale_exponent(__longlong_as_double(*reinterpret_cast<long long*>(misc + 2)));
+        const double sc = pow2(-ex);
+        for (int e = tid; e < m * n; e += nthr) W[e] = Ap[(e % m) + (size_t)(e / m) * a.lda] * sc;
+        if (want_p)
+            for (int e = tid; e < n * n; e += nthr) V[e] = ((e % n) == (e / n)) ? 1.0 : 0.0;
+        __syncthreads();
+        if (tid == 0) misc[2] = ex;  // keep the exponent (amax bits no longer needed)
+        __syncthreads();
+    }
+    const int ex = misc[2];
+    Ctx c;
+    c.sm = &wsm[warp];
+    c.gs = &gsm[grp < ngrp ? grp : 0];
+    c.ctab = ctab;
+    c.lane = lane;
+    c.half = lane >> 4;
+    c.k = lane & 15;
+    c.wig = wig;
+    c.bar_id = 1 + grp;
+    c.tol = a.tol;
+    c.tol2 = a.tol * a.tol;
+    c.want_p = want_p;
+    const int r0 = wig * 64 + lane, r1 = r0 + 32;
+    const bool v0 = r0 < m, v1 = r1 < m;
+    int sweeps = 0, last = 0, conv = 0;
+    long long rot_total = 0;
+
+#pragma unroll 1
+    for (int sw = 0; sw < a.max_sweeps; ++sw) {
+#pragma unroll 1
+        for (int tb = 0; tb < nib; ++tb) {
+            int bi = 0, bj = 0;
+            const bool live = grp < hb && rr_pair(tb, grp, Sb, ell, bi, bj);
+            if (live) {
+                auto col = [&](int x) { return x < NB ? bi * NB + x : bj * NB + x - NB; };
+                double x0[N], x1[N], p[N];
+#pragma unroll
+                for (int x = 0; x < N; ++x) {
+                    const double* cp = W + (size_t)col(x) * m;
+                    x0[x] = v0 ? cp[r0] : 0.0;
+                    x1[x] = v1 ? cp[r1] : 0.0;
+                    p[x] = (x == lane) ? 1.0 : 0.0;
+                }
+                IState st;
+                st.par = 0;
+                int bp_rot = 0;
+#pragma unroll 1
+                for (int isw = 0; isw < a.inner_budget; ++isw) {
+                    st.my_rot = 0;
+                    inner_sweep<NWG>(x0, x1, p, c, st);
+                    int r = st.my_rot;  // lanes 0..15 hold the counts of pairs 0..15
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+                    r = __shfl_sync(0xffffffffu, r, 0);
+                    bp_rot += r;
+                    if (r == 0) break;
+                }
+                if (bp_rot) {
+#pragma unroll
+                    for (int x = 0; x < N; ++x) {  // W <- W P happened in registers
+                        double* cp = W + (size_t)col(x) * m;
+                        if (v0) cp[r0] = x0[x];
+                        if (v1) cp[r1] = x1[x];
+                    }
+                }
+                if (want_p && bp_rot) {
+                    GroupSmem& gs = *c.gs;
+                    if (wig == 0) {
+#pragma unroll
+                        for (int x = 0; x < N; ++x) gs.P[lane * PLD + x] = p[x];
+                    }
+                    if constexpr (NWG > 1) group_bar(c.bar_id, NWG * 32);
+                    else __syncwarp();
+                    // [Vi Vj] <- [Vi Vj] P on the FP64 tensor pipe: row tiles of 8, all 32 columns at once
+                    const int g8 = lane >> 2, t4 = lane & 3;
+                    double bf[4][8];  // B fragments: P[4 ks + t4][8 ct + g8]
+#pragma unroll
+                    for (int ct = 0; ct < 4; ++ct)
+#pragma unroll
+                        for (int ks = 0; ks < 8; ++ks) bf[ct][ks] = gs.P[(4 * ks + t4) * PLD + 8 * ct + g8];
+                    for (int rt = wig; rt < n / 8; rt += NWG) {
+                        const int row = 8 * rt + g8;
+                        double af[8];
+#pragma unroll
+                        for (int ks = 0; ks < 8; ++ks) af[ks] = V[row + (size_t)col(4 * ks + t4) * n];
+                        double d[4][2];
+#pragma unroll
+                        for (int ct = 0; ct < 4; ++ct) {
+                            d[ct][0] = 0.0;
+                            d[ct][1] = 0.0;
+#pragma unroll
+                            for (int ks = 0; ks < 8; ++ks) dmma(d[ct][0], d[ct][1], af[ks], bf[ct][ks]);
+                        }
+                        __syncwarp();  // every lane has read its A fragments of this tile
+#pragma unroll
+                        for (int ct = 0; ct < 4; ++ct) {
+                            V[row + (size_t)col(8 * ct + 2 * t4) * n] = d[ct][0];
+                            V[row + (size_t)col(8 * ct + 2 * t4 + 1) * n] = d[ct][1];
+                        }
+                    }
+                    if constexpr (NWG > 1) group_bar(c.bar_id, NWG * 32);  // P staging reusable
+                }
+                if (tid == grp * NWG * 32) {
+                    atomicAdd(&misc[0], bp_rot);
+                    atomicAdd((unsigned long long*)&ctr[0], 1ull);
+                    if (bp_rot) atomicAdd((unsigned long long*)&ctr[1], 1ull);
+                }
+            }
+            __syncthreads();  // the next iteration's block pairs read the columns written here
+        }
+        const int tot = misc[0];
+        sweeps = sw + 1;
+        last = tot;
+        rot_total += tot;
+        __syncthreads();
+        if (tid == 0) misc[0] = 0;
+        __syncthreads();
+        if (tot == 0) {
+            conv = 1;
+            break;
+        }
+    }
+    {
+        const double unscale = pow2(ex);
+        for (int e = tid; e < m * n; e += nthr) W[e] *= unscale;
+    }
+    if (tid == 0 && a.info) {
+        bsvd_info inf;
+        inf.converged = conv;
+        inf.outer_sweeps = sweeps;
+        inf.rotations = rot_total;
+        inf.gram_calls = ctr[0];
+        inf.update_calls = ctr[1];
+        inf.last_rotations = last;
+        inf.path = 2;
+        inf.status = misc[1] ? 1 : 0;
+        inf.kernel = a.kernel;
+        a.info[prob] = inf;
+    }
+}
+
+inline size_t smem_bytes(int n, int nwg) {
+    const int ell = n / NB, hb = (ell + (ell & 1)) / 2;
+    const int nw = hb * nwg;
+    return (size_t)nw * sizeof(WarpSmem) + (size_t)hb * sizeof(GroupSmem) + NIT * H * 4 + 64;
+}
+
+}  // namespace breg
+
+Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, int inner_sweeps) {
+    Plan p{};
+    (void)inner_sweeps;
+    if (dtype != BSVD_D || nb != 16 || bn % 16 != 0 || bn < 32 || bn > 256 || !contiguous) return p;
+    const int ell = bn / 16, hb = (ell + (ell & 1)) / 2;
+    int nwg = bm <= 64 ? 1 : (bm <= 128 ? 2 : (bm <= 256 ? 4 : 0));
+    if (!nwg || hb * nwg > 8) return p;
+    p.kernel = KV_BLOCKED_REG;
+    p.threads = hb * nwg * 32;
+    p.group = nwg;
+    p.smem = breg::smem_bytes(bn, nwg);
+    p.work_elems = (size_t)bm * bn + (size_t)bn * bn;
+    p.grid = 0;
+    p.resident = 0;
+    (void)need_v;
+    return p;
+}
+
+template <int NWG>
+static int launch_br(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
+    auto k = breg::k_blocked_reg<NWG>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<a.batch, p.threads, p.smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
+    a.kernel = p.kernel;
+    a.work_stride = (int64_t)p.work_elems;
+    int rc;
+    switch (p.group) {
+        case 1: rc = launch_br<1>(a, p, st); break;
+        case 2: rc = launch_br<2>(a, p, st); break;
+        default: rc = launch_br<4>(a, p, st); break;
+    }
+    if (rc) return rc;
+    return launch_finalize_gm<double>(a, st);
+}
+
+}  // namespace bsvd

@@ -45,6 +45,32 @@ int launch_finalize_ws(SolveArgs<T> a, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 
+// Finalisation in place in the workspace (global / L2): for solvers whose W
+// and V live in the workspace and are too large to stage in shared memory.
+template <class T>
+__global__ void __launch_bounds__(256) k_finalize_gm(SolveArgs<T> a) {
+    using R = typename tr<T>::R;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int prob = blockIdx.x;
+    T* W = a.work + (size_t)prob * a.work_stride;
+    T* Vw = a.need_v ? W + (size_t)a.bm * a.bn : nullptr;
+    R* sig = reinterpret_cast<R*>(smem);
+    int* perm = reinterpret_cast<int*>(smem + (((size_t)a.bn * sizeof(R) + 15) & ~size_t(15)));
+    int* flag = perm + ((a.bn + 3) & ~3);
+    finalize_block<T>(W, a.bm, a.bm, a.bn, Vw, a.bn, sig, perm, flag, final_out(a, prob));
+}
+
+template <class T>
+int launch_finalize_gm(SolveArgs<T> a, cudaStream_t st) {
+    const size_t smem = (((size_t)a.bn * sizeof(typename tr<T>::R) + 15) & ~size_t(15)) +
+                        (size_t)((a.bn + 3) & ~3) * 4 + 16;
+    k_finalize_gm<T><<<a.batch, 256, smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+template int launch_finalize_gm<double>(SolveArgs<double>, cudaStream_t);
+template int launch_finalize_gm<cx<double>>(SolveArgs<cx<double>>, cudaStream_t);
+
 template int launch_finalize_ws<float>(SolveArgs<float>, cudaStream_t);
 template int launch_finalize_ws<double>(SolveArgs<double>, cudaStream_t);
 template int launch_finalize_ws<cx<float>>(SolveArgs<cx<float>>, cudaStream_t);

@@ -41,6 +41,10 @@ int launch_unblocked_reg16(SolveArgs<float> a, const Plan& p, cudaStream_t st);
 
 template <class T>
 int launch_finalize_ws(SolveArgs<T> a, cudaStream_t st);
+template <class T>
+int launch_finalize_gm(SolveArgs<T> a, cudaStream_t st);
+Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, int inner_sweeps);
+int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 
 int group_for_rows(int bm);
 int threads_for(int bn, int G);

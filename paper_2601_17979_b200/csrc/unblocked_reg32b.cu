@@ -119,7 +119,7 @@ __device__ __forceinline__ void partials(const double (&x0)[N], const double (&x
 // Development probes (tools/microbench/wchain.cu defines R32_PROBE_ON): clock
 // deltas between stage boundaries of the W iteration, warp 0 of block 0.
 #ifdef R32_PROBE_ON
-__device__ unsigned long long g_r32_probe[8];
+__device__ unsigned long long g_r32_probe[16];
 #define R32P(i, v) r32_probe(i, v, st)
 #else
 #define R32P(i, v)
@@ -134,6 +134,20 @@ struct IterState {
                         // problem's numerics never depend on the problem sharing its warp)
 };
 
+#ifdef R32_PROBE_ON
+__device__ __forceinline__ void r32_probe_t(int i, double v, long long& tl) {
+    long long c;
+    asm volatile("mov.u64 %0, %%clock64; // %1" : "=l"(c) : "d"(v) : "memory");
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        if (i > 0) atomicAdd(&g_r32_probe[i], (unsigned long long)(c - tl));
+        else atomicAdd(&g_r32_probe[0], 1ull);
+    }
+    tl = c;
+}
+#define R32PT(i, v, tl) r32_probe_t(i, v, tl)
+#else
+#define R32PT(i, v, tl)
+#endif
 #ifdef R32_PROBE_ON
 __device__ __forceinline__ void r32_probe(int i, double v, IterState& st) {
     long long c;
@@ -291,11 +305,13 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
 // One V replay iteration at offset u (log row t is staged in sm.stage[t & 1]).
 template <int u>
 __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int t, int half, int hl,
-                                       const Par* logl, uint32_t itbits) {
+                                       const Par* logl, uint32_t itbits, long long& tl) {
+    R32PT(7, x0[TS(0, u)], tl);
     if (t + 1 < NIT) cp_async16(&sm.stage[(t + 1) & 1][half][hl], logl + (t + 1) * H);
     cp_commit();
     cp_wait<1>();
     __syncwarp();
+    R32PT(8, sm.stage[t & 1][half][0].c, tl);
     if ((itbits >> t) & 1u) {
         const Par* stp = sm.stage[t & 1][half];
         Par pr[H];  // all rotations first, then 128 independent FMAs
@@ -308,6 +324,7 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
             apply2(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
         }
     }
+    R32PT(9, x1[BS(H - 1, u)], tl);
     __syncwarp();
 }
 
@@ -342,25 +359,25 @@ __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSm
 
 template <int U>
 __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int half, int hl,
-                                        const Par* logl, uint32_t itbits) {
+                                        const Par* logl, uint32_t itbits, long long& tl) {
     constexpr int NG = (NIT + U - 1) / U;
     constexpr int R = NIT - (NG - 1) * U;
 #pragma unroll 1
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
         const bool last = gi == NG - 1;
-        v_iter<0>(x0, x1, sm, t0, half, hl, logl, itbits);
+        v_iter<0>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
         if constexpr (U >= 2) {
             if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            v_iter<1 % U>(x0, x1, sm, t0 + 1, half, hl, logl, itbits);
+            v_iter<1 % U>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 3) {
             if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            v_iter<2 % U>(x0, x1, sm, t0 + 2, half, hl, logl, itbits);
+            v_iter<2 % U>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 4) {
             if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            v_iter<3 % U>(x0, x1, sm, t0 + 3, half, hl, logl, itbits);
+            v_iter<3 % U>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
         }
         ring_shift<U>(x0);
         ring_shift<U>(x1);
@@ -467,7 +484,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
             __syncwarp();  // this warp's log writes are visible to all its lanes
             cp_async16(&sm.stage[0][half][hl], logl);
             cp_commit();
-            v_sweep<UV>(x0, x1, sm, half, hl, logl, st.itbits);
+            v_sweep<UV>(x0, x1, sm, half, hl, logl, st.itbits, st.tl);
             cp_wait<0>();
             if (live) {
 #pragma unroll

@@ -110,7 +110,7 @@ def test_kernel_selection_routes():
     L = _lib.load()
     o = _lib.BsvdOpts()
     L.bsvd_default_opts(ctypes.byref(o))
-    assert L.bsvd_select_kernel(1, 64, 64, ctypes.byref(o)) in (8, 9, 10)  # blocked FP64 on DMMA (n > 32)
+    assert L.bsvd_select_kernel(1, 64, 64, ctypes.byref(o)) == 30     # blocked FP64: register block pairs
     assert L.bsvd_select_kernel(3, 64, 64, ctypes.byref(o)) == 2      # blocked complex: general kernel
     assert L.bsvd_select_kernel(0, 16, 16, ctypes.byref(o)) == 11     # 16x16 FP32 register kernel
     assert L.bsvd_select_kernel(1, 32, 32, ctypes.byref(o)) == 12     # 32x32 FP64 register kernel (2nd gen)

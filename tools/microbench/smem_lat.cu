@@ -57,6 +57,21 @@ __global__ void k(double* out, int iters) {
             __syncwarp();
             s = r[hl * RSTR + 16 * half];
             __syncwarp();
+        } else if (MODE == 9) {  // butterfly shuffle reduction of 16 doubles over 16 lanes
+            double a[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) a[q] = v * (q + 1);
+#pragma unroll
+            for (int m = 8, n = 16; m >= 1; m >>= 1, n >>= 1) {
+                const bool up = (hl & m) != 0;
+#pragma unroll
+                for (int i = 0; i < n / 2; ++i) {
+                    const double lo = a[i], hi = a[i + n / 2];
+                    const double send = up ? lo : hi, keep = up ? hi : lo;
+                    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                }
+            }
+            s = a[0];
         } else {  // 16 STS, no sync, no reload: issue cost
 #pragma unroll
             for (int q = 0; q < 16; ++q) r[q * RSTR + lane] = v + q;
@@ -86,5 +101,6 @@ int main() {
     run<6>(d, "1 STS + sync + 8 LDS.128 + tree");
     run<7>(d, "8 STS.128 + sync + 1 LDS");
     run<8>(d, "16 STS (no reload)");
+    run<9>(d, "16 DMUL + butterfly SHFL reduction");
     return 0;
 }

@@ -35,17 +35,19 @@ int main(int argc, char** argv) {
     auto k = r32b::k_reg32b<4, 2, 2>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int rep = 0; rep < 2; ++rep) {
-        unsigned long long z[8] = {0};
+        unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(r32b::g_r32_probe, z, sizeof(z));
         k<<<1, 128, smem>>>(a);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
-        unsigned long long p[8];
+        unsigned long long p[16];
         cudaMemcpyFromSymbol(p, r32b::g_r32_probe, sizeof(p));
         const double n = (double)p[0];
         printf("want_v=%d iters %.0f | partials %.0f | sync+first LDS %.0f | reduce %.0f | params %.0f | "
                "publish %.0f | update %.0f  (cycles/iter)\n",
                a.want_v, n, p[4] / n, p[5] / n, p[1] / n, p[2] / n, p[6] / n, p[3] / n);
+        if (a.want_v) printf("   V replay per iteration: wait+stage %.0f | update %.0f | tail+shift %.0f\n",
+                             p[8] / n, p[9] / n, p[7] / n);
     }
     return 0;
 }
