@@ -379,11 +379,19 @@ __global__ void __launch_bounds__(256, 1) k_blocked_reg(SolveArgs<double> a) {
                     for (int ct = 0; ct < 4; ++ct)
 #pragma unroll
                         for (int ks = 0; ks < 8; ++ks) bf[ct][ks] = gs.P[(4 * ks + t4) * PLD + 8 * ct + g8];
+                    // A fragments of the next row tile are in flight while this one multiplies
+                    double afn[8];
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks) afn[ks] = V[8 * wig + g8 + (size_t)col(4 * ks + t4) * n];
                     for (int rt = wig; rt < n / 8; rt += NWG) {
                         const int row = 8 * rt + g8;
                         double af[8];
 #pragma unroll
-                        for (int ks = 0; ks < 8; ++ks) af[ks] = V[row + (size_t)col(4 * ks + t4) * n];
+                        for (int ks = 0; ks < 8; ++ks) af[ks] = afn[ks];
+                        if (rt + NWG < n / 8) {
+#pragma unroll
+                            for (int ks = 0; ks < 8; ++ks) afn[ks] = V[row + 8 * NWG + (size_t)col(4 * ks + t4) * n];
+                        }
                         double d[4][2];
 #pragma unroll
                         for (int ct = 0; ct < 4; ++ct) {
