@@ -36,8 +36,9 @@ extern "C" {
 /* element types; codes equal src/fileio.py:49-54 (s, d, c, z) */
 typedef enum { BSVD_S = 0, BSVD_D = 1, BSVD_C = 2, BSVD_Z = 3 } bsvd_dtype;
 
-/* solver routes (src/svd.py:559-582): dispatch = svd_dispatch, the others force */
-enum { BSVD_DISPATCH = 0, BSVD_FORCE_UNBLOCKED = 1, BSVD_FORCE_BLOCKED = 2 };
+/* solver routes (src/svd.py:559-582): dispatch = svd_dispatch, the others force
+   (FORCE_QR = svd_qr_preprocessed: Householder QR first whatever the aspect ratio) */
+enum { BSVD_DISPATCH = 0, BSVD_FORCE_UNBLOCKED = 1, BSVD_FORCE_BLOCKED = 2, BSVD_FORCE_QR = 3 };
 
 /* JacobiOptions (src/svd.py:58-91) as a POD. */
 typedef struct {
@@ -51,7 +52,8 @@ typedef struct {
     int fused_updates;  /* accepted for parity; updates are always fused     */
     int row_block;      /* accepted for parity (tiling is the kernel's own)  */
     int kernel;         /* 0 = auto; >0 forces a kernel variant (tests/bench) */
-    int reserved[3];
+    int use_qr;         /* use_qr_preprocess: dispatch takes the "qr+" route when m >= 3n (QR_RATIO) */
+    int reserved[2];
 } bsvd_opts;
 
 /* Per-problem telemetry, written by the device (mirrors SolveInfo / BatchState). */
@@ -62,7 +64,7 @@ typedef struct {
     int64_t gram_calls;     /* blocked path: Gram formations                      */
     int64_t update_calls;   /* blocked path: pair updates applied                 */
     int32_t last_rotations; /* rotations applied in the final sweep               */
-    int32_t path;           /* 1 unblocked, 2 blocked (| 0x100 when transposed)   */
+    int32_t path;           /* 1 unblocked, 2 blocked (| 0x100 transposed, | 0x200 qr) */
     int32_t status;         /* 0 ok, 1 non-finite input                           */
     int32_t kernel;         /* kernel variant that ran                            */
 } bsvd_info;

@@ -502,6 +502,95 @@ void finalize(int m, int n, T* w, int ldw, T* v, int ldv, int vrows, typename tr
     for (int c = 0; c < n; ++c) sigma[c] = sig[order[c]];
 }
 
+// ---- householder_qr  (src/core.py:118-168) --------------------------------
+// Reduced non-pivoted QR by Householder reflections in the working precision;
+// norms in float64 (np.linalg.norm's BLAS order is not reproduced: this part
+// of the restatement is pinned by tolerance, like the reference's own tests).
+template <class T>
+double norm2v(const T* x, int len) {
+    double s = 0.0;
+    for (int i = 0; i < len; ++i) {
+        if constexpr (tr<T>::cplx) s += (double)x[i].re * x[i].re + (double)x[i].im * x[i].im;
+        else s += (double)x[i] * x[i];
+    }
+    return std::sqrt(s);
+}
+template <class T>
+T scaleT(T x, double c) {
+    if constexpr (tr<T>::cplx) return {(decltype(x.re))(x.re * c), (decltype(x.re))(x.im * c)};
+    else return (T)(x * c);
+}
+template <class T>
+T subT(T a, T b) {
+    if constexpr (tr<T>::cplx) return {a.re - b.re, a.im - b.im};
+    else return a - b;
+}
+template <class T>
+T phase_of(T x) {  // x / |x|, 1 for x == 0
+    if constexpr (tr<T>::cplx) {
+        const double a = std::hypot((double)x.re, (double)x.im);
+        if (a == 0.0) return one<T>();
+        return {(decltype(x.re))(x.re / a), (decltype(x.re))(x.im / a)};
+    } else {
+        return x == 0 ? (T)1 : (x > 0 ? (T)1 : (T)-1);
+    }
+}
+// a (m x n, ld m) -> q (m x n), r (n x n); requires m >= n
+template <class T>
+void householder_qr(int m, int n, const T* a, std::vector<T>& q, std::vector<T>& r_out) {
+    std::vector<T> r(a, a + (size_t)m * n);
+    std::vector<std::pair<int, std::vector<T>>> refl;
+    for (int k = 0; k < n; ++k) {
+        T* x = r.data() + k + (size_t)k * m;
+        const int len = m - k;
+        const double norm_x = norm2v(x, len);
+        if (norm_x == 0.0) continue;
+        const T ph = phase_of(x[0]);
+        std::vector<T> v(x, x + len);
+        v[0] = addT(v[0], scaleT(ph, norm_x));
+        const double vn = norm2v(v.data(), len);
+        if (vn == 0.0) continue;
+        for (auto& e : v) e = scaleT(e, 1.0 / vn);
+        for (int j = k; j < n; ++j) {  // r[k:, k:] -= 2 outer(v, v^H r[k:, k:])
+            T* cj = r.data() + k + (size_t)j * m;
+            T w = zero<T>();
+            for (int i = 0; i < len; ++i) w = addT(w, mulT(conjv(v[i]), cj[i]));
+            const T w2 = scaleT(w, 2.0);
+            for (int i = 0; i < len; ++i) cj[i] = subT(cj[i], mulT(v[i], w2));
+        }
+        x[0] = scaleT(ph, -norm_x);
+        for (int i = 1; i < len; ++i) x[i] = zero<T>();
+        refl.push_back({k, std::move(v)});
+    }
+    q.assign((size_t)m * n, zero<T>());
+    for (int k = 0; k < n; ++k) q[k + (size_t)k * m] = one<T>();
+    for (auto it = refl.rbegin(); it != refl.rend(); ++it) {
+        const int k = it->first, len = m - k;
+        const std::vector<T>& v = it->second;
+        for (int j = 0; j < n; ++j) {
+            T* cj = q.data() + k + (size_t)j * m;
+            T w = zero<T>();
+            for (int i = 0; i < len; ++i) w = addT(w, mulT(conjv(v[i]), cj[i]));
+            const T w2 = scaleT(w, 2.0);
+            for (int i = 0; i < len; ++i) cj[i] = subT(cj[i], mulT(v[i], w2));
+        }
+    }
+    for (int k = 0; k < n; ++k) {  // diag(r) real >= 0
+        const T dkk = r[k + (size_t)k * m];
+        const T p = phase_of(dkk);
+        bool is_zero;
+        if constexpr (tr<T>::cplx) is_zero = dkk.re == 0 && dkk.im == 0; else is_zero = dkk == 0;
+        if (is_zero) continue;
+        for (int j = k; j < n; ++j) r[k + (size_t)j * m] = mulT(r[k + (size_t)j * m], conjv(p));
+        for (int i = 0; i < m; ++i) q[i + (size_t)k * m] = mulT(q[i + (size_t)k * m], p);
+        if constexpr (tr<T>::cplx) r[k + (size_t)k * m] = {(decltype(dkk.re))std::hypot((double)dkk.re, (double)dkk.im), 0};
+        else r[k + (size_t)k * m] = (T)std::fabs((double)dkk);
+    }
+    r_out.assign((size_t)n * n, zero<T>());
+    for (int j = 0; j < n; ++j)
+        for (int i = 0; i <= j; ++i) r_out[i + (size_t)j * n] = r[i + (size_t)j * m];
+}
+
 // ---- _ProblemRun + _run_standalone  (src/svd.py:312-556) -----------------
 template <class T>
 int solve(int m, int n, const T* a, T* u, typename tr<T>::R* s, T* vout, const orc_opts* o,
@@ -525,6 +614,18 @@ int solve(int m, int n, const T* a, T* u, typename tr<T>::R* s, T* vout, const o
     for (int c = 0; c < bn; ++c)
         for (int r = 0; r < bm; ++r)
             W[r + (size_t)c * bm] = transposed ? conjv(a[c + (size_t)r * m]) : a[r + (size_t)c * m];
+    // QR first (src/svd.py:364-371): forced, or dispatch with use_qr_preprocess and bm >= 3 bn
+    const bool use_qr = o->force == 3 || (o->force == 0 && o->use_qr && (double)bm >= 3.0 * bn);
+    std::vector<T> Q;
+    const int bm_in = bm;
+    int bmw = bm;
+    if (use_qr) {
+        std::vector<T> Rm;
+        householder_qr<T>(bm, bn, W.data(), Q, Rm);
+        W = Rm;
+        bmw = bn;
+        info->qr = 1;
+    }
     bool blocked;
     if (o->force == 1) blocked = false;
     else if (o->force == 2) blocked = true;
@@ -569,7 +670,7 @@ int solve(int m, int n, const T* a, T* u, typename tr<T>::R* s, T* vout, const o
         if (!blocked) {
             if (bn >= 2) {  // _sweep_unblocked  src/svd.py:433-447
                 int sw, cv;
-                const int64_t rot = onesided<T>(bm, W.data(), bm, vrows, Vp, bn, sc, tol, 1, &sw, &cv);
+                const int64_t rot = onesided<T>(bmw, W.data(), bmw, vrows, Vp, bn, sc, tol, 1, &sw, &cv);
                 eig_calls += 1;
                 inner_rot += rot;
                 quiet = rot == 0;
@@ -577,7 +678,7 @@ int solve(int m, int n, const T* a, T* u, typename tr<T>::R* s, T* vout, const o
         } else if (blocks.size() == 1) {  // _sweep_single_block  src/svd.py:461-479
             const int w = bn;
             G.assign((size_t)w * w, zero<T>());
-            gram<T>(bm, w, 0, W.data(), bm, W.data(), bm, G.data(), w);
+            gram<T>(bmw, w, 0, W.data(), bmw, W.data(), bmw, G.data(), w);
             gram_calls += 1;
             d.assign(w, 0);
             for (int c = 0; c < w; ++c) d[c] = (R)realpart(G[c + (size_t)c * w]);
@@ -593,7 +694,7 @@ int solve(int m, int n, const T* a, T* u, typename tr<T>::R* s, T* vout, const o
             inner_rot += rot;
             if (rot != 0) {
                 quiet = false;
-                fused_update<T>(bm, w, 0, W.data(), bm, W.data(), bm, D.data(), w, true, false);
+                fused_update<T>(bmw, w, 0, W.data(), bmw, W.data(), bmw, D.data(), w, true, false);
                 if (need_v) fused_update<T>(bn, w, 0, V.data(), bn, V.data(), bn, D.data(), w, true, false);
                 update_calls += 1;
             }
@@ -604,10 +705,10 @@ int solve(int m, int n, const T* a, T* u, typename tr<T>::R* s, T* vout, const o
                 const int i0 = blocks[bi].first, i1 = blocks[bi].second;
                 const int j0 = blocks[bj].first, j1 = blocks[bj].second;
                 const int wi = i1 - i0, wj = j1 - j0, w = wi + wj;
-                T* Wi = W.data() + (size_t)i0 * bm;
-                T* Wj = W.data() + (size_t)j0 * bm;
+                T* Wi = W.data() + (size_t)i0 * bmw;
+                T* Wj = W.data() + (size_t)j0 * bmw;
                 G.assign((size_t)w * w, zero<T>());
-                gram<T>(bm, wi, wj, Wi, bm, Wj, bm, G.data(), w);
+                gram<T>(bmw, wi, wj, Wi, bmw, Wj, bmw, G.data(), w);
                 gram_calls += 1;
                 // _eig_delta  src/eig.py:151-174
                 d.assign(w, 0);
@@ -622,7 +723,7 @@ int solve(int m, int n, const T* a, T* u, typename tr<T>::R* s, T* vout, const o
                 if (rot == 0) continue;
                 quiet = false;
                 const bool two = !o->fused_updates;
-                fused_update<T>(bm, wi, wj, Wi, bm, Wj, bm, D.data(), w, true, two);
+                fused_update<T>(bmw, wi, wj, Wi, bmw, Wj, bmw, D.data(), w, true, two);
                 if (need_v)
                     fused_update<T>(bn, wi, wj, V.data() + (size_t)i0 * bn, bn, V.data() + (size_t)j0 * bn,
                                     bn, D.data(), w, true, two);
@@ -632,7 +733,17 @@ int solve(int m, int n, const T* a, T* u, typename tr<T>::R* s, T* vout, const o
         outer += 1;
         if (quiet) converged = true;
     }
-    finalize<T>(bm, bn, W.data(), bm, Vp, bn, vrows, s);
+    finalize<T>(bmw, bn, W.data(), bmw, Vp, bn, vrows, s);
+    if (use_qr) {  // U = Q @ Uhat  (src/svd.py:529-530)
+        std::vector<T> Uf((size_t)bm_in * bn, zero<T>());
+        for (int j = 0; j < bn; ++j)
+            for (int l = 0; l < bn; ++l) {
+                const T wl = W[l + (size_t)j * bn];
+                for (int i = 0; i < bm_in; ++i)
+                    Uf[i + (size_t)j * bm_in] = addT(Uf[i + (size_t)j * bm_in], mulT(Q[i + (size_t)l * bm_in], wl));
+            }
+        W.swap(Uf);
+    }
     // outputs: k = bn.  U is m x k, V is n x k.
     if (!transposed) {
         std::memcpy(u, W.data(), sizeof(T) * (size_t)bm * bn);

@@ -23,7 +23,7 @@ extern "C" {
 /* dtype codes follow src/fileio.py:49-54 (s, d, c, z) */
 enum { ORC_S = 0, ORC_D = 1, ORC_C = 2, ORC_Z = 3 };
 
-/* force codes: 0 = svd_dispatch, 1 = svd_unblocked, 2 = svd_blocked */
+/* force codes: 0 = svd_dispatch, 1 = svd_unblocked, 2 = svd_blocked, 3 = svd_qr_preprocessed */
 typedef struct {
     double k;            /* JacobiOptions.k            src/svd.py:70 */
     int max_nsweeps;     /* JacobiOptions.max_nsweeps  src/svd.py:71 */
@@ -32,7 +32,8 @@ typedef struct {
     int want_v;          /* compute_right_vectors      src/svd.py:76 */
     int fused_updates;   /* JacobiOptions.fused_updates src/svd.py:77 */
     int row_block;       /* JacobiOptions.row_block    src/svd.py:78 */
-    int force;           /* 0 dispatch, 1 unblocked, 2 blocked */
+    int force;           /* 0 dispatch, 1 unblocked, 2 blocked, 3 qr */
+    int use_qr;          /* JacobiOptions.use_qr_preprocess src/svd.py:75 */
 } orc_opts;
 
 /* path codes */
@@ -48,7 +49,7 @@ typedef struct {
     int64_t eig_calls;
     int64_t update_calls;
     int32_t status;           /* 0 ok, <0 error */
-    int32_t pad;
+    int32_t qr;               /* "qr+" route taken          */
 } orc_info;
 
 /*

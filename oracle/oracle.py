@@ -35,7 +35,7 @@ REAL_OF = {
     np.dtype(np.complex128): np.dtype(np.float64),
 }
 PATHS = {0: "empty", 1: "unblocked", 2: "blocked"}
-FORCE = {None: 0, "unblocked": 1, "blocked": 2}
+FORCE = {None: 0, "unblocked": 1, "blocked": 2, "qr": 3}
 
 
 class OrcOpts(ctypes.Structure):
@@ -48,6 +48,7 @@ class OrcOpts(ctypes.Structure):
         ("fused_updates", ctypes.c_int),
         ("row_block", ctypes.c_int),
         ("force", ctypes.c_int),
+        ("use_qr", ctypes.c_int),
     ]
 
 
@@ -62,7 +63,7 @@ class OrcInfo(ctypes.Structure):
         ("eig_calls", ctypes.c_int64),
         ("update_calls", ctypes.c_int64),
         ("status", ctypes.c_int32),
-        ("pad", ctypes.c_int32),
+        ("qr", ctypes.c_int32),
     ]
 
 
@@ -113,6 +114,7 @@ def _opts(opts=None, force=None) -> OrcOpts:
     o.fused_updates = int(bool(getattr(opts, "fused_updates", True)))
     o.row_block = int(getattr(opts, "row_block", 64))
     o.force = FORCE[force]
+    o.use_qr = int(bool(getattr(opts, "use_qr_preprocess", False)))
     return o
 
 
@@ -126,6 +128,8 @@ def unit_roundoff(dtype) -> float:
 
 def _info_dict(inf: OrcInfo) -> dict:
     path = PATHS[inf.path]
+    if inf.qr and path != "empty":
+        path = "qr+" + path
     if inf.transposed and path != "empty":
         path = "transpose+" + path
     return dict(

@@ -29,6 +29,7 @@ from .svd import (
     WorkCounters,
     svd_blocked,
     svd_dispatch,
+    svd_qr_preprocessed,
     svd_unblocked,
 )
 
@@ -61,6 +62,7 @@ __all__ = [
     "solve_tensor",
     "svd_blocked",
     "svd_dispatch",
+    "svd_qr_preprocessed",
     "svd_unblocked",
     "unit_roundoff",
     "__version__",

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libbsvd_b200.so")
 
 BSVD_OK = 0
-DISPATCH, FORCE_UNBLOCKED, FORCE_BLOCKED = 0, 1, 2
+DISPATCH, FORCE_UNBLOCKED, FORCE_BLOCKED, FORCE_QR = 0, 1, 2, 3
 
 
 class BsvdOpts(ctypes.Structure):
@@ -29,7 +29,8 @@ class BsvdOpts(ctypes.Structure):
         ("fused_updates", ctypes.c_int),
         ("row_block", ctypes.c_int),
         ("kernel", ctypes.c_int),
-        ("reserved", ctypes.c_int * 3),
+        ("use_qr", ctypes.c_int),
+        ("reserved", ctypes.c_int * 2),
     ]
 
 

@@ -29,7 +29,8 @@ from .svd import QR_RATIO, SMALL_CUTOFF, JacobiOptions, SolveInfo, SvdResult, Wo
 
 __all__ = ["BatchState", "batch_svd", "convergence_scan"]
 
-_ROUTE = {None: _lib.DISPATCH, "unblocked": _lib.FORCE_UNBLOCKED, "blocked": _lib.FORCE_BLOCKED}
+_ROUTE = {None: _lib.DISPATCH, "unblocked": _lib.FORCE_UNBLOCKED, "blocked": _lib.FORCE_BLOCKED,
+          "qr": _lib.FORCE_QR}
 
 
 @dataclass
@@ -91,6 +92,7 @@ class _Prep:
     blocked: bool
     trivial: bool
     pairs_per_sweep: int
+    qr: bool = False
 
 
 def _prepare(a, opts: JacobiOptions, force: str | None) -> _Prep:
@@ -105,8 +107,8 @@ def _prepare(a, opts: JacobiOptions, force: str | None) -> _Prep:
     trans = force is None and m < n
     bm, bn = (n, m) if trans else (m, n)
     trivial = bm == 0 or bn == 0
-    if not trivial and force is None and opts.use_qr_preprocess and bm >= QR_RATIO * bn:
-        raise NotImplementedError("QR-preprocessed route (use_qr_preprocess) is not built on the B200 path yet")
+    # QR first (src/svd.py:364-371): forced, or dispatch with use_qr_preprocess and bm >= 3 bn
+    qr = not trivial and (force == "qr" or (force is None and opts.use_qr_preprocess and bm >= QR_RATIO * bn))
     if force == "unblocked":
         blocked = False
     elif force == "blocked":
@@ -120,7 +122,7 @@ def _prepare(a, opts: JacobiOptions, force: str | None) -> _Prep:
     else:
         ell = ceil(bn / opts.nb)
         pps = ell * (ell - 1) // 2 if ell >= 2 else 1
-    return _Prep(a=a, m=m, n=n, bn=bn, trans=trans, blocked=blocked, trivial=trivial, pairs_per_sweep=pps)
+    return _Prep(a=a, m=m, n=n, bn=bn, trans=trans, blocked=blocked, trivial=trivial, pairs_per_sweep=pps, qr=qr)
 
 
 def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rounds: bool):
@@ -209,7 +211,7 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
         cnt.masked_pair_skips = masked
         cnt.t_eig = dtime
         base = "blocked" if (int(inf["path"]) & 0xFF) == 2 else "unblocked"
-        path = ("transpose+" if int(inf["path"]) & 0x100 else "") + base
+        path = ("transpose+" if int(inf["path"]) & 0x100 else "") + ("qr+" if int(inf["path"]) & 0x200 else "") + base
         info = SolveInfo(converged=conv, outer_sweeps=s_i, inner_rotations=int(inf["rotations"]),
                          masked_pair_skips=masked, path=path, counters=cnt)
         results[idx] = SvdResult(u=U, sigma=S, v=V if opts.compute_right_vectors else None, info=info)

@@ -29,7 +29,7 @@ int esize_of(int dt) { return dt == BSVD_S ? 4 : dt == BSVD_D ? 8 : dt == BSVD_C
 int rsize_of(int dt) { return (dt == BSVD_S || dt == BSVD_C) ? 4 : 8; }
 
 struct Route {
-    int trans, bm, bn, blocked, need_v;
+    int trans, bm, bn, blocked, need_v, qr;
 };
 
 int make_route(int m, int n, const bsvd_opts* o, Route* r) {
@@ -37,6 +37,10 @@ int make_route(int m, int n, const bsvd_opts* o, Route* r) {
     r->trans = (o->route == BSVD_DISPATCH && m < n) ? 1 : 0;
     r->bm = r->trans ? n : m;
     r->bn = r->trans ? m : n;
+    // QR first (src/svd.py:364-371): forced, or dispatch with use_qr_preprocess and bm >= 3 bn (QR_RATIO)
+    r->qr = (r->bn > 0 && (o->route == BSVD_FORCE_QR ||
+                           (o->route == BSVD_DISPATCH && o->use_qr && (double)r->bm >= 3.0 * r->bn)))
+                ? 1 : 0;
     if (o->route == BSVD_FORCE_UNBLOCKED) r->blocked = 0;
     else if (o->route == BSVD_FORCE_BLOCKED) r->blocked = 1;
     else r->blocked = r->bn > 32;  // SMALL_CUTOFF, src/svd.py:52
@@ -87,7 +91,7 @@ int check_opts(const bsvd_opts* o) {
     if (!o) return BSVD_ERR_ARG;
     if (!(o->k > 0) || o->max_sweeps < 1 || o->nb < 1 || o->inner_sweeps < 0 || o->row_block < 1)
         return BSVD_ERR_ARG;
-    if (o->route < 0 || o->route > 2) return BSVD_ERR_ARG;
+    if (o->route < 0 || o->route > 3) return BSVD_ERR_ARG;
     return BSVD_OK;
 }
 
@@ -209,6 +213,15 @@ int bsvd_select_kernel(int dtype, int m, int n, const bsvd_opts* opts) {
     Route r;
     if (make_route(m, n, opts, &r)) return BSVD_ERR_ARG;
     if (r.bn == 0 || r.bm == 0) return 0;
+    if (r.qr) {  // the kernel that solves R
+        Route rr = r;
+        rr.trans = 0;
+        rr.bm = r.bn;
+        rr.blocked = r.bn > 32;
+        rr.need_v = 1;
+        rr.qr = 0;
+        return make_plan(dtype, rr, opts).kernel;
+    }
     return make_plan(dtype, r, opts).kernel;
 }
 
@@ -304,14 +317,85 @@ int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch, const void* A, v
     return rc;
 }
 
+extern "C++" {
+namespace {
+// QR route workspace: reflectors (bm x bn) | R (bn x bn) | phases (bn) | U_R (bn x bn) | inner solve
+struct QrWs {
+    size_t refl, r, ph, ur, inner_off, total;
+    bsvd_opts io;
+};
+QrWs qr_ws(int dtype, const Route& r, int batch, const bsvd_opts* o) {
+    QrWs q{};
+    const size_t es = (size_t)esize_of(dtype), B = (size_t)batch;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    q.io = *o;
+    q.io.route = r.bn <= 32 ? BSVD_FORCE_UNBLOCKED : BSVD_FORCE_BLOCKED;
+    q.io.use_qr = 0;
+    q.io.want_v = r.trans ? 1 : o->want_v;
+    q.refl = 0;
+    q.r = al(B * r.bm * r.bn * es);
+    q.ph = q.r + al(B * r.bn * r.bn * es);
+    q.ur = q.ph + al(B * r.bn * es);
+    q.inner_off = q.ur + al(B * r.bn * r.bn * es);
+    q.total = q.inner_off + bsvd_workspace_bytes(dtype, r.bn, r.bn, batch, &q.io);
+    return q;
+}
+}  // namespace
+}  // extern "C++"
+
 size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts* opts) {
     if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || check_opts(opts)) return 0;
     Route r;
     if (make_route(m, n, opts, &r)) return 0;
     if (r.bn == 0 || r.bm == 0) return 0;
+    if (r.qr) return qr_ws(dtype, r, batch, opts).total;
     const Plan p = make_plan(dtype, r, opts);
     return p.work_elems * (size_t)esize_of(dtype) * (size_t)batch;
 }
+
+extern "C++" {
+namespace {
+template <class T>
+int run_qr(int dtype, const Route& r, int m, int n, int batch, const void* A, int64_t lda, int64_t sA, void* U,
+           int64_t ldu, int64_t sU, void* S, int64_t sS, void* V, int64_t ldv, int64_t sV, const bsvd_opts* o,
+           bsvd_info* info, void* work, size_t work_bytes, cudaStream_t st) {
+    const QrWs q = qr_ws(dtype, r, batch, o);
+    if (q.total > work_bytes || !work) return BSVD_ERR_WORKSPACE;
+    if (qr_smem(sizeof(T), r.bm, r.bn) > smem_limit()) return BSVD_ERR_UNSUPPORTED;
+    unsigned char* w = static_cast<unsigned char*>(work);
+    T* refl = reinterpret_cast<T*>(w + q.refl);
+    T* R = reinterpret_cast<T*>(w + q.r);
+    T* ph = reinterpret_cast<T*>(w + q.ph);
+    T* UR = reinterpret_cast<T*>(w + q.ur);
+    SolveArgs<T> a{};
+    a.A = static_cast<const T*>(A);
+    a.lda = lda;
+    a.strideA = sA;
+    a.m = m;
+    a.n = n;
+    a.trans = r.trans;
+    a.bm = r.bm;
+    a.bn = r.bn;
+    a.batch = batch;
+    a.info = info;
+    int rc = launch_qr<T>(a, R, refl, ph, st);
+    if (rc) return rc;
+    const int bn = r.bn;
+    // Jacobi SVD of R (bn x bn): U_R to the workspace; V_R is the caller's V (or, transposed, the caller's U)
+    void* Vi = r.trans ? U : (o->want_v ? V : nullptr);
+    const int64_t ldvi = r.trans ? ldu : ldv, svi = r.trans ? sU : sV;
+    rc = bsvd_gesvj_batched(dtype, bn, bn, batch, R, bn, (int64_t)bn * bn, UR, bn, (int64_t)bn * bn, S, sS, Vi,
+                            ldvi, svi, &q.io, info, w + q.inner_off, work_bytes - q.inner_off, st);
+    if (rc) return rc;
+    // left factor U = Q diag(p) U_R (src/svd.py:529-530); transposed: that is the caller's V
+    if (!r.trans) rc = launch_applyq<T>(r.bm, bn, batch, refl, ph, UR, static_cast<T*>(U), ldu, sU, st);
+    else if (o->want_v) rc = launch_applyq<T>(r.bm, bn, batch, refl, ph, UR, static_cast<T*>(V), ldv, sV, st);
+    if (rc) return rc;
+    if (info) rc = launch_qr_path(info, batch, 0x200 | (r.trans ? 0x100 : 0), st);
+    return rc;
+}
+}  // namespace
+}  // extern "C++"
 
 int bsvd_gesvj_batched(int dtype, int m, int n, int batch, const void* A, int64_t lda, int64_t strideA, void* U,
                        int64_t ldu, int64_t strideU, void* S, int64_t strideS, void* V, int64_t ldv,
@@ -337,6 +421,22 @@ int bsvd_gesvj_batched(int dtype, int m, int n, int batch, const void* A, int64_
     if (opts->want_v && (!V || ldv < n)) return BSVD_ERR_ARG;
     if (batch > 1 && (strideA < lda * (int64_t)n || strideU < ldu * (int64_t)k || strideS < k)) return BSVD_ERR_ARG;
     if (batch > 1 && opts->want_v && strideV < ldv * (int64_t)k) return BSVD_ERR_ARG;
+    if (r.qr) {
+        switch (dtype) {
+            case BSVD_S:
+                return run_qr<float>(dtype, r, m, n, batch, A, lda, strideA, U, ldu, strideU, S, strideS, V, ldv,
+                                     strideV, opts, info, work, work_bytes, st);
+            case BSVD_D:
+                return run_qr<double>(dtype, r, m, n, batch, A, lda, strideA, U, ldu, strideU, S, strideS, V, ldv,
+                                      strideV, opts, info, work, work_bytes, st);
+            case BSVD_C:
+                return run_qr<cx<float>>(dtype, r, m, n, batch, A, lda, strideA, U, ldu, strideU, S, strideS, V,
+                                         ldv, strideV, opts, info, work, work_bytes, st);
+            default:
+                return run_qr<cx<double>>(dtype, r, m, n, batch, A, lda, strideA, U, ldu, strideU, S, strideS, V,
+                                          ldv, strideV, opts, info, work, work_bytes, st);
+        }
+    }
     const Plan p = make_plan(dtype, r, opts, lda == m);
     if (!p.kernel) return BSVD_ERR_UNSUPPORTED;
     const size_t need = p.work_elems * (size_t)esize_of(dtype) * (size_t)batch;

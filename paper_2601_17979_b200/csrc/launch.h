@@ -43,6 +43,13 @@ template <class T>
 int launch_finalize_ws(SolveArgs<T> a, cudaStream_t st);
 template <class T>
 int launch_finalize_gm(SolveArgs<T> a, cudaStream_t st);
+template <class T>
+int launch_qr(SolveArgs<T> a, T* R, T* refl, T* phase, cudaStream_t st);
+template <class T>
+int launch_applyq(int bm, int bn, int batch, const T* refl, const T* phase, const T* UR, T* Out, int64_t ldo,
+                  int64_t so, cudaStream_t st);
+int launch_qr_path(bsvd_info* info, int batch, int bits, cudaStream_t st);
+size_t qr_smem(int esize, int bm, int bn);
 Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, int inner_sweeps);
 int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 

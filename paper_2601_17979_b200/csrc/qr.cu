@@ -1,0 +1,264 @@
+// qr.cu -- the "qr+" route: batched Householder QR pre-processing of tall
+// problems and the back-transformation of the left factor.
+//
+// householder_qr (src/core.py:118-168) per problem, one CTA each, the working
+// matrix b (A, or A^H on the transpose route) staged in shared memory:
+//   for k: x = b[k:, k]; ||x|| (float64); phase = x0/|x0| (1 if x0 = 0);
+//          v = x + phase ||x|| e1, v /= ||v||; b[k:, k:] -= 2 v (v^H b[k:, k:]);
+//          b[k, k] = -phase ||x||, b[k+1:, k] = 0   (zero x or zero v: no reflector)
+//   sign convention: p_k = r_kk/|r_kk|, R row k *= conj(p_k), Q column k *= p_k.
+// The reflectors v_k (zero when skipped) and the phases p_k go to the
+// workspace; Q is never formed.  The Jacobi solve then runs on the n x n R
+// (src/svd.py:364-371) and the left factor is U = Q diag(p) U_R (src/svd.py:
+// 529-530), applied as H_0 ... H_{n-1} [diag(p) U_R; 0] (the reflectors in
+// reverse order, like LAPACK's ormqr) by k_applyq.
+#include "kernel_args.cuh"
+#include "launch.h"
+
+namespace bsvd {
+namespace qr {
+
+template <class T>
+BSVD_DEV T mulT(T a, T b) {
+    if constexpr (tr<T>::cplx) return T{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+    else return a * b;
+}
+template <class T>
+BSVD_DEV T conjT_(T a) {
+    if constexpr (tr<T>::cplx) return T{a.re, -a.im};
+    else return a;
+}
+template <class T>
+BSVD_DEV T subT(T a, T b) {
+    if constexpr (tr<T>::cplx) return T{a.re - b.re, a.im - b.im};
+    else return a - b;
+}
+template <class T>
+BSVD_DEV T addT(T a, T b) {
+    if constexpr (tr<T>::cplx) return T{a.re + b.re, a.im + b.im};
+    else return a + b;
+}
+template <class T>
+BSVD_DEV T scaleT(T a, double s) {
+    if constexpr (tr<T>::cplx) return T{(decltype(a.re))(a.re * s), (decltype(a.re))(a.im * s)};
+    else return (T)(a * s);
+}
+template <class T>
+BSVD_DEV double abs2T(T a) {
+    if constexpr (tr<T>::cplx) return (double)a.re * a.re + (double)a.im * a.im;
+    else return (double)a * a;
+}
+template <class T>
+BSVD_DEV T fromRe(double x) {
+    if constexpr (tr<T>::cplx) return T{(decltype(T{}.re))x, 0};
+    else return (T)x;
+}
+// x / |x| (1 for x = 0), computed in float64
+template <class T>
+BSVD_DEV T unit_phase(T x) {
+    const double a2 = abs2T(x);
+    if (!(a2 > 0.0)) return fromRe<T>(1.0);
+    if constexpr (tr<T>::cplx) {
+        const double inv = 1.0 / sqrt(a2);
+        return T{(decltype(x.re))(x.re * inv), (decltype(x.re))(x.im * inv)};
+    } else {
+        return x > 0 ? (T)1 : (T)-1;
+    }
+}
+
+// CTA sum of a double (blockDim multiple of 32, <= 1024); all threads get the result
+BSVD_DEV double cta_sum(double v, double* scratch) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) scratch[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < nw; ++i) s += scratch[i];  // fixed order: identical on every thread
+    return s;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_qr(SolveArgs<T> a, T* R, T* refl, T* phase) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int prob = blockIdx.x;
+    const int bm = a.bm, bn = a.bn, tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    T* B = reinterpret_cast<T*>(smem);  // bm x bn, ld bm
+    double* scratch = reinterpret_cast<double*>(smem + (((size_t)bm * bn * sizeof(T) + 15) & ~size_t(15)));
+    T* bc = reinterpret_cast<T*>(scratch + 32);  // broadcast slots: [0] v0/||v||, [1] inv||v||, [2] r_kk
+    int* flag = reinterpret_cast<int*>(bc + 4);
+    T* Vk = refl + (size_t)prob * bm * bn;
+    const T* Ap = a.A + (size_t)prob * a.strideA;
+    int bad = 0;
+    for (int e = tid; e < bm * bn; e += nt) {  // kernel (1): b = A, or A^H on the transpose route
+        const int r = e % bm, c = e / bm;
+        const T x = a.trans ? conjT_(Ap[c + (size_t)r * a.lda]) : Ap[r + (size_t)c * a.lda];
+        bad |= !finiteT(x);
+        B[e] = x;
+    }
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    if (bad) atomicOr(flag, 1);
+    for (int k = 0; k < bn; ++k) {
+        double s = 0.0;
+        for (int r = k + tid; r < bm; r += nt) s += abs2T(B[r + k * bm]);
+        s = cta_sum(s, scratch);
+        const double norm_x = sqrt(s);
+        const T alpha = B[k + k * bm];
+        const T ph = unit_phase(alpha);
+        const T v0 = addT(alpha, scaleT(ph, norm_x));
+        const double vn = sqrt(fmax(s - abs2T(alpha), 0.0) + abs2T(v0));
+        const bool skip = !(norm_x > 0.0) || !(vn > 0.0);
+        const double iv = skip ? 0.0 : 1.0 / vn;
+        // v (zero when skipped) -> workspace and column k of B
+        for (int r = tid; r < bm; r += nt) {
+            T v = fromRe<T>(0.0);
+            if (r == k) v = scaleT(v0, iv);
+            else if (r > k) v = scaleT(B[r + k * bm], iv);
+            Vk[r + (size_t)k * bm] = v;
+            if (r > k) B[r + k * bm] = v;
+        }
+        if (tid == 0) bc[0] = scaleT(v0, iv);
+        __syncthreads();
+        if (!skip) {
+            const T vk0 = bc[0];
+            // trailing columns j > k: w_j = v^H b[k:, j]; b[k:, j] -= 2 v w_j (one warp per column)
+            for (int j = k + 1 + warp; j < bn; j += nw) {
+                double wr = 0.0, wi = 0.0;
+                for (int r = k + lane; r < bm; r += 32) {
+                    const T v = (r == k) ? vk0 : B[r + k * bm];
+                    const T p = mulT(conjT_(v), B[r + j * bm]);
+                    if constexpr (tr<T>::cplx) {
+                        wr += p.re;
+                        wi += p.im;
+                    } else {
+                        wr += p;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    wr += __shfl_xor_sync(0xffffffffu, wr, o);
+                    wi += __shfl_xor_sync(0xffffffffu, wi, o);
+                }
+                T w2;
+                if constexpr (tr<T>::cplx) w2 = T{(decltype(w2.re))(2.0 * wr), (decltype(w2.re))(2.0 * wi)};
+                else w2 = (T)(2.0 * wr);
+                for (int r = k + lane; r < bm; r += 32) {
+                    const T v = (r == k) ? vk0 : B[r + k * bm];
+                    B[r + j * bm] = subT(B[r + j * bm], mulT(v, w2));
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && !skip) B[k + k * bm] = scaleT(ph, -norm_x);  // exact value (src/core.py:142)
+        __syncthreads();
+    }
+    // sign convention and R out (bn x bn, ld bn, zeros below the diagonal)
+    T* Rp = R + (size_t)prob * bn * bn;
+    T* Pp = phase + (size_t)prob * bn;
+    for (int e = tid; e < bn * bn; e += nt) {
+        const int r = e % bn, c = e / bn;
+        T x = fromRe<T>(0.0);
+        if (r <= c) {
+            const T dkk = B[r + r * bm];
+            const T p = unit_phase(dkk);
+            x = (r == c) ? fromRe<T>(sqrt(abs2T(dkk))) : mulT(B[r + c * bm], conjT_(p));
+        }
+        Rp[e] = x;
+    }
+    for (int k = tid; k < bn; k += nt) Pp[k] = unit_phase(B[k + k * bm]);
+    if (tid == 0 && a.info) a.info[prob].status = *flag;  // provisional; the inner solve rewrites info
+}
+
+// Out (bm x bn, ld ldo) = H_0 ... H_{bn-1} [diag(p) U_R; 0]
+template <class T>
+__global__ void __launch_bounds__(256) k_applyq(int bm, int bn, const T* refl, const T* phase, const T* UR,
+                                                T* Out, int64_t ldo, int64_t so) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int prob = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    T* Y = reinterpret_cast<T*>(smem);  // bm x bn
+    const T* Vk = refl + (size_t)prob * bm * bn;
+    const T* Pp = phase + (size_t)prob * bn;
+    const T* U = UR + (size_t)prob * bn * bn;
+    for (int e = tid; e < bm * bn; e += nt) {
+        const int r = e % bm, c = e / bm;
+        Y[e] = r < bn ? mulT(Pp[r], U[r + (size_t)c * bn]) : fromRe<T>(0.0);
+    }
+    __syncthreads();
+    for (int k = bn - 1; k >= 0; --k) {
+        const T* v = Vk + (size_t)k * bm;
+        for (int j = warp; j < bn; j += nw) {
+            double wr = 0.0, wi = 0.0;
+            for (int r = k + lane; r < bm; r += 32) {
+                const T p = mulT(conjT_(v[r]), Y[r + j * bm]);
+                if constexpr (tr<T>::cplx) {
+                    wr += p.re;
+                    wi += p.im;
+                } else {
+                    wr += p;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                wr += __shfl_xor_sync(0xffffffffu, wr, o);
+                wi += __shfl_xor_sync(0xffffffffu, wi, o);
+            }
+            T w2;
+            if constexpr (tr<T>::cplx) w2 = T{(decltype(w2.re))(2.0 * wr), (decltype(w2.re))(2.0 * wi)};
+            else w2 = (T)(2.0 * wr);
+            for (int r = k + lane; r < bm; r += 32) Y[r + j * bm] = subT(Y[r + j * bm], mulT(v[r], w2));
+        }
+        __syncthreads();
+    }
+    T* O = Out + (size_t)prob * so;
+    for (int e = tid; e < bm * bn; e += nt) O[(e % bm) + (size_t)(e / bm) * ldo] = Y[e];
+}
+
+__global__ void k_qr_path(bsvd_info* info, int batch, int bits) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < batch) info[i].path |= bits;
+}
+
+}  // namespace qr
+
+size_t qr_smem(int esize, int bm, int bn) { return (((size_t)bm * bn * esize + 15) & ~size_t(15)) + 32 * 8 + 4 * 16 + 16; }
+
+template <class T>
+int launch_qr(SolveArgs<T> a, T* R, T* refl, T* phase, cudaStream_t st) {
+    const size_t smem = qr_smem(sizeof(T), a.bm, a.bn);
+    auto k = qr::k_qr<T>;
+    if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<a.batch, 256, smem, st>>>(a, R, refl, phase);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+template <class T>
+int launch_applyq(int bm, int bn, int batch, const T* refl, const T* phase, const T* UR, T* Out, int64_t ldo,
+                  int64_t so, cudaStream_t st) {
+    const size_t smem = (size_t)bm * bn * sizeof(T);
+    auto k = qr::k_applyq<T>;
+    if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<batch, 256, smem, st>>>(bm, bn, refl, phase, UR, Out, ldo, so);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+int launch_qr_path(bsvd_info* info, int batch, int bits, cudaStream_t st) {
+    qr::k_qr_path<<<(batch + 255) / 256, 256, 0, st>>>(info, batch, bits);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+#define BSVD_QR_INST(T)                                                                                   \
+    template int launch_qr<T>(SolveArgs<T>, T*, T*, T*, cudaStream_t);                                    \
+    template int launch_applyq<T>(int, int, int, const T*, const T*, const T*, T*, int64_t, int64_t,      \
+                                  cudaStream_t);
+BSVD_QR_INST(float)
+BSVD_QR_INST(double)
+BSVD_QR_INST(cx<float>)
+BSVD_QR_INST(cx<double>)
+
+}  // namespace bsvd

@@ -80,6 +80,7 @@ def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0, stagger: int = 
     o.fused_updates = int(bool(opts.fused_updates))
     o.row_block = int(opts.row_block)
     o.kernel = int(kernel)
+    o.use_qr = int(bool(opts.use_qr_preprocess))
     o.reserved[0] = int(stagger)
     return o
 

@@ -120,6 +120,11 @@ def svd_blocked(a, opts: JacobiOptions | None = None) -> SvdResult:
     return _run_standalone(a, opts, force="blocked")
 
 
+def svd_qr_preprocessed(a, opts: JacobiOptions | None = None) -> SvdResult:
+    """QR first, Jacobi SVD on the small R factor, then U = Q @ Uhat (src/svd.py:569-571); m >= n."""
+    return _run_standalone(a, opts, force="qr")
+
+
 def svd_dispatch(a, opts: JacobiOptions | None = None) -> SvdResult:
     """Shape-aware entry point (src/svd.py:574-582)."""
     return _run_standalone(a, opts, force=None)

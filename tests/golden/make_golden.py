@@ -53,7 +53,8 @@ cases: list[dict] = []
 
 def add_solve(cid, a, force=None, **kw):
     opts = bsvd.JacobiOptions(**kw)
-    fn = {None: bsvd.svd_dispatch, "unblocked": bsvd.svd_unblocked, "blocked": bsvd.svd_blocked}[force]
+    fn = {None: bsvd.svd_dispatch, "unblocked": bsvd.svd_unblocked, "blocked": bsvd.svd_blocked,
+          "qr": bsvd.svd_qr_preprocessed}[force]
     r = fn(a, opts)
     arrays[f"{cid}__a"] = np.asarray(a)
     arrays[f"{cid}__u"] = r.u
@@ -123,6 +124,14 @@ def main():
     add_solve("blk_wide_40x96", random_matrix(40, 96, seed=38))
     add_solve("unb_k1_20", random_matrix(20, 20, seed=39), force="unblocked", k=1.0, max_nsweeps=100)
     add_solve("unb_cap_32", random_matrix(32, 32, seed=40), force="unblocked", max_nsweeps=3)
+    # --- QR-preprocessed route (src/core.py:118-168, src/svd.py:364-371; tests/test_svd.py:250-262) ---
+    add_solve("qr_f64_600x16", random_matrix(600, 16, seed=50), use_qr_preprocess=True)
+    add_solve("qr_f64_300x90", random_matrix(300, 90, seed=51), use_qr_preprocess=True)
+    add_solve("qr_c128_256x32", random_matrix(256, 32, np.complex128, seed=52), use_qr_preprocess=True)
+    add_solve("qr_f32_96x20", random_matrix(96, 20, np.float32, seed=53), force="qr")
+    add_solve("qr_c64_20x70", random_matrix(20, 70, np.complex64, seed=54), use_qr_preprocess=True)
+    add_solve("qr_f64_512x16_c07", random_matrix(512, 16, seed=7000), force="qr")
+    add_solve("qr_f64_40x30_forced", random_matrix(40, 30, seed=55), force="qr", compute_right_vectors=False)
 
     # --- kernel-level vectors (bitwise restatement checks) ---
     kern = []

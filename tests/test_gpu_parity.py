@@ -17,7 +17,8 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
-FORCE_FN = {None: bs.svd_dispatch, "unblocked": bs.svd_unblocked, "blocked": bs.svd_blocked}
+FORCE_FN = {None: bs.svd_dispatch, "unblocked": bs.svd_unblocked, "blocked": bs.svd_blocked,
+            "qr": bs.svd_qr_preprocessed}
 
 
 def _opts(d):

@@ -24,7 +24,9 @@ def _solve_case(golden, cid):
 def _unblocked_bitwise(c):
     # the unblocked path is bitwise except where finalize's zero-column completion
     # calls BLAS (np.vdot / np.linalg.norm, src/svd.py:224-240)
-    return c["path"].endswith("unblocked") and c["id"] not in ("ka_zerocol", "ka_zero4")
+    # the qr+ route runs numpy/BLAS Householder QR first (src/core.py:118-168): tolerance only
+    return (c["path"].endswith("unblocked") and "qr+" not in c["path"]
+            and c["id"] not in ("ka_zerocol", "ka_zero4"))
 
 
 def test_golden_cases_unblocked_bitwise(golden):
