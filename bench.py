@@ -63,6 +63,9 @@ CONFIGS = {
                        route="blocked"),
     "c5": dict(desc="C5: 2000 x 128x128 FP64 random, blocked (ell=8)", family="random", m=128, n=128, batch=2000,
                dtype="float64", kappa=1.0, want_v=True, route=None),
+    "c4-qr": dict(desc="C4: 5000 x 256x32 complex128 random, QR-preprocessed route (use_qr_preprocess)",
+                  family="random", m=256, n=32, batch=5000, dtype="complex128", kappa=1.0, want_v=True,
+                  route=None, use_qr=True),
 }
 
 
@@ -76,13 +79,18 @@ def log(*a):
 def flops_per_problem(info: dict, m: int, n: int, cplx: bool, want_v: bool, nb: int = 16) -> float:
     bm, bn = max(m, n), min(m, n)
     f = 0.0
+    if "qr+" in info["path"]:
+        # Householder QR (2 m n^2 - 2/3 n^3) and U = Q Uhat applied as reflectors (4 m n^2 - 2 n^3),
+        # then the Jacobi solve of the n x n R by the formulas below
+        f += 2.0 * bm * bn * bn - 2.0 * bn ** 3 / 3.0 + 4.0 * bm * bn * bn - 2.0 * bn ** 3
+        bm = bn
     if info["path"].endswith("unblocked"):
         S, R = info["outer_sweeps"], info["inner_rotations"]
-        f = S * bn * (bn - 1) / 2 * 6 * bm + R * 6 * (bm + (bn if want_v else 0))
+        f += S * bn * (bn - 1) / 2 * 6 * bm + R * 6 * (bm + (bn if want_v else 0))
     else:
         w = min(2 * nb, bn)
         G, R, Up = info["gram_calls"], info["inner_rotations"], info["update_calls"]
-        f = G * w * (w + 1) * bm + R * 12 * w + Up * 2 * w * w * (bm + (bn if want_v else 0))
+        f += G * w * (w + 1) * bm + R * 12 * w + Up * 2 * w * w * (bm + (bn if want_v else 0))
     return f * (4.0 if cplx else 1.0)
 
 
@@ -149,7 +157,7 @@ def oracle_time(a_host3, cfg, nthreads, count):
     from oracle import oracle as O
     from paper_2601_17979_b200 import JacobiOptions
 
-    opts = JacobiOptions(compute_right_vectors=cfg["want_v"])
+    opts = JacobiOptions(compute_right_vectors=cfg["want_v"], use_qr_preprocess=cfg.get("use_qr", False))
     t = time.perf_counter()
     _, _, _, infos = O.solve_batch(a_host3[:count], opts, cfg["route"], nthreads=nthreads)
     return count, time.perf_counter() - t, infos
@@ -160,7 +168,7 @@ def oracle_sample(a_host3, cfg, nthreads, max_seconds=None, min_count=16):
     from oracle import oracle as O
     from paper_2601_17979_b200 import JacobiOptions
 
-    opts = JacobiOptions(compute_right_vectors=cfg["want_v"])
+    opts = JacobiOptions(compute_right_vectors=cfg["want_v"], use_qr_preprocess=cfg.get("use_qr", False))
     B = a_host3.shape[0]
     count = min(B, max(min_count, nthreads * 2))
     t = time.perf_counter()
@@ -221,7 +229,8 @@ def dtype_tag(cfg):
 
 def config_block(cfg, args):
     return {"workload": cfg["desc"], "config_id": args.config, "batch_per_gpu": cfg["batch"], "m": cfg["m"],
-            "n": cfg["n"], "dtype": cfg["dtype"], "want_v": cfg["want_v"], "route": cfg["route"] or "dispatch",
+            "n": cfg["n"], "dtype": cfg["dtype"], "want_v": cfg["want_v"],
+            "route": (cfg["route"] or "dispatch") + ("+use_qr_preprocess" if cfg.get("use_qr") else ""),
             "parallelism": f"batch split x{args.gpus} (no collective)",
             "l2": "flushed between timed steps (512 MiB write); inputs device-resident"}
 
@@ -281,7 +290,7 @@ def run_b200(args, cfg):
     cplx = dt.kind == "c"
     m, n, B = cfg["m"], cfg["n"], cfg["batch"]
     k = min(m, n)
-    opts = bs.JacobiOptions(compute_right_vectors=cfg["want_v"])
+    opts = bs.JacobiOptions(compute_right_vectors=cfg["want_v"], use_qr_preprocess=cfg.get("use_qr", False))
     route = {None: _lib.DISPATCH, "blocked": _lib.FORCE_BLOCKED, "unblocked": _lib.FORCE_UNBLOCKED}[cfg["route"]]
     # each rank its own problems (weak scaling): seed offset by rank
     a = gen_batch_device(cfg["family"], m, n, B, dt, kappa=cfg["kappa"], seed=1000 * rank, rank=cfg.get("rank"),

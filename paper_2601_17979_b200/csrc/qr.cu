@@ -84,11 +84,15 @@ __global__ void __launch_bounds__(256) k_qr(SolveArgs<T> a, T* R, T* refl, T* ph
     extern __shared__ __align__(16) unsigned char smem[];
     const int prob = blockIdx.x;
     const int bm = a.bm, bn = a.bn, tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-    T* B = reinterpret_cast<T*>(smem);  // bm x bn, ld bm
-    double* scratch = reinterpret_cast<double*>(smem + (((size_t)bm * bn * sizeof(T) + 15) & ~size_t(15)));
-    T* bc = reinterpret_cast<T*>(scratch + 32);  // broadcast slots: [0] v0/||v||, [1] inv||v||, [2] r_kk
-    int* flag = reinterpret_cast<int*>(bc + 4);
+    const int ldb = bm + 1;                     // padded: thread (segment, column) accesses spread over banks
+    T* B = reinterpret_cast<T*>(smem);          // bm x bn, ld bm + 1
+    T* vs = B + (size_t)ldb * bn;               // reflector k
+    const int nseg = nt / bn;
+    T* part = vs + bm;                          // partial dots [segments][bn]
+    T* wv = part + (size_t)nseg * bn;           // 2 w_j
+    const size_t soff = ((size_t)((bm + 1) * bn + bm + nseg * bn + bn) * sizeof(T) + 15) & ~size_t(15);
+    double* scratch = reinterpret_cast<double*>(smem + soff);
+    int* flag = reinterpret_cast<int*>(scratch + 32);
     T* Vk = refl + (size_t)prob * bm * bn;
     const T* Ap = a.A + (size_t)prob * a.strideA;
     int bad = 0;
@@ -96,63 +100,68 @@ __global__ void __launch_bounds__(256) k_qr(SolveArgs<T> a, T* R, T* refl, T* ph
         const int r = e % bm, c = e / bm;
         const T x = a.trans ? conjT_(Ap[c + (size_t)r * a.lda]) : Ap[r + (size_t)c * a.lda];
         bad |= !finiteT(x);
-        B[e] = x;
+        B[r + (size_t)c * ldb] = x;
     }
     if (tid == 0) *flag = 0;
     __syncthreads();
     if (bad) atomicOr(flag, 1);
+    const int j = tid % bn, sg = tid / bn;
     for (int k = 0; k < bn; ++k) {
         double s = 0.0;
-        for (int r = k + tid; r < bm; r += nt) s += abs2T(B[r + k * bm]);
+        for (int r = k + tid; r < bm; r += nt) s += abs2T(B[r + (size_t)k * ldb]);
         s = cta_sum(s, scratch);
         const double norm_x = sqrt(s);
-        const T alpha = B[k + k * bm];
+        const T alpha = B[k + (size_t)k * ldb];
         const T ph = unit_phase(alpha);
         const T v0 = addT(alpha, scaleT(ph, norm_x));
         const double vn = sqrt(fmax(s - abs2T(alpha), 0.0) + abs2T(v0));
         const bool skip = !(norm_x > 0.0) || !(vn > 0.0);
         const double iv = skip ? 0.0 : 1.0 / vn;
-        // v (zero when skipped) -> workspace and column k of B
-        for (int r = tid; r < bm; r += nt) {
+        for (int r = tid; r < bm; r += nt) {  // v (zero when skipped) -> workspace and smem
             T v = fromRe<T>(0.0);
             if (r == k) v = scaleT(v0, iv);
-            else if (r > k) v = scaleT(B[r + k * bm], iv);
+            else if (r > k) v = scaleT(B[r + (size_t)k * ldb], iv);
             Vk[r + (size_t)k * bm] = v;
-            if (r > k) B[r + k * bm] = v;
+            vs[r] = v;
         }
-        if (tid == 0) bc[0] = scaleT(v0, iv);
         __syncthreads();
-        if (!skip) {
-            const T vk0 = bc[0];
-            // trailing columns j > k: w_j = v^H b[k:, j]; b[k:, j] -= 2 v w_j (one warp per column)
-            for (int j = k + 1 + warp; j < bn; j += nw) {
-                double wr = 0.0, wi = 0.0;
-                for (int r = k + lane; r < bm; r += 32) {
-                    const T v = (r == k) ? vk0 : B[r + k * bm];
-                    const T p = mulT(conjT_(v), B[r + j * bm]);
-                    if constexpr (tr<T>::cplx) {
-                        wr += p.re;
-                        wi += p.im;
-                    } else {
-                        wr += p;
-                    }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    wr += __shfl_xor_sync(0xffffffffu, wr, o);
-                    wi += __shfl_xor_sync(0xffffffffu, wi, o);
-                }
-                T w2;
-                if constexpr (tr<T>::cplx) w2 = T{(decltype(w2.re))(2.0 * wr), (decltype(w2.re))(2.0 * wi)};
-                else w2 = (T)(2.0 * wr);
-                for (int r = k + lane; r < bm; r += 32) {
-                    const T v = (r == k) ? vk0 : B[r + k * bm];
-                    B[r + j * bm] = subT(B[r + j * bm], mulT(v, w2));
+        const int len = bm - k, seg = (len + nseg - 1) / nseg;
+        const int r0 = k + sg * seg, r1 = min(bm, r0 + seg);
+        const bool act = !skip && sg < nseg && j > k;
+        if (act) {  // trailing columns j > k: w_j = v^H b[k:, j]
+            double wr = 0.0, wi = 0.0;
+            for (int r = r0; r < r1; ++r) {
+                const T p = mulT(conjT_(vs[r]), B[r + (size_t)j * ldb]);
+                if constexpr (tr<T>::cplx) {
+                    wr += p.re;
+                    wi += p.im;
+                } else {
+                    wr += p;
                 }
             }
+            if constexpr (tr<T>::cplx) part[sg * bn + j] = T{(decltype(T{}.re))wr, (decltype(T{}.re))wi};
+            else part[sg * bn + j] = (T)wr;
         }
         __syncthreads();
-        if (tid == 0 && !skip) B[k + k * bm] = scaleT(ph, -norm_x);  // exact value (src/core.py:142)
+        if (!skip && tid < bn && tid > k) {
+            double wr = 0.0, wi = 0.0;
+            for (int q = 0; q < nseg; ++q) {
+                if constexpr (tr<T>::cplx) {
+                    wr += part[q * bn + tid].re;
+                    wi += part[q * bn + tid].im;
+                } else {
+                    wr += part[q * bn + tid];
+                }
+            }
+            if constexpr (tr<T>::cplx) wv[tid] = T{(decltype(T{}.re))(2.0 * wr), (decltype(T{}.re))(2.0 * wi)};
+            else wv[tid] = (T)(2.0 * wr);
+        }
+        __syncthreads();
+        if (act) {  // b[k:, j] -= 2 v w_j
+            const T w2 = wv[j];
+            for (int r = r0; r < r1; ++r) B[r + (size_t)j * ldb] = subT(B[r + (size_t)j * ldb], mulT(vs[r], w2));
+        }
+        if (tid == 0 && !skip) B[k + (size_t)k * ldb] = scaleT(ph, -norm_x);  // exact value (src/core.py:142)
         __syncthreads();
     }
     // sign convention and R out (bn x bn, ld bn, zeros below the diagonal)
@@ -162,38 +171,48 @@ __global__ void __launch_bounds__(256) k_qr(SolveArgs<T> a, T* R, T* refl, T* ph
         const int r = e % bn, c = e / bn;
         T x = fromRe<T>(0.0);
         if (r <= c) {
-            const T dkk = B[r + r * bm];
+            const T dkk = B[r + (size_t)r * ldb];
             const T p = unit_phase(dkk);
-            x = (r == c) ? fromRe<T>(sqrt(abs2T(dkk))) : mulT(B[r + c * bm], conjT_(p));
+            x = (r == c) ? fromRe<T>(sqrt(abs2T(dkk))) : mulT(B[r + (size_t)c * ldb], conjT_(p));
         }
         Rp[e] = x;
     }
-    for (int k = tid; k < bn; k += nt) Pp[k] = unit_phase(B[k + k * bm]);
+    for (int k = tid; k < bn; k += nt) Pp[k] = unit_phase(B[k + (size_t)k * ldb]);
     if (tid == 0 && a.info) a.info[prob].status = *flag;  // provisional; the inner solve rewrites info
 }
 
-// Out (bm x bn, ld ldo) = H_0 ... H_{bn-1} [diag(p) U_R; 0]
+// Out (bm x bn, ld ldo) = H_0 ... H_{bn-1} [diag(p) U_R; 0].  Y staged in shared memory with a
+// padded leading dimension; thread (segment s, column j) owns rows [s*seg, (s+1)*seg) of column j:
+// partial v^H Y[:, j] per segment -> smem -> summed per column -> rank-1 update of the own rows.
 template <class T>
 __global__ void __launch_bounds__(256) k_applyq(int bm, int bn, const T* refl, const T* phase, const T* UR,
                                                 T* Out, int64_t ldo, int64_t so) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int prob = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-    T* Y = reinterpret_cast<T*>(smem);  // bm x bn
+    const int ldy = bm + 1;
+    T* Y = reinterpret_cast<T*>(smem);                 // bm x bn, ld bm + 1
+    T* vs = Y + (size_t)ldy * bn;                      // reflector k (bm)
+    T* part = vs + bm;                                 // partial dots [segments][bn]
+    T* wv = part + (size_t)(nt / bn + 1) * bn;         // 2 w_j per column
     const T* Vk = refl + (size_t)prob * bm * bn;
     const T* Pp = phase + (size_t)prob * bn;
     const T* U = UR + (size_t)prob * bn * bn;
     for (int e = tid; e < bm * bn; e += nt) {
         const int r = e % bm, c = e / bm;
-        Y[e] = r < bn ? mulT(Pp[r], U[r + (size_t)c * bn]) : fromRe<T>(0.0);
+        Y[r + (size_t)c * ldy] = r < bn ? mulT(Pp[r], U[r + (size_t)c * bn]) : fromRe<T>(0.0);
     }
-    __syncthreads();
+    const int nseg = nt / bn;                          // row segments per column (threads beyond idle)
+    const int j = tid % bn, sg = tid / bn;
     for (int k = bn - 1; k >= 0; --k) {
         const T* v = Vk + (size_t)k * bm;
-        for (int j = warp; j < bn; j += nw) {
+        for (int r = k + tid; r < bm; r += nt) vs[r] = v[r];
+        __syncthreads();
+        const int len = bm - k, seg = (len + nseg - 1) / nseg;
+        const int r0 = k + sg * seg, r1 = min(bm, r0 + seg);
+        if (sg < nseg) {
             double wr = 0.0, wi = 0.0;
-            for (int r = k + lane; r < bm; r += 32) {
-                const T p = mulT(conjT_(v[r]), Y[r + j * bm]);
+            for (int r = r0; r < r1; ++r) {
+                const T p = mulT(conjT_(vs[r]), Y[r + (size_t)j * ldy]);
                 if constexpr (tr<T>::cplx) {
                     wr += p.re;
                     wi += p.im;
@@ -201,20 +220,32 @@ __global__ void __launch_bounds__(256) k_applyq(int bm, int bn, const T* refl, c
                     wr += p;
                 }
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                wr += __shfl_xor_sync(0xffffffffu, wr, o);
-                wi += __shfl_xor_sync(0xffffffffu, wi, o);
+            if constexpr (tr<T>::cplx) part[sg * bn + j] = T{(decltype(T{}.re))wr, (decltype(T{}.re))wi};
+            else part[sg * bn + j] = (T)wr;
+        }
+        __syncthreads();
+        if (tid < bn) {
+            double wr = 0.0, wi = 0.0;
+            for (int q = 0; q < nseg; ++q) {
+                if constexpr (tr<T>::cplx) {
+                    wr += part[q * bn + tid].re;
+                    wi += part[q * bn + tid].im;
+                } else {
+                    wr += part[q * bn + tid];
+                }
             }
-            T w2;
-            if constexpr (tr<T>::cplx) w2 = T{(decltype(w2.re))(2.0 * wr), (decltype(w2.re))(2.0 * wi)};
-            else w2 = (T)(2.0 * wr);
-            for (int r = k + lane; r < bm; r += 32) Y[r + j * bm] = subT(Y[r + j * bm], mulT(v[r], w2));
+            if constexpr (tr<T>::cplx) wv[tid] = T{(decltype(T{}.re))(2.0 * wr), (decltype(T{}.re))(2.0 * wi)};
+            else wv[tid] = (T)(2.0 * wr);
+        }
+        __syncthreads();
+        if (sg < nseg) {
+            const T w2 = wv[j];
+            for (int r = r0; r < r1; ++r) Y[r + (size_t)j * ldy] = subT(Y[r + (size_t)j * ldy], mulT(vs[r], w2));
         }
         __syncthreads();
     }
     T* O = Out + (size_t)prob * so;
-    for (int e = tid; e < bm * bn; e += nt) O[(e % bm) + (size_t)(e / bm) * ldo] = Y[e];
+    for (int e = tid; e < bm * bn; e += nt) O[(e % bm) + (size_t)(e / bm) * ldo] = Y[(e % bm) + (size_t)(e / bm) * ldy];
 }
 
 __global__ void k_qr_path(bsvd_info* info, int batch, int bits) {
@@ -224,7 +255,12 @@ __global__ void k_qr_path(bsvd_info* info, int batch, int bits) {
 
 }  // namespace qr
 
-size_t qr_smem(int esize, int bm, int bn) { return (((size_t)bm * bn * esize + 15) & ~size_t(15)) + 32 * 8 + 4 * 16 + 16; }
+int qr_threads(int bn) { return bn > 256 ? 0 : 256; }  // 256 / bn row segments per column, rest idle
+size_t qr_smem(int esize, int bm, int bn) {
+    const int nt = qr_threads(bn);
+    if (!nt) return ~(size_t)0;
+    return ((((size_t)(bm + 1) * bn + bm + (size_t)(nt / bn) * bn + bn) * esize + 15) & ~size_t(15)) + 32 * 8 + 16;
+}
 
 template <class T>
 int launch_qr(SolveArgs<T> a, T* R, T* refl, T* phase, cudaStream_t st) {
@@ -232,18 +268,20 @@ int launch_qr(SolveArgs<T> a, T* R, T* refl, T* phase, cudaStream_t st) {
     auto k = qr::k_qr<T>;
     if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
-    k<<<a.batch, 256, smem, st>>>(a, R, refl, phase);
+    k<<<a.batch, qr_threads(a.bn), smem, st>>>(a, R, refl, phase);
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 
 template <class T>
 int launch_applyq(int bm, int bn, int batch, const T* refl, const T* phase, const T* UR, T* Out, int64_t ldo,
                   int64_t so, cudaStream_t st) {
-    const size_t smem = (size_t)bm * bn * sizeof(T);
+    if (bn > 256) return BSVD_ERR_UNSUPPORTED;
+    const int nt = 256;  // 256 / bn row segments per column; the remaining threads only stage data
+    const size_t smem = ((size_t)(bm + 1) * bn + bm + (size_t)(nt / bn + 1) * bn + bn) * sizeof(T);
     auto k = qr::k_applyq<T>;
     if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
-    k<<<batch, 256, smem, st>>>(bm, bn, refl, phase, UR, Out, ldo, so);
+    k<<<batch, nt, smem, st>>>(bm, bn, refl, phase, UR, Out, ldo, so);
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 
