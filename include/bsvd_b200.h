@@ -122,6 +122,24 @@ int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch,
 /* Device scratch needed by bsvd_gesvj_batched_host for (chunk, nstreams). */
 size_t bsvd_host_workspace_bytes(int dtype, int m, int n, int chunk, int nstreams, const bsvd_opts* opts);
 
+/*
+ * Batched Hermitian eigensolver by cyclic Jacobi rotations (the reference's
+ * standalone jacobi_hermitian_eig, src/eig.py:90-148, on eig_sweeps
+ * src/_kernels_numba.py:17-82).  G_b: n x n Hermitian (DEVICE, ldg; only the
+ * upper triangle and the real part of the diagonal are read), D_b: n real
+ * eigenvalues (unsorted, like the reference), M_b: n x n eigenvector matrix
+ * (ldm) with G ~= M diag(D) M^H; when m_init != 0 M_b holds the starting
+ * matrix and the rotations are accumulated into it (the reference's eigvecs=
+ * argument), else it starts as the identity.  Guard k*u*sqrt(|d_i||d_j|),
+ * at most max_sweeps sweeps; info (may be NULL): outer_sweeps = sweeps_run
+ * (quiet sweep included), rotations, converged.  work: DEVICE scratch of
+ * bsvd_heevj_workspace_bytes(...) bytes (0 when G and M fit in shared memory).
+ */
+int bsvd_heevj_batched(int dtype, int n, int batch, const void* G, int64_t ldg, int64_t strideG,
+                       void* D, int64_t strideD, void* M, int64_t ldm, int64_t strideM, int m_init,
+                       double k, int max_sweeps, bsvd_info* info, void* work, size_t work_bytes, void* stream);
+size_t bsvd_heevj_workspace_bytes(int dtype, int n, int batch);
+
 /* Device scratch needed by bsvd_gesvj_batched for this problem class. */
 size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts* opts);
 

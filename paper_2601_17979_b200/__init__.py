@@ -18,7 +18,7 @@ from .core import (
     real_dtype,
     unit_roundoff,
 )
-from .eig import Rotation, compute_rotation
+from .eig import EigInfo, Rotation, batch_hermitian_eig, compute_rotation, jacobi_hermitian_eig
 from .kernels import compute_gram, fused_pair_update, onesided_sweeps
 from .ordering import Schedule, round_robin_schedule, schedule_arrays
 from .solver import DeviceResult, solve_tensor
@@ -39,6 +39,7 @@ __all__ = [
     "BatchState",
     "DeviceResult",
     "DomainError",
+    "EigInfo",
     "JacobiOptions",
     "Rotation",
     "Schedule",
@@ -47,6 +48,7 @@ __all__ = [
     "SUPPORTED_DTYPES",
     "SvdResult",
     "WorkCounters",
+    "batch_hermitian_eig",
     "batch_svd",
     "check_dtype",
     "compute_gram",
@@ -55,6 +57,7 @@ __all__ = [
     "fmatrix",
     "fused_pair_update",
     "is_complex",
+    "jacobi_hermitian_eig",
     "onesided_sweeps",
     "real_dtype",
     "round_robin_schedule",

@@ -64,6 +64,8 @@ EXPORTS = (
     "bsvd_gram_batched",
     "bsvd_fused_pair_update_batched",
     "bsvd_bench_fma_peak",
+    "bsvd_heevj_batched",
+    "bsvd_heevj_workspace_bytes",
 )
 
 _lib = None
@@ -106,6 +108,11 @@ def load():
     L.bsvd_gram_batched.restype = ci
     L.bsvd_fused_pair_update_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, vp, i64, i64, ci, vp]
     L.bsvd_fused_pair_update_batched.restype = ci
+    L.bsvd_heevj_batched.argtypes = [ci, ci, ci, vp, i64, i64, vp, i64, vp, i64, i64, ci, ctypes.c_double, ci, vp,
+                                     vp, sz, vp]
+    L.bsvd_heevj_batched.restype = ci
+    L.bsvd_heevj_workspace_bytes.argtypes = [ci, ci, ci]
+    L.bsvd_heevj_workspace_bytes.restype = sz
     L.bsvd_bench_fma_peak.argtypes = [ci, ci, ci, vp, vp]
     L.bsvd_bench_fma_peak.restype = ci
     _lib = L

@@ -180,6 +180,22 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
 
 extern "C" {
 
+size_t bsvd_heevj_workspace_bytes(int dtype, int n, int batch) {
+    if (dtype < 0 || dtype > 3 || n < 0 || batch < 0) return 0;
+    return heevj_workspace(dtype, n, batch, smem_limit());
+}
+
+int bsvd_heevj_batched(int dtype, int n, int batch, const void* G, int64_t ldg, int64_t strideG, void* D,
+                       int64_t strideD, void* M, int64_t ldm, int64_t strideM, int m_init, double k, int max_sweeps,
+                       bsvd_info* info, void* work, size_t work_bytes, void* stream) {
+    if (dtype < 0 || dtype > 3 || n < 0 || batch < 0 || !(k > 0) || max_sweeps < 1) return BSVD_ERR_ARG;
+    if (batch == 0 || n == 0) return BSVD_OK;
+    if (!G || !D || !M || ldg < n || ldm < n) return BSVD_ERR_ARG;
+    if (batch > 1 && (strideG < ldg * (int64_t)n || strideD < n || strideM < ldm * (int64_t)n)) return BSVD_ERR_ARG;
+    return launch_heevj(dtype, n, batch, G, ldg, strideG, D, strideD, M, ldm, strideM, m_init, k, max_sweeps, info,
+                        work, work_bytes, smem_limit(), static_cast<cudaStream_t>(stream));
+}
+
 int bsvd_abi_version(void) { return BSVD_ABI_VERSION; }
 
 void bsvd_default_opts(bsvd_opts* o) {

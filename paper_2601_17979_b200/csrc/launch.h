@@ -50,6 +50,10 @@ int launch_applyq(int bm, int bn, int batch, const T* refl, const T* phase, cons
                   int64_t so, cudaStream_t st);
 int launch_qr_path(bsvd_info* info, int batch, int bits, cudaStream_t st);
 size_t qr_smem(int esize, int bm, int bn);
+size_t heevj_workspace(int dtype, int n, int batch, size_t smem_limit);
+int launch_heevj(int dtype, int n, int batch, const void* G, int64_t ldg, int64_t sG, void* D, int64_t sD, void* M,
+                 int64_t ldm, int64_t sM, int m_init, double k, int max_sweeps, bsvd_info* info, void* work,
+                 size_t work_bytes, size_t smem_limit, cudaStream_t st);
 Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, int inner_sweeps);
 int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 

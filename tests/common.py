@@ -33,6 +33,7 @@ class Golden:
         self.meta = meta
         self.cases = {c["id"]: c for c in meta["cases"]}
         self.kernels = {k["id"]: k for k in meta["kernels"]}
+        self.eig = {e["id"]: e for e in meta.get("eig", [])}
 
     def get(self, cid, key):
         k = f"{cid}__{key}"

@@ -173,6 +173,29 @@ def main():
         arrays[f"k_fu_{nm}__bj1"] = bj
         kern.append(dict(id=f"k_fu_{nm}", kind="fused_delta", dtype=nm))
 
+    # --- standalone Hermitian eigensolver (src/eig.py:90-148; tests/test_eig.py:88-160) ---
+    eig = []
+    for dt in ALL:
+        nm = np.dtype(dt).name
+        for n_, seed in ((12, 3), (33, 11)):
+            rng = np.random.default_rng(seed)
+            x = rng.random((n_, n_))
+            if np.dtype(dt).kind == "c":
+                x = x + 1j * rng.random((n_, n_))
+            g = np.asfortranarray(((x + x.conj().T) / 2).astype(dt))
+            d, m, inf = bsvd.jacobi_hermitian_eig(g)
+            eid = f"eig_{nm}_{n_}"
+            arrays[f"{eid}__g"] = g
+            arrays[f"{eid}__d"] = d
+            arrays[f"{eid}__m"] = m
+            eig.append(dict(id=eid, dtype=nm, n=n_, sweeps_run=int(inf.sweeps_run), rotations=int(inf.rotations),
+                            converged=bool(inf.converged)))
+    g = np.asfortranarray([[9.0, 12.0], [12.0, 41.0]])
+    d, m, inf = bsvd.jacobi_hermitian_eig(g)
+    arrays["eig_ka2__g"], arrays["eig_ka2__d"], arrays["eig_ka2__m"] = g, d, m
+    eig.append(dict(id="eig_ka2", dtype="float64", n=2, sweeps_run=int(inf.sweeps_run), rotations=int(inf.rotations),
+                    converged=bool(inf.converged)))
+
     for ell in (2, 3, 4, 5, 7, 8, 9, 16, 31, 32):
         pairs, starts = bsvd.schedule_arrays(ell)
         arrays[f"sched_{ell}__pairs"] = np.asarray(pairs)
@@ -181,6 +204,7 @@ def main():
     meta = dict(
         cases=cases,
         kernels=kern,
+        eig=eig,
         rotation_9_41_12=dict(c=rot.c, s=rot.s, t=rot.t),
         generator="tests/golden/make_golden.py",
         reference="bsvd " + bsvd.__version__ + " (numba backend) from /root/reference/pkg/src",

@@ -9,7 +9,7 @@ tolerance and the reference's accuracy thresholds.
 import numpy as np
 import pytest
 
-from common import ALL_DTYPES, Opts, check_factors, check_sigma_parity, unit_roundoff
+from common import ALL_DTYPES, REAL_OF, Opts, check_factors, check_sigma_parity, unit_roundoff
 from oracle import oracle as O
 
 
@@ -119,3 +119,25 @@ def test_oracle_batch_equals_standalone(golden):
         u, s, v, info = O.solve(a3[b], Opts())
         assert np.array_equal(U[b], u) and np.array_equal(S[b], s) and np.array_equal(V[b], v)
         assert infos[b] == info
+
+
+def _oracle_heev(g, k=30.0, max_sweeps=30):
+    """jacobi_hermitian_eig (src/eig.py:90-148) through the oracle's eig_sweeps (non-delta)."""
+    n = g.shape[0]
+    d = np.ascontiguousarray(np.real(np.diag(g)), dtype=np.dtype(REAL_OF[np.dtype(g.dtype)]))
+    w = np.triu(g, 1)
+    w = np.asfortranarray(w + w.conj().T)
+    m = np.asfortranarray(np.eye(n, dtype=g.dtype))
+    sw, rot, cv = O.eig_sweeps(w, d, m, k * unit_roundoff(g.dtype), max_sweeps, delta=False)
+    return d, m, sw, rot, cv
+
+
+def test_golden_hermitian_eig(golden):
+    # the eigensolver's arithmetic is the eig_sweeps kernel the oracle restates bitwise
+    assert len(golden.eig) >= 9
+    for eid, e in golden.eig.items():
+        g = golden.get(eid, "g")
+        d, m, sw, rot, cv = _oracle_heev(g)
+        assert (sw, rot, cv) == (e["sweeps_run"], e["rotations"], e["converged"]), eid
+        assert np.array_equal(d, golden.get(eid, "d")), eid
+        assert np.array_equal(m, golden.get(eid, "m")), eid
