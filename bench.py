@@ -342,6 +342,12 @@ def run_b200(args, cfg):
         dev_s = float(tt.item())
     info = np.frombuffer(res.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
     kernel_id = int(info["kernel"][0])
+    # accuracy of the whole timed batch on the device (bsvd_verify_batched; outside the timed region)
+    from paper_2601_17979_b200.verify import verify_tensor
+
+    met = verify_tensor(a, m, n, res).cpu().numpy()
+    u_r = bs.unit_roundoff(dt)
+    e_max = [float(np.nanmax(met[:, i])) / u_r if not np.isnan(met[:, i]).all() else None for i in range(3)]
 
     # end-to-end through the host-buffer C-ABI call (bsvd_gesvj_batched_host) with pinned buffers:
     # every step moves the inputs H2D and all factors D2H, pipelined in chunks over three streams
@@ -421,7 +427,8 @@ def run_b200(args, cfg):
         "gpu_launches": args.steps,
         "kernel_variant": kernel_id,
         "parity": {"converged_frac": float(info["converged"].mean()), "gpu_mean_sweeps": float(
-            info["outer_sweeps"].mean()), "ref_mean_sweeps_sample": o_sweeps},
+            info["outer_sweeps"].mean()), "ref_mean_sweeps_sample": o_sweeps,
+            "max_e1_e2_e3_over_u_full_batch": e_max, "threshold_over_u": 30.0},
         "wall_s_timed_region": t_wall1 - t_wall0,
     }
     print(json.dumps(line), flush=True)

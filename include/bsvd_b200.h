@@ -140,6 +140,21 @@ int bsvd_heevj_batched(int dtype, int n, int batch, const void* G, int64_t ldg, 
                        double k, int max_sweeps, bsvd_info* info, void* work, size_t work_bytes, void* stream);
 size_t bsvd_heevj_workspace_bytes(int dtype, int n, int batch);
 
+/*
+ * On-device accuracy metrics of a solved batch (the reference's verify.py:44-84,
+ * float64 accumulation), written to out[4*b .. 4*b+3] (DEVICE doubles):
+ *   e1 = |A - U diag(S) V^H|_1 / (n |A|_1)   (NaN when V is NULL)
+ *   e2 = |I - U^H U|_1 / m,  e3 = |I - V^H V|_1 / n   (e3 NaN without V)
+ *   e4 = |S - Sref|_F / min(m, n)             (NaN when Sref is NULL; Sref float64)
+ * All pointers DEVICE, column-major, the layouts of bsvd_gesvj_batched's outputs.
+ */
+int bsvd_verify_batched(int dtype, int m, int n, int batch,
+                        const void* A, int64_t lda, int64_t strideA,
+                        const void* U, int64_t ldu, int64_t strideU,
+                        const void* S, int64_t strideS,
+                        const void* V, int64_t ldv, int64_t strideV,
+                        const double* Sref, int64_t strideSref, double* out, void* stream);
+
 /* Device scratch needed by bsvd_gesvj_batched for this problem class. */
 size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts* opts);
 

@@ -22,6 +22,7 @@ from .eig import EigInfo, Rotation, batch_hermitian_eig, compute_rotation, jacob
 from .kernels import compute_gram, fused_pair_update, onesided_sweeps
 from .ordering import Schedule, round_robin_schedule, schedule_arrays
 from .solver import DeviceResult, solve_tensor
+from .verify import ErrorReport, error_report, threshold, verify_tensor
 from .svd import (
     JacobiOptions,
     SolveInfo,
@@ -40,6 +41,7 @@ __all__ = [
     "DeviceResult",
     "DomainError",
     "EigInfo",
+    "ErrorReport",
     "JacobiOptions",
     "Rotation",
     "Schedule",
@@ -54,6 +56,7 @@ __all__ = [
     "compute_gram",
     "compute_rotation",
     "convergence_scan",
+    "error_report",
     "fmatrix",
     "fused_pair_update",
     "is_complex",
@@ -67,6 +70,8 @@ __all__ = [
     "svd_dispatch",
     "svd_qr_preprocessed",
     "svd_unblocked",
+    "threshold",
     "unit_roundoff",
+    "verify_tensor",
     "__version__",
 ]

@@ -66,6 +66,7 @@ EXPORTS = (
     "bsvd_bench_fma_peak",
     "bsvd_heevj_batched",
     "bsvd_heevj_workspace_bytes",
+    "bsvd_verify_batched",
 )
 
 _lib = None
@@ -113,6 +114,9 @@ def load():
     L.bsvd_heevj_batched.restype = ci
     L.bsvd_heevj_workspace_bytes.argtypes = [ci, ci, ci]
     L.bsvd_heevj_workspace_bytes.restype = sz
+    L.bsvd_verify_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, vp, i64, i64, vp, i64, vp, i64, i64, vp, i64,
+                                      vp, vp]
+    L.bsvd_verify_batched.restype = ci
     L.bsvd_bench_fma_peak.argtypes = [ci, ci, ci, vp, vp]
     L.bsvd_bench_fma_peak.restype = ci
     _lib = L

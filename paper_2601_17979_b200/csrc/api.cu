@@ -196,6 +196,17 @@ int bsvd_heevj_batched(int dtype, int n, int batch, const void* G, int64_t ldg, 
                         work, work_bytes, smem_limit(), static_cast<cudaStream_t>(stream));
 }
 
+int bsvd_verify_batched(int dtype, int m, int n, int batch, const void* A, int64_t lda, int64_t strideA,
+                        const void* U, int64_t ldu, int64_t strideU, const void* S, int64_t strideS, const void* V,
+                        int64_t ldv, int64_t strideV, const double* Sref, int64_t strideSref, double* out,
+                        void* stream) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0) return BSVD_ERR_ARG;
+    if (batch == 0) return BSVD_OK;
+    if (!A || !U || !S || !out || lda < m || ldu < m || (V && ldv < n)) return BSVD_ERR_ARG;
+    return launch_verify(dtype, m, n, batch, A, lda, strideA, U, ldu, strideU, S, strideS, V, ldv, strideV, Sref,
+                         strideSref, out, static_cast<cudaStream_t>(stream));
+}
+
 int bsvd_abi_version(void) { return BSVD_ABI_VERSION; }
 
 void bsvd_default_opts(bsvd_opts* o) {

@@ -54,6 +54,9 @@ size_t heevj_workspace(int dtype, int n, int batch, size_t smem_limit);
 int launch_heevj(int dtype, int n, int batch, const void* G, int64_t ldg, int64_t sG, void* D, int64_t sD, void* M,
                  int64_t ldm, int64_t sM, int m_init, double k, int max_sweeps, bsvd_info* info, void* work,
                  size_t work_bytes, size_t smem_limit, cudaStream_t st);
+int launch_verify(int dtype, int m, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* U,
+                  int64_t ldu, int64_t sU, const void* S, int64_t sS, const void* V, int64_t ldv, int64_t sV,
+                  const double* Sref, int64_t sR, double* out, cudaStream_t st);
 Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, int inner_sweeps);
 int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 
