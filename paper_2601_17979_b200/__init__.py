@@ -22,6 +22,7 @@ from .eig import EigInfo, Rotation, batch_hermitian_eig, compute_rotation, jacob
 from .kernels import compute_gram, fused_pair_update, onesided_sweeps
 from .ordering import Schedule, round_robin_schedule, schedule_arrays
 from .solver import DeviceResult, solve_tensor
+from . import fileio
 from .verify import ErrorReport, error_report, threshold, verify_tensor
 from .svd import (
     JacobiOptions,
@@ -57,6 +58,7 @@ __all__ = [
     "compute_rotation",
     "convergence_scan",
     "error_report",
+    "fileio",
     "fmatrix",
     "fused_pair_update",
     "is_complex",
