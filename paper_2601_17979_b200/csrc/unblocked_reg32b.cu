@@ -225,7 +225,7 @@ __device__ __forceinline__ void all_partials(const double (&x0)[N], const double
 // update is fused with the partials of iteration t + 1 (offset u + 1 in the
 // pre-shift register naming: next pair k = columns of this iteration's pairs
 // k - 1 and k + 1), so they are ready when the next reduction starts.
-template <int u>
+template <int u, int PD>
 __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab, int t,
                                        int lane, int half, int hl, bool done, double tol, double tol2,
                                        Par* logl, IterState& st) {
@@ -282,16 +282,17 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     st.itbits |= (mask != 0u ? 1u : 0u) << t;
     constexpr int un = u + 1;  // offset of iteration t + 1 (pre-shift naming)
     if (mask) {
-        Par pq[H];  // all rotations first: the loop below interleaves stores to red[]
+        // rotations PD ahead (PD = 16: all first) -- the loop interleaves stores to red[]
+        Par pq[PD];
 #pragma unroll
-        for (int q = 0; q < H; ++q) pq[q] = sm.pub[half][q];
-        apply2(x0[TS(0, u)], x0[BS(0, u)], pq[0].cm1, pq[0].c);
-        apply2(x1[TS(0, u)], x1[BS(0, u)], pq[0].cm1, pq[0].c);
+        for (int q = 0; q < PD; ++q) pq[q] = sm.pub[half][q];
 #pragma unroll
-        for (int q = 1; q < H; ++q) {
-            apply2(x0[TS(q, u)], x0[BS(q, u)], pq[q].cm1, pq[q].c);
-            apply2(x1[TS(q, u)], x1[BS(q, u)], pq[q].cm1, pq[q].c);
-            cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs this iteration's pairs q - 2 and q
+        for (int q = 0; q < H; ++q) {
+            const Par cur = pq[q % PD];
+            if (q + PD < H) pq[q % PD] = sm.pub[half][q + PD];
+            apply2(x0[TS(q, u)], x0[BS(q, u)], cur.cm1, cur.c);
+            apply2(x1[TS(q, u)], x1[BS(q, u)], cur.cm1, cur.c);
+            if (q >= 1) cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs this iteration's pairs q-2, q
         }
         cross_partial<un>(x0, x1, sm.red, lane, H - 1);
     } else {
@@ -303,7 +304,7 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
 }
 
 // One V replay iteration at offset u (log row t is staged in sm.stage[t & 1]).
-template <int u>
+template <int u, int PD>
 __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int t, int half, int hl,
                                        const Par* logl, uint32_t itbits, long long& tl) {
     R32PT(7, x0[TS(0, u)], tl);
@@ -314,12 +315,13 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
     R32PT(8, sm.stage[t & 1][half][0].c, tl);
     if ((itbits >> t) & 1u) {
         const Par* stp = sm.stage[t & 1][half];
-        Par pr[H];  // all rotations first, then 128 independent FMAs
+        Par pr[PD];  // rotations PD ahead, then independent FMAs
 #pragma unroll
-        for (int q = 0; q < H; ++q) pr[q] = stp[q];
+        for (int q = 0; q < PD; ++q) pr[q] = stp[q];
 #pragma unroll
         for (int q = 0; q < H; ++q) {
-            const Par pq = pr[q];
+            const Par pq = pr[q % PD];
+            if (q + PD < H) pr[q % PD] = stp[q + PD];
             apply2(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
             apply2(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
         }
@@ -328,7 +330,7 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
     __syncwarp();
 }
 
-template <int U>
+template <int U, int PD>
 __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab,
                                         int lane, int half, int hl, bool done, double tol, double tol2, Par* logl,
                                         IterState& st) {
@@ -339,25 +341,25 @@ __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSm
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
         const bool last = gi == NG - 1;
-        w_iter<0>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
+        w_iter<0, PD>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
         if constexpr (U >= 2) {
             if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            w_iter<1 % U>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<1 % U, PD>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
         }
         if constexpr (U >= 3) {
             if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            w_iter<2 % U>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<2 % U, PD>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
         }
         if constexpr (U >= 4) {
             if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            w_iter<3 % U>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<3 % U, PD>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
         }
         ring_shift<U>(x0);
         ring_shift<U>(x1);
     }
 }
 
-template <int U>
+template <int U, int PD>
 __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int half, int hl,
                                         const Par* logl, uint32_t itbits, long long& tl) {
     constexpr int NG = (NIT + U - 1) / U;
@@ -366,25 +368,25 @@ __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSm
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
         const bool last = gi == NG - 1;
-        v_iter<0>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
+        v_iter<0, PD>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
         if constexpr (U >= 2) {
             if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            v_iter<1 % U>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
+            v_iter<1 % U, PD>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 3) {
             if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            v_iter<2 % U>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
+            v_iter<2 % U, PD>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 4) {
             if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            v_iter<3 % U>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
+            v_iter<3 % U, PD>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
         }
         ring_shift<U>(x0);
         ring_shift<U>(x1);
     }
 }
 
-template <int NW, int MINB, int U, int UV = U>
+template <int NW, int MINB, int U, int UV, int PD>
 __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         st.itbits = 0;
         st.full = true;  // fresh norms at the start of every sweep
         st.fmask = 0xffffffffu;
-        w_sweep<U>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, logw, st);
+        w_sweep<U, PD>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, logw, st);
         // ---- sweep end: per-problem rotation count over the half warp ----
         int tot = st.my_rot;
 #pragma unroll
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
             __syncwarp();  // this warp's log writes are visible to all its lanes
             cp_async16(&sm.stage[0][half][hl], logl);
             cp_commit();
-            v_sweep<UV>(x0, x1, sm, half, hl, logl, st.itbits, st.tl);
+            v_sweep<UV, PD>(x0, x1, sm, half, hl, logl, st.itbits, st.tl);
             cp_wait<0>();
             if (live) {
 #pragma unroll
@@ -552,12 +554,12 @@ Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, i
     return p;
 }
 
-template <int NW, int MINB, int U, int UV = U>
+template <int NW, int MINB, int U, int UV, int PD>
 static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
     const int per_cta = 2 * NW;
     const int grid = (a.batch + per_cta - 1) / per_cta;
     const size_t smem = NW * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
-    auto k = r32b::k_reg32b<NW, MINB, U, UV>;
+    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<grid, NW * 32, smem, st>>>(a);
@@ -569,11 +571,11 @@ int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st)
     a.work_stride = (int64_t)p.work_elems;
     int rc;
     switch (p.kernel) {
-        case KV_UNBLOCKED_REG32B + 1: rc = launch_r32b<4, 3, 2, 2>(a, st); break;  // 168 regs, 12 warps/SM
-        case KV_UNBLOCKED_REG32B + 2: rc = launch_r32b<4, 2, 2, 4>(a, st); break;  // V unroll 4
-        case KV_UNBLOCKED_REG32B + 3: rc = launch_r32b<1, 11, 2, 2>(a, st); break; // one-warp CTAs
-        case KV_UNBLOCKED_REG32B + 4: rc = launch_r32b<4, 3, 2, 4>(a, st); break;
-        default: rc = launch_r32b<4, 2, 2, 2>(a, st); break;                       // 255 regs, 8 warps/SM
+        case KV_UNBLOCKED_REG32B + 1: rc = launch_r32b<4, 3, 2, 2, 4>(a, st); break;   // 168 regs, 12 warps/SM
+        case KV_UNBLOCKED_REG32B + 2: rc = launch_r32b<4, 2, 2, 4, 16>(a, st); break;  // V unroll 4
+        case KV_UNBLOCKED_REG32B + 3: rc = launch_r32b<1, 11, 2, 2, 4>(a, st); break;  // one-warp CTAs
+        case KV_UNBLOCKED_REG32B + 4: rc = launch_r32b<4, 3, 2, 2, 2>(a, st); break;   // 168 regs, depth 2
+        default: rc = launch_r32b<4, 2, 2, 2, 16>(a, st); break;                       // 255 regs, 8 warps/SM
     }
     if (rc) return rc;
     return launch_finalize_ws<double>(a, st);
