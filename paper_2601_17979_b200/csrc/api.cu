@@ -72,11 +72,11 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
     }
     if (is_reg32e(o->kernel)) return plan_unblocked_reg32e(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
     if (is_reg32b(o->kernel)) {
-        Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
+        Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel, o->max_sweeps);
         return p;  // forced variant unavailable => kernel 0 => unsupported
     }
     if (o->kernel == 0) {  // default for 32x32 FP64: the second-generation register kernel
-        Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, 0);
+        Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, 0, o->max_sweeps);
         if (p.kernel) return p;
     }
     if (o->kernel == 0 || (o->kernel >= KV_UNBLOCKED_REG32 && o->kernel <= KV_UNBLOCKED_REG32_F2)) {
@@ -156,6 +156,9 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_UNBLOCKED_REG32B + 1:
         case KV_UNBLOCKED_REG32B + 2:
         case KV_UNBLOCKED_REG32B + 3:
+        case KV_UNBLOCKED_REG32B + 4:
+        case KV_UNBLOCKED_REG32B + 5:
+        case KV_UNBLOCKED_REG32B + 6:
         case KV_UNBLOCKED_REG32B_LAST:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32b(a, p, st);
             return BSVD_ERR_UNSUPPORTED;

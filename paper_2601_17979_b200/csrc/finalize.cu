@@ -8,13 +8,19 @@
 
 namespace bsvd {
 
-template <class T>
+template <class T, bool FLAGGED = false>
 __global__ void __launch_bounds__(128) k_finalize_ws(SolveArgs<T> a) {
     using R = typename tr<T>::R;
     extern __shared__ __align__(16) unsigned char smem[];
     const int prob = blockIdx.x;
     const int bm = a.bm, bn = a.bn;
     const T* src = a.work + (size_t)prob * a.work_stride;
+    if constexpr (FLAGGED) {  // the solver finalised this problem itself unless its flag is set
+        const T f = src[a.work_stride - 1];
+        bool set;
+        if constexpr (tr<T>::cplx) set = f.re != 0; else set = f != 0;
+        if (!set) return;
+    }
     T* W = reinterpret_cast<T*>(smem);
     T* Vw = a.need_v ? W + (size_t)bm * bn : nullptr;
     size_t off = ((size_t)bm * bn + (a.need_v ? (size_t)bn * bn : 0)) * sizeof(T);
@@ -30,20 +36,30 @@ __global__ void __launch_bounds__(128) k_finalize_ws(SolveArgs<T> a) {
     finalize_block<T>(W, bm, bm, bn, Vw, bn, sig, perm, flag, final_out(a, prob));
 }
 
-template <class T>
-int launch_finalize_ws(SolveArgs<T> a, cudaStream_t st) {
+template <class T, bool FLAGGED>
+static int launch_finalize_impl(SolveArgs<T> a, cudaStream_t st) {
     const size_t es = sizeof(T);
     size_t smem = ((size_t)a.bm * a.bn + (a.need_v ? (size_t)a.bn * a.bn : 0)) * es;
     smem = ((smem + 15) & ~size_t(15)) + (((size_t)a.bn * sizeof(typename tr<T>::R) + 15) & ~size_t(15)) +
            (((size_t)a.bn * 4 + 15) & ~size_t(15)) + 16;
+    auto k = k_finalize_ws<T, FLAGGED>;
     if (smem > 48 * 1024) {
-        if (cudaFuncSetAttribute(k_finalize_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return BSVD_ERR_CUDA;
     }
-    k_finalize_ws<T><<<a.batch, 128, smem, st>>>(a);
+    k<<<a.batch, 128, smem, st>>>(a);
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
+
+template <class T>
+int launch_finalize_ws(SolveArgs<T> a, cudaStream_t st) {
+    return launch_finalize_impl<T, false>(a, st);
+}
+template <class T>
+int launch_finalize_flagged(SolveArgs<T> a, cudaStream_t st) {
+    return launch_finalize_impl<T, true>(a, st);
+}
+template int launch_finalize_flagged<double>(SolveArgs<double>, cudaStream_t);
 
 // Finalisation in place in the workspace (global / L2): for solvers whose W
 // and V live in the workspace and are too large to stage in shared memory.

@@ -50,7 +50,7 @@ enum {
     KV_BLOCKED_DMMA_512 = 10,   // same, 512-thread CTAs (16 warps) for one-CTA-per-SM sizes
     KV_UNBLOCKED_REG16F = 11,   // 16x16 FP32 register-resident, 4 problems per warp
     KV_UNBLOCKED_REG32B = 12,   // 32x32 FP64 second generation: unrolled ring, maintained norms, two-FMA
-    KV_UNBLOCKED_REG32B_LAST = 16,  // 13..16: tuning variants (registers, V unroll, CTA shape)
+    KV_UNBLOCKED_REG32B_LAST = 19,  // 13..19: tuning variants (registers, V unroll, CTA shape, split W/V, unfused finalize)
     KV_UNBLOCKED_REG32E = 26,   // 32x32 FP64 warp-specialised: W warp + V warp per problem pair, smem ring
     KV_UNBLOCKED_REG32E_LAST = 29,  // 27..29: tuning variants (pairs per CTA, V unroll)
     KV_HEEVJ = 31,              // batched Hermitian Jacobi eigensolver (bsvd_heevj_batched)

@@ -31,7 +31,7 @@ template <class T>
 int launch_blocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
 int launch_unblocked_reg_d32(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 bool is_reg32b(int kv);
-Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
+Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant, int max_sweeps);
 int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 bool is_reg32e(int kv);
 Plan plan_unblocked_reg32e(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
@@ -43,6 +43,8 @@ template <class T>
 int launch_finalize_ws(SolveArgs<T> a, cudaStream_t st);
 template <class T>
 int launch_finalize_gm(SolveArgs<T> a, cudaStream_t st);
+template <class T>
+int launch_finalize_flagged(SolveArgs<T> a, cudaStream_t st);
 template <class T>
 int launch_qr(SolveArgs<T> a, T* R, T* refl, T* phase, cudaStream_t st);
 template <class T>

@@ -76,12 +76,13 @@ __device__ __forceinline__ void cp_wait() {
 // move every column SH ring positions forward (compile-time register moves)
 template <int SH>
 __device__ __forceinline__ void ring_shift(double (&x)[N]) {
+    // x[slot(q)] <- x[slot(q - SH)] for every ring position; 31 is prime, so the
+    // permutation is one cycle: follow it with a single temporary (32 moves)
     if constexpr (md(SH) != 0) {
-        double y[NIT];
+        const double t = x[ring_slot(0)];
 #pragma unroll
-        for (int q = 0; q < NIT; ++q) y[q] = x[ring_slot(q)];
-#pragma unroll
-        for (int q = 0; q < NIT; ++q) x[ring_slot(q)] = y[md(q - SH)];
+        for (int i = 0; i < NIT - 1; ++i) x[ring_slot(md(-i * SH))] = x[ring_slot(md(-(i + 1) * SH))];
+        x[ring_slot(md(-(NIT - 1) * SH))] = t;
     }
 }
 
@@ -98,6 +99,25 @@ __device__ __forceinline__ double sum16(const double* p) {  // 16 consecutive do
     const double s0 = (p0.x + p0.y) + (p1.x + p1.y), s1 = (p2.x + p2.y) + (p3.x + p3.y);
     const double s2 = (p4.x + p4.y) + (p5.x + p5.y), s3 = (p6.x + p6.y) + (p7.x + p7.y);
     return (s0 + s1) + (s2 + s3);
+}
+
+// 16 consecutive doubles summed in the order of a 16-8-4-2-1 xor butterfly over rows (i, i + 16) first:
+// the column-norm order of finalize_block (finalize.cuh step 1), so the fused and the standalone
+// finalisation give the same sigma bits.
+__device__ __forceinline__ double rcp_refined(double b) {  // 1/b, b in [2^-960, 2^960]
+    double r = rcp_approx(b);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r = fma(r, fma(-b, r, 1.0), r);
+    return r;
+}
+
+__device__ __forceinline__ double sum16_butterfly(const double* p) {
+    double t[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t[i] = p[i] + p[i + 8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t[i] = t[i] + t[i + 4];
+    return (t[0] + t[2]) + (t[1] + t[3]);
 }
 
 // partial dot products of this lane's two rows for the 16 pairs at offset u
@@ -304,7 +324,7 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
 }
 
 // One V replay iteration at offset u (log row t is staged in sm.stage[t & 1]).
-template <int u, int PD>
+template <int u, int PD, bool ZCHECK = false>
 __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int t, int half, int hl,
                                        const Par* logl, uint32_t itbits, long long& tl) {
     R32PT(7, x0[TS(0, u)], tl);
@@ -313,7 +333,14 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
     cp_wait<1>();
     __syncwarp();
     R32PT(8, sm.stage[t & 1][half][0].c, tl);
-    if ((itbits >> t) & 1u) {
+    bool go;
+    if constexpr (ZCHECK) {  // split replay: skip an iteration whose 32 rotations are all the identity
+        const Par own = sm.stage[t & 1][half][hl];
+        go = __ballot_sync(0xffffffffu, own.cm1 != 0.0 || own.c != 0.0) != 0u;
+    } else {
+        go = (itbits >> t) & 1u;
+    }
+    if (go) {
         const Par* stp = sm.stage[t & 1][half];
         Par pr[PD];  // rotations PD ahead, then independent FMAs
 #pragma unroll
@@ -359,7 +386,7 @@ __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSm
     }
 }
 
-template <int U, int PD>
+template <int U, int PD, bool ZCHECK = false>
 __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int half, int hl,
                                         const Par* logl, uint32_t itbits, long long& tl) {
     constexpr int NG = (NIT + U - 1) / U;
@@ -368,25 +395,25 @@ __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSm
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
         const bool last = gi == NG - 1;
-        v_iter<0, PD>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
+        v_iter<0, PD, ZCHECK>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
         if constexpr (U >= 2) {
             if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            v_iter<1 % U, PD>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
+            v_iter<1 % U, PD, ZCHECK>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 3) {
             if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            v_iter<2 % U, PD>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
+            v_iter<2 % U, PD, ZCHECK>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 4) {
             if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            v_iter<3 % U, PD>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
+            v_iter<3 % U, PD, ZCHECK>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
         }
         ring_shift<U>(x0);
         ring_shift<U>(x1);
     }
 }
 
-template <int NW, int MINB, int U, int UV, int PD>
+template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true>
 __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -404,6 +431,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     // aliases problem 0's workspace) but may read
     Par* logl = want_v ? logp + hl : nullptr;
     Par* logw = live ? logl : nullptr;
+    // SPLIT: every sweep logged ([sweep][31][16] after a 2-double header), V replayed by k_vreplay
+    double* hdr = wsW + 2 * N * N;
+    if (SPLIT) {
+        logl = want_v ? reinterpret_cast<Par*>(hdr + 2) + hl : nullptr;
+        logw = live ? logl : nullptr;
+    }
     uint32_t* ctab = reinterpret_cast<uint32_t*>(smem_raw + NW * sizeof(WarpSmem));
     for (int e = threadIdx.x; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
     __syncthreads();
@@ -447,7 +480,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         st.itbits = 0;
         st.full = true;  // fresh norms at the start of every sweep
         st.fmask = 0xffffffffu;
-        w_sweep<U, PD>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, logw, st);
+        w_sweep<U, PD>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2,
+                       (SPLIT && logw) ? logw + (size_t)sw * NIT * H : logw, st);
         // ---- sweep end: per-problem rotation count over the half warp ----
         int tot = st.my_rot;
 #pragma unroll
@@ -460,6 +494,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         }
         const int partner_done = __shfl_xor_sync(0xffffffffu, done, 16);
         const bool both_done = done && partner_done;
+        if (SPLIT) {
+            if (both_done || sw + 1 == a.max_sweeps) {
+                if (live && hl == 0) hdr[0] = (double)(sw + 1);  // sweeps k_vreplay replays
+                break;
+            }
+            continue;
+        }
         // ======================= V phase: replay the sweep =======================
         if (want_v && st.itbits) {
             if (live) {
@@ -504,14 +545,94 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         }
         if (both_done) break;
     }
-    if (live) {
+    // ======== kernel (5) fused (phase-alternating path): sigma, order, U = W / sigma, V permuted ========
+    // A problem with a column below tiny/u (orthogonal completion, finalize.cuh step 3) is left to
+    // the standalone finalisation pass: W and V go to the workspace with its flag set.
+    double* flagp = wsW + pstride - 1;  // last double of the problem's workspace (log padding)
+    bool fused = false;
+    if (!SPLIT && FF) {
+        const double unscale = pow2(ex);
+#pragma unroll
+        for (int c = 0; c < N; ++c) sm.red[c * RSTR + lane] = __dadd_rn(__dmul_rn(x0[c], x0[c]), __dmul_rn(x1[c], x1[c]));
+        __syncwarp();
+        // lane hl: columns 2 hl, 2 hl + 1.  Sigma of the scaled W (ssa); the power-of-two scale is
+        // exact, so sa = ssa * 2^ex and x / ssa are the unscaled sigma and quotient.
+        const double ssa = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl) * RSTR + 16 * half));
+        const double ssb = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl + 1) * RSTR + 16 * half));
+        const double sa = ssa * unscale, sb = ssb * unscale;
+        // holes (sigma < tiny/u) and scaled sigmas outside the reciprocal's safe range take the
+        // standalone pass
+        const bool tiny = !(sa >= dtiny<double>() && sb >= dtiny<double>() && ssa >= 0x1p-960 && ssb >= 0x1p-960 &&
+                            ssa <= 0x1p+960 && ssb <= 0x1p+960);
+        const unsigned tm = __ballot_sync(0xffffffffu, tiny);
+        fused = ((tm >> (16 * half)) & 0xFFFFu) == 0u;
+        __syncwarp();
+        // [half][32] (scaled sigma, reciprocal) and rank by column, in rows 32.. of red
+        double2* sr = reinterpret_cast<double2*>(sm.red + 32 * RSTR) + 32 * half;
+        int* rk = reinterpret_cast<int*>(sm.red + 32 * RSTR + 128) + 32 * half;
+        sr[2 * hl] = make_double2(ssa, rcp_refined(ssa));
+        sr[2 * hl + 1] = make_double2(ssb, rcp_refined(ssb));
+        __syncwarp();
+        int ra = 0, rb = 0;  // stable descending ranks (finalize.cuh step 4)
+#pragma unroll 8
+        for (int c2 = 0; c2 < N; ++c2) {
+            const double s2 = sr[c2].x;
+            ra += sig_before(s2, ssa) || (c2 < 2 * hl && sig_tie(s2, ssa));
+            rb += sig_before(s2, ssb) || (c2 < 2 * hl + 1 && sig_tie(s2, ssb));
+        }
+        rk[2 * hl] = ra;
+        rk[2 * hl + 1] = rb;
+        __syncwarp();
+        if (live && fused) {
+            const FinalOut<double> o = final_out(a, prob);
+            o.S[ra] = sa;
+            o.S[rb] = sb;
+            double* u0 = o.U + r0;
+            double* u1 = o.U + r1;
+#pragma unroll
+            for (int c = 0; c < N; ++c) {  // U = W / sigma: reciprocal, then one residual correction
+                const int rc = rk[c];
+                const double2 t = sr[c];
+                const double q0 = x0[c] * t.y, q1 = x1[c] * t.y;
+                u0[(size_t)rc * o.ldu] = fma(fma(-t.x, q0, x0[c]), t.y, q0);
+                u1[(size_t)rc * o.ldu] = fma(fma(-t.x, q1, x1[c]), t.y, q1);
+            }
+            if (o.want_v && o.V) {
+                // all 64 loads ahead of the stores (the compiler cannot prove o.V and wsV disjoint,
+                // so interleaving would serialise one L2 round trip per element)
+                if (v_started) {
+#pragma unroll
+                    for (int c = 0; c < N; ++c) {
+                        x0[c] = wsV[r0 + c * N];
+                        x1[c] = wsV[r1 + c * N];
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < N; ++c) {
+                        x0[c] = (c == r0) ? 1.0 : 0.0;
+                        x1[c] = (c == r1) ? 1.0 : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    const int rc = rk[c];
+                    o.V[r0 + (size_t)rc * o.ldv] = x0[c];
+                    o.V[r1 + (size_t)rc * o.ldv] = x1[c];
+                }
+            }
+        }
+        if (live && hl == 0) *flagp = fused ? 0.0 : 1.0;
+    } else {
+        (void)flagp;
+    }
+    if (live && !fused) {
         const double unscale = pow2(ex);
 #pragma unroll
         for (int c = 0; c < N; ++c) {
             wsW[r0 + c * N] = x0[c] * unscale;
             wsW[r1 + c * N] = x1[c] * unscale;
         }
-        if (want_v && !v_started) {
+        if (want_v && !v_started && !SPLIT) {
 #pragma unroll
             for (int c = 0; c < N; ++c) {
                 wsV[r0 + c * N] = (c == r0) ? 1.0 : 0.0;
@@ -535,18 +656,108 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     }
 }
 
+// Split design, second kernel: replay every logged sweep onto V = I (pure FP64 throughput: no
+// dependency chain) and leave V in the workspace.  The log streams from HBM, so it is staged DEPTH
+// iterations ahead with cp.async (one 16-byte rotation per lane per iteration).
+constexpr int VDEPTH = 8;
+struct VSmem {
+    Par stage[VDEPTH][2][H];
+};
+
+template <int u, int PD>
+__device__ __forceinline__ void vr_iter(double (&x0)[N], double (&x1)[N], VSmem& sm, int g, int half, int hl,
+                                        const Par* src, int total) {
+    // issue iteration g + VDEPTH - 1, then wait until iteration g has landed
+    const int gl = g + VDEPTH - 1;
+    if (gl < total) cp_async16(&sm.stage[gl % VDEPTH][half][hl], src + (size_t)gl * H);
+    cp_commit();
+    cp_wait<VDEPTH - 1>();
+    __syncwarp();
+    const Par* stp = sm.stage[g % VDEPTH][half];
+    const Par own = stp[hl];
+    if (__ballot_sync(0xffffffffu, own.cm1 != 0.0 || own.c != 0.0)) {  // all-identity iterations skipped
+        Par pr[PD];
+#pragma unroll
+        for (int q = 0; q < PD; ++q) pr[q] = stp[q];
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            const Par pq = pr[q % PD];
+            if (q + PD < H) pr[q % PD] = stp[q + PD];
+            apply2(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
+            apply2(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
+        }
+    }
+    __syncwarp();  // the slot is refilled VDEPTH - 1 iterations later
+}
+
+template <int NW, int MINB, int PD>
+__global__ void __launch_bounds__(NW * 32, MINB) k_vreplay(SolveArgs<double> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    VSmem& sm = reinterpret_cast<VSmem*>(smem_raw)[warp];
+    const int half = lane >> 4, hl = lane & 15;
+    const int prob = (blockIdx.x * NW + warp) * 2 + half;
+    const bool live = prob < a.batch;
+    const int r0 = hl, r1 = hl + 16;
+    const int pair0 = (blockIdx.x * NW + warp) * 2;  // the warp's first problem (always live)
+    double* wsW = a.work + (size_t)(live ? prob : pair0) * (size_t)a.work_stride;
+    double* wsV = wsW + N * N;
+    const double* hdr0 = a.work + (size_t)pair0 * (size_t)a.work_stride + 2 * N * N;
+    const int nsw = (int)hdr0[0];  // both problems of the warp ran the same sweeps in the W kernel
+    const Par* src = reinterpret_cast<const Par*>(wsW + 2 * N * N + 2) + hl;  // [sweep][31][16]
+    const int total = nsw * NIT;
+    double x0[N], x1[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+        x0[c] = (c == r0) ? 1.0 : 0.0;
+        x1[c] = (c == r1) ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int d = 0; d < VDEPTH - 1; ++d) {
+        if (d < total) cp_async16(&sm.stage[d][half][hl], src + (size_t)d * H);
+        cp_commit();
+    }
+    int g = 0;
+#pragma unroll 1
+    for (int sw = 0; sw < nsw; ++sw) {
+        // one sweep: 15 pairs of iterations (ring moved by two) and a last one (moved by one)
+#pragma unroll 1
+        for (int gi = 0; gi < 15; ++gi) {
+            vr_iter<0, PD>(x0, x1, sm, g, half, hl, src, total);
+            vr_iter<1, PD>(x0, x1, sm, g + 1, half, hl, src, total);
+            g += 2;
+            ring_shift<2>(x0);
+            ring_shift<2>(x1);
+        }
+        vr_iter<0, PD>(x0, x1, sm, g, half, hl, src, total);
+        g += 1;
+        ring_shift<1>(x0);
+        ring_shift<1>(x1);
+    }
+    cp_wait<0>();
+    if (live) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            wsV[r0 + c * N] = x0[c];
+            wsV[r1 + c * N] = x1[c];
+        }
+    }
+}
+
 }  // namespace r32b
 
 // variants: (warps per CTA, min CTAs per SM, unroll, per-pair skip)
 bool is_reg32b(int kv) { return kv >= KV_UNBLOCKED_REG32B && kv <= KV_UNBLOCKED_REG32B_LAST; }
 
-Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant) {
+size_t reg32b_work_elems(int kv, int max_sweeps);
+
+Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant, int max_sweeps) {
     Plan p{};
     if (dtype == BSVD_D && bm == 32 && bn == 32 && lda_ok) {
         p.kernel = is_reg32b(variant) ? variant : KV_UNBLOCKED_REG32B;
         p.threads = 128;
         p.smem = 4 * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
-        p.work_elems = 2 * 32 * 32 + r32b::LOG_ELEMS;
+        p.work_elems = reg32b_work_elems(p.kernel, max_sweeps);
         p.grid = 0;
         p.resident = 0;
         (void)need_v;
@@ -554,12 +765,31 @@ Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, i
     return p;
 }
 
-template <int NW, int MINB, int U, int UV, int PD>
+// split variants log every sweep: W, V, a 2-double header, max_sweeps x 31 x 16 rotations
+bool reg32b_split(int kv) { return kv == KV_UNBLOCKED_REG32B + 5 || kv == KV_UNBLOCKED_REG32B + 6; }
+size_t reg32b_work_elems(int kv, int max_sweeps) {
+    return reg32b_split(kv) ? 2 * 32 * 32 + 2 + (size_t)max_sweeps * r32b::NIT * r32b::H * 2
+                            : 2 * 32 * 32 + r32b::LOG_ELEMS;
+}
+
+template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true>
 static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
     const int per_cta = 2 * NW;
     const int grid = (a.batch + per_cta - 1) / per_cta;
     const size_t smem = NW * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
-    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD>;
+    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD, SPLIT, FF>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<grid, NW * 32, smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+template <int NW, int MINB, int PD>
+static int launch_vreplay(SolveArgs<double> a, cudaStream_t st) {
+    const int per_cta = 2 * NW;
+    const int grid = (a.batch + per_cta - 1) / per_cta;
+    const size_t smem = NW * sizeof(r32b::VSmem);
+    auto k = r32b::k_vreplay<NW, MINB, PD>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<grid, NW * 32, smem, st>>>(a);
@@ -568,17 +798,27 @@ static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
 
 int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
     a.kernel = p.kernel;
-    a.work_stride = (int64_t)p.work_elems;
+    a.work_stride = (int64_t)reg32b_work_elems(p.kernel, a.max_sweeps);
     int rc;
     switch (p.kernel) {
+        case KV_UNBLOCKED_REG32B + 5:  // split: W kernel (255 regs) + V replay (168 regs, 12 warps/SM)
+            rc = launch_r32b<4, 2, 2, 2, 16, true>(a, st);
+            if (!rc && a.need_v) rc = launch_vreplay<4, 3, 4>(a, st);
+            break;
+        case KV_UNBLOCKED_REG32B + 6:  // split, V replay at 255 registers (8 warps/SM), all rotations ahead
+            rc = launch_r32b<4, 2, 2, 2, 16, true>(a, st);
+            if (!rc && a.need_v) rc = launch_vreplay<4, 2, 16>(a, st);
+            break;
         case KV_UNBLOCKED_REG32B + 1: rc = launch_r32b<4, 3, 2, 2, 4>(a, st); break;   // 168 regs, 12 warps/SM
         case KV_UNBLOCKED_REG32B + 2: rc = launch_r32b<4, 2, 2, 4, 16>(a, st); break;  // V unroll 4
         case KV_UNBLOCKED_REG32B + 3: rc = launch_r32b<1, 11, 2, 2, 4>(a, st); break;  // one-warp CTAs
         case KV_UNBLOCKED_REG32B + 4: rc = launch_r32b<4, 3, 2, 2, 2>(a, st); break;   // 168 regs, depth 2
+        case KV_UNBLOCKED_REG32B + 7: rc = launch_r32b<4, 2, 2, 2, 16, false, false>(a, st); break;  // unfused finalize
         default: rc = launch_r32b<4, 2, 2, 2, 16>(a, st); break;                       // 255 regs, 8 warps/SM
     }
     if (rc) return rc;
-    return launch_finalize_ws<double>(a, st);
+    if (reg32b_split(p.kernel) || p.kernel == KV_UNBLOCKED_REG32B + 7) return launch_finalize_ws<double>(a, st);
+    return launch_finalize_flagged<double>(a, st);  // only problems the fused finalisation left over
 }
 
 }  // namespace bsvd

@@ -266,7 +266,7 @@ def test_reg32_partial_ctas(batch):
         check_factors(a, r.u, r.sigma, r.v)
 
 
-@pytest.mark.parametrize("kernel", [1, 3, 4, 5, 6, 7, 12, 13, 14, 15, 16, 26, 27, 28, 29])
+@pytest.mark.parametrize("kernel", [1, 3, 4, 5, 6, 7, 12, 13, 14, 15, 16, 17, 18, 19, 26, 27, 28, 29])
 def test_c1_kernel_variants_agree(kernel):
     """Every 32x32 FP64 kernel variant meets the parity contract on the same inputs."""
     import torch
@@ -285,6 +285,38 @@ def test_c1_kernel_variants_agree(kernel):
         _, s_ref, _, oi = O.solve(A[b], None, None)
         check_sigma_parity(S[b], s_ref, 32, 2.0 ** -53, c=4.0 if kernel == 7 else 2.0)
         check_factors(A[b], U[b], S[b], V[b])
+
+
+@pytest.mark.parametrize("want_v", [True, False])
+def test_c1_fused_finalize_with_holes(want_v):
+    """The default 32x32 kernel finalises in-kernel; problems with sigma < tiny/u columns (orthogonal
+    completion, src/svd.py:224-240) are flagged to the standalone pass.  Mixed batch: both paths agree
+    with the oracle, and sigma is bitwise equal to the unfused variant (19, same norm order)."""
+    import torch
+
+    B = 40
+    A = np.stack([random_matrix(32, 32, np.float64, seed=1700 + b) for b in range(B)])
+    A[1][:, 5] = 0.0                      # one zero column
+    A[6] = 0.0                            # zero matrix
+    A[11] = A[11][:, :6] @ np.random.default_rng(3).standard_normal((6, 32))  # rank 6
+    A[12][:, 30] = A[12][:, 2]            # repeated column
+    A[25][:, ::2] = 0.0                   # half the columns zero
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    opts = bs.JacobiOptions(compute_right_vectors=want_v)
+    r = bs.solve_tensor(a, 32, 32, opts, kernel=12)
+    r19 = bs.solve_tensor(a, 32, 32, opts, kernel=19)
+    torch.cuda.synchronize()
+    assert torch.equal(r.s, r19.s)
+    du = (r.u - r19.u).abs().max().item()
+    assert du <= 4 * 2.0 ** -53, du  # U = W * (1/sigma) + residual correction vs W / sigma
+    if want_v:
+        assert torch.equal(r.v, r19.v)
+    U, S = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy()
+    V = np.swapaxes(r.v.cpu().numpy(), 1, 2) if want_v else None
+    for b in [0, 1, 6, 11, 12, 25, 39]:
+        _, s_ref, _, _ = O.solve(A[b], Opts(compute_right_vectors=want_v), None)
+        check_sigma_parity(S[b], s_ref, 32, 2.0 ** -53)
+        check_factors(A[b], U[b], S[b], V[b] if want_v else None)
 
 
 @pytest.mark.parametrize("want_v", [True, False])
@@ -342,7 +374,7 @@ def test_host_pipeline_matches_device_path(dt, m, n, want_v):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kernel", [0, 26])
+@pytest.mark.parametrize("kernel", [0, 17, 19, 26])
 def test_problem_results_independent_of_warp_partner(kernel):
     """Two problems share a warp in the 32x32 register kernels; a problem's bits must not depend on its
     partner (the reference's batch == standalone guarantee, tests/test_batch.py:19-28)."""

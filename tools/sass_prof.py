@@ -2,8 +2,9 @@
 and the hottest instructions.  Development aid."""
 import csv, sys
 from collections import Counter
-rows = list(csv.reader(open(sys.argv[1])))
-hdr = rows[1]; data = rows[2:]
+rows = list(csv.reader(open(sys.argv[1], errors='replace')))
+hdr = next(r for r in rows if r and r[0] == 'Address')
+data = [r for r in rows if len(r) == len(hdr) and r[0] not in ('Address', 'Kernel Name')]
 ix = {h: i for i, h in enumerate(hdr)}
 stalls = [h for h in hdr if h.startswith('stall_') and 'Not Issued' not in h]
 f = lambda r, k: float(r[ix[k]] or 0)
