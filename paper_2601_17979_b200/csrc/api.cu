@@ -51,6 +51,11 @@ int make_route(int m, int n, const bsvd_opts* o, Route* r) {
 Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = true) {
     const size_t lim = smem_limit();
     const int es = esize_of(dt), rs = rsize_of(dt);
+    if (o->kernel == 0 || o->kernel == KV_CREG32) {  // complex FP64, n = 32: both routes
+        Plan p = plan_creg32(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, r.blocked, o->nb);
+        if (p.kernel) return p;
+        if (o->kernel != 0) return p;
+    }
     if (r.blocked) {
         if (o->kernel == 0 || o->kernel == KV_BLOCKED_REG) {
             Plan p = plan_blocked_reg(dt, r.bm, r.bn, o->nb, r.need_v, contiguous && !r.trans, o->inner_sweeps);
@@ -146,6 +151,9 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
             return BSVD_ERR_UNSUPPORTED;
         case KV_BLOCKED_REG:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_blocked_reg(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
+        case KV_CREG32:
+            if constexpr (sizeof(T) == 16 && tr<T>::cplx) return launch_creg32(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_BLOCKED_DMMA:
         case KV_BLOCKED_DMMA_VG:

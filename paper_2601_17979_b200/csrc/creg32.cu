@@ -1,0 +1,451 @@
+// creg32.cu -- kernel (2)/(3), complex FP64 (c128) register-resident Jacobi for
+// n = 32 columns and m <= 256 rows (BASELINE config C4: 256 x 32 c128, both the
+// reference's dispatch route and its blocked Gram route, and the 32 x 32 R
+// factor of the QR-preprocessed route).
+//
+// Reference iteration (onesided_sweeps, src/_kernels_numba.py:85-138): for
+// each of the 31 iterations of the round-robin schedule (src/ordering.py:
+// 32-75) and each of its 16 disjoint pairs (i < j):
+//   g_ji = sum_r conj(a_rj) a_ri,  skip if |g_ji| <= 0 or |g_ji| < tol sqrt(g_ii g_jj)
+//   w = conj(g_ji)/|g_ji|, tau = (g_ii - g_jj)/(2|g_ji|), t, s, c - 1 (F5)
+//   a_i <- a_i + (cm1 a_i + s conj(w) a_j),  a_j <- a_j + (cm1 a_j - s w a_i)
+// For n = 32 with nb = 16 the blocked route (_sweep_blocked, src/svd.py:
+// 481-522) has exactly one block pair, the whole matrix: its Gram eigensolve
+// (eig_sweeps on G = W^H W, src/_kernels_numba.py:17-82) applies the same
+// rotation sequence two-sidedly to G, and W <- W (I + Delta), V <- V (I + Delta)
+// (fused_pair_update, src/_kernels_numba.py:141-175) -- so one kernel serves
+// both routes; only the telemetry (gram/update calls, path) and the inner
+// sweep budget differ.
+//
+// B200 mapping: one CTA per problem, NW = ceil(m / 32) warps, lane l of warp w
+// holds row 32 w + l of W (32 complex = 64 doubles) in registers with the
+// tournament ring in compile-time register slots (unrolled by 2, as in
+// unblocked_reg32b.cu).  Per iteration: each lane forms its row's 16
+// conj(x_b) x_t partials, a smem transpose reduces them over the warp, the NW
+// warp sums go through a parity-double-buffered smem slot and ONE named
+// barrier, and every warp then evaluates all 16 rotations itself (identical
+// bits in every warp: same sums, same order), so no second barrier is needed.
+// Column norms are maintained (d_i +- t|g|, recomputed at sweep start and after
+// a >4x shrink).  Rotation parameters use the half-angle chain of
+// rotation.cuh without ever forming |g|: A = +-(1/r)(1/c) p and
+// t|g| = |g|^2 (1/r)(1/c)^2, so the complex phase costs no division.
+// V never leaves shared memory: since V starts as I and only ever gets
+// right-multiplied by the rotations, V = P, the running product, updated
+// every iteration by all threads (one (row, pair) task each) in smem.
+#include "kernel_args.cuh"
+#include "launch.h"
+#include "rotation.cuh"
+
+namespace bsvd {
+namespace creg {
+
+constexpr int N = 32;      // columns
+constexpr int H = 16;      // pairs per iteration
+constexpr int NIT = 31;    // iterations per sweep
+constexpr int RSTR = 34;   // transpose buffer row stride (doubles)
+constexpr int PS = 33;     // column stride of the smem P planes (doubles)
+constexpr int MAXW = 8;    // warps per CTA (m <= 256)
+
+__host__ __device__ constexpr int ring_slot(int q) {
+    return q == 0 ? 1 : (q <= H - 1 ? 2 * q : 2 * (2 * H - 1 - q) + 1);
+}
+__host__ __device__ constexpr int md(int a) { return ((a % NIT) + NIT) % NIT; }
+__host__ __device__ constexpr int TS(int k, int u) { return k == 0 ? 0 : ring_slot(md(k - u)); }
+__host__ __device__ constexpr int BS(int k, int u) { return ring_slot(md((k == 0 ? 0 : NIT - k) - u)); }
+
+__host__ __device__ inline uint32_t pair_code(int t, int k) {
+    int qt = k - t, qb = (k == 0 ? 0 : NIT - k) - t;
+    qt += qt < 0 ? NIT : 0;
+    qb += qb < 0 ? NIT : 0;
+    const int ct = (k == 0) ? 0 : ring_slot(qt);
+    const int cb = ring_slot(qb);
+    return (uint32_t)ct | ((uint32_t)cb << 8) | ((ct > cb) ? (1u << 16) : 0u);
+}
+
+struct __align__(16) Par {
+    double cm1, ar, ai, pad;  // x_t += cm1 x_t + A x_b;  x_b += cm1 x_b - conj(A) x_t
+};
+
+struct WarpSmem {
+    double red[2 * H * RSTR];  // transpose buffer (32 partial rows x 32 lanes)
+    Par pub[H];
+    double nrm[N];             // maintained squared column norms (identical in every warp)
+};
+
+struct CtaSmem {
+    double P[2][N * PS];           // running rotation product (= V), real / imaginary planes, column-major
+    double gsum[2][MAXW][4 * H];   // cross-warp partial sums [parity][warp][value]
+    int misc[4];                   // [0] bad input, [2..3] amax bits (8-byte aligned)
+};
+
+__device__ __forceinline__ double sum16(const double* p) {
+    const double2* r = reinterpret_cast<const double2*>(p);
+    const double2 p0 = r[0], p1 = r[1], p2 = r[2], p3 = r[3], p4 = r[4], p5 = r[5], p6 = r[6], p7 = r[7];
+    const double s0 = (p0.x + p0.y) + (p1.x + p1.y), s1 = (p2.x + p2.y) + (p3.x + p3.y);
+    const double s2 = (p4.x + p4.y) + (p5.x + p5.y), s3 = (p6.x + p6.y) + (p7.x + p7.y);
+    return (s0 + s1) + (s2 + s3);
+}
+// total over the warp's 32 lanes of transpose row `row` (identical bits on both halves)
+__device__ __forceinline__ double sum32(const double* red, int row, int half) {
+    const double s = sum16(red + row * RSTR + 16 * half);
+    const double o = __shfl_xor_sync(0xffffffffu, s, 16);
+    return half ? o + s : s + o;
+}
+__device__ __forceinline__ void bar_named(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+template <int SH>
+__device__ __forceinline__ void ring_shift(double (&x)[N]) {
+    if constexpr (md(SH) != 0) {
+        const double t = x[ring_slot(0)];
+#pragma unroll
+        for (int i = 0; i < NIT - 1; ++i) x[ring_slot(md(-i * SH))] = x[ring_slot(md(-(i + 1) * SH))];
+        x[ring_slot(md(-(NIT - 1) * SH))] = t;
+    }
+}
+
+// x_t += cm1 x_t + A x_b,  x_b += cm1 x_b - conj(A) x_t   (old values on every right-hand side)
+__device__ __forceinline__ void capply(double& tr, double& ti, double& br, double& bi, const Par& p) {
+    const double ntr = fma(p.cm1, tr, fma(p.ar, br, fma(-p.ai, bi, tr)));
+    const double nti = fma(p.cm1, ti, fma(p.ar, bi, fma(p.ai, br, ti)));
+    const double nbr = fma(p.cm1, br, fma(-p.ar, tr, fma(-p.ai, ti, br)));
+    const double nbi = fma(p.cm1, bi, fma(-p.ar, ti, fma(p.ai, tr, bi)));
+    tr = ntr;
+    ti = nti;
+    br = nbr;
+    bi = nbi;
+}
+
+// Half-angle rotation for (|d|, p = g_tb): kk = (1/r)(1/c) with r = sqrt(d^2 + 4|p|^2),
+// so that A = +-kk p, cm1 = -|s|^2 / (1 + c), dn = t |g| = |p|^2 kk / c.
+__device__ __forceinline__ void cparams_core(double dabs, double pr, double pi, double& cm1, double& kk, double& dn) {
+    const double q2 = fma(pr, pr, pi * pi);
+    const double q = fma(4.0, q2, dabs * dabs);
+    const double ir = rsqrt_cubic(q);
+    const double c2 = fma(0.5 * dabs, ir, 0.5);
+    const double ic = rsqrt_cubic(c2);
+    const double c = c2 * ic;
+    kk = ir * ic;
+    cm1 = -(q2 * kk * kk) * rcp_cubic(1.0 + c);
+    dn = q2 * kk * ic;
+}
+__device__ __forceinline__ void cparams(double dabs, double pr, double pi, double& cm1, double& kk, double& dn) {
+    cparams_core(dabs, pr, pi, cm1, kk, dn);
+    if (fmax(dabs, fmax(fabs(pr), fabs(pi))) < 0x1p-500) {  // exact power-of-two rescale of tiny inputs
+        cparams_core(dabs * 0x1p+600, pr * 0x1p+600, pi * 0x1p+600, cm1, kk, dn);
+        kk *= 0x1p+600;
+        dn *= 0x1p-600;
+    }
+}
+
+struct Ctx {
+    WarpSmem* sm;
+    CtaSmem* cs;
+    const uint32_t* ctab;
+    int lane, half, k, warp;
+    double tol, tol2;
+    bool want_p;
+};
+
+struct IState {
+    int my_rot;  // rotations of pair k in this sweep (lanes < 16)
+    bool full;   // this iteration reads fresh norms
+    int par;     // cross-warp buffer parity
+};
+
+template <int u, int NW>
+__device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx& c, int t, IState& st) {
+    WarpSmem& sm = *c.sm;
+    // ---- partial products of this lane's row: p_q = conj(x_b) x_t ----
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+        const double tr = xr[TS(q, u)], ti = xi[TS(q, u)], br = xr[BS(q, u)], bi = xi[BS(q, u)];
+        sm.red[q * RSTR + c.lane] = fma(bi, ti, br * tr);
+        sm.red[(H + q) * RSTR + c.lane] = fma(-bi, tr, br * ti);
+    }
+    const uint32_t code = c.ctab[t * H + c.k];
+    __syncwarp();
+    double v[4];
+    v[0] = sum32(sm.red, c.k, c.half);
+    v[1] = sum32(sm.red, H + c.k, c.half);
+    int nval = 2;
+    if (st.full) {  // fresh squared norms through the same buffer (rare: sweep start, >4x shrink)
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            const double tr = xr[TS(q, u)], ti = xi[TS(q, u)], br = xr[BS(q, u)], bi = xi[BS(q, u)];
+            sm.red[q * RSTR + c.lane] = fma(ti, ti, tr * tr);
+            sm.red[(H + q) * RSTR + c.lane] = fma(bi, bi, br * br);
+        }
+        __syncwarp();
+        v[2] = sum32(sm.red, c.k, c.half);
+        v[3] = sum32(sm.red, H + c.k, c.half);
+        nval = 4;
+    }
+    if constexpr (NW > 1) {  // sum over the CTA's warps: one barrier, fixed warp order
+        double* g = c.cs->gsum[st.par][0];
+        if (c.lane < H)
+            for (int x = 0; x < nval; ++x) g[c.warp * 4 * H + x * H + c.k] = v[x];
+        bar_named(NW * 32);
+        for (int x = 0; x < nval; ++x) {
+            double s = g[x * H + c.k];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) s += g[w * 4 * H + x * H + c.k];
+            v[x] = s;
+        }
+        st.par ^= 1;
+    }
+    // ---- rotation of pair k (every warp, identical bits) ----
+    const int ct = code & 0xff, cb = (code >> 8) & 0xff;
+    const bool flip = (code >> 16) != 0;
+    const double pr = v[0], pi = v[1];
+    const double gt = st.full ? v[2] : sm.nrm[ct];
+    const double gb = st.full ? v[3] : sm.nrm[cb];
+    const double q2 = fma(pr, pr, pi * pi);
+    const double pp = gt * gb;
+    const double pm = fmax(fabs(pr), fabs(pi));
+    bool rot = !(q2 < c.tol2 * pp);
+    if (pm < 0x1p-400 && pm > 0.0) {  // |g| from the rescaled components (squares would underflow)
+        const double sr = pr * 0x1p+600, si = pi * 0x1p+600;
+        rot = !(fsqrt(fma(sr, sr, si * si)) < c.tol * fsqrt(pp) * 0x1p+600);
+    }
+    rot = rot && pm > 0.0;
+    const double d = gt - gb;
+    double cm1, kk, dn;
+    cparams(fabs(d), pr, pi, cm1, kk, dn);
+    const bool eneg = d < 0.0 || (d == 0.0 && flip);
+    const double ks = eneg ? -kk : kk;
+    Par par;
+    par.cm1 = rot ? cm1 : 0.0;
+    par.ar = rot ? ks * pr : 0.0;
+    par.ai = rot ? ks * pi : 0.0;
+    par.pad = 0.0;
+    const double dtg = rot ? (eneg ? -dn : dn) : 0.0;
+    const double nt = gt + dtg, nb = gb - dtg;
+    const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
+    __syncwarp();  // every lane has read nrm[] and red[] of this iteration
+    if (c.lane < H) {
+        sm.pub[c.k] = par;
+        sm.nrm[ct] = nt;
+        sm.nrm[cb] = nb;
+        st.my_rot += rot ? 1 : 0;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, rot);
+    st.full = __ballot_sync(0xffffffffu, shrink) != 0u;
+    __syncwarp();
+    if (!mask) return;
+    // ---- W update in registers ----
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+        const Par pq = sm.pub[q];
+        capply(xr[TS(q, u)], xi[TS(q, u)], xr[BS(q, u)], xi[BS(q, u)], pq);
+    }
+    // ---- P (= V) update in smem: task (row = lane, pair q) for q = warp, warp + NW, ... ----
+    if (c.want_p) {
+        double* Pr = c.cs->P[0];
+        double* Pi = c.cs->P[1];
+        for (int q = c.warp; q < H; q += NW) {
+            const Par pq = sm.pub[q];
+            if (pq.cm1 == 0.0 && pq.ar == 0.0 && pq.ai == 0.0) continue;  // skipped pair (warp-uniform)
+            const uint32_t cq = c.ctab[t * H + q];
+            const int a0 = (cq & 0xff) * PS + c.lane, b0 = ((cq >> 8) & 0xff) * PS + c.lane;
+            double tr = Pr[a0], ti = Pi[a0], br = Pr[b0], bi = Pi[b0];
+            capply(tr, ti, br, bi, pq);
+            Pr[a0] = tr;
+            Pi[a0] = ti;
+            Pr[b0] = br;
+            Pi[b0] = bi;
+        }
+    }
+}
+
+// one sweep (31 iterations, ring unrolled by 2); returns with the columns in natural order
+template <int NW>
+__device__ __forceinline__ void sweep(double (&xr)[N], double (&xi)[N], const Ctx& c, IState& st) {
+    st.full = true;
+#pragma unroll 1
+    for (int gi = 0; gi < 16; ++gi) {
+        const int t0 = 2 * gi;
+        iter<0, NW>(xr, xi, c, t0, st);
+        if (gi == 15) {
+            ring_shift<1>(xr);
+            ring_shift<1>(xi);
+            break;
+        }
+        iter<1, NW>(xr, xi, c, t0 + 1, st);
+        ring_shift<2>(xr);
+        ring_shift<2>(xi);
+    }
+}
+
+inline size_t smem_bytes(int nw) {
+    return (size_t)nw * sizeof(WarpSmem) + sizeof(CtaSmem) + NIT * H * 4;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 8 / NW) k_creg32(SolveArgs<cx<double>> a, int blocked) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int prob = blockIdx.x;
+    const int m = a.bm;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem);
+    CtaSmem* cs = reinterpret_cast<CtaSmem*>(smem + NW * sizeof(WarpSmem));
+    uint32_t* ctab = reinterpret_cast<uint32_t*>(smem + NW * sizeof(WarpSmem) + sizeof(CtaSmem));
+    const bool want_p = a.need_v != 0;
+    for (int e = tid; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
+    if (tid < 4) cs->misc[tid] = 0;
+    if (want_p)
+        for (int e = tid; e < N * N; e += NW * 32) {
+            const int r = e % N, col = e / N;
+            cs->P[0][col * PS + r] = (r == col) ? 1.0 : 0.0;
+            cs->P[1][col * PS + r] = 0.0;
+        }
+    // ---- kernel (1): this lane's row of A, exact power-of-two prescale ----
+    const int row = warp * 32 + lane;
+    const bool live = row < m;
+    const cx<double>* Ap = a.A + (size_t)prob * a.strideA;
+    double xr[N], xi[N];
+    double amax = 0.0;
+    int bad = 0;
+#pragma unroll
+    for (int col = 0; col < N; ++col) {
+        cx<double> z{0.0, 0.0};
+        if (live) z = Ap[row + (size_t)col * a.lda];
+        xr[col] = z.re;
+        xi[col] = z.im;
+        bad |= !(isfinite(z.re) && isfinite(z.im));
+        amax = fmax(amax, fmax(fabs(z.re), fabs(z.im)));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if (lane == 0) {
+        if (bad) atomicOr(&cs->misc[0], 1);
+        atomicMax(reinterpret_cast<unsigned long long*>(&cs->misc[2]), (unsigned long long)__double_as_longlong(amax));
+    }
+    __syncthreads();
+    const int ex = prescale_exponent(__longlong_as_double(*reinterpret_cast<long long*>(&cs->misc[2])));
+    {
+        const double sc = pow2(-ex);
+#pragma unroll
+        for (int col = 0; col < N; ++col) {
+            xr[col] *= sc;
+            xi[col] *= sc;
+        }
+    }
+    Ctx c;
+    c.sm = &wsm[warp];
+    c.cs = cs;
+    c.ctab = ctab;
+    c.lane = lane;
+    c.half = lane >> 4;
+    c.k = lane & 15;
+    c.warp = warp;
+    c.tol = a.tol;
+    c.tol2 = a.tol * a.tol;
+    c.want_p = want_p;
+    const int budget = blocked ? a.inner_budget : 1;
+    int sweeps = 0, last = 0, conv = 0;
+    long long rot_total = 0, grams = 0, updates = 0;
+    IState st;
+    st.par = 0;
+#pragma unroll 1
+    for (int sw = 0; sw < a.max_sweeps; ++sw) {
+        int bp_rot = 0;
+#pragma unroll 1
+        for (int isw = 0; isw < budget; ++isw) {
+            st.my_rot = 0;
+            sweep<NW>(xr, xi, c, st);
+            int r = st.my_rot;  // lanes 0..15: counts of pairs 0..15 (identical in every warp)
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+            r = __shfl_sync(0xffffffffu, r, 0);
+            bp_rot += r;
+            if (r == 0) break;
+        }
+        ++grams;
+        updates += bp_rot ? 1 : 0;
+        sweeps = sw + 1;
+        last = bp_rot;
+        rot_total += bp_rot;
+        if (bp_rot == 0) {
+            conv = 1;
+            break;
+        }
+    }
+    // ---- raw W (unscaled) and V = P to the workspace for the finalisation pass ----
+    cx<double>* W = a.work + (size_t)prob * (size_t)a.work_stride;
+    if (live) {
+        const double us = pow2(ex);
+#pragma unroll
+        for (int col = 0; col < N; ++col) W[row + (size_t)col * m] = cx<double>{xr[col] * us, xi[col] * us};
+    }
+    if (want_p) {
+        __syncthreads();
+        cx<double>* V = W + (size_t)m * N;
+        for (int e = tid; e < N * N; e += NW * 32) {
+            const int r = e % N, col = e / N;
+            V[e] = cx<double>{cs->P[0][col * PS + r], cs->P[1][col * PS + r]};
+        }
+    }
+    if (tid == 0 && a.info) {
+        bsvd_info inf;
+        inf.converged = conv;
+        inf.outer_sweeps = sweeps;
+        inf.rotations = rot_total;
+        inf.gram_calls = blocked ? grams : 0;
+        inf.update_calls = blocked ? updates : 0;
+        inf.last_rotations = last;
+        inf.path = blocked ? 2 : 1;
+        inf.status = cs->misc[0] ? 1 : 0;
+        inf.kernel = a.kernel;
+        a.info[prob] = inf;
+    }
+}
+
+}  // namespace creg
+
+Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blocked, int nb) {
+    Plan p{};
+    if (dtype != BSVD_Z || bn != 32 || bm < 32 || bm > 256 || !contiguous) return p;
+    if (blocked && nb != 16) return p;  // one block pair = the whole matrix only when nb = 16
+    const int nw = (bm + 31) / 32;
+    const int nwp = nw <= 1 ? 1 : nw <= 2 ? 2 : nw <= 4 ? 4 : 8;
+    p.kernel = KV_CREG32;
+    p.threads = nwp * 32;
+    p.group = nwp;
+    p.smem = creg::smem_bytes(nwp);
+    p.work_elems = (size_t)bm * bn + (need_v ? (size_t)bn * bn : 0);
+    p.grid = 0;
+    p.resident = blocked ? 1 : 0;  // route flag for the launcher
+    return p;
+}
+
+template <int NW>
+static int launch_c(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st) {
+    auto k = creg::k_creg32<NW>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<a.batch, NW * 32, p.smem, st>>>(a, p.resident);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+int launch_creg32(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st) {
+    a.kernel = p.kernel;
+    a.work_stride = (int64_t)p.work_elems;
+    int rc;
+    switch (p.group) {
+        case 1: rc = launch_c<1>(a, p, st); break;
+        case 2: rc = launch_c<2>(a, p, st); break;
+        case 4: rc = launch_c<4>(a, p, st); break;
+        default: rc = launch_c<8>(a, p, st); break;
+    }
+    if (rc) return rc;
+    return launch_finalize_gm<cx<double>>(a, st);
+}
+
+}  // namespace bsvd

@@ -114,7 +114,15 @@ def test_kernel_selection_routes():
     assert L.bsvd_select_kernel(3, 64, 64, ctypes.byref(o)) == 2      # blocked complex: general kernel
     assert L.bsvd_select_kernel(0, 16, 16, ctypes.byref(o)) == 11     # 16x16 FP32 register kernel
     assert L.bsvd_select_kernel(1, 32, 32, ctypes.byref(o)) == 12     # 32x32 FP64 register kernel (2nd gen)
-    assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) in (1, 3)  # unblocked route
+    assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) == 32    # c128 n = 32: complex register kernel
+    assert L.bsvd_select_kernel(3, 300, 32, ctypes.byref(o)) == 1     # m > 256: general unblocked kernel
+    assert L.bsvd_select_kernel(2, 256, 32, ctypes.byref(o)) == 1     # c64: general unblocked kernel
+    o.route = _lib.FORCE_BLOCKED
+    assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) == 32    # blocked route, ell = 2: same kernel
+    o.nb = 8
+    assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) == 2     # ell = 4: general blocked kernel
+    o.nb = 16
+    o.route = _lib.DISPATCH
     assert L.bsvd_select_kernel(1, 0, 5, ctypes.byref(o)) == 0        # empty
 
 
