@@ -399,7 +399,8 @@ int run_qr(int dtype, const Route& r, int m, int n, int batch, const void* A, in
            bsvd_info* info, void* work, size_t work_bytes, cudaStream_t st) {
     const QrWs q = qr_ws(dtype, r, batch, o);
     if (q.total > work_bytes || !work) return BSVD_ERR_WORKSPACE;
-    if (qr_smem(sizeof(T), r.bm, r.bn) > smem_limit()) return BSVD_ERR_UNSUPPORTED;
+    if (!qr_reg_ok(sizeof(T), tr<T>::cplx, r.bm, r.bn) && qr_smem(sizeof(T), r.bm, r.bn) > smem_limit())
+        return BSVD_ERR_UNSUPPORTED;
     unsigned char* w = static_cast<unsigned char*>(work);
     T* refl = reinterpret_cast<T*>(w + q.refl);
     T* R = reinterpret_cast<T*>(w + q.r);

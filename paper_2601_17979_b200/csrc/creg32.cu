@@ -73,9 +73,11 @@ struct WarpSmem {
 };
 
 struct CtaSmem {
-    double P[2][N * PS];           // running rotation product (= V), real / imaginary planes, column-major
     double gsum[2][MAXW][4 * H];   // cross-warp partial sums [parity][warp][value]
     int misc[4];                   // [0] bad input, [2..3] amax bits (8-byte aligned)
+};
+struct PSmem {
+    double P[2][N * PS];           // running rotation product (= V), real / imaginary planes, column-major
 };
 
 __device__ __forceinline__ double sum16(const double* p) {
@@ -142,8 +144,11 @@ __device__ __forceinline__ void cparams(double dabs, double pr, double pi, doubl
 struct Ctx {
     WarpSmem* sm;
     CtaSmem* cs;
+    PSmem* ps;                 // smem P (SP kernels)
     const uint32_t* ctab;
     int lane, half, k, warp;
+    int nww;                   // warps holding rows of W (the rest hold V rows / padding)
+    bool wrow;                 // this lane holds a row of W
     double tol, tol2;
     bool want_p;
 };
@@ -154,15 +159,17 @@ struct IState {
     int par;     // cross-warp buffer parity
 };
 
-template <int u, int NW>
+template <int u, int NW, bool SP>
 __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx& c, int t, IState& st) {
     WarpSmem& sm = *c.sm;
-    // ---- partial products of this lane's row: p_q = conj(x_b) x_t ----
+    // ---- partial products of this lane's row: p_q = conj(x_b) x_t (V / padding lanes keep 0) ----
+    if (SP || c.wrow) {  // SP: every lane is a W (or zero padding) row
 #pragma unroll
-    for (int q = 0; q < H; ++q) {
-        const double tr = xr[TS(q, u)], ti = xi[TS(q, u)], br = xr[BS(q, u)], bi = xi[BS(q, u)];
-        sm.red[q * RSTR + c.lane] = fma(bi, ti, br * tr);
-        sm.red[(H + q) * RSTR + c.lane] = fma(-bi, tr, br * ti);
+        for (int q = 0; q < H; ++q) {
+            const double tr = xr[TS(q, u)], ti = xi[TS(q, u)], br = xr[BS(q, u)], bi = xi[BS(q, u)];
+            sm.red[q * RSTR + c.lane] = fma(bi, ti, br * tr);
+            sm.red[(H + q) * RSTR + c.lane] = fma(-bi, tr, br * ti);
+        }
     }
     const uint32_t code = c.ctab[t * H + c.k];
     __syncwarp();
@@ -172,11 +179,13 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
     int nval = 2;
     if (st.full) {  // fresh squared norms through the same buffer (rare: sweep start, >4x shrink)
         __syncwarp();
+        if (SP || c.wrow) {
 #pragma unroll
-        for (int q = 0; q < H; ++q) {
-            const double tr = xr[TS(q, u)], ti = xi[TS(q, u)], br = xr[BS(q, u)], bi = xi[BS(q, u)];
-            sm.red[q * RSTR + c.lane] = fma(ti, ti, tr * tr);
-            sm.red[(H + q) * RSTR + c.lane] = fma(bi, bi, br * br);
+            for (int q = 0; q < H; ++q) {
+                const double tr = xr[TS(q, u)], ti = xi[TS(q, u)], br = xr[BS(q, u)], bi = xi[BS(q, u)];
+                sm.red[q * RSTR + c.lane] = fma(ti, ti, tr * tr);
+                sm.red[(H + q) * RSTR + c.lane] = fma(bi, bi, br * br);
+            }
         }
         __syncwarp();
         v[2] = sum32(sm.red, c.k, c.half);
@@ -185,13 +194,14 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
     }
     if constexpr (NW > 1) {  // sum over the CTA's warps: one barrier, fixed warp order
         double* g = c.cs->gsum[st.par][0];
-        if (c.lane < H)
+        if (c.lane < H && (SP || c.warp < c.nww))
             for (int x = 0; x < nval; ++x) g[c.warp * 4 * H + x * H + c.k] = v[x];
         bar_named(NW * 32);
         for (int x = 0; x < nval; ++x) {
             double s = g[x * H + c.k];
 #pragma unroll
-            for (int w = 1; w < NW; ++w) s += g[w * 4 * H + x * H + c.k];
+            for (int w = 1; w < NW; ++w)
+                if (SP || w < c.nww) s += g[w * 4 * H + x * H + c.k];
             v[x] = s;
         }
         st.par ^= 1;
@@ -242,9 +252,9 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
         capply(xr[TS(q, u)], xi[TS(q, u)], xr[BS(q, u)], xi[BS(q, u)], pq);
     }
     // ---- P (= V) update in smem: task (row = lane, pair q) for q = warp, warp + NW, ... ----
-    if (c.want_p) {
-        double* Pr = c.cs->P[0];
-        double* Pi = c.cs->P[1];
+    if (SP && c.want_p) {
+        double* Pr = c.ps->P[0];
+        double* Pi = c.ps->P[1];
         for (int q = c.warp; q < H; q += NW) {
             const Par pq = sm.pub[q];
             if (pq.cm1 == 0.0 && pq.ar == 0.0 && pq.ai == 0.0) continue;  // skipped pair (warp-uniform)
@@ -261,49 +271,55 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
 }
 
 // one sweep (31 iterations, ring unrolled by 2); returns with the columns in natural order
-template <int NW>
+template <int NW, bool SP>
 __device__ __forceinline__ void sweep(double (&xr)[N], double (&xi)[N], const Ctx& c, IState& st) {
     st.full = true;
 #pragma unroll 1
     for (int gi = 0; gi < 16; ++gi) {
         const int t0 = 2 * gi;
-        iter<0, NW>(xr, xi, c, t0, st);
+        iter<0, NW, SP>(xr, xi, c, t0, st);
         if (gi == 15) {
             ring_shift<1>(xr);
             ring_shift<1>(xi);
             break;
         }
-        iter<1, NW>(xr, xi, c, t0 + 1, st);
+        iter<1, NW, SP>(xr, xi, c, t0 + 1, st);
         ring_shift<2>(xr);
         ring_shift<2>(xi);
     }
 }
 
-inline size_t smem_bytes(int nw) {
-    return (size_t)nw * sizeof(WarpSmem) + sizeof(CtaSmem) + NIT * H * 4;
+inline size_t smem_bytes(int nw, bool sp) {
+    return (size_t)nw * sizeof(WarpSmem) + sizeof(CtaSmem) + (sp ? sizeof(PSmem) : 0) + NIT * H * 4;
 }
 
-template <int NW>
-__global__ void __launch_bounds__(NW * 32, 8 / NW) k_creg32(SolveArgs<cx<double>> a, int blocked) {
+// NW warps; SP: V as the smem product P (m > 224), else V rows ride along in registers below
+// W's rows (rows m .. m + 31 of the CTA, rotated like W, excluded from the dot products).
+template <int NW, bool SP>
+__global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_creg32(SolveArgs<cx<double>> a, int blocked) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int prob = blockIdx.x;
     const int m = a.bm;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem);
     CtaSmem* cs = reinterpret_cast<CtaSmem*>(smem + NW * sizeof(WarpSmem));
-    uint32_t* ctab = reinterpret_cast<uint32_t*>(smem + NW * sizeof(WarpSmem) + sizeof(CtaSmem));
+    PSmem* ps = reinterpret_cast<PSmem*>(smem + NW * sizeof(WarpSmem) + sizeof(CtaSmem));
+    uint32_t* ctab =
+        reinterpret_cast<uint32_t*>(smem + NW * sizeof(WarpSmem) + sizeof(CtaSmem) + (SP ? sizeof(PSmem) : 0));
     const bool want_p = a.need_v != 0;
     for (int e = tid; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
+    for (int e = lane; e < 2 * H * RSTR; e += 32) wsm[warp].red[e] = 0.0;  // V / padding lanes stay 0
     if (tid < 4) cs->misc[tid] = 0;
-    if (want_p)
+    if (SP && want_p)
         for (int e = tid; e < N * N; e += NW * 32) {
             const int r = e % N, col = e / N;
-            cs->P[0][col * PS + r] = (r == col) ? 1.0 : 0.0;
-            cs->P[1][col * PS + r] = 0.0;
+            ps->P[0][col * PS + r] = (r == col) ? 1.0 : 0.0;
+            ps->P[1][col * PS + r] = 0.0;
         }
     // ---- kernel (1): this lane's row of A, exact power-of-two prescale ----
     const int row = warp * 32 + lane;
     const bool live = row < m;
+    const int vrow = (!SP && want_p && row >= m && row < m + N) ? row - m : -1;  // row of V this lane holds
     const cx<double>* Ap = a.A + (size_t)prob * a.strideA;
     double xr[N], xi[N];
     double amax = 0.0;
@@ -333,7 +349,7 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW) k_creg32(SolveArgs<cx<double>
         const double sc = pow2(-ex);
 #pragma unroll
         for (int col = 0; col < N; ++col) {
-            xr[col] *= sc;
+            xr[col] = vrow >= 0 ? (col == vrow ? 1.0 : 0.0) : xr[col] * sc;  // V = I
             xi[col] *= sc;
         }
     }
@@ -345,6 +361,9 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW) k_creg32(SolveArgs<cx<double>
     c.half = lane >> 4;
     c.k = lane & 15;
     c.warp = warp;
+    c.ps = ps;
+    c.nww = (m + 31) / 32;
+    c.wrow = live;
     c.tol = a.tol;
     c.tol2 = a.tol * a.tol;
     c.want_p = want_p;
@@ -359,7 +378,7 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW) k_creg32(SolveArgs<cx<double>
 #pragma unroll 1
         for (int isw = 0; isw < budget; ++isw) {
             st.my_rot = 0;
-            sweep<NW>(xr, xi, c, st);
+            sweep<NW, SP>(xr, xi, c, st);
             int r = st.my_rot;  // lanes 0..15: counts of pairs 0..15 (identical in every warp)
 #pragma unroll
             for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
@@ -384,13 +403,18 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW) k_creg32(SolveArgs<cx<double>
 #pragma unroll
         for (int col = 0; col < N; ++col) W[row + (size_t)col * m] = cx<double>{xr[col] * us, xi[col] * us};
     }
-    if (want_p) {
+    if (SP && want_p) {
         __syncthreads();
         cx<double>* V = W + (size_t)m * N;
         for (int e = tid; e < N * N; e += NW * 32) {
             const int r = e % N, col = e / N;
-            V[e] = cx<double>{cs->P[0][col * PS + r], cs->P[1][col * PS + r]};
+            V[e] = cx<double>{ps->P[0][col * PS + r], ps->P[1][col * PS + r]};
         }
+    }
+    if (vrow >= 0) {
+        cx<double>* V = W + (size_t)m * N;
+#pragma unroll
+        for (int col = 0; col < N; ++col) V[vrow + (size_t)col * N] = cx<double>{xr[col], xi[col]};
     }
     if (tid == 0 && a.info) {
         bsvd_info inf;
@@ -413,21 +437,22 @@ Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blo
     Plan p{};
     if (dtype != BSVD_Z || bn != 32 || bm < 32 || bm > 256 || !contiguous) return p;
     if (blocked && nb != 16) return p;  // one block pair = the whole matrix only when nb = 16
-    const int nw = (bm + 31) / 32;
-    const int nwp = nw <= 1 ? 1 : nw <= 2 ? 2 : nw <= 4 ? 4 : 8;
+    const int rows = bm + (need_v ? 32 : 0);  // V rows ride in registers when they fit
+    const bool sp = rows > 256;
+    const int nw = ((sp ? bm : rows) + 31) / 32;
     p.kernel = KV_CREG32;
-    p.threads = nwp * 32;
-    p.group = nwp;
-    p.smem = creg::smem_bytes(nwp);
+    p.threads = nw * 32;
+    p.group = nw | (sp ? 0x100 : 0);
+    p.smem = creg::smem_bytes(nw, sp);
     p.work_elems = (size_t)bm * bn + (need_v ? (size_t)bn * bn : 0);
     p.grid = 0;
     p.resident = blocked ? 1 : 0;  // route flag for the launcher
     return p;
 }
 
-template <int NW>
+template <int NW, bool SP>
 static int launch_c(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st) {
-    auto k = creg::k_creg32<NW>;
+    auto k = creg::k_creg32<NW, SP>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<a.batch, NW * 32, p.smem, st>>>(a, p.resident);
@@ -439,10 +464,16 @@ int launch_creg32(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st) {
     a.work_stride = (int64_t)p.work_elems;
     int rc;
     switch (p.group) {
-        case 1: rc = launch_c<1>(a, p, st); break;
-        case 2: rc = launch_c<2>(a, p, st); break;
-        case 4: rc = launch_c<4>(a, p, st); break;
-        default: rc = launch_c<8>(a, p, st); break;
+        case 1: rc = launch_c<1, false>(a, p, st); break;
+        case 2: rc = launch_c<2, false>(a, p, st); break;
+        case 3: rc = launch_c<3, false>(a, p, st); break;
+        case 4: rc = launch_c<4, false>(a, p, st); break;
+        case 5: rc = launch_c<5, false>(a, p, st); break;
+        case 6: rc = launch_c<6, false>(a, p, st); break;
+        case 7: rc = launch_c<7, false>(a, p, st); break;
+        case 8: rc = launch_c<8, false>(a, p, st); break;
+        case 8 | 0x100: rc = launch_c<8, true>(a, p, st); break;
+        default: return BSVD_ERR_UNSUPPORTED;
     }
     if (rc) return rc;
     return launch_finalize_gm<cx<double>>(a, st);
