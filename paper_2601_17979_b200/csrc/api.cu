@@ -76,6 +76,7 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         if (o->kernel != 0) return p;
     }
     if (is_reg32e(o->kernel)) return plan_unblocked_reg32e(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
+    if (is_reg32c(o->kernel)) return plan_unblocked_reg32c(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
     if (is_reg32b(o->kernel)) {
         Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel, o->max_sweeps);
         return p;  // forced variant unavailable => kernel 0 => unsupported
@@ -151,6 +152,12 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
             return BSVD_ERR_UNSUPPORTED;
         case KV_BLOCKED_REG:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_blocked_reg(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
+        case KV_UNBLOCKED_REG32C:
+        case KV_UNBLOCKED_REG32C + 1:
+        case KV_UNBLOCKED_REG32C + 2:
+        case KV_UNBLOCKED_REG32C_LAST:
+            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32c(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_CREG32:
             if constexpr (sizeof(T) == 16 && tr<T>::cplx) return launch_creg32(a, p, st);

@@ -266,7 +266,7 @@ def test_reg32_partial_ctas(batch):
         check_factors(a, r.u, r.sigma, r.v)
 
 
-@pytest.mark.parametrize("kernel", [1, 3, 4, 5, 6, 7, 12, 13, 14, 15, 16, 17, 18, 19, 26, 27, 28, 29])
+@pytest.mark.parametrize("kernel", [1, 3, 4, 5, 6, 7, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 26, 27, 28, 29])
 def test_c1_kernel_variants_agree(kernel):
     """Every 32x32 FP64 kernel variant meets the parity contract on the same inputs."""
     import torch
@@ -374,7 +374,7 @@ def test_host_pipeline_matches_device_path(dt, m, n, want_v):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kernel", [0, 17, 19, 26])
+@pytest.mark.parametrize("kernel", [0, 17, 19, 20, 26])
 def test_problem_results_independent_of_warp_partner(kernel):
     """Two problems share a warp in the 32x32 register kernels; a problem's bits must not depend on its
     partner (the reference's batch == standalone guarantee, tests/test_batch.py:19-28)."""
