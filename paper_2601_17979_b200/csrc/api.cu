@@ -70,6 +70,11 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         }
         return plan_blocked_general(es, rs, r.bm, r.bn, o->nb, r.need_v, lim);
     }
+    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG16B || o->kernel == KV_UNBLOCKED_REG16B + 1) {
+        Plan p = plan_unblocked_reg16b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
+        if (p.kernel) return p;
+        if (o->kernel != 0) return p;
+    }
     if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG16F) {
         Plan p = plan_unblocked_reg16(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans);
         if (p.kernel) return p;
@@ -147,6 +152,10 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
     switch (p.kernel) {
         case KV_UNBLOCKED_GENERAL: return launch_unblocked_general<T>(a, p, st);
         case KV_BLOCKED_GENERAL: return launch_blocked_general<T>(a, p, st);
+        case KV_UNBLOCKED_REG16B:
+        case KV_UNBLOCKED_REG16B + 1:
+            if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16b(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG16F:
             if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16(a, p, st);
             return BSVD_ERR_UNSUPPORTED;

@@ -60,6 +60,7 @@ int launch_finalize_flagged(SolveArgs<T> a, cudaStream_t st) {
     return launch_finalize_impl<T, true>(a, st);
 }
 template int launch_finalize_flagged<double>(SolveArgs<double>, cudaStream_t);
+template int launch_finalize_flagged<float>(SolveArgs<float>, cudaStream_t);
 
 // Finalisation in place in the workspace (global / L2): for solvers whose W
 // and V live in the workspace and are too large to stage in shared memory.

@@ -53,6 +53,7 @@ enum {
     KV_UNBLOCKED_REG32B_LAST = 19,  // 13..19: tuning variants (registers, V unroll, CTA shape, split W/V, unfused finalize)
     KV_UNBLOCKED_REG32C = 20,   // 32x32 FP64 third generation: one problem per warp, row per lane, 3-4 warps/SMSP
     KV_UNBLOCKED_REG32C_LAST = 23,  // 21..23: register budget / rotation prefetch variants
+    KV_UNBLOCKED_REG16B = 24,   // 16x16 FP32 second generation: 2 problems per warp, row per lane (25: 56-register cap)
     KV_UNBLOCKED_REG32E = 26,   // 32x32 FP64 warp-specialised: W warp + V warp per problem pair, smem ring
     KV_UNBLOCKED_REG32E_LAST = 29,  // 27..29: tuning variants (pairs per CTA, V unroll)
     KV_HEEVJ = 31,              // batched Hermitian Jacobi eigensolver (bsvd_heevj_batched)

@@ -319,8 +319,9 @@ def test_c1_fused_finalize_with_holes(want_v):
         check_factors(A[b], U[b], S[b], V[b] if want_v else None)
 
 
+@pytest.mark.parametrize("kernel", [0, 11, 24, 25])
 @pytest.mark.parametrize("want_v", [True, False])
-def test_c2_fp32_register_kernel(want_v):
+def test_c2_fp32_register_kernel(want_v, kernel):
     """BASELINE C2 shape (16x16 FP32, values-only and full) through the FP32 register kernel."""
     import torch
 
@@ -329,10 +330,10 @@ def test_c2_fp32_register_kernel(want_v):
     B = 203  # not a multiple of the 16 problems per CTA
     A = np.stack([random_matrix(16, 16, np.float32, seed=800 + b) for b in range(B)])
     a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
-    r = bs.solve_tensor(a, 16, 16, bs.JacobiOptions(compute_right_vectors=want_v))
+    r = bs.solve_tensor(a, 16, 16, bs.JacobiOptions(compute_right_vectors=want_v), kernel=kernel)
     torch.cuda.synchronize()
     info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
-    assert (info["kernel"] == 11).all() and info["converged"].all()
+    assert (info["kernel"] == (kernel or 24)).all() and info["converged"].all()
     U, S = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy()
     V = np.swapaxes(r.v.cpu().numpy(), 1, 2) if want_v else None
     u = 2.0 ** -24
@@ -392,3 +393,23 @@ def test_problem_results_independent_of_warp_partner(kernel):
     assert torch.equal(r0.u[torch.from_numpy(perm).cuda()], r1.u)
     assert torch.equal(r0.s[torch.from_numpy(perm).cuda()], r1.s)
     assert torch.equal(r0.v[torch.from_numpy(perm).cuda()], r1.v)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", [11, 24, 25])
+def test_fp32_16x16_results_independent_of_warp_partner(kernel):
+    """Several problems share a warp in the 16x16 FP32 register kernels; batch == standalone bitwise
+    (tests/test_batch.py:19-28), including a problem whose norms shrink >4x (fresh-norm iterations)."""
+    import torch
+
+    B = 21
+    A = np.stack([random_matrix(16, 16, np.float32, seed=1300 + b) for b in range(B)])
+    A[4] = (np.diag(np.geomspace(1.0, 1e-5, 16)) @ A[4]).astype(np.float32)
+    perm = np.random.default_rng(6).permutation(B)
+    a0 = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    a1 = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A[perm], 1, 2))).cuda()
+    r0 = bs.solve_tensor(a0, 16, 16, bs.JacobiOptions(), kernel=kernel)
+    r1 = bs.solve_tensor(a1, 16, 16, bs.JacobiOptions(), kernel=kernel)
+    torch.cuda.synchronize()
+    p = torch.from_numpy(perm).cuda()
+    assert torch.equal(r0.u[p], r1.u) and torch.equal(r0.s[p], r1.s) and torch.equal(r0.v[p], r1.v)

@@ -112,7 +112,7 @@ def test_kernel_selection_routes():
     L.bsvd_default_opts(ctypes.byref(o))
     assert L.bsvd_select_kernel(1, 64, 64, ctypes.byref(o)) == 30     # blocked FP64: register block pairs
     assert L.bsvd_select_kernel(3, 64, 64, ctypes.byref(o)) == 2      # blocked complex: general kernel
-    assert L.bsvd_select_kernel(0, 16, 16, ctypes.byref(o)) == 11     # 16x16 FP32 register kernel
+    assert L.bsvd_select_kernel(0, 16, 16, ctypes.byref(o)) == 24     # 16x16 FP32 register kernel (2nd gen)
     assert L.bsvd_select_kernel(1, 32, 32, ctypes.byref(o)) == 12     # 32x32 FP64 register kernel (2nd gen)
     assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) == 32    # c128 n = 32: complex register kernel
     assert L.bsvd_select_kernel(3, 300, 32, ctypes.byref(o)) == 1     # m > 256: general unblocked kernel
