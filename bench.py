@@ -266,6 +266,17 @@ def load_traffic(config_id):
     return None
 
 
+def count_launches(fn) -> int:
+    """Kernels of this library (namespace bsvd) that one call of fn launches, from the CUDA activity trace."""
+    import torch
+
+    torch.cuda.synchronize()
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    return sum(1 for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and "bsvd" in e.name)
+
+
 def run_b200(args, cfg):
     import torch
 
@@ -342,6 +353,8 @@ def run_b200(args, cfg):
         dev_s = float(tt.item())
     info = np.frombuffer(res.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
     kernel_id = int(info["kernel"][0])
+    # our kernel launches per step, counted by the CUDA activity trace of one more (untimed) step
+    launches_per_step = count_launches(lambda: solve_tensor(a, m, n, opts, route, out=out))
     # accuracy of the whole timed batch on the device (bsvd_verify_batched; outside the timed region)
     from paper_2601_17979_b200.verify import verify_tensor
 
@@ -424,7 +437,8 @@ def run_b200(args, cfg):
                 "d2h_bytes_per_step": d2h, "path": "bsvd_gesvj_batched_host: pinned host buffers, H2D / solve / D2H "
                 f"pipelined in chunks of {e2e_chunk} over 3 streams"},
         "clocks": clocks,
-        "gpu_launches": args.steps,
+        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches_per_step": launches_per_step,
         "kernel_variant": kernel_id,
         "parity": {"converged_frac": float(info["converged"].mean()), "gpu_mean_sweeps": float(
             info["outer_sweeps"].mean()), "ref_mean_sweeps_sample": o_sweeps,
