@@ -192,6 +192,27 @@ int bsvd_fused_pair_update_batched(int dtype, int m, int w, int batch, void* b, 
                                    int delta, void* stream);
 
 /*
+ * finalize(work_a, v) (src/svd.py:278-303; _finalize_factors src/svd.py:243-275) as a batched
+ * operator: W m x n (ldw, m >= n) -> sigma (float64 column norms cast to the real dtype),
+ * U = W / sigma with orthogonal completion of columns below tiny/u, stable descending order;
+ * V (vrows x n, ldv) or NULL is permuted alike into Vout.  Inputs are not modified.
+ */
+int bsvd_finalize_batched(int dtype, int m, int n, int batch, const void* W, int64_t ldw, int64_t stride_w,
+                          int vrows, const void* V, int64_t ldv, int64_t stride_v, void* U, int64_t ldu,
+                          int64_t stride_u, void* S, int64_t stride_s, void* Vout, int64_t ldvo,
+                          int64_t stride_vout, void* stream);
+
+/*
+ * householder_qr(a) (src/core.py:118-168) as a batched operator: A m x n (m >= n) -> Q m x n with
+ * orthonormal columns and R n x n upper triangular with a real non-negative diagonal (the
+ * reference's sign convention), A = Q R.  Device workspace: bsvd_householder_qr_workspace_bytes.
+ */
+size_t bsvd_householder_qr_workspace_bytes(int dtype, int m, int n, int batch);
+int bsvd_householder_qr_batched(int dtype, int m, int n, int batch, const void* a, int64_t lda,
+                                int64_t stride_a, void* q, int64_t ldq, int64_t stride_q, void* r, int64_t ldr,
+                                int64_t stride_r, void* work, size_t work_bytes, void* stream);
+
+/*
  * Diagnostics: FMA-pipe peak microbenchmark used as the roofline denominator
  * (dtype BSVD_D or BSVD_S).  Launches blocks x 256 threads, each running
  * iters x 128 dependent-free FMAs; out: device scratch of `blocks` elements.

@@ -19,16 +19,35 @@ from .core import (
     unit_roundoff,
 )
 from .eig import EigInfo, Rotation, batch_hermitian_eig, compute_rotation, jacobi_hermitian_eig
-from .kernels import compute_gram, fused_pair_update, onesided_sweeps
+from .kernels import compute_gram, fused_pair_update, householder_qr, onesided_sweeps
 from .ordering import Schedule, round_robin_schedule, schedule_arrays
 from .solver import DeviceResult, solve_tensor
 from . import fileio
-from .verify import ErrorReport, error_report, threshold, verify_tensor
+from .fileio import (
+    DTYPE_CODES,
+    FormatError,
+    ResultRecord,
+    read_matrices,
+    read_results,
+    write_matrices,
+    write_results,
+)
+from .matgen import FAMILIES, make_sigma
+from .verify import (
+    ErrorReport,
+    error_report,
+    orthogonality_e2_e3,
+    residual_e1,
+    sigma_error_e4,
+    threshold,
+    verify_tensor,
+)
 from .svd import (
     JacobiOptions,
     SolveInfo,
     SvdResult,
     WorkCounters,
+    finalize,
     svd_blocked,
     svd_dispatch,
     svd_qr_preprocessed,
@@ -75,5 +94,19 @@ __all__ = [
     "threshold",
     "unit_roundoff",
     "verify_tensor",
+    "finalize",
+    "householder_qr",
+    "residual_e1",
+    "orthogonality_e2_e3",
+    "sigma_error_e4",
+    "DTYPE_CODES",
+    "FormatError",
+    "ResultRecord",
+    "read_matrices",
+    "read_results",
+    "write_matrices",
+    "write_results",
+    "FAMILIES",
+    "make_sigma",
     "__version__",
 ]

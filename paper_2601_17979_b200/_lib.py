@@ -67,6 +67,9 @@ EXPORTS = (
     "bsvd_heevj_batched",
     "bsvd_heevj_workspace_bytes",
     "bsvd_verify_batched",
+    "bsvd_finalize_batched",
+    "bsvd_householder_qr_workspace_bytes",
+    "bsvd_householder_qr_batched",
 )
 
 _lib = None
@@ -117,6 +120,14 @@ def load():
     L.bsvd_verify_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, vp, i64, i64, vp, i64, vp, i64, i64, vp, i64,
                                       vp, vp]
     L.bsvd_verify_batched.restype = ci
+    L.bsvd_finalize_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, ci, vp, i64, i64, vp, i64, i64, vp, i64, vp,
+                                        i64, i64, vp]
+    L.bsvd_finalize_batched.restype = ci
+    L.bsvd_householder_qr_workspace_bytes.argtypes = [ci, ci, ci, ci]
+    L.bsvd_householder_qr_workspace_bytes.restype = ctypes.c_size_t
+    L.bsvd_householder_qr_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, vp, i64, i64, vp, i64, i64, vp,
+                                              ctypes.c_size_t, vp]
+    L.bsvd_householder_qr_batched.restype = ci
     L.bsvd_bench_fma_peak.argtypes = [ci, ci, ci, vp, vp]
     L.bsvd_bench_fma_peak.restype = ci
     _lib = L

@@ -234,6 +234,50 @@ int bsvd_verify_batched(int dtype, int m, int n, int batch, const void* A, int64
                          strideSref, out, static_cast<cudaStream_t>(stream));
 }
 
+int bsvd_finalize_batched(int dtype, int m, int n, int batch, const void* W, int64_t ldw, int64_t strideW,
+                          int vrows, const void* V, int64_t ldv, int64_t strideV, void* U, int64_t ldu,
+                          int64_t strideU, void* S, int64_t strideS, void* Vout, int64_t ldvo, int64_t strideVout,
+                          void* stream) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || vrows < 0) return BSVD_ERR_ARG;
+    if (n > m) return BSVD_ERR_ARG;  // finalize expects m >= n (src/svd.py:246-247)
+    if (batch == 0 || n == 0) return BSVD_OK;
+    if (!W || !U || !S || ldw < m || ldu < m) return BSVD_ERR_ARG;
+    if (V && (!Vout || ldv < vrows || ldvo < vrows)) return BSVD_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t lim = smem_limit();
+    switch (dtype) {
+        case BSVD_S: return launch_finalize_ext<float>(m, n, vrows, batch, W, ldw, strideW, V, ldv, strideV, U, ldu, strideU, S, strideS, Vout, ldvo, strideVout, lim, st);
+        case BSVD_D: return launch_finalize_ext<double>(m, n, vrows, batch, W, ldw, strideW, V, ldv, strideV, U, ldu, strideU, S, strideS, Vout, ldvo, strideVout, lim, st);
+        case BSVD_C: return launch_finalize_ext<cx<float>>(m, n, vrows, batch, W, ldw, strideW, V, ldv, strideV, U, ldu, strideU, S, strideS, Vout, ldvo, strideVout, lim, st);
+        case BSVD_Z: return launch_finalize_ext<cx<double>>(m, n, vrows, batch, W, ldw, strideW, V, ldv, strideV, U, ldu, strideU, S, strideS, Vout, ldvo, strideVout, lim, st);
+    }
+    return BSVD_ERR_ARG;
+}
+
+size_t bsvd_householder_qr_workspace_bytes(int dtype, int m, int n, int batch) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0) return 0;
+    return householder_qr_work_bytes(esize_of(dtype), m, n, batch);
+}
+
+int bsvd_householder_qr_batched(int dtype, int m, int n, int batch, const void* A, int64_t lda, int64_t strideA,
+                                void* Q, int64_t ldq, int64_t strideQ, void* R, int64_t ldr, int64_t strideR,
+                                void* work, size_t work_bytes, void* stream) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0) return BSVD_ERR_ARG;
+    if (m < n) return BSVD_ERR_ARG;  // householder_qr needs m >= n (src/core.py:125-126)
+    if (batch == 0 || n == 0) return BSVD_OK;
+    if (!A || !Q || !R || lda < m || ldq < m || ldr < n) return BSVD_ERR_ARG;
+    if (!work || work_bytes < householder_qr_work_bytes(esize_of(dtype), m, n, batch)) return BSVD_ERR_WORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t lim = smem_limit();
+    switch (dtype) {
+        case BSVD_S: return launch_householder_qr<float>(m, n, batch, A, lda, strideA, Q, ldq, strideQ, R, ldr, strideR, work, lim, st);
+        case BSVD_D: return launch_householder_qr<double>(m, n, batch, A, lda, strideA, Q, ldq, strideQ, R, ldr, strideR, work, lim, st);
+        case BSVD_C: return launch_householder_qr<cx<float>>(m, n, batch, A, lda, strideA, Q, ldq, strideQ, R, ldr, strideR, work, lim, st);
+        case BSVD_Z: return launch_householder_qr<cx<double>>(m, n, batch, A, lda, strideA, Q, ldq, strideQ, R, ldr, strideR, work, lim, st);
+    }
+    return BSVD_ERR_ARG;
+}
+
 int bsvd_abi_version(void) { return BSVD_ABI_VERSION; }
 
 void bsvd_default_opts(bsvd_opts* o) {

@@ -85,6 +85,72 @@ int launch_finalize_gm(SolveArgs<T> a, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 
+// The finalize operator on caller buffers (finalize(work_a, v), src/svd.py:278-303): W (m x n, ldw) and
+// V (vrows x n, ldv) staged in shared memory, U / sigma / permuted V written to the outputs.
+template <class T>
+__global__ void __launch_bounds__(128) k_finalize_ext(int m, int n, int vrows, const T* W, int64_t ldw, int64_t sW,
+                                                      const T* V, int64_t ldv, int64_t sV, T* U, int64_t ldu,
+                                                      int64_t sU, typename tr<T>::R* S, int64_t sS, T* Vo,
+                                                      int64_t ldvo, int64_t svo) {
+    using R = typename tr<T>::R;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int prob = blockIdx.x;
+    T* Ws = reinterpret_cast<T*>(smem);
+    T* Vs = Ws + (size_t)m * n;
+    size_t off = ((size_t)m * n + (size_t)vrows * n) * sizeof(T);
+    off = (off + 15) & ~size_t(15);
+    R* sig = reinterpret_cast<R*>(smem + off);
+    off += ((size_t)n * sizeof(R) + 15) & ~size_t(15);
+    int* perm = reinterpret_cast<int*>(smem + off);
+    off += ((size_t)n * sizeof(int) + 15) & ~size_t(15);
+    int* flag = reinterpret_cast<int*>(smem + off);
+    const T* Wp = W + (size_t)prob * sW;
+    for (int e = threadIdx.x; e < m * n; e += blockDim.x) Ws[e] = Wp[(e % m) + (size_t)(e / m) * ldw];
+    if (V) {
+        const T* Vp = V + (size_t)prob * sV;
+        for (int e = threadIdx.x; e < vrows * n; e += blockDim.x) Vs[e] = Vp[(e % vrows) + (size_t)(e / vrows) * ldv];
+    }
+    __syncthreads();
+    FinalOut<T> o;
+    o.U = U + (size_t)prob * sU;
+    o.ldu = ldu;
+    o.S = S + (size_t)prob * sS;
+    o.V = V ? Vo + (size_t)prob * svo : nullptr;
+    o.ldv = ldvo;
+    o.trans = false;
+    o.want_v = V != nullptr;
+    finalize_block<T>(Ws, m, m, n, V ? Vs : nullptr, vrows, sig, perm, flag, o, vrows);
+}
+
+size_t finalize_ext_smem(int esize, int rsize, int m, int n, int vrows) {
+    size_t smem = ((size_t)m * n + (size_t)vrows * n) * esize;
+    return ((smem + 15) & ~size_t(15)) + (((size_t)n * rsize + 15) & ~size_t(15)) + (((size_t)n * 4 + 15) & ~size_t(15)) +
+           16;
+}
+
+template <class T>
+int launch_finalize_ext(int m, int n, int vrows, int batch, const void* W, int64_t ldw, int64_t sW, const void* V,
+                        int64_t ldv, int64_t sV, void* U, int64_t ldu, int64_t sU, void* S, int64_t sS, void* Vo,
+                        int64_t ldvo, int64_t svo, size_t smem_limit, cudaStream_t st) {
+    const size_t smem = finalize_ext_smem(sizeof(T), sizeof(typename tr<T>::R), m, n, V ? vrows : 0);
+    if (smem > smem_limit) return BSVD_ERR_UNSUPPORTED;
+    auto k = k_finalize_ext<T>;
+    if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<batch, 128, smem, st>>>(m, n, V ? vrows : 0, static_cast<const T*>(W), ldw, sW, static_cast<const T*>(V), ldv,
+                                sV, static_cast<T*>(U), ldu, sU, static_cast<typename tr<T>::R*>(S), sS,
+                                static_cast<T*>(Vo), ldvo, svo);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+#define BSVD_FIN_EXT(T)                                                                                          \
+    template int launch_finalize_ext<T>(int, int, int, int, const void*, int64_t, int64_t, const void*, int64_t, \
+                                        int64_t, void*, int64_t, int64_t, void*, int64_t, void*, int64_t, int64_t, \
+                                        size_t, cudaStream_t);
+BSVD_FIN_EXT(float)
+BSVD_FIN_EXT(double)
+BSVD_FIN_EXT(cx<float>)
+BSVD_FIN_EXT(cx<double>)
+
 template int launch_finalize_gm<double>(SolveArgs<double>, cudaStream_t);
 template int launch_finalize_gm<cx<double>>(SolveArgs<cx<double>>, cudaStream_t);
 

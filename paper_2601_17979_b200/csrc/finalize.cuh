@@ -51,7 +51,8 @@ BSVD_DEV bool sig_tie(R a, R b) {
 template <class T>
 __device__ void finalize_block(T* W, int ldw, int bm, int bn, T* Vw, int ldvw,
                                typename tr<T>::R* sig, int* perm, int* flag,
-                               const FinalOut<T>& o) {
+                               const FinalOut<T>& o, int vrows = -1) {
+    if (vrows < 0) vrows = bn;  // rows of Vw (the standalone finalize operator allows any)
     using R = typename tr<T>::R;
     using Wt = typename tr<T>::W;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -186,8 +187,8 @@ __device__ void finalize_block(T* W, int ldw, int bm, int bn, T* Vw, int ldvw,
     const int64_t ldVo = o.trans ? o.ldu : o.ldv;
     const bool writeV = o.trans ? true : o.want_v;
     if (writeV && Vo && Vw) {
-        for (int e = tid; e < bn * bn; e += nt) {
-            const int r = e % bn, c = e / bn;
+        for (int e = tid; e < vrows * bn; e += nt) {
+            const int r = e % vrows, c = e / vrows;
             Vo[r + (size_t)c * ldVo] = Vw[r + (size_t)perm[c] * ldvw];
         }
     }

@@ -55,6 +55,14 @@ int launch_applyq(int bm, int bn, int batch, const T* refl, const T* phase, cons
 int launch_qr_path(bsvd_info* info, int batch, int bits, cudaStream_t st);
 size_t qr_smem(int esize, int bm, int bn);
 bool qr_reg_ok(int esize, bool cplx, int bm, int bn);
+template <class T>
+int launch_finalize_ext(int m, int n, int vrows, int batch, const void* W, int64_t ldw, int64_t sW, const void* V,
+                        int64_t ldv, int64_t sV, void* U, int64_t ldu, int64_t sU, void* S, int64_t sS, void* Vo,
+                        int64_t ldvo, int64_t svo, size_t smem_limit, cudaStream_t st);
+template <class T>
+int launch_householder_qr(int m, int n, int batch, const void* A, int64_t lda, int64_t sA, void* Q, int64_t ldq,
+                          int64_t sQ, void* R, int64_t ldr, int64_t sR, void* work, size_t smem_limit, cudaStream_t st);
+size_t householder_qr_work_bytes(int esize, int m, int n, int batch);
 template <bool CX>
 int launch_qr_reg(SolveArgs<typename std::conditional<CX, cx<double>, double>::type> a,
                   typename std::conditional<CX, cx<double>, double>::type* R,

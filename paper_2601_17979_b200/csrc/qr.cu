@@ -298,10 +298,59 @@ int launch_qr_path(bsvd_info* info, int batch, int bits, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 
+// householder_qr(a) (src/core.py:118-168) as a batched operator: reflectors + R by launch_qr, then
+// Q = H_0 ... H_{n-1} [diag(p); 0] (the sign convention folded in), R copied to the caller's layout.
+namespace qr {
+template <class T>
+__global__ void k_eye_copy(int n, int batch, T* eye, const T* Rw, T* R, int64_t ldr, int64_t sR) {
+    const int prob = blockIdx.x;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int r = e % n, c = e / n;
+        eye[(size_t)prob * n * n + e] = fromRe<T>(r == c ? 1.0 : 0.0);
+        R[(size_t)prob * sR + r + (size_t)c * ldr] = Rw[(size_t)prob * n * n + e];
+    }
+}
+}  // namespace qr
+
+size_t householder_qr_work_bytes(int esize, int m, int n, int batch) {
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t B = (size_t)batch, es = (size_t)esize;
+    return al(B * m * n * es) + al(B * n * es) + 2 * al(B * n * n * es);
+}
+
+template <class T>
+int launch_householder_qr(int m, int n, int batch, const void* A, int64_t lda, int64_t sA, void* Q, int64_t ldq,
+                          int64_t sQ, void* R, int64_t ldr, int64_t sR, void* work, size_t smem_limit, cudaStream_t st) {
+    if (!qr_reg_ok(sizeof(T), tr<T>::cplx, m, n) && qr_smem(sizeof(T), m, n) > smem_limit) return BSVD_ERR_UNSUPPORTED;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t B = (size_t)batch, es = sizeof(T);
+    unsigned char* w = static_cast<unsigned char*>(work);
+    T* refl = reinterpret_cast<T*>(w);
+    T* ph = reinterpret_cast<T*>(w + al(B * m * n * es));
+    T* Rw = reinterpret_cast<T*>(w + al(B * m * n * es) + al(B * n * es));
+    T* eye = reinterpret_cast<T*>(w + al(B * m * n * es) + al(B * n * es) + al(B * n * n * es));
+    SolveArgs<T> a{};
+    a.A = static_cast<const T*>(A);
+    a.lda = lda;
+    a.strideA = sA;
+    a.m = m;
+    a.n = n;
+    a.bm = m;
+    a.bn = n;
+    a.batch = batch;
+    int rc = launch_qr<T>(a, Rw, refl, ph, st);
+    if (rc) return rc;
+    qr::k_eye_copy<T><<<batch, 128, 0, st>>>(n, batch, eye, Rw, static_cast<T*>(R), ldr, sR);
+    if (cudaPeekAtLastError() != cudaSuccess) return BSVD_ERR_CUDA;
+    return launch_applyq<T>(m, n, batch, refl, ph, eye, static_cast<T*>(Q), ldq, sQ, st);
+}
+
 #define BSVD_QR_INST(T)                                                                                   \
     template int launch_qr<T>(SolveArgs<T>, T*, T*, T*, cudaStream_t);                                    \
     template int launch_applyq<T>(int, int, int, const T*, const T*, const T*, T*, int64_t, int64_t,      \
-                                  cudaStream_t);
+                                  cudaStream_t);                                                          \
+    template int launch_householder_qr<T>(int, int, int, const void*, int64_t, int64_t, void*, int64_t,    \
+                                          int64_t, void*, int64_t, int64_t, void*, size_t, cudaStream_t);
 BSVD_QR_INST(float)
 BSVD_QR_INST(double)
 BSVD_QR_INST(cx<float>)

@@ -131,3 +131,78 @@ def fused_pair_update(bi: np.ndarray, bj: np.ndarray, j: np.ndarray, row_block: 
     wi = b_i.shape[1]
     bi[...] = out[:, :wi]
     bj[...] = out[:, wi:]
+
+
+def householder_qr(a) -> tuple[np.ndarray, np.ndarray]:
+    """Reduced non-pivoted Householder QR on the device (src/core.py:118-168): (q m x n, r n x n upper
+    triangular with a real non-negative diagonal), through bsvd_householder_qr_batched."""
+    from .core import fmatrix
+    from .solver import _torch, torch_dtype
+
+    torch = _torch()
+    a = fmatrix(a)
+    m, n = a.shape
+    if m < n:
+        raise ShapeError(f"householder_qr needs m >= n, got {m}x{n}")
+    dt = a.dtype
+    tdt = torch_dtype(dt)
+    L = _lib.load()
+    if n == 0:
+        return np.zeros((m, 0), dtype=dt, order="F"), np.zeros((0, 0), dtype=dt, order="F")
+    at = _dev(a)
+    qt = torch.empty((n, m), dtype=tdt, device="cuda")
+    rt = torch.empty((n, n), dtype=tdt, device="cuda")
+    wb = L.bsvd_householder_qr_workspace_bytes(DTYPE_CODE[dt], m, n, 1)
+    ws = torch.empty(max(int(wb), 1), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = L.bsvd_householder_qr_batched(DTYPE_CODE[dt], m, n, 1, at.data_ptr(), m, m * n, qt.data_ptr(), m, m * n,
+                                       rt.data_ptr(), n, n * n, ws.data_ptr(), int(wb), stream)
+    _lib.check(rc, "bsvd_householder_qr_batched")
+    return _back(qt, (m, n)), _back(rt, (n, n))
+
+
+def finalize_factors(w, v=None):
+    """(u, sigma, v_permuted) of a converged working copy on the device (src/svd.py:243-275) through
+    bsvd_finalize_batched; inputs are not modified."""
+    from .core import real_dtype
+    from .solver import _torch, torch_dtype
+
+    torch = _torch()
+    w = np.asarray(w)
+    dt = check_dtype(w.dtype)
+    if w.ndim != 2:
+        raise ShapeError("finalize expects a 2-d working copy")
+    m, n = w.shape
+    if n > m:
+        raise ShapeError(f"finalize expects m >= n, got {w.shape}")
+    vrows = 0
+    if v is not None:
+        v = np.asarray(v)
+        if v.ndim != 2 or v.shape[1] != n:
+            raise ShapeError("V must be 2-d with the same column count as workA")
+        if v.dtype != dt:
+            raise DomainError(f"V dtype {v.dtype} differs from workA dtype {dt}")
+        vrows = v.shape[0]
+    rdt = real_dtype(dt)
+    if n == 0:
+        return (np.zeros((m, 0), dtype=dt, order="F"), np.zeros(0, dtype=rdt),
+                None if v is None else np.zeros((vrows, 0), dtype=dt, order="F"))
+    tdt = torch_dtype(dt)
+    L = _lib.load()
+    wt = _dev(w)
+    vt = _dev(v) if v is not None and vrows else None
+    ut = torch.empty((n, m), dtype=tdt, device="cuda")
+    st_ = torch.empty((n,), dtype=torch_dtype(rdt), device="cuda")
+    vo = torch.empty((n, vrows), dtype=tdt, device="cuda") if vt is not None else None
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = L.bsvd_finalize_batched(DTYPE_CODE[dt], m, n, 1, wt.data_ptr(), m, m * n, vrows,
+                                 vt.data_ptr() if vt is not None else None, max(vrows, 1), vrows * n, ut.data_ptr(),
+                                 m, m * n, st_.data_ptr(), n, vo.data_ptr() if vo is not None else None,
+                                 max(vrows, 1), vrows * n, stream)
+    _lib.check(rc, "bsvd_finalize_batched")
+    u = _back(ut, (m, n))
+    s = st_.cpu().numpy().astype(rdt, copy=False)
+    vv = None
+    if v is not None:
+        vv = _back(vo, (vrows, n)) if vo is not None else np.zeros((0, n), dtype=dt, order="F")
+    return u, s, vv

@@ -138,3 +138,14 @@ def _check_2d(a) -> np.ndarray:
     if a.ndim != 2:
         raise ShapeError(f"expected a 2-d matrix, got ndim={a.ndim}")
     return a
+
+
+def finalize(work_a, v=None) -> SvdResult:
+    """Turn a converged working copy into (U, sigma, V) on the device (src/svd.py:278-303):
+    sigma_i = ||w_i|| (float64), U = W / sigma with orthogonal completion of columns below tiny/u,
+    stable descending order, V permuted identically."""
+    from .kernels import finalize_factors
+
+    u, sigma, vv = finalize_factors(work_a, v)
+    info = SolveInfo(converged=True, outer_sweeps=0, inner_rotations=0, masked_pair_skips=0, path="finalize")
+    return SvdResult(u=u, sigma=sigma, v=vv, info=info)
