@@ -57,8 +57,9 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         if (o->kernel != 0) return p;
     }
     if (r.blocked) {
-        if (o->kernel == 0 || o->kernel == KV_BLOCKED_REG) {
-            Plan p = plan_blocked_reg(dt, r.bm, r.bn, o->nb, r.need_v, contiguous && !r.trans, o->inner_sweeps);
+        if (o->kernel == 0 || o->kernel == KV_BLOCKED_REG || o->kernel == KV_BLOCKED_REG_U4) {
+            Plan p = plan_blocked_reg(dt, r.bm, r.bn, o->nb, r.need_v, contiguous && !r.trans, o->inner_sweeps,
+                                      o->kernel);
             if (p.kernel) return p;
             if (o->kernel != 0) return p;
         }
@@ -160,6 +161,7 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
             if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_BLOCKED_REG:
+        case KV_BLOCKED_REG_U4:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_blocked_reg(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG32C:

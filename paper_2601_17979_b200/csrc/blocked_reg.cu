@@ -85,7 +85,7 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 
 template <int SH>
 __device__ __forceinline__ void ring_shift(double (&x)[N]) {
-    if constexpr (md(SH) != 0) {
+    if constexpr (md(SH) != 0) {  // (a copy-based permutation: the cycle-following form spills here)
         double y[NIT];
 #pragma unroll
         for (int q = 0; q < NIT; ++q) y[q] = x[ring_slot(q)];
@@ -242,29 +242,38 @@ __device__ __forceinline__ void inner_iter(double (&x0)[N], double (&x1)[N], dou
     }
 }
 
-// one inner sweep (31 iterations, ring unrolled by 2); returns with columns in natural order
-template <int NWG>
+// one inner sweep (31 iterations, ring unrolled by U: registers move once per U iterations); returns
+// with the columns in natural order
+template <int U, int NWG>
 __device__ __forceinline__ void inner_sweep(double (&x0)[N], double (&x1)[N], double (&p)[N], const Ctx& c,
                                             IState& st) {
+    constexpr int NG = (NIT + U - 1) / U;
+    constexpr int R = NIT - (NG - 1) * U;  // iterations in the last group
     st.full = true;
 #pragma unroll 1
-    for (int gi = 0; gi < 16; ++gi) {
-        const int t0 = 2 * gi;
+    for (int gi = 0; gi < NG; ++gi) {
+        const int t0 = gi * U;
+        const bool last = gi == NG - 1;
         inner_iter<0, NWG>(x0, x1, p, c, t0, st);
-        if (gi == 15) {
-            ring_shift<1>(x0);
-            ring_shift<1>(x1);
-            ring_shift<1>(p);
-            break;
+        if constexpr (U >= 2) {
+            if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); ring_shift<1>(p); break; }
+            inner_iter<1 % U, NWG>(x0, x1, p, c, t0 + 1, st);
         }
-        inner_iter<1, NWG>(x0, x1, p, c, t0 + 1, st);
-        ring_shift<2>(x0);
-        ring_shift<2>(x1);
-        ring_shift<2>(p);
+        if constexpr (U >= 3) {
+            if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); ring_shift<2>(p); break; }
+            inner_iter<2 % U, NWG>(x0, x1, p, c, t0 + 2, st);
+        }
+        if constexpr (U >= 4) {
+            if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); ring_shift<3>(p); break; }
+            inner_iter<3 % U, NWG>(x0, x1, p, c, t0 + 3, st);
+        }
+        ring_shift<U>(x0);
+        ring_shift<U>(x1);
+        ring_shift<U>(p);
     }
 }
 
-template <int NWG>
+template <int NWG, int U = 2>
 __global__ void __launch_bounds__(256, 1) k_blocked_reg(SolveArgs<double> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int prob = blockIdx.x;
@@ -348,7 +357,7 @@ __global__ void __launch_bounds__(256, 1) k_blocked_reg(SolveArgs<double> a) {
 #pragma unroll 1
                 for (int isw = 0; isw < a.inner_budget; ++isw) {
                     st.my_rot = 0;
-                    inner_sweep<NWG>(x0, x1, p, c, st);
+                    inner_sweep<U, NWG>(x0, x1, p, c, st);
                     int r = st.my_rot;  // lanes 0..15 hold the counts of pairs 0..15
 #pragma unroll
                     for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
@@ -456,14 +465,14 @@ inline size_t smem_bytes(int n, int nwg) {
 
 }  // namespace breg
 
-Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, int inner_sweeps) {
+Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, int inner_sweeps, int variant) {
     Plan p{};
     (void)inner_sweeps;
     if (dtype != BSVD_D || nb != 16 || bn % 16 != 0 || bn < 32 || bn > 256 || !contiguous) return p;
     const int ell = bn / 16, hb = (ell + (ell & 1)) / 2;
     int nwg = bm <= 64 ? 1 : (bm <= 128 ? 2 : (bm <= 256 ? 4 : 0));
     if (!nwg || hb * nwg > 8) return p;
-    p.kernel = KV_BLOCKED_REG;
+    p.kernel = variant == KV_BLOCKED_REG_U4 ? KV_BLOCKED_REG_U4 : KV_BLOCKED_REG;
     p.threads = hb * nwg * 32;
     p.group = nwg;
     p.smem = breg::smem_bytes(bn, nwg);
@@ -474,9 +483,9 @@ Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contig
     return p;
 }
 
-template <int NWG>
+template <int NWG, int U = 2>
 static int launch_br(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
-    auto k = breg::k_blocked_reg<NWG>;
+    auto k = breg::k_blocked_reg<NWG, U>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<a.batch, p.threads, p.smem, st>>>(a);
@@ -487,10 +496,18 @@ int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
     a.kernel = p.kernel;
     a.work_stride = (int64_t)p.work_elems;
     int rc;
-    switch (p.group) {
-        case 1: rc = launch_br<1>(a, p, st); break;
-        case 2: rc = launch_br<2>(a, p, st); break;
-        default: rc = launch_br<4>(a, p, st); break;
+    if (p.kernel == KV_BLOCKED_REG_U4) {  // ring unrolled by 4 (half the register moves, twice the code)
+        switch (p.group) {
+            case 1: rc = launch_br<1, 4>(a, p, st); break;
+            case 2: rc = launch_br<2, 4>(a, p, st); break;
+            default: rc = launch_br<4, 4>(a, p, st); break;
+        }
+    } else {
+        switch (p.group) {
+            case 1: rc = launch_br<1>(a, p, st); break;
+            case 2: rc = launch_br<2>(a, p, st); break;
+            default: rc = launch_br<4>(a, p, st); break;
+        }
     }
     if (rc) return rc;
     return launch_finalize_gm<double>(a, st);

@@ -57,8 +57,9 @@ enum {
     KV_UNBLOCKED_REG32E = 26,   // 32x32 FP64 warp-specialised: W warp + V warp per problem pair, smem ring
     KV_UNBLOCKED_REG32E_LAST = 29,  // 27..29: tuning variants (pairs per CTA, V unroll)
     KV_HEEVJ = 31,              // batched Hermitian Jacobi eigensolver (bsvd_heevj_batched)
-    KV_BLOCKED_REG = 30,
-    KV_CREG32 = 32,             // complex FP64, n = 32, m <= 256: CTA per problem, rows in registers, V in smem        // blocked FP64: block pairs register-resident (kernel (2) on X), V P on DMMA
+    KV_BLOCKED_REG = 30,        // blocked FP64: block pairs register-resident (kernel (2) on X), V P on DMMA
+    KV_CREG32 = 32,             // complex FP64, n = 32, m <= 256: CTA per problem, rows in registers, V in smem
+    KV_BLOCKED_REG_U4 = 33,     // KV_BLOCKED_REG with the ring unrolled by 4
 };
 
 template <class T>

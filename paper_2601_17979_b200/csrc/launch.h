@@ -81,7 +81,7 @@ int launch_heevj(int dtype, int n, int batch, const void* G, int64_t ldg, int64_
 int launch_verify(int dtype, int m, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* U,
                   int64_t ldu, int64_t sU, const void* S, int64_t sS, const void* V, int64_t ldv, int64_t sV,
                   const double* Sref, int64_t sR, double* out, cudaStream_t st);
-Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, int inner_sweeps);
+Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, int inner_sweeps, int variant = 0);
 int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 Plan plan_unblocked_reg16b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
 int launch_unblocked_reg16b(SolveArgs<float> a, const Plan& p, cudaStream_t st);

@@ -413,3 +413,27 @@ def test_fp32_16x16_results_independent_of_warp_partner(kernel):
     torch.cuda.synchronize()
     p = torch.from_numpy(perm).cuda()
     assert torch.equal(r0.u[p], r1.u) and torch.equal(r0.s[p], r1.s) and torch.equal(r0.v[p], r1.v)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", [2, 8, 9, 10, 30, 33])
+@pytest.mark.parametrize("m,n", [(64, 64), (128, 128), (96, 48)])
+def test_blocked_fp64_kernel_variants(kernel, m, n):
+    """Every blocked FP64 kernel variant meets the parity contract against the blocked restatement."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    B = 5
+    A = np.stack([random_matrix(m, n, np.float64, seed=2100 + 3 * b + m) for b in range(B)])
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, m, n, bs.JacobiOptions(), route=2, kernel=kernel)
+    torch.cuda.synchronize()
+    info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (info["kernel"] == kernel).all() and info["converged"].all()
+    U, S, V = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy(), np.swapaxes(r.v.cpu().numpy(), 1, 2)
+    for b in range(B):
+        _, s_ref, _, oi = O.solve(A[b], Opts(), "blocked")
+        check_sigma_parity(S[b], s_ref, max(m, n), 2.0 ** -53)
+        check_factors(A[b], U[b], S[b], V[b])
+        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 2
