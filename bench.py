@@ -372,8 +372,8 @@ def run_b200(args, cfg):
     s_h = torch.empty(s_t.shape, dtype=s_t.dtype, pin_memory=True)
     v_h = torch.empty(v_t.shape, dtype=v_t.dtype, pin_memory=True) if v_t is not None else None
     i_h = torch.empty(info_t.shape, dtype=info_t.dtype, pin_memory=True)
-    e2e_streams = [stream, torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-    e2e_chunk = max(1, -(-B // 8))
+    e2e_streams = [stream] + [torch.cuda.Stream(dev) for _ in range(3)]
+    e2e_chunk = max(1, -(-B // 16))  # 4 streams x B/16: best of the sweep in tools/e2e_sweep.py
     e2e_ms = []
     for it in range(args.warmup + args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -435,7 +435,7 @@ def run_b200(args, cfg):
         "cpu_baseline": cpu_line,
         "e2e": {"value": B * steps_total / e2e_s, "unit": "matrices/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "path": "bsvd_gesvj_batched_host: pinned host buffers, H2D / solve / D2H "
-                f"pipelined in chunks of {e2e_chunk} over 3 streams"},
+                f"pipelined in chunks of {e2e_chunk} over 4 streams"},
         "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,
         "gpu_launches_per_step": launches_per_step,

@@ -167,9 +167,9 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
     o = make_opts(opts, route, kernel)
     dev = torch.device("cuda", torch.cuda.current_device())
     if streams is None:
-        streams = [torch.cuda.current_stream(dev)] + _side_streams(dev, 2)
+        streams = [torch.cuda.current_stream(dev)] + _side_streams(dev, 3)
     if chunk <= 0:
-        chunk = max(1, -(-B // (2 * len(streams))))
+        chunk = max(1, -(-B // (4 * len(streams))))  # measured best on B200 (tools/e2e_sweep.py)
     ws_bytes = L.bsvd_host_workspace_bytes(code, m, n, chunk, len(streams), ctypes.byref(o))
     ws = _workspace(ws_bytes, dev)
     arr = (ctypes.c_void_p * len(streams))(*[st.cuda_stream for st in streams])

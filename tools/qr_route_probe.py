@@ -1,3 +1,4 @@
+"""QR-route timing probe for C4 (qr vs plain), with a torch.profiler kernel table (development aid)."""
 import sys, os, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
