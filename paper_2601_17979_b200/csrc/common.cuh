@@ -195,6 +195,21 @@ BSVD_DEV double rsqrt_approx(double x) {
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     return r;
 }
+// 1/b by three Newton steps on the MUFU seed (b normal, 1/b normal); scale-invariant under exact
+// powers of two, so a prescaled kernel and the standalone finalisation get the same bits.
+BSVD_DEV double rcp_refined(double b) {
+    double r = rcp_approx(b);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r = fma(r, fma(-b, r, 1.0), r);
+    return r;
+}
+// x / s as U = W / sigma is formed everywhere in FP64 (finalize.cuh and the fused finalisations):
+// reciprocal, product, one residual correction (within 1 ulp of the IEEE quotient; identical bits
+// whichever kernel finalises a problem)
+BSVD_DEV double div_by_sigma(double x, double s, double rs) {
+    const double q = x * rs;
+    return fma(fma(-s, q, x), rs, q);
+}
 // a / b for b > 0 (b may be tiny or +inf); a finite.
 BSVD_DEV double fdiv(double a, double b) {
     const bool sm = b < 0x1p-960;

@@ -30,6 +30,8 @@ BSVD_DEV T scale_by_sigma(T x, typename tr<T>::R s) {
     if constexpr (tr<T>::cplx) {
         const typename tr<T>::R r = (typename tr<T>::R)1 / s;  // numpy complex / real
         return T{x.re * r, x.im * r};
+    } else if constexpr (sizeof(T) == 8) {
+        return div_by_sigma(x, s, rcp_refined(s));  // the fused finalisations' formula, bit for bit
     } else {
         return x / s;
     }

@@ -90,12 +90,6 @@ __device__ __forceinline__ void rot_abs(double dabs, double g, double& s, double
     if (fmax(dabs, g) < 0x1p-500) rot_abs_core(dabs * 0x1p+600, g * 0x1p+600, s, cm1, tabs);
 }
 
-__device__ __forceinline__ double rcp_refined(double b) {  // 1/b, b in [2^-960, 2^960]
-    double r = rcp_approx(b);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) r = fma(r, fma(-b, r, 1.0), r);
-    return r;
-}
 // 16 consecutive doubles summed in the order of a 16-8-4-2-1 xor butterfly (p_i = v_i + v_{i+16} given):
 // the column-norm order of finalize_block, so fused and standalone finalisation give the same sigma bits
 __device__ __forceinline__ double sum16_butterfly(const double* p) {

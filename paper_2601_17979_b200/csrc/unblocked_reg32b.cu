@@ -104,12 +104,6 @@ __device__ __forceinline__ double sum16(const double* p) {  // 16 consecutive do
 // 16 consecutive doubles summed in the order of a 16-8-4-2-1 xor butterfly over rows (i, i + 16) first:
 // the column-norm order of finalize_block (finalize.cuh step 1), so the fused and the standalone
 // finalisation give the same sigma bits.
-__device__ __forceinline__ double rcp_refined(double b) {  // 1/b, b in [2^-960, 2^960]
-    double r = rcp_approx(b);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) r = fma(r, fma(-b, r, 1.0), r);
-    return r;
-}
 
 __device__ __forceinline__ double sum16_butterfly(const double* p) {
     double t[8];
@@ -593,9 +587,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
             for (int c = 0; c < N; ++c) {  // U = W / sigma: reciprocal, then one residual correction
                 const int rc = rk[c];
                 const double2 t = sr[c];
-                const double q0 = x0[c] * t.y, q1 = x1[c] * t.y;
-                u0[(size_t)rc * o.ldu] = fma(fma(-t.x, q0, x0[c]), t.y, q0);
-                u1[(size_t)rc * o.ldu] = fma(fma(-t.x, q1, x1[c]), t.y, q1);
+                u0[(size_t)rc * o.ldu] = div_by_sigma(x0[c], t.x, t.y);
+                u1[(size_t)rc * o.ldu] = div_by_sigma(x1[c], t.x, t.y);
             }
             if (o.want_v && o.V) {
                 // all 64 loads ahead of the stores (the compiler cannot prove o.V and wsV disjoint,

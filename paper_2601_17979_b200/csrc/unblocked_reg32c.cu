@@ -296,8 +296,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32c(SolveArgs<double> a) {
             for (int c = 0; c < N; ++c) {  // U = W / sigma: reciprocal, then one residual correction
                 const int rc = rk[c];
                 const double2 t = sr[c];
-                const double q = x[c] * t.y;
-                u[(size_t)rc * o.ldu] = fma(fma(-t.x, q, x[c]), t.y, q);
+                u[(size_t)rc * o.ldu] = div_by_sigma(x[c], t.x, t.y);
             }
             if (o.want_v && o.V) {
                 if (v_started) {
