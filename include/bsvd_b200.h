@@ -135,6 +135,18 @@ size_t bsvd_host_workspace_bytes(int dtype, int m, int n, int chunk, int nstream
  * (quiet sweep included), rotations, converged.  work: DEVICE scratch of
  * bsvd_heevj_workspace_bytes(...) bytes (0 when G and M fit in shared memory).
  */
+/*
+ * eig_sweeps(g, d, m, pairs, starts, tol, max_sweeps, delta) (src/_kernels_numba.py:17-82), the
+ * reference's Backend operator, batch-granular and in place: G_b n x n (only the off-diagonal is read;
+ * rotated in place, pivots zeroed, diagonal untouched), D_b the n real pivots (in/out), M_b n x n
+ * accumulator (in/out; delta != 0: M accumulates P - I including the identity columns' terms, start
+ * it at zero).  Absolute guard tol (= k u).  info: sweeps run, rotations, converged.  Workspace as
+ * bsvd_heevj_workspace_bytes.  Disjoint pairs of an iteration are applied together (2 x 2 block
+ * updates), so results match the sequential reference to rounding.
+ */
+int bsvd_eig_sweeps_batched(int dtype, int n, int batch, void* G, int64_t ldg, int64_t strideG, void* D,
+                            int64_t strideD, void* M, int64_t ldm, int64_t strideM, double tol, int max_sweeps,
+                            int delta, bsvd_info* info, void* work, size_t work_bytes, void* stream);
 int bsvd_heevj_batched(int dtype, int n, int batch, const void* G, int64_t ldg, int64_t strideG,
                        void* D, int64_t strideD, void* M, int64_t ldm, int64_t strideM, int m_init,
                        double k, int max_sweeps, bsvd_info* info, void* work, size_t work_bytes, void* stream);

@@ -19,7 +19,7 @@ from .core import (
     unit_roundoff,
 )
 from .eig import EigInfo, Rotation, batch_hermitian_eig, compute_rotation, jacobi_hermitian_eig
-from .kernels import compute_gram, fused_pair_update, householder_qr, onesided_sweeps
+from .kernels import compute_gram, eig_sweeps, fused_pair_update, householder_qr, onesided_sweeps
 from .ordering import Schedule, round_robin_schedule, schedule_arrays
 from .solver import DeviceResult, solve_tensor
 from . import fileio
@@ -96,6 +96,7 @@ __all__ = [
     "verify_tensor",
     "finalize",
     "householder_qr",
+    "eig_sweeps",
     "residual_e1",
     "orthogonality_e2_e3",
     "sigma_error_e4",

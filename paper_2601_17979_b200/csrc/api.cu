@@ -228,6 +228,18 @@ int bsvd_heevj_batched(int dtype, int n, int batch, const void* G, int64_t ldg, 
                         work, work_bytes, smem_limit(), static_cast<cudaStream_t>(stream));
 }
 
+int bsvd_eig_sweeps_batched(int dtype, int n, int batch, void* G, int64_t ldg, int64_t strideG, void* D,
+                            int64_t strideD, void* M, int64_t ldm, int64_t strideM, double tol, int max_sweeps,
+                            int delta, bsvd_info* info, void* work, size_t work_bytes, void* stream) {
+    if (dtype < 0 || dtype > 3 || n < 0 || batch < 0 || !(tol >= 0) || max_sweeps < 1) return BSVD_ERR_ARG;
+    if (batch == 0 || n == 0) return BSVD_OK;
+    if (!G || !D || !M || ldg < n || ldm < n) return BSVD_ERR_ARG;
+    // caller's M (delta: the P - I accumulator), caller's d, g written back, absolute tolerance
+    const int mode = 1 | (delta ? 2 : 0) | 4 | 8 | 16;
+    return launch_heevj(dtype, n, batch, G, ldg, strideG, D, strideD, M, ldm, strideM, mode, tol, max_sweeps, info,
+                        work, work_bytes, smem_limit(), static_cast<cudaStream_t>(stream));
+}
+
 int bsvd_verify_batched(int dtype, int m, int n, int batch, const void* A, int64_t lda, int64_t strideA,
                         const void* U, int64_t ldu, int64_t strideU, const void* S, int64_t strideS, const void* V,
                         int64_t ldv, int64_t strideV, const double* Sref, int64_t strideSref, double* out,

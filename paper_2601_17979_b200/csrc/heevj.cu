@@ -26,6 +26,16 @@ BSVD_DEV double realpart(T x) {
     else return (double)x;
 }
 
+BSVD_DEV double addW(double a, double b) { return a + b; }
+BSVD_DEV cx<double> addW(cx<double> a, cx<double> b) { return {a.re + b.re, a.im + b.im}; }
+BSVD_DEV double subW(double a, double b) { return a - b; }
+BSVD_DEV cx<double> subW(cx<double> a, cx<double> b) { return {a.re - b.re, a.im - b.im}; }
+template <class W>
+BSVD_DEV W fromD(double x) {
+    if constexpr (sizeof(W) == sizeof(double)) return x;
+    else return W{x, 0.0};
+}
+
 template <class T>
 struct Rot {
     typename tr<T>::W ws, wsc;
@@ -35,9 +45,12 @@ struct Rot {
 };
 
 template <class T>
-__global__ void __launch_bounds__(256) k_heevj(int n, const T* G, int64_t ldg, int64_t sG,
+// mode bits: 1 M starts from the caller's M (else I), 2 delta form (M accumulates P - I: the implicit
+// identity columns' contribution, src/_kernels_numba.py:75-80), 4 d from the caller's D (else real diag G),
+// 8 write G's rotated off-diagonal back (eig_sweeps mutates g in place)
+__global__ void __launch_bounds__(256) k_heevj(int n, T* G, int64_t ldg, int64_t sG,
                                                typename tr<T>::R* D, int64_t sD, T* M, int64_t ldm, int64_t sM,
-                                               int m_init, double tol, int max_sweeps, bsvd_info* info, T* work,
+                                               int mode, double tol, int max_sweeps, bsvd_info* info, T* work,
                                                int in_smem) {
     using R = typename tr<T>::R;
     using Wt = typename tr<T>::W;
@@ -62,16 +75,18 @@ __global__ void __launch_bounds__(256) k_heevj(int n, const T* G, int64_t ldg, i
     Rot<T>* prm = reinterpret_cast<Rot<T>*>(smem + off);
     off += (size_t)hw * sizeof(Rot<T>);
     int* cnt = reinterpret_cast<int*>(smem + ((off + 15) & ~size_t(15)));
-    const T* Gp = G + (size_t)prob * sG;
+    T* Gp = G + (size_t)prob * sG;
     T* Mp = M + (size_t)prob * sM;
+    const R* Dp_in = D + (size_t)prob * sD;
+    const bool delta = (mode & 2) != 0;
     for (int e = tid; e < n * n; e += nt) {
         const int r = e % n, c = e / n;
         T x = zero<T>();
         if (r < c) x = Gp[r + (size_t)c * ldg];
         else if (r > c) x = conjT(Gp[c + (size_t)r * ldg]);
-        else d[r] = (R)realpart(Gp[r + (size_t)r * ldg]);
+        else d[r] = (mode & 4) ? Dp_in[r] : (R)realpart(Gp[r + (size_t)r * ldg]);
         Gw[e] = x;
-        Mw[e] = m_init ? Mp[r + (size_t)c * ldm] : ((r == c) ? one<T>() : zero<T>());
+        Mw[e] = (mode & 1) ? Mp[r + (size_t)c * ldm] : ((r == c) ? one<T>() : zero<T>());
     }
     if (tid < 2) cnt[tid] = 0;
     __syncthreads();
@@ -148,6 +163,15 @@ __global__ void __launch_bounds__(256) k_heevj(int n, const T* G, int64_t ldg, i
                 if (!P.rot) continue;
                 Wt xi = wide(Mw[r + (size_t)P.i * n]), xj = wide(Mw[r + (size_t)P.j * n]);
                 rot_pair(xi, xj, P.cm1, P.ws, P.wsc);
+                if (delta) {  // + J - I: m_ii += cm1, m_ji += wsc, m_ij -= ws, m_jj += cm1
+                    if (r == P.i) {
+                        xi = addW(xi, fromD<Wt>(P.cm1));
+                        xj = subW(xj, P.ws);
+                    } else if (r == P.j) {
+                        xi = addW(xi, P.wsc);
+                        xj = addW(xj, fromD<Wt>(P.cm1));
+                    }
+                }
                 store(&Mw[r + (size_t)P.i * n], xi);
                 store(&Mw[r + (size_t)P.j * n], xj);
             }
@@ -162,6 +186,9 @@ __global__ void __launch_bounds__(256) k_heevj(int n, const T* G, int64_t ldg, i
     R* Dp = D + (size_t)prob * sD;
     for (int r = tid; r < n; r += nt) Dp[r] = d[r];
     for (int e = tid; e < n * n; e += nt) Mp[(e % n) + (size_t)(e / n) * ldm] = Mw[e];
+    if (mode & 8)  // rotated off-diagonal back into g (its diagonal is never touched by eig_sweeps)
+        for (int e = tid; e < n * n; e += nt)
+            if ((e % n) != (e / n)) Gp[(e % n) + (size_t)(e / n) * ldg] = Gw[e];
     if (tid == 0 && info) {
         bsvd_info inf;
         inf.converged = converged ? 1 : 0;
@@ -189,7 +216,7 @@ size_t smem_bytes(int n, bool in_smem) {
 
 template <class T>
 int launch(int n, int batch, const void* G, int64_t ldg, int64_t sG, void* D, int64_t sD, void* M, int64_t ldm,
-           int64_t sM, int m_init, double k, int max_sweeps, bsvd_info* info, void* work, size_t work_bytes,
+           int64_t sM, int mode, double k, int max_sweeps, bsvd_info* info, void* work, size_t work_bytes,
            size_t smem_limit, cudaStream_t st) {
     const bool in_smem = smem_bytes<T>(n, true) <= smem_limit;
     const size_t need = in_smem ? 0 : 2 * (size_t)n * n * sizeof(T) * (size_t)batch;
@@ -199,9 +226,11 @@ int launch(int n, int batch, const void* G, int64_t ldg, int64_t sG, void* D, in
     if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
                                 cudaSuccess)
         return BSVD_ERR_CUDA;
-    kern<<<batch, 256, smem, st>>>(n, static_cast<const T*>(G), ldg, sG, static_cast<typename tr<T>::R*>(D), sD,
-                                   static_cast<T*>(M), ldm, sM, m_init, k * tr<T>::u, max_sweeps, info,
-                                   static_cast<T*>(work), in_smem ? 1 : 0);
+    // mode bit 16: k is already the absolute tolerance (eig_sweeps(tol)), else k * u
+    const double tol = (mode & 16) ? k : k * tr<T>::u;
+    kern<<<batch, 256, smem, st>>>(n, const_cast<T*>(static_cast<const T*>(G)), ldg, sG,
+                                   static_cast<typename tr<T>::R*>(D), sD, static_cast<T*>(M), ldm, sM, mode & 15,
+                                   tol, max_sweeps, info, static_cast<T*>(work), in_smem ? 1 : 0);
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 

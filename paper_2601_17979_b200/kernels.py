@@ -206,3 +206,43 @@ def finalize_factors(w, v=None):
     if v is not None:
         vv = _back(vo, (vrows, n)) if vo is not None else np.zeros((0, n), dtype=dt, order="F")
     return u, s, vv
+
+
+def eig_sweeps(g, d, m, pairs=None, starts=None, tol=None, max_sweeps=1, delta=False):
+    """In place on g (n x n Hermitian; off-diagonal rotated, pivots zeroed), d (n real pivots) and m
+    (n x n accumulator; delta: P - I, start it at zero); returns (sweeps, rotations, converged).
+
+    Mirrors src/_kernels_numba.py:17-82 through bsvd_eig_sweeps_batched.  ``pairs``/``starts`` are
+    accepted for signature parity; the device evaluates the same round-robin schedule in closed form.
+    """
+    from .solver import INFO_DTYPE, _torch, torch_dtype
+
+    torch = _torch()
+    g = np.asarray(g)
+    dt = check_dtype(g.dtype)
+    n = g.shape[0]
+    if g.ndim != 2 or g.shape[1] != n:
+        raise ShapeError(f"expected a square matrix, got shape {g.shape}")
+    if m.shape != (n, n):
+        raise ShapeError(f"m must be {n} x {n}, got {m.shape}")
+    if d.shape != (n,):
+        raise ShapeError(f"d must have length {n}, got {d.shape}")
+    L = _lib.load()
+    gt = _dev(g)
+    mt = _dev(np.asarray(m, dtype=dt))
+    dtt = torch.from_numpy(np.ascontiguousarray(d)).cuda()
+    info = torch.zeros((_lib.INFO_BYTES,), dtype=torch.uint8, device="cuda")
+    wb = int(L.bsvd_heevj_workspace_bytes(DTYPE_CODE[dt], n, 1))
+    ws = torch.empty(max(wb, 1), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = L.bsvd_eig_sweeps_batched(DTYPE_CODE[dt], n, 1, gt.data_ptr(), max(n, 1), n * n, dtt.data_ptr(), n,
+                                   mt.data_ptr(), max(n, 1), n * n, float(tol), int(max_sweeps), 1 if delta else 0,
+                                   info.data_ptr(), ws.data_ptr() if wb else None, wb, stream)
+    _lib.check(rc, "bsvd_eig_sweeps_batched")
+    g[...] = _back(gt, g.shape)
+    m[...] = _back(mt, m.shape)
+    d[...] = dtt.cpu().numpy()
+    if n == 0:
+        return 1, 0, True
+    inf = np.frombuffer(info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)[0]
+    return int(inf["outer_sweeps"]), int(inf["rotations"]), bool(inf["converged"])

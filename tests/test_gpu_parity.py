@@ -437,3 +437,44 @@ def test_blocked_fp64_kernel_variants(kernel, m, n):
         check_factors(A[b], U[b], S[b], V[b])
         assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 2
 
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt", ALL_DTYPES)
+def test_eig_sweeps_operator_matches_golden(golden, dt):
+    """eig_sweeps (src/_kernels_numba.py:17-82), the Backend operator, in delta mode on the reference's
+    own kernel-level golden case: same rotation count, g / d / m = P - I to rounding (disjoint pairs
+    are applied together on the device)."""
+    nm = np.dtype(dt).name
+    kid = f"k_eig_{nm}"
+    g = np.asfortranarray(golden.get(kid, "g0").copy())
+    d = golden.get(kid, "d0").copy()
+    mm = np.zeros(g.shape, dtype=g.dtype, order="F")
+    sw, rot, cv = bs.eig_sweeps(g, d, mm, tol=golden.kernels[kid]["tol"], max_sweeps=1, delta=True)
+    assert rot == golden.kernels[kid]["rotations"] and sw == 1
+    u = unit_roundoff(dt)
+    scale = float(np.max(np.abs(golden.get(kid, "g0"))))
+    n = g.shape[0]
+    # one sweep = 66 rotations whose angles see the other order's roundings: M = P - I to ~n u per rotation
+    assert np.max(np.abs(g - golden.get(kid, "g1"))) <= 16 * n * u * scale
+    assert np.max(np.abs(d - golden.get(kid, "d1"))) <= 16 * n * u * scale
+    assert np.max(np.abs(mm - golden.get(kid, "m1"))) <= 30 * n * u
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt", ALL_DTYPES)
+def test_eig_sweeps_operator_full_solve(dt):
+    """Non-delta eig_sweeps to convergence from M = I: the Backend-level path of jacobi_hermitian_eig."""
+    n = 12
+    a = random_matrix(n, n, dt, seed=44)
+    h = np.asfortranarray(a + a.conj().T)
+    g = h.copy(order="F")
+    d = np.real(np.diag(g)).astype(bs.real_dtype(dt)).copy()
+    w = np.asfortranarray(np.triu(g, 1) + np.triu(g, 1).conj().T)
+    m = np.asfortranarray(np.eye(n, dtype=dt))
+    u = unit_roundoff(dt)
+    sw, rot, cv = bs.eig_sweeps(w, d, m, tol=30 * u, max_sweeps=30, delta=False)
+    assert cv and rot > 0 and sw >= 2
+    rec = (m * d) @ m.conj().T
+    assert np.max(np.abs(rec - h)) <= 60 * n * u * np.max(np.abs(h))
+    assert np.max(np.abs(m.conj().T @ m - np.eye(n))) <= 60 * n * u
