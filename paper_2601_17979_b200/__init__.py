@@ -7,6 +7,8 @@ behind the C-ABI in include/bsvd_b200.h (paper_2601_17979_b200/_lib/
 libbsvd_b200.so); there is no CPU fallback.
 """
 
+from . import backend
+from .backend import Backend, active, select, use
 from .batch import BatchState, batch_svd, convergence_scan
 from .core import (
     SUPPORTED_DTYPES,
@@ -97,6 +99,11 @@ __all__ = [
     "finalize",
     "householder_qr",
     "eig_sweeps",
+    "Backend",
+    "active",
+    "select",
+    "use",
+    "backend",
     "residual_e1",
     "orthogonality_e2_e3",
     "sigma_error_e4",

@@ -160,3 +160,16 @@ def test_no_cpu_fallback():
     assert isinstance(st.errors[0], RuntimeError)
     with pytest.raises(RuntimeError):
         bs.svd_dispatch(a)
+
+
+def test_backend_interface_single_b200_backend():
+    """src/backend.py:30-35 interface: one B200 backend, CPU backends rejected (no fallback)."""
+    b = bs.active()
+    assert b.name == "b200" and b is bs.select("auto") and b is bs.select("b200")
+    assert b.onesided_sweeps is bs.onesided_sweeps and b.eig_sweeps is bs.eig_sweeps
+    assert b.fused_pair_update is bs.fused_pair_update
+    for bad in ("numba", "numpy", "cuda"):
+        with pytest.raises(ValueError):
+            bs.select(bad)
+    with bs.use("b200") as bb:
+        assert bb is b
