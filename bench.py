@@ -366,6 +366,8 @@ def run_b200(args, cfg):
     # every step moves the inputs H2D and all factors D2H, pipelined in chunks over three streams
     from paper_2601_17979_b200.solver import solve_host_buffers
 
+    h2d_per = m * n * es
+    d2h_per = m * k * es + k * rs + (n * k * es if v_t is not None else 0)
     a_host = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
     a_host.copy_(a)
     u_h = torch.empty(u_t.shape, dtype=u_t.dtype, pin_memory=True)
@@ -373,7 +375,9 @@ def run_b200(args, cfg):
     v_h = torch.empty(v_t.shape, dtype=v_t.dtype, pin_memory=True) if v_t is not None else None
     i_h = torch.empty(info_t.shape, dtype=info_t.dtype, pin_memory=True)
     e2e_streams = [stream] + [torch.cuda.Stream(dev) for _ in range(3)]
-    e2e_chunk = max(1, -(-B // 16))  # 4 streams x B/16: best of the sweep in tools/e2e_sweep.py
+    from paper_2601_17979_b200.solver import default_chunk
+
+    e2e_chunk = default_chunk(B, h2d_per + d2h_per)  # ~4 MB per chunk, 4..16 chunks over 4 streams
     e2e_ms = []
     for it in range(args.warmup + args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -156,7 +156,7 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
     (B * INFO_BYTES,) are CPU tensors (pinned for full PCIe bandwidth).  The
     batch is cut into ``chunk``-problem pieces whose H2D, solve and D2H
     overlap across ``streams`` (torch streams; default: the current stream
-    plus two side streams).  Asynchronous on streams[0]: synchronise it
+    plus three side streams; chunk default: ``default_chunk``).  Asynchronous on streams[0]: synchronise it
     before reading the outputs.
     """
     torch = _torch()
@@ -169,7 +169,10 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
     if streams is None:
         streams = [torch.cuda.current_stream(dev)] + _side_streams(dev, 3)
     if chunk <= 0:
-        chunk = max(1, -(-B // (4 * len(streams))))  # measured best on B200 (tools/e2e_sweep.py)
+        k = min(m, n)
+        es = np.dtype(dt).itemsize
+        per = m * n * es + m * k * es + (n * k * es if opts.compute_right_vectors else 0)  # bytes in + out
+        chunk = default_chunk(B, per)
     ws_bytes = L.bsvd_host_workspace_bytes(code, m, n, chunk, len(streams), ctypes.byref(o))
     ws = _workspace(ws_bytes, dev)
     arr = (ctypes.c_void_p * len(streams))(*[st.cuda_stream for st in streams])
@@ -180,6 +183,14 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
         ws.data_ptr() if ws is not None else None, ws_bytes, arr, len(streams))
     _lib.check(rc, f"bsvd_gesvj_batched_host({dt.name}, {m}x{n}, batch={B})")
     return int(L.bsvd_select_kernel(code, m, n, ctypes.byref(o)))
+
+
+def default_chunk(batch: int, bytes_per_problem: int) -> int:
+    """Host-pipeline chunk: about 4 MB of copies per chunk, between 4 and 16 chunks (measured on B200,
+    tools/e2e_sweep.py: C1-10k best at B/16, C2 at ~B/8, C4 at B/16)."""
+    lo, hi = -(-batch // 16), -(-batch // 4)
+    want = -(-(4 << 20) // max(1, bytes_per_problem))
+    return max(1, min(max(want, lo), hi))
 
 
 _SIDE: dict = {}
