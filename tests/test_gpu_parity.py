@@ -478,3 +478,61 @@ def test_eig_sweeps_operator_full_solve(dt):
     rec = (m * d) @ m.conj().T
     assert np.max(np.abs(rec - h)) <= 60 * n * u * np.max(np.abs(h))
     assert np.max(np.abs(m.conj().T @ m - np.eye(n))) <= 60 * n * u
+
+
+_DEFAULT_KERNEL_SHAPES = [(np.float64, 32, 32, 12), (np.float32, 16, 16, 24), (np.float64, 64, 64, 30),
+                          (np.complex128, 256, 32, 32), (np.complex128, 40, 24, 1), (np.float32, 48, 48, 2)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt,m,n,kid", _DEFAULT_KERNEL_SHAPES)
+def test_every_default_kernel_isolates_nonfinite_problems(dt, m, n, kid):
+    """A NaN / Inf input is flagged per problem (info status) without touching the problems sharing its
+    warp or CTA; the batch API returns it like the reference does (NaN factors, no exception)."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    B = 5
+    A = np.stack([random_matrix(m, n, dt, seed=3100 + b) for b in range(B)])
+    A[1][2, 3] = np.nan
+    A[3][0, 0] = np.inf
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, m, n, bs.JacobiOptions())
+    torch.cuda.synchronize()
+    info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (info["kernel"] == kid).all()
+    assert info["status"][1] != 0 and info["status"][3] != 0
+    good = [0, 2, 4]
+    assert (info["status"][good] == 0).all() and info["converged"][good].all()
+    S = r.s.cpu().numpy()
+    for b in good:
+        _, s_ref, _, _ = O.solve(A[b], None, None)
+        check_sigma_parity(S[b], s_ref, max(m, n), unit_roundoff(dt))
+    # like the reference (no finiteness check on the path), the poisoned problems still return a result
+    # record -- NaN-valued -- and never disturb the others
+    res = bs.batch_svd(list(A), bs.JacobiOptions())
+    assert not np.isfinite(res[1].sigma).all() and not np.isfinite(res[3].sigma).all()
+    for b in good:
+        assert res[b].info.converged and np.array_equal(res[b].sigma, S[b].astype(res[b].sigma.dtype))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt,m,n,kid", _DEFAULT_KERNEL_SHAPES)
+def test_every_default_kernel_reports_sweep_cap(dt, m, n, kid):
+    """max_nsweeps = 1 on random matrices: not converged, exactly one sweep, still a valid (unsorted-
+    accuracy) factor output with descending sigma (non-convergence is reported, not raised)."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    B = 3
+    A = np.stack([random_matrix(m, n, dt, seed=3200 + b) for b in range(B)])
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, m, n, bs.JacobiOptions(max_nsweeps=1))
+    torch.cuda.synchronize()
+    info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (info["kernel"] == kid).all()
+    assert (info["converged"] == 0).all() and (info["outer_sweeps"] == 1).all() and (info["rotations"] > 0).all()
+    S = r.s.cpu().numpy().astype(np.float64)
+    assert np.all(np.diff(S, axis=1) <= 0) and np.all(np.isfinite(S))
