@@ -64,6 +64,17 @@ int launch_householder_qr(int m, int n, int batch, const void* A, int64_t lda, i
                           int64_t sQ, void* R, int64_t ldr, int64_t sR, void* work, size_t smem_limit, cudaStream_t st);
 size_t householder_qr_work_bytes(int esize, int m, int n, int batch);
 template <bool CX>
+int launch_qr_col(SolveArgs<typename std::conditional<CX, cx<double>, double>::type> a,
+                  typename std::conditional<CX, cx<double>, double>::type* R,
+                  typename std::conditional<CX, cx<double>, double>::type* refl,
+                  typename std::conditional<CX, cx<double>, double>::type* phase, cudaStream_t st);
+template <bool CX>
+int launch_applyq_col(int bm, int bn, int batch, const typename std::conditional<CX, cx<double>, double>::type* refl,
+                      const typename std::conditional<CX, cx<double>, double>::type* phase,
+                      const typename std::conditional<CX, cx<double>, double>::type* UR,
+                      typename std::conditional<CX, cx<double>, double>::type* Out, int64_t ldo, int64_t so,
+                      cudaStream_t st);
+template <bool CX>
 int launch_qr_reg(SolveArgs<typename std::conditional<CX, cx<double>, double>::type> a,
                   typename std::conditional<CX, cx<double>, double>::type* R,
                   typename std::conditional<CX, cx<double>, double>::type* refl,

@@ -265,7 +265,7 @@ size_t qr_smem(int esize, int bm, int bn) {
 template <class T>
 int launch_qr(SolveArgs<T> a, T* R, T* refl, T* phase, cudaStream_t st) {
     if constexpr (std::is_same<T, double>::value || std::is_same<T, cx<double>>::value) {
-        if (qr_reg_ok(sizeof(T), tr<T>::cplx, a.bm, a.bn)) return launch_qr_reg<tr<T>::cplx>(a, R, refl, phase, st);
+        if (qr_reg_ok(sizeof(T), tr<T>::cplx, a.bm, a.bn)) return launch_qr_col<tr<T>::cplx>(a, R, refl, phase, st);
     }
     const size_t smem = qr_smem(sizeof(T), a.bm, a.bn);
     if (smem > 232448) return BSVD_ERR_UNSUPPORTED;
@@ -281,7 +281,7 @@ int launch_applyq(int bm, int bn, int batch, const T* refl, const T* phase, cons
                   int64_t so, cudaStream_t st) {
     if constexpr (std::is_same<T, double>::value || std::is_same<T, cx<double>>::value) {
         if (qr_reg_ok(sizeof(T), tr<T>::cplx, bm, bn))
-            return launch_applyq_reg<tr<T>::cplx>(bm, bn, batch, refl, phase, UR, Out, ldo, so, st);
+            return launch_applyq_col<tr<T>::cplx>(bm, bn, batch, refl, phase, UR, Out, ldo, so, st);
     }
     if (bn > 256) return BSVD_ERR_UNSUPPORTED;
     const int nt = 256;  // 256 / bn row segments per column; the remaining threads only stage data
