@@ -225,6 +225,12 @@ int bsvd_householder_qr_batched(int dtype, int m, int n, int batch, const void* 
                                 int64_t stride_r, void* work, size_t work_bytes, void* stream);
 
 /*
+ * Host helper for the list API: dst[i * bytes .. ] = src[i][0 .. bytes) for i < count, over
+ * nthreads host threads (packs a list of column-major matrices into the pinned batch layout).
+ */
+int bsvd_pack_host(const void* const* src, int count, size_t bytes, void* dst, int nthreads);
+
+/*
  * Diagnostics: FMA-pipe peak microbenchmark used as the roofline denominator
  * (dtype BSVD_D or BSVD_S).  Launches blocks x 256 threads, each running
  * iters x 128 dependent-free FMAs; out: device scratch of `blocks` elements.

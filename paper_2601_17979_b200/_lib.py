@@ -68,6 +68,7 @@ EXPORTS = (
     "bsvd_heevj_workspace_bytes",
     "bsvd_verify_batched",
     "bsvd_finalize_batched",
+    "bsvd_pack_host",
     "bsvd_eig_sweeps_batched",
     "bsvd_householder_qr_workspace_bytes",
     "bsvd_householder_qr_batched",
@@ -124,6 +125,8 @@ def load():
     L.bsvd_eig_sweeps_batched.argtypes = [ci, ci, ci, vp, i64, i64, vp, i64, vp, i64, i64, ctypes.c_double, ci, ci,
                                           vp, vp, ctypes.c_size_t, vp]
     L.bsvd_eig_sweeps_batched.restype = ci
+    L.bsvd_pack_host.argtypes = [vp, ci, ctypes.c_size_t, vp, ci]
+    L.bsvd_pack_host.restype = ci
     L.bsvd_finalize_batched.argtypes = [ci, ci, ci, ci, vp, i64, i64, ci, vp, i64, i64, vp, i64, i64, vp, i64, vp,
                                         i64, i64, vp]
     L.bsvd_finalize_batched.restype = ci

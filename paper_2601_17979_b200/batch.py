@@ -17,6 +17,7 @@ the batch never aborts (:105-111).
 
 from __future__ import annotations
 
+import gc
 import time
 from dataclasses import dataclass, field
 from math import ceil
@@ -125,102 +126,119 @@ def _prepare(a, opts: JacobiOptions, force: str | None) -> _Prep:
     return _Prep(a=a, m=m, n=n, bn=bn, trans=trans, blocked=blocked, trivial=trivial, pairs_per_sweep=pps, qr=qr)
 
 
+def _clone_exc(exc: Exception) -> Exception:
+    try:
+        return type(exc)(*exc.args)
+    except Exception:  # pragma: no cover - exotic exception signatures
+        return exc
+
+
 def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rounds: bool):
-    """Solve a list of problems on the device; returns (results, errors, telemetry)."""
+    """Solve a list of problems on the device; returns (results, errors, telemetry).
+
+    Validation depends only on (dtype, shape), so it runs once per distinct pair; each uniform group is
+    one device launch; the per-problem records are built from column lists of the device telemetry.
+    """
     from .solver import solve_host
 
     n_prob = len(problems)
-    preps: list[_Prep | None] = [None] * n_prob
     errors: dict = {}
-    for idx, a in enumerate(problems):
-        try:
-            preps[idx] = _prepare(a, opts, force)
-        except Exception as exc:  # per-problem isolation (src/batch.py:105-111)
-            errors[idx] = exc
-
-    # group by (dtype, m, n): one launch per group
+    preps: list = [None] * n_prob
+    arrays: list = [None] * n_prob
+    proto: dict = {}
     groups: dict = {}
-    for idx, p in enumerate(preps):
-        if p is None or p.trivial:
+    trivial: list = []
+    for idx, a in enumerate(problems):
+        if type(a) is not np.ndarray:
+            try:
+                a = np.asarray(a)
+            except Exception as exc:  # per-problem isolation (src/batch.py:105-111)
+                errors[idx] = exc
+                continue
+        key = (a.dtype.str, a.shape)
+        t = proto.get(key)
+        if t is None:
+            try:
+                t = _prepare(a, opts, force)
+            except Exception as exc:
+                t = exc
+            proto[key] = t
+        if isinstance(t, Exception):
+            errors[idx] = _clone_exc(t)
             continue
-        groups.setdefault((p.a.dtype.str, p.m, p.n), []).append(idx)
+        arrays[idx] = a
+        preps[idx] = t
+        if t.trivial:
+            trivial.append(idx)
+        else:
+            groups.setdefault(key, []).append(idx)
 
-    raw: dict = {}
+    solved: list = []  # (idxs, prep, U, S, V, columns, dt, kern)
     for key, idxs in groups.items():
         t0 = time.perf_counter()
-        mats = [preps[i].a for i in idxs]
         try:
-            U, S, V, info, kern = solve_host(mats, opts, route=_ROUTE[force])
+            U, S, V, info, kern = solve_host([arrays[i] for i in idxs], opts, route=_ROUTE[force])
         except Exception as exc:
             for i in idxs:
                 errors[i] = exc
             continue
         dt = (time.perf_counter() - t0) / len(idxs)
-        for j, i in enumerate(idxs):
-            raw[i] = (U[j], S[j], V[j] if V is not None else None, info[j], dt, kern)
+        cols = {f: info[f].tolist() for f in ("outer_sweeps", "converged", "rotations", "update_calls", "path",
+                                             "last_rotations")}
+        solved.append((idxs, preps[idxs[0]], U, S, V, cols, dt, kern))
 
     # rounds the reference's lockstep loop would run (src/batch.py:113-142)
-    sweeps_of = {}
-    unconverged = False
-    for idx, p in enumerate(preps):
-        if p is None or idx in errors:
-            continue
-        if p.trivial:
-            sweeps_of[idx] = (0, True)
-        else:
-            inf = raw[idx][3]
-            sweeps_of[idx] = (int(inf["outer_sweeps"]), bool(inf["converged"]))
-            unconverged |= not bool(inf["converged"])
-    if sweeps_of:
-        rounds = opts.max_nsweeps if unconverged else max(max(s, 1) for s, _ in sweeps_of.values())
-    else:
-        rounds = 0
+    unconverged = any(not all(c["converged"]) for *_, c, _dt, _k in solved)
+    mx = max([max(max(c["outer_sweeps"]), 1) for *_, c, _dt, _k in solved] + ([1] if trivial else []), default=0)
+    rounds = opts.max_nsweeps if unconverged else mx
 
     results: list = [None] * n_prob
     tele: dict = {}
-    for idx, p in enumerate(preps):
-        if p is None or idx in errors:
-            continue
+    want_v = opts.compute_right_vectors
+    for idx in trivial:
+        p = preps[idx]
         m, n = p.m, p.n
         k = min(m, n)
-        dt = p.a.dtype
-        cnt = WorkCounters()
-        if p.trivial:
-            u = np.zeros((m, k), dtype=dt, order="F")
-            sigma = np.zeros(k, dtype=real_dtype(dt))
-            v = np.zeros((n, k), dtype=dt, order="F") if opts.compute_right_vectors else None
-            info = SolveInfo(converged=True, outer_sweeps=0, inner_rotations=0, masked_pair_skips=0,
-                             path="empty", counters=cnt)
-            results[idx] = SvdResult(u=u, sigma=sigma, v=v, info=info)
-            tele[idx] = dict(outer_sweeps=0, converged=True, last=0, pair_stats=[])
-            continue
-        U, S, V, inf, dtime, kern = raw[idx]
-        s_i = int(inf["outer_sweeps"])
-        conv = bool(inf["converged"])
-        pps = p.pairs_per_sweep
-        calls = s_i if masked_rounds is False or opts.masking else rounds
-        if p.blocked:
-            cnt.gram_calls = calls * pps
-            cnt.eig_calls = calls * pps
-            cnt.update_calls = int(inf["update_calls"])
-        else:
-            cnt.eig_calls = calls if p.bn >= 2 else 0
-        masked = 0
-        if masked_rounds and opts.masking and conv:
-            masked = (rounds - max(s_i, 1)) * pps
-        cnt.masked_pair_skips = masked
-        cnt.t_eig = dtime
-        base = "blocked" if (int(inf["path"]) & 0xFF) == 2 else "unblocked"
-        path = ("transpose+" if int(inf["path"]) & 0x100 else "") + ("qr+" if int(inf["path"]) & 0x200 else "") + base
-        info = SolveInfo(converged=conv, outer_sweeps=s_i, inner_rotations=int(inf["rotations"]),
-                         masked_pair_skips=masked, path=path, counters=cnt)
-        results[idx] = SvdResult(u=U, sigma=S, v=V if opts.compute_right_vectors else None, info=info)
-        last = int(inf["last_rotations"])
-        if not p.blocked:
-            stats = [(last == 0, 1, last)]
-        else:
-            stats = [(True, 1, 0)] * pps if last == 0 else [(False, 1, last)] + [(True, 1, 0)] * (pps - 1)
-        tele[idx] = dict(outer_sweeps=s_i, converged=conv, last=last, pair_stats=stats, kernel=kern)
+        dt = arrays[idx].dtype
+        u = np.zeros((m, k), dtype=dt, order="F")
+        sigma = np.zeros(k, dtype=real_dtype(dt))
+        v = np.zeros((n, k), dtype=dt, order="F") if want_v else None
+        info = SolveInfo(converged=True, outer_sweeps=0, inner_rotations=0, masked_pair_skips=0, path="empty",
+                         counters=WorkCounters())
+        results[idx] = SvdResult(u=u, sigma=sigma, v=v, info=info)
+        tele[idx] = dict(outer_sweeps=0, converged=True, last=0, pair_stats=[])
+    paths: dict = {}
+    for idxs, p, U, S, V, cols, dtime, kern in solved:
+        pps, blocked = p.pairs_per_sweep, p.blocked
+        eig_unit = 0 if (not blocked and p.bn < 2) else 1
+        masking = bool(masked_rounds and opts.masking)
+        sw_l, cv_l, rot_l, up_l, path_l, last_l = (cols["outer_sweeps"], cols["converged"], cols["rotations"],
+                                                   cols["update_calls"], cols["path"], cols["last_rotations"])
+        for j, idx in enumerate(idxs):
+            s_i = sw_l[j]
+            conv = bool(cv_l[j])
+            calls = s_i if masked_rounds is False or opts.masking else rounds
+            masked = (rounds - max(s_i, 1)) * pps if (masking and conv) else 0
+            if blocked:
+                cnt = WorkCounters(gram_calls=calls * pps, eig_calls=calls * pps, update_calls=up_l[j],
+                                   masked_pair_skips=masked, t_eig=dtime)
+            else:
+                cnt = WorkCounters(eig_calls=calls * eig_unit, masked_pair_skips=masked, t_eig=dtime)
+            pv = path_l[j]
+            path = paths.get(pv)
+            if path is None:
+                base = "blocked" if (pv & 0xFF) == 2 else "unblocked"
+                path = ("transpose+" if pv & 0x100 else "") + ("qr+" if pv & 0x200 else "") + base
+                paths[pv] = path
+            info = SolveInfo(converged=conv, outer_sweeps=s_i, inner_rotations=rot_l[j], masked_pair_skips=masked,
+                             path=path, counters=cnt)
+            results[idx] = SvdResult(u=U[j], sigma=S[j], v=V[j] if (want_v and V is not None) else None, info=info)
+            last = last_l[j]
+            if not blocked:
+                stats = [(last == 0, 1, last)]
+            else:
+                stats = [(True, 1, 0)] * pps if last == 0 else [(False, 1, last)] + [(True, 1, 0)] * (pps - 1)
+            tele[idx] = dict(outer_sweeps=s_i, converged=conv, last=last, pair_stats=stats, kernel=kern)
     return results, errors, tele
 
 
@@ -233,11 +251,27 @@ def batch_svd(problems, opts: JacobiOptions | None = None, state: BatchState | N
         raise DomainError("batch must contain at least one problem")
     st = state if state is not None else BatchState.for_batch(len(problems))
     st._reset(len(problems))
-    results, errors, tele = _solve_problems(problems, opts, force=None, masked_rounds=True)
+    # the records are tens of thousands of small objects: keep the cyclic collector out of the way
+    gc_was = gc.isenabled()
+    gc.disable()
+    try:
+        results, errors, tele = _solve_problems(problems, opts, force=None, masked_rounds=True)
+    finally:
+        if gc_was:
+            gc.enable()
     st.errors = dict(errors)
+    c = st.counters
     for idx, t in tele.items():
         st.outer_sweeps[idx] = t["outer_sweeps"]
         st.pair_stats[idx] = t["pair_stats"]
         st.active[idx] = not t["converged"]
-        st.counters.add(results[idx].info.counters)
+        w = results[idx].info.counters
+        c.gram_calls += w.gram_calls
+        c.eig_calls += w.eig_calls
+        c.update_calls += w.update_calls
+        c.masked_pair_skips += w.masked_pair_skips
+        c.t_aux += w.t_aux
+        c.t_gram += w.t_gram
+        c.t_eig += w.t_eig
+        c.t_vec += w.t_vec
     return results

@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <string.h>
 
+#include <thread>
+#include <vector>
+
 #include "launch.h"
 
 using namespace bsvd;
@@ -293,6 +296,24 @@ int bsvd_householder_qr_batched(int dtype, int m, int n, int batch, const void* 
         case BSVD_Z: return launch_householder_qr<cx<double>>(m, n, batch, A, lda, strideA, Q, ldq, strideQ, R, ldr, strideR, work, lim, st);
     }
     return BSVD_ERR_ARG;
+}
+
+int bsvd_pack_host(const void* const* src, int count, size_t bytes, void* dst, int nthreads) {
+    if (count < 0 || (count > 0 && (!src || !dst))) return BSVD_ERR_ARG;
+    unsigned char* d = static_cast<unsigned char*>(dst);
+    auto work = [&](int lo, int hi) {
+        for (int i = lo; i < hi; ++i) memcpy(d + (size_t)i * bytes, src[i], bytes);
+    };
+    const int nt = nthreads < 1 ? 1 : (nthreads > 32 ? 32 : nthreads);
+    if (nt == 1 || count < 2 * nt) {
+        work(0, count);
+        return BSVD_OK;
+    }
+    std::vector<std::thread> pool;
+    const int step = (count + nt - 1) / nt;
+    for (int lo = 0; lo < count; lo += step) pool.emplace_back(work, lo, lo + step < count ? lo + step : count);
+    for (auto& t : pool) t.join();
+    return BSVD_OK;
 }
 
 int bsvd_abi_version(void) { return BSVD_ABI_VERSION; }

@@ -173,3 +173,16 @@ def test_backend_interface_single_b200_backend():
             bs.select(bad)
     with bs.use("b200") as bb:
         assert bb is b
+
+
+def test_pack_host_helper_packs_column_major_batches():
+    """bsvd_pack_host (host-only, no GPU): the list API's packing of F-ordered matrices."""
+    L = _lib.load()
+    rng = np.random.default_rng(3)
+    mats = [np.asfortranarray(rng.random((5, 3))) for _ in range(37)]
+    out = np.empty((37, 3, 5))
+    ptrs = np.fromiter((a.__array_interface__["data"][0] for a in mats), dtype=np.uintp, count=len(mats))
+    for nt in (1, 4):
+        out[...] = 0
+        assert L.bsvd_pack_host(ptrs.ctypes.data, len(mats), 15 * 8, out.ctypes.data, nt) == 0
+        assert np.array_equal(out, np.stack([a.T for a in mats]))
