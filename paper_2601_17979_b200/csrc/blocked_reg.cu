@@ -213,6 +213,7 @@ __device__ __forceinline__ void inner_iter(double (&x0)[N], double (&x1)[N], dou
     const double dtg = rot ? xor_sign(tabs * absg, eneg) : 0.0;
     const double nt = gt + dtg, nb = gb - dtg;
     const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
+    __syncwarp();  // both half-warps evaluate pair k: lane k + 16 has read nrm[] before lane k rewrites it
     if (c.lane < H) {
         sm.pub[c.k] = par;
         sm.nrm[ct] = nt;

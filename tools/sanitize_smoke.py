@@ -1,0 +1,48 @@
+"""One small batch through every kernel family, for compute-sanitizer runs (development aid):
+    compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+    compute-sanitizer --tool racecheck python tools/sanitize_smoke.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2601_17979_b200 as bs
+
+rng = np.random.default_rng(1)
+
+
+def run(dt, m, n, route=0, kernel=0, B=3, **kw):
+    A = rng.random((B, n, m))
+    if np.dtype(dt).kind == "c":
+        A = A + 1j * rng.random((B, n, m))
+    a = torch.from_numpy(A.astype(dt)).cuda()
+    r = bs.solve_tensor(a, m, n, bs.JacobiOptions(**kw), route=route, kernel=kernel)
+    torch.cuda.synchronize()
+    print(dt.__name__, m, n, route, kernel, "ok", float(r.s[0, 0]), flush=True)
+
+
+run(np.float64, 32, 32)                       # r32b + fused finalise
+run(np.float64, 32, 32, kernel=19)            # unfused
+run(np.float64, 32, 32, kernel=20)            # r32c
+run(np.float64, 32, 32, kernel=26)            # reg32e
+run(np.float32, 16, 16)                       # reg16b
+run(np.float32, 16, 16, kernel=11)            # reg16
+run(np.float64, 64, 64)                       # blocked_reg
+run(np.float64, 128, 128, B=2)                # blocked_reg NWG 2
+run(np.complex128, 256, 32, B=2)              # creg32 SP
+run(np.complex128, 64, 32)                    # creg32 register V
+run(np.complex128, 256, 32, B=2, use_qr_preprocess=True)  # qr_col + creg32 + applyq_col
+run(np.float64, 96, 20, use_qr_preprocess=True)
+run(np.complex64, 40, 24)                     # general unblocked
+run(np.float32, 48, 48)                       # general blocked
+q, r = bs.householder_qr(rng.random((40, 12)))
+f = bs.finalize(rng.random((20, 7)), rng.random((7, 7)))
+g = rng.random((10, 10)); g = g + g.T
+d = np.diag(g).copy(); m = np.zeros((10, 10))
+w = np.triu(g, 1); w = np.asfortranarray(w + w.T)
+bs.eig_sweeps(w, d, m, tol=1e-14, max_sweeps=5, delta=True)
+ev = bs.jacobi_hermitian_eig(g)
+print("all ok")
