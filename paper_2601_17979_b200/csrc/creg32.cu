@@ -43,7 +43,6 @@ constexpr int N = 32;      // columns
 constexpr int H = 16;      // pairs per iteration
 constexpr int NIT = 31;    // iterations per sweep
 constexpr int RSTR = 34;   // transpose buffer row stride (doubles)
-constexpr int PS = 33;     // column stride of the smem P planes (doubles)
 constexpr int MAXW = 8;    // warps per CTA (m <= 256)
 
 __host__ __device__ constexpr int ring_slot(int q) {
@@ -77,7 +76,7 @@ struct CtaSmem {
     int misc[4];                   // [0] bad input, [2..3] amax bits (8-byte aligned)
 };
 struct PSmem {
-    double P[2][N * PS];           // running rotation product (= V), real / imaginary planes, column-major
+    double2 P[N * N];              // running rotation product (= V), column-major, (re, im) interleaved
 };
 
 __device__ __forceinline__ double sum16(const double* p) {
@@ -253,19 +252,17 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
     }
     // ---- P (= V) update in smem: task (row = lane, pair q) for q = warp, warp + NW, ... ----
     if (SP && c.want_p) {
-        double* Pr = c.ps->P[0];
-        double* Pi = c.ps->P[1];
+        double2* P = c.ps->P;
         for (int q = c.warp; q < H; q += NW) {
             const Par pq = sm.pub[q];
             if (pq.cm1 == 0.0 && pq.ar == 0.0 && pq.ai == 0.0) continue;  // skipped pair (warp-uniform)
             const uint32_t cq = c.ctab[t * H + q];
-            const int a0 = (cq & 0xff) * PS + c.lane, b0 = ((cq >> 8) & 0xff) * PS + c.lane;
-            double tr = Pr[a0], ti = Pi[a0], br = Pr[b0], bi = Pi[b0];
+            const int a0 = (cq & 0xff) * N + c.lane, b0 = ((cq >> 8) & 0xff) * N + c.lane;
+            const double2 ta = P[a0], tb = P[b0];  // 16-byte accesses: 32 lanes, one column, conflict-free
+            double tr = ta.x, ti = ta.y, br = tb.x, bi = tb.y;
             capply(tr, ti, br, bi, pq);
-            Pr[a0] = tr;
-            Pi[a0] = ti;
-            Pr[b0] = br;
-            Pi[b0] = bi;
+            P[a0] = make_double2(tr, ti);
+            P[b0] = make_double2(br, bi);
         }
     }
 }
@@ -313,8 +310,7 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_creg32
     if (SP && want_p)
         for (int e = tid; e < N * N; e += NW * 32) {
             const int r = e % N, col = e / N;
-            ps->P[0][col * PS + r] = (r == col) ? 1.0 : 0.0;
-            ps->P[1][col * PS + r] = 0.0;
+            ps->P[col * N + r] = make_double2((r == col) ? 1.0 : 0.0, 0.0);
         }
     // ---- kernel (1): this lane's row of A, exact power-of-two prescale ----
     const int row = warp * 32 + lane;
@@ -408,7 +404,8 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_creg32
         cx<double>* V = W + (size_t)m * N;
         for (int e = tid; e < N * N; e += NW * 32) {
             const int r = e % N, col = e / N;
-            V[e] = cx<double>{ps->P[0][col * PS + r], ps->P[1][col * PS + r]};
+            const double2 z = ps->P[col * N + r];
+            V[e] = cx<double>{z.x, z.y};
         }
     }
     if (vrow >= 0) {
