@@ -239,12 +239,44 @@ __device__ __forceinline__ void all_partials(const double (&x0)[N], const double
 // update is fused with the partials of iteration t + 1 (offset u + 1 in the
 // pre-shift register naming: next pair k = columns of this iteration's pairs
 // k - 1 and k + 1), so they are ready when the next reduction starts.
-template <int u, int PD>
+// SH variant: the 16 g_ji partials of this lane's rows reduced over the half-warp by a transposing xor
+// butterfly (8, 4, 2, 1): lane hl ends with pair hl's sum, no shared-memory round trip
+__device__ __forceinline__ double reduce16_half(double (&v)[H], int hl) {
+    const bool b3 = hl & 8, b2 = hl & 4, b1 = hl & 2, b0 = hl & 1;
+    double a8[8], a4[4], a2[2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const double keep = b3 ? v[i + 8] : v[i], send = b3 ? v[i] : v[i + 8];
+        a8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double keep = b2 ? a8[i + 4] : a8[i], send = b2 ? a8[i] : a8[i + 4];
+        a4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double keep = b1 ? a4[i + 2] : a4[i], send = b1 ? a4[i] : a4[i + 2];
+        a2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    const double keep = b0 ? a2[1] : a2[0], send = b0 ? a2[0] : a2[1];
+    return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+}
+
+template <int u, int PD, bool SH = false>
 __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab, int t,
                                        int lane, int half, int hl, bool done, double tol, double tol2,
                                        Par* logl, IterState& st) {
     R32P(0, x0[TS(0, u)]);
     const uint32_t code = ctab[t * H + hl];
+    double gsh = 0.0;
+    if constexpr (SH) {
+        double v[H];
+#pragma unroll
+        for (int q = 0; q < H; ++q) v[q] = fma(x1[BS(q, u)], x1[TS(q, u)], x0[BS(q, u)] * x0[TS(q, u)]);
+        gsh = reduce16_half(v, hl);
+        if (st.full) norm_partials<u>(x0, x1, sm.red, lane);
+    }
     __syncwarp();
     // ---- lane hl owns pair k = hl of its half's problem ----
     const int k = hl;
@@ -258,7 +290,7 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
         gt = sm.nrm[half][ct];
         gb = sm.nrm[half][cb];
     }
-    const double g = sum16(sm.red + k * RSTR + 16 * half);
+    const double g = SH ? gsh : sum16(sm.red + k * RSTR + 16 * half);
     const double absg = fabs(g);
     R32P(1, g);
     // guard (F4): rotate unless |g| <= 0 or |g| < tol sqrt(gii gjj); squared
@@ -306,14 +338,14 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
             if (q + PD < H) pq[q % PD] = sm.pub[half][q + PD];
             apply2(x0[TS(q, u)], x0[BS(q, u)], cur.cm1, cur.c);
             apply2(x1[TS(q, u)], x1[BS(q, u)], cur.cm1, cur.c);
-            if (q >= 1) cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs this iteration's pairs q-2, q
+            if (!SH && q >= 1) cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs pairs q-2, q
         }
-        cross_partial<un>(x0, x1, sm.red, lane, H - 1);
-    } else {
+        if (!SH) cross_partial<un>(x0, x1, sm.red, lane, H - 1);
+    } else if (!SH) {
 #pragma unroll
         for (int q = 0; q < H; ++q) cross_partial<un>(x0, x1, sm.red, lane, q);
     }
-    if (st.full) norm_partials<un>(x0, x1, sm.red, lane);
+    if (!SH && st.full) norm_partials<un>(x0, x1, sm.red, lane);
     R32P(3, x1[BS(H - 1, u)]);
 }
 
@@ -351,29 +383,29 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
     __syncwarp();
 }
 
-template <int U, int PD>
+template <int U, int PD, bool SH = false>
 __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab,
                                         int lane, int half, int hl, bool done, double tol, double tol2, Par* logl,
                                         IterState& st) {
     constexpr int NG = (NIT + U - 1) / U;
     constexpr int R = NIT - (NG - 1) * U;  // iterations in the last group
-    all_partials<0>(x0, x1, sm.red, lane, true);  // first iteration of a sweep: fresh norms
+    if (!SH) all_partials<0>(x0, x1, sm.red, lane, true);  // first iteration of a sweep: fresh norms
 #pragma unroll 1
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
         const bool last = gi == NG - 1;
-        w_iter<0, PD>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
+        w_iter<0, PD, SH>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
         if constexpr (U >= 2) {
             if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            w_iter<1 % U, PD>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<1 % U, PD, SH>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
         }
         if constexpr (U >= 3) {
             if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            w_iter<2 % U, PD>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<2 % U, PD, SH>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
         }
         if constexpr (U >= 4) {
             if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            w_iter<3 % U, PD>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<3 % U, PD, SH>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
         }
         ring_shift<U>(x0);
         ring_shift<U>(x1);
@@ -407,7 +439,7 @@ __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSm
     }
 }
 
-template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true>
+template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true, bool SH = false>
 __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -474,7 +506,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         st.itbits = 0;
         st.full = true;  // fresh norms at the start of every sweep
         st.fmask = 0xffffffffu;
-        w_sweep<U, PD>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2,
+        w_sweep<U, PD, SH>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2,
                        (SPLIT && logw) ? logw + (size_t)sw * NIT * H : logw, st);
         // ---- sweep end: per-problem rotation count over the half warp ----
         int tot = st.my_rot;
@@ -765,12 +797,12 @@ size_t reg32b_work_elems(int kv, int max_sweeps) {
                             : 2 * 32 * 32 + r32b::LOG_ELEMS;
 }
 
-template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true>
+template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true, bool SH = false>
 static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
     const int per_cta = 2 * NW;
     const int grid = (a.batch + per_cta - 1) / per_cta;
     const size_t smem = NW * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
-    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD, SPLIT, FF>;
+    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD, SPLIT, FF, SH>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<grid, NW * 32, smem, st>>>(a);
@@ -804,7 +836,7 @@ int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st)
             break;
         case KV_UNBLOCKED_REG32B + 1: rc = launch_r32b<4, 3, 2, 2, 4>(a, st); break;   // 168 regs, 12 warps/SM
         case KV_UNBLOCKED_REG32B + 2: rc = launch_r32b<4, 2, 2, 4, 16>(a, st); break;  // V unroll 4
-        case KV_UNBLOCKED_REG32B + 3: rc = launch_r32b<1, 11, 2, 2, 4>(a, st); break;  // one-warp CTAs
+        case KV_UNBLOCKED_REG32B + 3: rc = launch_r32b<4, 2, 2, 2, 16, false, true, true>(a, st); break;  // shuffle g
         case KV_UNBLOCKED_REG32B + 4: rc = launch_r32b<4, 3, 2, 2, 2>(a, st); break;   // 168 regs, depth 2
         case KV_UNBLOCKED_REG32B + 7: rc = launch_r32b<4, 2, 2, 2, 16, false, false>(a, st); break;  // unfused finalize
         default: rc = launch_r32b<4, 2, 2, 2, 16>(a, st); break;                       // 255 regs, 8 warps/SM
