@@ -74,17 +74,6 @@ int launch_applyq_col(int bm, int bn, int batch, const typename std::conditional
                       const typename std::conditional<CX, cx<double>, double>::type* UR,
                       typename std::conditional<CX, cx<double>, double>::type* Out, int64_t ldo, int64_t so,
                       cudaStream_t st);
-template <bool CX>
-int launch_qr_reg(SolveArgs<typename std::conditional<CX, cx<double>, double>::type> a,
-                  typename std::conditional<CX, cx<double>, double>::type* R,
-                  typename std::conditional<CX, cx<double>, double>::type* refl,
-                  typename std::conditional<CX, cx<double>, double>::type* phase, cudaStream_t st);
-template <bool CX>
-int launch_applyq_reg(int bm, int bn, int batch, const typename std::conditional<CX, cx<double>, double>::type* refl,
-                      const typename std::conditional<CX, cx<double>, double>::type* phase,
-                      const typename std::conditional<CX, cx<double>, double>::type* UR,
-                      typename std::conditional<CX, cx<double>, double>::type* Out, int64_t ldo, int64_t so,
-                      cudaStream_t st);
 size_t heevj_workspace(int dtype, int n, int batch, size_t smem_limit);
 int launch_heevj(int dtype, int n, int batch, const void* G, int64_t ldg, int64_t sG, void* D, int64_t sD, void* M,
                  int64_t ldm, int64_t sM, int m_init, double k, int max_sweeps, bsvd_info* info, void* work,
