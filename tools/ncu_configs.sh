@@ -11,3 +11,5 @@ run c2-full k_reg16b "C2-full"
 run c3 k_blocked_reg "C3"
 run c4 k_creg32 "C4"
 run c5 k_blocked_reg "C5"
+# C4 on the QR route: the two QR kernels (quick_time has no qr config; use the probe)
+timeout 600 ncu --metrics $M --clock-control none -k regex:"k_qr_col|k_applyq_col" -c 2 --csv --log-file "$out/ncu_c4-qr.csv" python tools/qr_route_probe.py > /dev/null 2>&1
