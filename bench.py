@@ -433,6 +433,9 @@ def run_b200(args, cfg):
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": load_traffic(args.config),
                      "peak_source": "measured on this box by bsvd_bench_fma_peak (MEASURED_PEAKS.json has no "
                                     "FP64/FP32 pipe entry)",
+                     "timing": "CUDA events on the launching stream around each timed solve: the dominant kernel "
+                               "plus its finalisation pass (the dominant kernel is 97-99.8 % of a step in the ncu "
+                               "launch lists, profiles/r1_launches_c1.txt)",
                      "flops_per_matrix": f_mat, "flops_source": "SURVEY 8(d) formula on the CPU restatement's "
                      "sweep/rotation counts for the same inputs (bitwise equal to the reference's)",
                      "hbm_bytes_per_matrix": compulsory_bytes(m, n, es, rs, cfg["want_v"])},
