@@ -91,9 +91,13 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         return p;  // forced variant unavailable => kernel 0 => unsupported
     }
     if (o->kernel == 0) {  // default for 32x32 FP64: the second-generation register kernel
-        // (one kernel for every batch size: the warp-specialised variant 26 is 9 % faster at 1,000
-        // problems but not bit-identical, and batch == standalone must hold bitwise)
-        (void)batch;
+        // up to one wave of problem pairs (148 SMs x 8 warps) the warp-specialised W/V kernel finishes
+        // first (500 problems 0.32 vs 0.35 ms, 1,000: 0.33 vs 0.35; from 1,500 on gen. 2 wins); its
+        // arithmetic is bit-identical to gen. 2, so batch == standalone still holds bitwise
+        if (batch > 0 && batch <= 1184) {
+            Plan p = plan_unblocked_reg32e(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, KV_UNBLOCKED_REG32E);
+            if (p.kernel) return p;
+        }
         Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, 0, o->max_sweeps);
         if (p.kernel) return p;
     }

@@ -138,8 +138,7 @@ __device__ __forceinline__ void rot_abs(double dabs, double g, double& s, double
     const double mx = fmax(dabs, g);
     const double sc = mx < 0x1p-500 ? 0x1p+600 : 1.0;  // exact rescale of tiny pairs
     const double dn = dabs * sc, gn = g * sc;
-    const double g2 = gn + gn;
-    const double q = fma(dn, dn, g2 * g2);
+    const double q = fma(4.0 * gn, gn, dn * dn);  // the gen. 2 kernel's association: identical bits
     const double ir = rsqrt_cubic(q);
     const double c2 = fma(0.5 * dn, ir, 0.5);
     const double ic = rsqrt_cubic(c2);

@@ -480,7 +480,7 @@ def test_eig_sweeps_operator_full_solve(dt):
     assert np.max(np.abs(m.conj().T @ m - np.eye(n))) <= 60 * n * u
 
 
-_DEFAULT_KERNEL_SHAPES = [(np.float64, 32, 32, 12), (np.float32, 16, 16, 24), (np.float64, 64, 64, 30),
+_DEFAULT_KERNEL_SHAPES = [(np.float64, 32, 32, 26),  # small batches: the warp-specialised 32x32 kernel (np.float32, 16, 16, 24), (np.float64, 64, 64, 30),
                           (np.complex128, 256, 32, 32), (np.complex128, 40, 24, 1), (np.float32, 48, 48, 2)]
 
 
@@ -536,3 +536,29 @@ def test_every_default_kernel_reports_sweep_cap(dt, m, n, kid):
     assert (info["converged"] == 0).all() and (info["outer_sweeps"] == 1).all() and (info["rotations"] > 0).all()
     S = r.s.cpu().numpy().astype(np.float64)
     assert np.all(np.diff(S, axis=1) <= 0) and np.all(np.isfinite(S))
+
+
+@pytest.mark.gpu
+def test_c1_batch_size_kernel_choice_is_bitwise_invisible():
+    """Up to 1,184 32x32 FP64 problems run the warp-specialised kernel (26), more the gen. 2 kernel (12);
+    their arithmetic is bit-identical, so batch == standalone holds across the switch
+    (tests/test_batch.py:19-28), holes and fresh-norm iterations included."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    B = 1300
+    rng = np.random.default_rng(77)
+    A = rng.random((B, 32, 32))
+    A[5] = np.diag(np.geomspace(1.0, 1e-12, 32)) @ A[5]
+    A[9][:, 4] = 0.0
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    big = bs.solve_tensor(a, 32, 32, bs.JacobiOptions())
+    pick = [0, 5, 9, 1234, 1299]
+    small = bs.solve_tensor(a[pick].contiguous(), 32, 32, bs.JacobiOptions())
+    torch.cuda.synchronize()
+    kb = np.frombuffer(big.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"]
+    ks = np.frombuffer(small.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"]
+    assert (kb == 12).all() and (ks == 26).all()
+    p = torch.tensor(pick).cuda()
+    assert torch.equal(big.s[p], small.s) and torch.equal(big.u[p], small.u) and torch.equal(big.v[p], small.v)
