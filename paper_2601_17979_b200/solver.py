@@ -57,14 +57,29 @@ def torch_dtype(np_dtype):
     return _TORCH_OF[np.dtype(np_dtype)]
 
 
+_NP_OF: dict = {}
+
+
 def np_dtype_of(tdtype):
-    torch = _torch()
-    return {
-        torch.float32: np.dtype(np.float32),
-        torch.float64: np.dtype(np.float64),
-        torch.complex64: np.dtype(np.complex64),
-        torch.complex128: np.dtype(np.complex128),
-    }[tdtype]
+    if not _NP_OF:
+        torch = _torch()
+        _NP_OF.update({torch.float32: np.dtype(np.float32), torch.float64: np.dtype(np.float64),
+                       torch.complex64: np.dtype(np.complex64), torch.complex128: np.dtype(np.complex128)})
+    return _NP_OF[tdtype]
+
+
+_OPTS_CACHE: dict = {}
+_WSB_CACHE: dict = {}
+
+
+def _cached_opts(opts, route: int, kernel: int, stagger: int) -> _lib.BsvdOpts:
+    """make_opts memoised on the (frozen, hashable) JacobiOptions: the C side only reads the struct."""
+    key = (opts, int(route), int(kernel), int(stagger))
+    o = _OPTS_CACHE.get(key)
+    if o is None:
+        o = make_opts(opts, route, kernel, stagger)
+        _OPTS_CACHE[key] = o
+    return o
 
 
 def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0, stagger: int = 0) -> _lib.BsvdOpts:
@@ -88,11 +103,13 @@ def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0, stagger: int = 
 _WS_CACHE: dict = {}
 
 
-def _workspace(nbytes: int, device):
+def _workspace(nbytes: int, device, stream_handle=None):
     torch = _torch()
     if nbytes == 0:
         return None
-    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    if stream_handle is None:
+        stream_handle = torch.cuda.current_stream(device).cuda_stream
+    key = (str(device), stream_handle)
     buf = _WS_CACHE.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
@@ -123,7 +140,7 @@ def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: 
     dt = np_dtype_of(a_t.dtype)
     code = DTYPE_CODE[dt]
     k = min(m, n)
-    o = make_opts(opts, route, kernel, stagger)
+    o = _cached_opts(opts, route, kernel, stagger)
     dev = a_t.device
     if out is None:
         u = torch.empty((B, k, m), dtype=a_t.dtype, device=dev)
@@ -132,9 +149,13 @@ def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: 
         info = torch.empty((B * _lib.INFO_BYTES,), dtype=torch.uint8, device=dev)
     else:
         u, s, v, info = out
-    ws_bytes = L.bsvd_workspace_bytes(code, m, n, B, ctypes.byref(o))
-    ws = _workspace(ws_bytes, dev)
+    wkey = (code, m, n, B, id(o))
+    ws_bytes = _WSB_CACHE.get(wkey)
+    if ws_bytes is None:
+        ws_bytes = L.bsvd_workspace_bytes(code, m, n, B, ctypes.byref(o))
+        _WSB_CACHE[wkey] = ws_bytes
     stream = torch.cuda.current_stream(dev).cuda_stream
+    ws = _workspace(ws_bytes, dev, stream)
     rc = L.bsvd_gesvj_batched(
         code, m, n, B,
         a_t.data_ptr(), max(m, 1), m * n,
