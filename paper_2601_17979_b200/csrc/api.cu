@@ -74,6 +74,14 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         }
         return plan_blocked_general(es, rs, r.bm, r.bn, o->nb, r.need_v, lim);
     }
+    if (is_reg16c(o->kernel)) return plan_unblocked_reg16c(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
+    if (o->kernel == 0 && batch >= 3500) {
+        // 16x16 FP32 from ~3,500 problems on: the quarter-warp kernel (C2 10k: 172 vs 207 us); below it the
+        // half-warp kernel's shorter per-warp chain wins.  The two are bit-identical (same sums in the same
+        // tree, same parameter and update arithmetic), so batch == standalone still holds bitwise.
+        Plan p = plan_unblocked_reg16c(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, 0);
+        if (p.kernel) return p;
+    }
     if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG16B || o->kernel == KV_UNBLOCKED_REG16B + 1) {
         Plan p = plan_unblocked_reg16b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
         if (p.kernel) return p;
@@ -166,6 +174,11 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_UNBLOCKED_REG16B:
         case KV_UNBLOCKED_REG16B + 1:
             if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16b(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
+        case KV_UNBLOCKED_REG16C:
+        case KV_UNBLOCKED_REG16C + 1:
+        case KV_UNBLOCKED_REG16C_LAST:
+            if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16c(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG16F:
             if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16(a, p, st);

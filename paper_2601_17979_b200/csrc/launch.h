@@ -85,6 +85,9 @@ Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contig
 int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 Plan plan_unblocked_reg16b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
 int launch_unblocked_reg16b(SolveArgs<float> a, const Plan& p, cudaStream_t st);
+bool is_reg16c(int kernel);
+Plan plan_unblocked_reg16c(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
+int launch_unblocked_reg16c(SolveArgs<float> a, const Plan& p, cudaStream_t st);
 bool is_reg32c(int kv);
 Plan plan_unblocked_reg32c(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
 int launch_unblocked_reg32c(SolveArgs<double> a, const Plan& p, cudaStream_t st);

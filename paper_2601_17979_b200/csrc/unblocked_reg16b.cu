@@ -26,42 +26,13 @@
 // workspace and finalize.cu (sigma in float64) completes the factorisation.
 #include "kernel_args.cuh"
 #include "launch.h"
+#include "ring16.cuh"
 
 namespace bsvd {
 namespace reg16b {
 
-constexpr int N = 16;    // columns
-constexpr int H = 8;     // pairs per iteration
-constexpr int NIT = 15;  // iterations per sweep
 constexpr int NW = 4;    // warps per CTA (8 problems)
-
-__host__ __device__ constexpr int ring_slot(int q) {
-    return q == 0 ? 1 : (q <= H - 1 ? 2 * q : 2 * (2 * H - 1 - q) + 1);
-}
-__host__ __device__ constexpr int md(int a) { return ((a % NIT) + NIT) % NIT; }
-__host__ __device__ constexpr int TS(int k, int u) { return k == 0 ? 0 : ring_slot(md(k - u)); }
-__host__ __device__ constexpr int BS(int k, int u) { return ring_slot(md((k == 0 ? 0 : NIT - k) - u)); }
-
-__host__ __device__ inline uint32_t pair_code(int t, int k) {
-    int qt = k - t, qb = (k == 0 ? 0 : NIT - k) - t;
-    qt += qt < 0 ? NIT : 0;
-    qb += qb < 0 ? NIT : 0;
-    const int ct = (k == 0) ? 0 : ring_slot(qt);
-    const int cb = ring_slot(qb);
-    return (uint32_t)ct | ((uint32_t)cb << 8) | ((ct > cb) ? (1u << 16) : 0u);
-}
-
-// ring move by SH positions; 15 = 3 x 5 is not prime, so follow every cycle of the permutation
-template <int SH>
-__device__ __forceinline__ void ring_shift(float (&x)[N]) {
-    if constexpr (md(SH) != 0) {
-        float y[NIT];
-#pragma unroll
-        for (int q = 0; q < NIT; ++q) y[q] = x[ring_slot(q)];
-#pragma unroll
-        for (int q = 0; q < NIT; ++q) x[ring_slot(q)] = y[md(q - SH)];
-    }
-}
+using namespace ring16;
 
 struct __align__(16) WarpSmem {
     float2 pub[2][H];   // this iteration's rotations (cm1, c) [half][pair]
@@ -69,41 +40,6 @@ struct __align__(16) WarpSmem {
     float sig[2][N];    // finalisation: sigma by column
     int rk[2][N];       // finalisation: rank by column
 };
-
-__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
-__device__ __forceinline__ float rsqrt_nr(float x) {
-    const float r = rsqrtf(x);
-    return fmaf(0.5f * r, fmaf(-x * r, r, 1.0f), r);
-}
-__device__ __forceinline__ float rcp_nr(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return fmaf(r, fmaf(-x, r, 1.0f), r);
-}
-// |d|, g -> s = sin(th) >= 0, c - 1, |t| (half-angle form of the reference formula, rotation.cuh)
-__device__ __forceinline__ void rot_abs_core(float dabs, float g, float& s, float& cm1, float& tabs) {
-    const float q = fmaf(4.0f * g, g, dabs * dabs);
-    const float ir = rsqrt_nr(q);
-    const float c2 = fmaf(0.5f * dabs, ir, 0.5f);
-    const float ic = rsqrt_nr(c2);
-    const float c = c2 * ic;
-    s = (g * ir) * ic;
-    cm1 = -(s * s) * rcp_nr(1.0f + c);
-    tabs = s * ic;
-}
-__device__ __forceinline__ void rot_abs(float dabs, float g, float& s, float& cm1, float& tabs) {
-    rot_abs_core(dabs, g, s, cm1, tabs);
-    if (fmaxf(dabs, g) < 0x1p-50f) rot_abs_core(dabs * 0x1p+60f, g * 0x1p+60f, s, cm1, tabs);
-}
-__device__ __forceinline__ float xor_signf(float x, bool neg) {
-    return __int_as_float(__float_as_int(x) ^ ((int)neg << 31));
-}
-__device__ __forceinline__ void apply2(float& x, float& y, float cm1, float c) {
-    const float tx = fmaf(c, y, x);
-    const float ty = fmaf(-c, x, y);
-    x = fmaf(cm1, x, tx);
-    y = fmaf(cm1, y, ty);
-}
 
 // Transposing butterfly over the 16 lanes of a half: v[0..NV) per lane -> lane l ends with the
 // half's total of value index vidx(l) = (l >> 1) (NV = 8) -- 4 + 2 + 1 + 1 shuffles.
@@ -158,10 +94,7 @@ __device__ __forceinline__ void iter(float (&x)[N], float (&y)[N], WarpSmem& sm,
         }
     }
     const float absg = fabsf(g);
-    const float p = gt * gb;
-    bool rot = !(absg * absg < tol2 * p);
-    if (absg < 0x1p-60f && absg > 0.0f) rot = !(absg < tol * sqrtf(p));
-    rot = rot && !done && absg > 0.0f;
+    const bool rot = rot_guard(absg, gt, gb, tol2, tol) && !done && absg > 0.0f;
     const float d = gt - gb;
     float s, cm1, tabs;
     rot_abs(fabsf(d), absg, s, cm1, tabs);

@@ -1,0 +1,362 @@
+// unblocked_reg16c.cu -- kernel (2), third-generation register-resident
+// 16x16 FP32 path (BASELINE config C2).
+//
+// Same iteration, schedule and arithmetic as unblocked_reg16b.cu (the
+// iteration of src/_kernels_numba.py:85-138 on the round-robin ring of
+// src/ordering.py:32-75, per-problem exit after the first quiet sweep), with
+// a quarter-warp per problem: a warp owns FOUR problems, lane l of quarter q
+// holds rows l and l + 8 of problem q's W and V (32 + 32 floats).  Per
+// problem-iteration this removes the redundancy of gen. 2, where two lanes
+// evaluate every rotation and every lane holds one row:
+//  * each lane pre-sums its two rows' products, so the transposing xor
+//    butterfly over the 8 lanes of a quarter is 4 + 2 + 1 shuffles and lane l
+//    ends with pair l's g_ji alone (no duplicate parameter chain).  The
+//    pre-sum (rounded products, no FMA contraction) is gen. 2's xor-8 level
+//    and the remaining levels are its xor 4, 2, 1, so every dot product, and
+//    with it every rotation, has gen. 2's bits: the two kernels are
+//    bit-identical and the default switches between them on the batch size
+//    without breaking batch == standalone (reference tests/test_batch.py:19-28);
+//  * the rotation update is the same 4 FMAs per row and column pair, on twice
+//    the rows per lane, so the FMA count per problem is unchanged while the
+//    reduction / parameter / publish overhead per problem halves.
+// The fused finalisation sums sigma in float64 in finalize_block's tree
+// (rows l, l + 8 pre-summed in-lane = its xor-8 level, then xor 4, 2, 1), so
+// sigma and U are the bits of the standalone pass; problems with a
+// sigma < tiny/u column are flagged to it (orthogonal completion).
+#include "kernel_args.cuh"
+#include "launch.h"
+#include "ring16.cuh"
+
+namespace bsvd {
+namespace reg16c {
+
+using namespace ring16;
+
+struct __align__(16) QSmem {  // one problem (quarter-warp)
+    float2 pub[H];            // this iteration's rotations (cm1, c) by pair
+    float nrm[N];             // maintained squared column norms
+    float sig[N];             // finalisation: sigma by column
+    int rk[N];                // finalisation: rank by column
+};
+
+// Transposing xor butterfly over the 8 lanes of a quarter: lane ql ends with the quarter's total
+// of v[ql] (4 + 2 + 1 shuffles).
+__device__ __forceinline__ float reduce8q(const float (&v)[H], int ql) {
+    const bool b2 = ql & 4, b1 = ql & 2, b0 = ql & 1;
+    float a4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float keep = b2 ? v[i + 4] : v[i], send = b2 ? v[i] : v[i + 4];
+        a4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    float a2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float keep = b1 ? a4[i + 2] : a4[i], send = b1 ? a4[i] : a4[i + 2];
+        a2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    const float keep = b0 ? a2[1] : a2[0], send = b0 ? a2[0] : a2[1];
+    return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+}
+
+// any bit of a quarter set -> all 8 bits of that quarter (a problem's masks never depend on its neighbours)
+__device__ __forceinline__ uint32_t quarter_spread(uint32_t b) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r |= ((b >> (8 * q)) & 0xFFu) ? (0xFFu << (8 * q)) : 0u;
+    return r;
+}
+
+struct St {
+    int my_rot;
+    bool full;       // some lane of the warp takes fresh norms this iteration
+    uint32_t fmask;  // lanes whose problem takes them
+};
+
+template <int u, bool WANT_V>
+__device__ __forceinline__ void iter(float (&x0)[N], float (&x1)[N], float (&y0)[N], float (&y1)[N], QSmem& sm,
+                                     const uint32_t* ctab, int t, int lane, int ql, bool done, float tol2,
+                                     float tol, St& st) {
+    float v[H];
+#pragma unroll
+    for (int q = 0; q < H; ++q) v[q] = __fadd_rn(__fmul_rn(x0[BS(q, u)], x0[TS(q, u)]), __fmul_rn(x1[BS(q, u)], x1[TS(q, u)]));
+    const float g = reduce8q(v, ql);
+    const uint32_t code = ctab[t * H + ql];
+    const int ct = code & 0xff, cb = (code >> 8) & 0xff;
+    const bool flip = (code >> 16) != 0;
+    float gt = sm.nrm[ct], gb = sm.nrm[cb];
+    if (st.full) {
+        float a[H], b[H];
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            a[q] = __fadd_rn(__fmul_rn(x0[TS(q, u)], x0[TS(q, u)]), __fmul_rn(x1[TS(q, u)], x1[TS(q, u)]));
+            b[q] = __fadd_rn(__fmul_rn(x0[BS(q, u)], x0[BS(q, u)]), __fmul_rn(x1[BS(q, u)], x1[BS(q, u)]));
+        }
+        const float ft = reduce8q(a, ql), fb = reduce8q(b, ql);
+        if ((st.fmask >> lane) & 1u) {
+            gt = ft;
+            gb = fb;
+        }
+    }
+    const float absg = fabsf(g);
+    const bool rot = rot_guard(absg, gt, gb, tol2, tol) && !done && absg > 0.0f;
+    const float d = gt - gb;
+    float s, cm1, tabs;
+    rot_abs(fabsf(d), absg, s, cm1, tabs);
+    const bool eneg = d < 0.0f || (d == 0.0f && flip);  // sgn(0) = +1 in (i, j) orientation
+    const float c = rot ? xor_signf(s, (g < 0.0f) != eneg) : 0.0f;
+    cm1 = rot ? cm1 : 0.0f;
+    const float dtg = rot ? xor_signf(tabs * absg, eneg) : 0.0f;
+    const float nt = gt + dtg, nb = gb - dtg;
+    const bool shrink = rot && (nt < 0.25f * gt || nb < 0.25f * gb);
+    __syncwarp();  // every lane has read last iteration's pub[]
+    sm.pub[ql] = make_float2(cm1, c);
+    sm.nrm[ct] = nt;  // lane ql alone owns columns ct, cb of its problem this iteration
+    sm.nrm[cb] = nb;
+    st.my_rot += rot ? 1 : 0;
+    const unsigned mask = __ballot_sync(0xffffffffu, rot);
+    {
+        const uint32_t sb = __ballot_sync(0xffffffffu, shrink);
+        st.fmask = quarter_spread(sb);
+        st.full = sb != 0u;
+    }
+    __syncwarp();
+    if (mask) {
+        const float4* pp = reinterpret_cast<const float4*>(sm.pub);
+        float4 pr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pr[i] = pp[i];
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            const float pc = (q & 1) ? pr[q >> 1].z : pr[q >> 1].x;
+            const float pcc = (q & 1) ? pr[q >> 1].w : pr[q >> 1].y;
+            apply2(x0[TS(q, u)], x0[BS(q, u)], pc, pcc);
+            apply2(x1[TS(q, u)], x1[BS(q, u)], pc, pcc);
+            if (WANT_V) {
+                apply2(y0[TS(q, u)], y0[BS(q, u)], pc, pcc);
+                apply2(y1[TS(q, u)], y1[BS(q, u)], pc, pcc);
+            }
+        }
+    }
+}
+
+template <int NW, int MINB, bool WANT_V>
+__global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
+    __shared__ QSmem qsm[NW * 4];
+    __shared__ uint32_t ctab[NIT * H];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int qt = lane >> 3, ql = lane & 7;
+    for (int e = threadIdx.x; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
+    __syncthreads();
+    QSmem& sm = qsm[warp * 4 + qt];
+    const int prob = (blockIdx.x * NW + warp) * 4 + qt;
+    const bool live = prob < a.batch;
+    float x0[N], x1[N], y0[N], y1[N];
+    int bad = 0;
+    float amax = 0.0f;
+    {
+        const float* Ap = a.A + (size_t)(live ? prob : 0) * a.strideA;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            x0[c] = live ? Ap[ql + (size_t)c * a.lda] : 0.0f;
+            x1[c] = live ? Ap[ql + 8 + (size_t)c * a.lda] : 0.0f;
+            bad |= !isfinite(x0[c]) || !isfinite(x1[c]);
+            amax = fmaxf(amax, fmaxf(fabsf(x0[c]), fabsf(x1[c])));
+        }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    int ex = ((__float_as_int(amax) >> 23) & 0xff) - 126;
+    if (!(amax > 0.0f) || !isfinite(amax)) ex = 0;
+    ex = max(-100, min(100, ex));
+    {
+        const float sc = pow2f(-ex);
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            x0[c] *= sc;
+            x1[c] *= sc;
+            y0[c] = (c == ql) ? 1.0f : 0.0f;
+            y1[c] = (c == ql + 8) ? 1.0f : 0.0f;
+        }
+    }
+    const float tol = (float)a.tol, tol2 = tol * tol;
+    int sweeps = 0, last = 0, done = live ? 0 : 1;
+    long long rot_total = 0;
+#pragma unroll 1
+    for (int sw = 0; sw < a.max_sweeps; ++sw) {
+        St st;
+        st.my_rot = 0;
+        st.full = true;
+        st.fmask = 0xffffffffu;
+#pragma unroll 1
+        for (int gi = 0; gi < 8; ++gi) {
+            iter<0, WANT_V>(x0, x1, y0, y1, sm, ctab, 2 * gi, lane, ql, done != 0, tol2, tol, st);
+            if (gi == 7) {
+                ring_shift<1>(x0);
+                ring_shift<1>(x1);
+                if (WANT_V) {
+                    ring_shift<1>(y0);
+                    ring_shift<1>(y1);
+                }
+                break;
+            }
+            iter<1, WANT_V>(x0, x1, y0, y1, sm, ctab, 2 * gi + 1, lane, ql, done != 0, tol2, tol, st);
+            ring_shift<2>(x0);
+            ring_shift<2>(x1);
+            if (WANT_V) {
+                ring_shift<2>(y0);
+                ring_shift<2>(y1);
+            }
+        }
+        int tot = st.my_rot;  // lane ql counts pair ql of its problem
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (!done) {
+            sweeps = sw + 1;
+            last = tot;
+            rot_total += tot;
+            if (tot == 0) done = 1;
+        }
+        if (__all_sync(0xffffffffu, done != 0)) break;
+    }
+    // ======== kernel (5) fused: sigma (float64 sums in finalize_block's order), order, U, V ========
+    float* wsW = a.work + (size_t)(live ? prob : 0) * a.work_stride;
+    float* wsV = wsW + N * N;
+    const float us = pow2f(ex);
+    bool fused;
+    {
+        double v[N];
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            const double w0 = (double)(x0[c] * us), w1 = (double)(x1[c] * us);
+            v[c] = w0 * w0 + w1 * w1;  // finalize_block's xor-8 level (its xor-16 level adds zero rows)
+        }
+        // transposing xor butterfly (4, 2, 1): lane ql ends with columns 2 ql and 2 ql + 1
+        const bool b2 = ql & 4, b1 = ql & 2, b0 = ql & 1;
+        double a8[8], a4[4], a2[2];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double keep = b2 ? v[i + 8] : v[i], send = b2 ? v[i] : v[i + 8];
+            a8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double keep = b1 ? a8[i + 4] : a8[i], send = b1 ? a8[i] : a8[i + 4];
+            a4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double keep = b0 ? a4[i + 2] : a4[i], send = b0 ? a4[i] : a4[i + 2];
+            a2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        }
+        const float sg0 = (float)__dsqrt_rn(a2[0]);  // sigma of columns 2 ql, 2 ql + 1, cast like the reference
+        const float sg1 = (float)__dsqrt_rn(a2[1]);
+        const bool hole = !((double)sg0 >= dtiny<float>()) || !((double)sg1 >= dtiny<float>());
+        const unsigned hm = __ballot_sync(0xffffffffu, hole);
+        fused = ((hm >> (8 * qt)) & 0xFFu) == 0u;
+        const int c0 = 2 * ql, c1 = 2 * ql + 1;
+        sm.sig[c0] = sg0;
+        sm.sig[c1] = sg1;
+        __syncwarp();
+        int r0 = 0, r1 = 0;  // stable descending ranks (finalize.cuh step 4)
+#pragma unroll
+        for (int c2 = 0; c2 < N; ++c2) {
+            const float s2 = sm.sig[c2];
+            r0 += sig_before(s2, sg0) || (c2 < c0 && sig_tie(s2, sg0));
+            r1 += sig_before(s2, sg1) || (c2 < c1 && sig_tie(s2, sg1));
+        }
+        sm.rk[c0] = r0;
+        sm.rk[c1] = r1;
+        __syncwarp();
+        if (live && fused) {
+            const FinalOut<float> o = final_out(a, prob);
+            o.S[r0] = sg0;
+            o.S[r1] = sg1;
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                const size_t col = (size_t)sm.rk[c] * o.ldu;
+                const float sc = sm.sig[c];
+                o.U[ql + col] = __fdiv_rn(x0[c] * us, sc);
+                o.U[ql + 8 + col] = __fdiv_rn(x1[c] * us, sc);
+            }
+            if (WANT_V && o.want_v && o.V) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    const size_t col = (size_t)sm.rk[c] * o.ldv;
+                    o.V[ql + col] = y0[c];
+                    o.V[ql + 8 + col] = y1[c];
+                }
+            }
+        }
+    }
+    const unsigned badm = __ballot_sync(0xffffffffu, bad != 0);
+    if (live) {
+        if (ql == 0) wsW[a.work_stride - 1] = fused ? 0.0f : 1.0f;  // flag for the standalone pass
+        if (!fused) {
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                wsW[ql + c * N] = x0[c] * us;
+                wsW[ql + 8 + c * N] = x1[c] * us;
+            }
+            if (WANT_V) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    wsV[ql + c * N] = y0[c];
+                    wsV[ql + 8 + c * N] = y1[c];
+                }
+            }
+        }
+        if (ql == 0 && a.info) {
+            bsvd_info inf;
+            inf.converged = done;
+            inf.outer_sweeps = sweeps;
+            inf.rotations = rot_total;
+            inf.gram_calls = 0;
+            inf.update_calls = 0;
+            inf.last_rotations = last;
+            inf.path = 1;
+            inf.status = ((badm >> (8 * qt)) & 0xFFu) ? 1 : 0;
+            inf.kernel = a.kernel;
+            a.info[prob] = inf;
+        }
+    }
+}
+
+// C2's 10,000 problems are 2,500 warps = 16.9 per SM: MINB keeps the register count at <= 112 so
+// that 18 warps fit an SM and the launch is one wave
+template <int NW, int MINB>
+void launch_nw(const SolveArgs<float>& a, cudaStream_t st) {
+    const int per_cta = 4 * NW;
+    const int grid = (a.batch + per_cta - 1) / per_cta;
+    if (a.need_v) k_reg16c<NW, MINB, true><<<grid, NW * 32, 0, st>>>(a);
+    else k_reg16c<NW, MINB, false><<<grid, NW * 32, 0, st>>>(a);
+}
+
+}  // namespace reg16c
+
+bool is_reg16c(int kernel) { return kernel >= KV_UNBLOCKED_REG16C && kernel <= KV_UNBLOCKED_REG16C_LAST; }
+
+Plan plan_unblocked_reg16c(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant) {
+    Plan p{};
+    if (dtype == BSVD_S && bn == 16 && bm == 16 && lda_ok) {
+        p.kernel = is_reg16c(variant) ? variant : KV_UNBLOCKED_REG16C;
+        p.threads = 64;
+        p.work_elems = (size_t)bm * 16 + (need_v ? 16 * 16 : 0) + 1;  // + the finalisation flag
+    }
+    return p;
+}
+
+int launch_unblocked_reg16c(SolveArgs<float> a, const Plan& p, cudaStream_t st) {
+    a.kernel = p.kernel;
+    a.work_stride = (int64_t)p.work_elems;
+    // CTA shape variants: 2 warps (8 problems, default), 1 warp, 4 warps
+    switch (p.kernel - KV_UNBLOCKED_REG16C) {
+        case 1: reg16c::launch_nw<1, 18>(a, st); break;
+        case 2: reg16c::launch_nw<4, 5>(a, st); break;
+        default: reg16c::launch_nw<2, 9>(a, st); break;
+    }
+    if (cudaPeekAtLastError() != cudaSuccess) return BSVD_ERR_CUDA;
+    return launch_finalize_flagged<float>(a, st);  // only problems the fused finalisation left over
+}
+
+}  // namespace bsvd

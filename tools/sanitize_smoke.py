@@ -30,6 +30,8 @@ run(np.float64, 32, 32, kernel=20)            # r32c
 run(np.float64, 32, 32, kernel=26)            # reg32e
 run(np.float32, 16, 16)                       # reg16b
 run(np.float32, 16, 16, kernel=11)            # reg16
+run(np.float32, 16, 16, kernel=34, B=9)       # reg16c (quarter-warp)
+run(np.float32, 16, 16, kernel=35, B=5, compute_right_vectors=False)
 run(np.float64, 64, 64)                       # blocked_reg
 run(np.float64, 128, 128, B=2)                # blocked_reg NWG 2
 run(np.complex128, 256, 32, B=2)              # creg32 SP
