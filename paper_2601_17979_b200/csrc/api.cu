@@ -177,6 +177,7 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
             return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG16C:
         case KV_UNBLOCKED_REG16C + 1:
+        case KV_UNBLOCKED_REG16C + 2:
         case KV_UNBLOCKED_REG16C_LAST:
             if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16c(a, p, st);
             return BSVD_ERR_UNSUPPORTED;

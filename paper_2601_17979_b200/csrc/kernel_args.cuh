@@ -61,7 +61,7 @@ enum {
     KV_CREG32 = 32,             // complex FP64, n = 32, m <= 256: CTA per problem, rows in registers, V in smem
     KV_BLOCKED_REG_U4 = 33,     // KV_BLOCKED_REG with the ring unrolled by 4
     KV_UNBLOCKED_REG16C = 34,   // 16x16 FP32 third generation: 4 problems per warp, 2 rows per lane
-    KV_UNBLOCKED_REG16C_LAST = 36,  // 35, 36: CTA shape variants (1 / 4 warps)
+    KV_UNBLOCKED_REG16C_LAST = 37,  // 35, 36: ring unrolled by 3 / 5; 37: 2-warp CTAs
 };
 
 template <class T>

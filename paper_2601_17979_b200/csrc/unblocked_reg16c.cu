@@ -140,7 +140,26 @@ __device__ __forceinline__ void iter(float (&x0)[N], float (&x1)[N], float (&y0)
     }
 }
 
-template <int NW, int MINB, bool WANT_V>
+template <int SH, bool WANT_V>
+__device__ __forceinline__ void shift_all(float (&x0)[N], float (&x1)[N], float (&y0)[N], float (&y1)[N]) {
+    ring_shift<SH>(x0);
+    ring_shift<SH>(x1);
+    if (WANT_V) {
+        ring_shift<SH>(y0);
+        ring_shift<SH>(y1);
+    }
+}
+
+// iterations t0 + u .. t0 + U - 1 with compile-time register slots
+template <int U, int u, bool WANT_V>
+__device__ __forceinline__ void group(float (&x0)[N], float (&x1)[N], float (&y0)[N], float (&y1)[N], QSmem& sm,
+                                      const uint32_t* ctab, int t0, int lane, int ql, bool done, float tol2,
+                                      float tol, St& st) {
+    iter<u, WANT_V>(x0, x1, y0, y1, sm, ctab, t0 + u, lane, ql, done, tol2, tol, st);
+    if constexpr (u + 1 < U) group<U, u + 1, WANT_V>(x0, x1, y0, y1, sm, ctab, t0, lane, ql, done, tol2, tol, st);
+}
+
+template <int NW, int MINB, int U, bool WANT_V>
 __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
     __shared__ QSmem qsm[NW * 4];
     __shared__ uint32_t ctab[NIT * H];
@@ -188,24 +207,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
         st.my_rot = 0;
         st.full = true;
         st.fmask = 0xffffffffu;
+        if constexpr (U == 2) {
 #pragma unroll 1
-        for (int gi = 0; gi < 8; ++gi) {
-            iter<0, WANT_V>(x0, x1, y0, y1, sm, ctab, 2 * gi, lane, ql, done != 0, tol2, tol, st);
-            if (gi == 7) {
-                ring_shift<1>(x0);
-                ring_shift<1>(x1);
-                if (WANT_V) {
-                    ring_shift<1>(y0);
-                    ring_shift<1>(y1);
+            for (int gi = 0; gi < 8; ++gi) {
+                iter<0, WANT_V>(x0, x1, y0, y1, sm, ctab, 2 * gi, lane, ql, done != 0, tol2, tol, st);
+                if (gi == 7) {
+                    shift_all<1, WANT_V>(x0, x1, y0, y1);
+                    break;
                 }
-                break;
+                iter<1, WANT_V>(x0, x1, y0, y1, sm, ctab, 2 * gi + 1, lane, ql, done != 0, tol2, tol, st);
+                shift_all<2, WANT_V>(x0, x1, y0, y1);
             }
-            iter<1, WANT_V>(x0, x1, y0, y1, sm, ctab, 2 * gi + 1, lane, ql, done != 0, tol2, tol, st);
-            ring_shift<2>(x0);
-            ring_shift<2>(x1);
-            if (WANT_V) {
-                ring_shift<2>(y0);
-                ring_shift<2>(y1);
+        } else {  // U divides 15: the ring moves once per U iterations
+#pragma unroll 1
+            for (int gi = 0; gi < NIT / U; ++gi) {
+                group<U, 0, WANT_V>(x0, x1, y0, y1, sm, ctab, U * gi, lane, ql, done != 0, tol2, tol, st);
+                shift_all<U, WANT_V>(x0, x1, y0, y1);
             }
         }
         int tot = st.my_rot;  // lane ql counts pair ql of its problem
@@ -225,36 +242,38 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
     const float us = pow2f(ex);
     bool fused;
     {
-        double v[N];
-#pragma unroll
-        for (int c = 0; c < N; ++c) {
-            const double w0 = (double)(x0[c] * us), w1 = (double)(x1[c] * us);
-            v[c] = w0 * w0 + w1 * w1;  // finalize_block's xor-8 level (its xor-16 level adds zero rows)
-        }
-        // transposing xor butterfly (4, 2, 1): lane ql ends with columns 2 ql and 2 ql + 1
+        // per half of the columns: rows l, l + 8 pre-summed in-lane (finalize_block's xor-8 level; its
+        // xor-16 level adds zero rows), then a transposing xor butterfly (4, 2, 1) -> lane ql ends with
+        // columns ql and ql + 8 (eight doubles live at a time instead of sixteen: no spills at 96 registers)
         const bool b2 = ql & 4, b1 = ql & 2, b0 = ql & 1;
-        double a8[8], a4[4], a2[2];
+        double colsum[2];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const double keep = b2 ? v[i + 8] : v[i], send = b2 ? v[i] : v[i + 8];
-            a8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-        }
+        for (int h = 0; h < 2; ++h) {
+            double v[8], a4[4], a2[2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const double keep = b1 ? a8[i + 4] : a8[i], send = b1 ? a8[i] : a8[i + 4];
-            a4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-        }
+            for (int i = 0; i < 8; ++i) {
+                const double w0 = (double)(x0[8 * h + i] * us), w1 = (double)(x1[8 * h + i] * us);
+                v[i] = w0 * w0 + w1 * w1;
+            }
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const double keep = b0 ? a4[i + 2] : a4[i], send = b0 ? a4[i] : a4[i + 2];
-            a2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            for (int i = 0; i < 4; ++i) {
+                const double keep = b2 ? v[i + 4] : v[i], send = b2 ? v[i] : v[i + 4];
+                a4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const double keep = b1 ? a4[i + 2] : a4[i], send = b1 ? a4[i] : a4[i + 2];
+                a2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
+            const double keep = b0 ? a2[1] : a2[0], send = b0 ? a2[0] : a2[1];
+            colsum[h] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
         }
-        const float sg0 = (float)__dsqrt_rn(a2[0]);  // sigma of columns 2 ql, 2 ql + 1, cast like the reference
-        const float sg1 = (float)__dsqrt_rn(a2[1]);
+        const float sg0 = (float)__dsqrt_rn(colsum[0]);  // sigma of columns ql, ql + 8, cast like the reference
+        const float sg1 = (float)__dsqrt_rn(colsum[1]);
         const bool hole = !((double)sg0 >= dtiny<float>()) || !((double)sg1 >= dtiny<float>());
         const unsigned hm = __ballot_sync(0xffffffffu, hole);
         fused = ((hm >> (8 * qt)) & 0xFFu) == 0u;
-        const int c0 = 2 * ql, c1 = 2 * ql + 1;
+        const int c0 = ql, c1 = ql + 8;
         sm.sig[c0] = sg0;
         sm.sig[c1] = sg1;
         __syncwarp();
@@ -324,12 +343,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
 
 // C2's 10,000 problems are 2,500 warps = 16.9 per SM: MINB keeps the register count at <= 112 so
 // that 18 warps fit an SM and the launch is one wave
-template <int NW, int MINB>
+template <int NW, int MINB, int U>
 void launch_nw(const SolveArgs<float>& a, cudaStream_t st) {
     const int per_cta = 4 * NW;
     const int grid = (a.batch + per_cta - 1) / per_cta;
-    if (a.need_v) k_reg16c<NW, MINB, true><<<grid, NW * 32, 0, st>>>(a);
-    else k_reg16c<NW, MINB, false><<<grid, NW * 32, 0, st>>>(a);
+    if (a.need_v) k_reg16c<NW, MINB, U, true><<<grid, NW * 32, 0, st>>>(a);
+    else k_reg16c<NW, MINB, U, false><<<grid, NW * 32, 0, st>>>(a);
 }
 
 }  // namespace reg16c
@@ -340,7 +359,7 @@ Plan plan_unblocked_reg16c(int dtype, int bm, int bn, int need_v, bool lda_ok, i
     Plan p{};
     if (dtype == BSVD_S && bn == 16 && bm == 16 && lda_ok) {
         p.kernel = is_reg16c(variant) ? variant : KV_UNBLOCKED_REG16C;
-        p.threads = 64;
+        p.threads = 32;
         p.work_elems = (size_t)bm * 16 + (need_v ? 16 * 16 : 0) + 1;  // + the finalisation flag
     }
     return p;
@@ -349,11 +368,13 @@ Plan plan_unblocked_reg16c(int dtype, int bm, int bn, int need_v, bool lda_ok, i
 int launch_unblocked_reg16c(SolveArgs<float> a, const Plan& p, cudaStream_t st) {
     a.kernel = p.kernel;
     a.work_stride = (int64_t)p.work_elems;
-    // CTA shape variants: 2 warps (8 problems, default), 1 warp, 4 warps
+    // default: one-warp CTAs, ring unrolled by 2.  Variants (measured slower, tools/c2_cross.py): ring
+    // unrolled by 3 / 5 (fewer register moves, but longer bodies spill at the 96-register cap), 2-warp CTAs
     switch (p.kernel - KV_UNBLOCKED_REG16C) {
-        case 1: reg16c::launch_nw<1, 18>(a, st); break;
-        case 2: reg16c::launch_nw<4, 5>(a, st); break;
-        default: reg16c::launch_nw<2, 9>(a, st); break;
+        case 1: reg16c::launch_nw<2, 9, 3>(a, st); break;
+        case 2: reg16c::launch_nw<2, 9, 5>(a, st); break;
+        case 3: reg16c::launch_nw<2, 9, 2>(a, st); break;
+        default: reg16c::launch_nw<1, 18, 2>(a, st); break;
     }
     if (cudaPeekAtLastError() != cudaSuccess) return BSVD_ERR_CUDA;
     return launch_finalize_flagged<float>(a, st);  // only problems the fused finalisation left over
