@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import paper_2601_17979_b200 as bs
-from common import ALL_DTYPES, Opts, check_factors, check_sigma_parity, random_matrix, unit_roundoff
+from common import ALL_DTYPES, Opts, check_factors, check_sigma_parity, e2, random_matrix, unit_roundoff
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -592,6 +592,54 @@ def test_32x32_exactly_rank_deficient(dt, kernel):
             # follows it, only sigma is comparable
             continue
         check_factors(A[b], U[b], S[b], V[b])
+
+
+def _rank_deficient_mn(m, n, dt):
+    """m x n versions of _exactly_rank_deficient (complex dtypes get a complex phase pattern)."""
+    rng = np.random.default_rng(92)
+    out = [np.ones((m, n)), np.outer(np.arange(1, m + 1), np.arange(1, n + 1)), np.zeros((m, n))]
+    out[2][3, 5] = 7.0
+    d = rng.standard_normal((m, n))
+    d[:, 1::2] = d[:, 0::2][:, : d[:, 1::2].shape[1]]
+    out.append(d)
+    out.append(rng.standard_normal((m, 3)) @ rng.standard_normal((3, n)))
+    out.append(np.ones((m, n)) * 1e-20)
+    A = np.stack(out)
+    if np.dtype(dt).kind == "c":
+        A = A * np.exp(1j * np.outer(np.arange(m), np.arange(n)) * 0.37)[None]
+    return A.astype(dt)
+
+
+@pytest.mark.parametrize("dt,m,n,qr", [(np.float64, 64, 64, False), (np.float64, 128, 128, False),
+                                       (np.complex128, 256, 32, False), (np.complex128, 256, 32, True),
+                                       (np.float64, 96, 20, True), (np.complex64, 40, 24, False),
+                                       (np.float32, 48, 48, False), (np.complex128, 64, 32, False)])
+def test_exactly_rank_deficient_every_route(dt, m, n, qr):
+    """Exactly rank-deficient inputs through the blocked register, complex register, QR and general
+    kernels: finite factors, sigma vs the oracle, e1-e3 (single precision at 1e-20 scale excepted: the
+    reference's unscaled dots underflow there and the general kernels follow it)."""
+    import torch
+
+    A = _rank_deficient_mn(m, n, dt)
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, m, n, bs.JacobiOptions(use_qr_preprocess=qr))
+    torch.cuda.synchronize()
+    U, S, V = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy(), np.swapaxes(r.v.cpu().numpy(), 1, 2)
+    assert np.isfinite(U).all() and np.isfinite(S).all() and np.isfinite(V).all()
+    single = unit_roundoff(dt) > 1e-10
+    for b in range(A.shape[0]):
+        if single and b == 5:
+            continue  # the reference's own sigma is off by its underflowed dots here
+        o = Opts()
+        o.use_qr_preprocess = qr
+        u_ref, s_ref, _, oi = O.solve(A[b], o, None)
+        check_sigma_parity(S[b], s_ref, max(m, n), unit_roundoff(dt))
+        if oi["converged"]:
+            check_factors(A[b], U[b], S[b], V[b])
+        else:
+            # the reference itself stops at the sweep cap with rotating noise columns (outer product,
+            # all-ones): its U is not orthonormal either; ours must be no worse than ~its own
+            assert e2(U[b]) <= max(30 * unit_roundoff(dt), 4 * e2(u_ref))
 
 
 @pytest.mark.gpu
