@@ -131,11 +131,20 @@ __device__ __forceinline__ void cparams_core(double dabs, double pr, double pi, 
     cm1 = -(q2 * kk * kk) * rcp_cubic(1.0 + c);
     dn = q2 * kk * ic;
 }
-__device__ __forceinline__ void cparams(double dabs, double pr, double pi, double& cm1, double& kk, double& dn) {
+// -> cm1, (ar, ai) = kk p (the rotation's off-diagonal before its sign), dn
+__device__ __forceinline__ void cparams(double dabs, double pr, double pi, double& cm1, double& ar, double& ai,
+                                       double& dn) {
+    double kk;
     cparams_core(dabs, pr, pi, cm1, kk, dn);
+    ar = kk * pr;
+    ai = kk * pi;
     if (fmax(dabs, fmax(fabs(pr), fabs(pi))) < 0x1p-500) {  // exact power-of-two rescale of tiny inputs
-        cparams_core(dabs * 0x1p+600, pr * 0x1p+600, pi * 0x1p+600, cm1, kk, dn);
-        kk *= 0x1p+600;
+        // kk p = kk' (2^600 p) with kk' of the rescaled inputs: kk itself (~1/|p|) overflows for
+        // subnormal p (columns graded over more than the exponent range), 2^600 p does not
+        const double sr = pr * 0x1p+600, si = pi * 0x1p+600;
+        cparams_core(dabs * 0x1p+600, sr, si, cm1, kk, dn);
+        ar = kk * sr;
+        ai = kk * si;
         dn *= 0x1p-600;
     }
 }
@@ -221,14 +230,13 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
     }
     rot = rot && pm > 0.0;
     const double d = gt - gb;
-    double cm1, kk, dn;
-    cparams(fabs(d), pr, pi, cm1, kk, dn);
+    double cm1, ar, ai, dn;
+    cparams(fabs(d), pr, pi, cm1, ar, ai, dn);
     const bool eneg = d < 0.0 || (d == 0.0 && flip);
-    const double ks = eneg ? -kk : kk;
     Par par;
     par.cm1 = rot ? cm1 : 0.0;
-    par.ar = rot ? ks * pr : 0.0;
-    par.ai = rot ? ks * pi : 0.0;
+    par.ar = rot ? (eneg ? -ar : ar) : 0.0;
+    par.ai = rot ? (eneg ? -ai : ai) : 0.0;
     par.pad = 0.0;
     const double dtg = rot ? (eneg ? -dn : dn) : 0.0;
     const double nt = gt + dtg, nb = gb - dtg;

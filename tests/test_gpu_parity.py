@@ -642,6 +642,73 @@ def test_exactly_rank_deficient_every_route(dt, m, n, qr):
             assert e2(U[b]) <= max(30 * unit_roundoff(dt), 4 * e2(u_ref))
 
 
+_SCALE_CASES = [(np.float64, 32, 32, 0, False), (np.float64, 32, 32, 12, False), (np.float32, 16, 16, 0, False),
+                (np.float32, 16, 16, 34, False), (np.float64, 64, 64, 0, False), (np.complex128, 256, 32, 0, False),
+                (np.complex128, 40, 24, 0, False), (np.float32, 48, 48, 0, False), (np.float64, 96, 20, 0, True),
+                (np.complex128, 256, 32, 0, True), (np.float64, 128, 128, 0, False)]
+
+
+@pytest.mark.parametrize("dt,m,n,kernel,qr", _SCALE_CASES)
+def test_extreme_scales_and_graded_columns(dt, m, n, kernel, qr):
+    """Uniform scalings across the range where the reference's guard product g_ii g_jj neither overflows
+    nor underflows (FP64 1e+-60, FP32 1e+-6; beyond it the reference itself stops after one sweep with
+    O(1) errors or never converges, oracle-checked), columns and rows graded over 1e+-30 / 1e+-3:
+    sigma vs the oracle, factors, every default kernel and route."""
+    import torch
+
+    single = unit_roundoff(dt) > 1e-10
+    e = 6 if single else 60
+    g = 3 if single else 30
+    base = [random_matrix(m, n, dt, seed=9100 + i) for i in range(4)]
+    A = [base[0] * 10.0 ** -e, base[1] * 10.0 ** e, base[2] * 10.0 ** (-e // 3),
+         base[3] * np.geomspace(10.0 ** -g, 10.0 ** g, n)[None, :],
+         base[0] * np.geomspace(10.0 ** g, 10.0 ** -g, m)[:, None]]
+    A = np.stack([x.astype(dt) for x in A])
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, m, n, bs.JacobiOptions(use_qr_preprocess=qr), kernel=kernel)
+    torch.cuda.synchronize()
+    U, S, V = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy(), np.swapaxes(r.v.cpu().numpy(), 1, 2)
+    assert np.isfinite(U).all() and np.isfinite(S).all() and np.isfinite(V).all()
+    for b in range(A.shape[0]):
+        o = Opts()
+        o.use_qr_preprocess = qr
+        u_ref, s_ref, _, oi = O.solve(A[b], o, None)
+        check_sigma_parity(S[b], s_ref, max(m, n), unit_roundoff(dt))
+        if oi["converged"]:
+            check_factors(A[b], U[b], S[b], V[b], e3_k=100.0)
+        else:
+            assert e2(U[b]) <= max(30 * unit_roundoff(dt), 4 * e2(u_ref))
+
+
+@pytest.mark.parametrize("dt,m,n,kernel", [(np.float64, 32, 32, 0), (np.float64, 32, 32, 12),
+                                           (np.float32, 16, 16, 0), (np.float32, 16, 16, 34),
+                                           (np.float64, 64, 64, 0), (np.float64, 128, 128, 0),
+                                           (np.complex128, 256, 32, 0), (np.complex128, 64, 32, 0)])
+def test_register_kernels_beyond_reference_range(dt, m, n, kernel):
+    """The register kernels scale each problem by a power of two at load, so uniform scalings of 1e+-150
+    (FP64) / 1e+-15 (FP32), where the reference's guard product over/underflows, solve normally; columns
+    or rows graded over 1e+-100 / 1e+-8 keep finite factors and accurate sigma (vs float64 LAPACK) even
+    where the smallest columns' squares leave the exponent range."""
+    import torch
+
+    single = unit_roundoff(dt) > 1e-10
+    e, g = (15, 8) if single else (150, 100)
+    base = [random_matrix(m, n, dt, seed=9100 + i) for i in range(4)]
+    A = [base[0] * 10.0 ** -e, base[1] * 10.0 ** e, base[3] * np.geomspace(10.0 ** -g, 10.0 ** g, n)[None, :],
+         base[0] * np.geomspace(10.0 ** g, 10.0 ** -g, m)[:, None]]
+    A = np.stack([x.astype(dt) for x in A])
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, m, n, bs.JacobiOptions(), kernel=kernel)
+    torch.cuda.synchronize()
+    U, S, V = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy(), np.swapaxes(r.v.cpu().numpy(), 1, 2)
+    assert np.isfinite(U).all() and np.isfinite(S).all() and np.isfinite(V).all()
+    for b in range(A.shape[0]):
+        st = np.linalg.svd(A[b].astype(np.complex128 if np.iscomplexobj(A[b]) else np.float64), compute_uv=False)
+        check_sigma_parity(S[b], st, max(m, n), unit_roundoff(dt))
+        if b < 2:
+            check_factors(A[b], U[b], S[b], V[b])
+
+
 @pytest.mark.gpu
 def test_c2_batch_size_kernel_choice_is_bitwise_invisible():
     """From 3,500 16x16 FP32 problems on the quarter-warp kernel (34) runs, below it the half-warp
