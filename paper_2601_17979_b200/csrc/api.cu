@@ -1,5 +1,6 @@
 // api.cu -- the C-ABI (include/bsvd_b200.h): argument checks, route
 // selection (src/svd.py:375-381 dispatch), kernel planning and launch.
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <string.h>
 
@@ -380,6 +381,13 @@ int bsvd_select_kernel(int dtype, int m, int n, const bsvd_opts* opts) {
 }
 
 namespace {
+bool host_direct_enabled() {
+    static const int v = [] {
+        const char* e = getenv("BSVD_HOST_DIRECT");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return v != 0;
+}
 // Staging layout of one pipeline slot (device): A | U | V | S | info | solver workspace.
 struct HostSlot {
     size_t a, u, v, s, info, ws, total;
@@ -419,6 +427,33 @@ int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch, const void* A, v
     if (hs.total * (size_t)nstreams > work_bytes || !work) return BSVD_ERR_WORKSPACE;
     const size_t es = (size_t)esize_of(dtype), rs = (size_t)rsize_of(dtype);
     cudaStream_t s0 = static_cast<cudaStream_t>(streams[0]);
+    // Direct mode (opt-in, BSVD_HOST_DIRECT=1): when every output buffer is page-locked host memory mapped
+    // into the device address space, the kernels write U, S, V and info straight into it over PCIe
+    // instead of staging them for per-chunk D2H copies.  Measured on B200 (bench.py e2e): C2 +6 %
+    // (15.1 vs 14.2 M/s), but C1-10k -15 % (2.04 vs 2.39 M/s) and C4 -20 %: the kernels' column-wise
+    // 128-256 B stores over PCIe stall them and move fewer bytes per second than the copy engines.
+    unsigned char *Uh = static_cast<unsigned char*>(U), *Sh = static_cast<unsigned char*>(S),
+                  *Vh = static_cast<unsigned char*>(V);
+    bsvd_info* Ih = info;
+    bool direct = host_direct_enabled();
+    if (direct) {
+        auto mapped = [](void* p, unsigned char** dev) {
+            if (!p) return true;
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            if (at.type != cudaMemoryTypeHost || !at.devicePointer) return false;
+            *dev = static_cast<unsigned char*>(at.devicePointer);
+            return true;
+        };
+        unsigned char* ih = reinterpret_cast<unsigned char*>(info);
+        direct = mapped(U, &Uh) && mapped(S, &Sh) && (!opts->want_v || mapped(V, &Vh)) && mapped(info, &ih);
+        Ih = reinterpret_cast<bsvd_info*>(ih);
+        if (!direct) Uh = static_cast<unsigned char*>(U), Sh = static_cast<unsigned char*>(S),
+                     Vh = static_cast<unsigned char*>(V), Ih = info;
+    }
     // fork: every stream starts after the work already queued on streams[0]
     cudaEvent_t fork = nullptr;
     cudaEvent_t* joins = new cudaEvent_t[nstreams]();
@@ -443,6 +478,14 @@ int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch, const void* A, v
         const size_t abytes = (size_t)cb * m * n * es;
         if (abytes && cudaMemcpyAsync(Ad, static_cast<const unsigned char*>(A) + (size_t)b0 * m * n * es, abytes,
                                       cudaMemcpyHostToDevice, st) != cudaSuccess) { rc = BSVD_ERR_CUDA; break; }
+        if (direct) {  // outputs land in host memory from the kernels; no copies back
+            rc = bsvd_gesvj_batched(dtype, m, n, cb, Ad, m > 0 ? m : 1, (int64_t)m * n, Uh + (size_t)b0 * m * k * es,
+                                    m > 0 ? m : 1, (int64_t)m * k, Sh + (size_t)b0 * k * rs, k,
+                                    opts->want_v ? Vh + (size_t)b0 * n * k * es : nullptr, n > 0 ? n : 1,
+                                    (int64_t)n * k, opts, Ih ? Ih + b0 : Id, Wd, hs.ws, st);
+            if (rc) break;
+            continue;
+        }
         rc = bsvd_gesvj_batched(dtype, m, n, cb, Ad, m > 0 ? m : 1, (int64_t)m * n, Ud, m > 0 ? m : 1,
                                 (int64_t)m * k, Sd, k, Vd, n > 0 ? n : 1, (int64_t)n * k, opts, Id, Wd, hs.ws, st);
         if (rc) break;

@@ -374,6 +374,45 @@ def test_host_pipeline_matches_device_path(dt, m, n, want_v):
 
 
 @pytest.mark.gpu
+def test_host_pipeline_direct_mode_matches_device_path():
+    """BSVD_HOST_DIRECT=1 (kernels write U, S, V, info straight into mapped pinned host memory): same bits
+    as the device call, for the register, blocked, complex, wide and QR routes (fresh process: the switch
+    is read once)."""
+    import subprocess
+    import sys
+
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
+import paper_2601_17979_b200 as bs
+from common import random_matrix
+from paper_2601_17979_b200.solver import solve_host_buffers, solve_tensor, torch_dtype
+for dt, m, n, qr in ((np.float64, 32, 32, False), (np.float32, 16, 16, False), (np.float64, 64, 64, False),
+                     (np.complex128, 256, 32, False), (np.float64, 12, 20, False), (np.float64, 96, 20, True)):
+    B = 23
+    A = np.stack([random_matrix(m, n, dt, seed=950 + b) for b in range(B)])
+    opts = bs.JacobiOptions(use_qr_preprocess=qr)
+    ref = solve_tensor(torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda(), m, n, opts)
+    torch.cuda.synchronize()
+    k = min(m, n); tdt = torch_dtype(dt)
+    a_h = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).pin_memory()
+    u_h = torch.empty((B, k, m), dtype=tdt).pin_memory(); s_h = torch.empty((B, k), dtype=ref.s.dtype).pin_memory()
+    v_h = torch.empty((B, k, n), dtype=tdt).pin_memory(); i_h = torch.empty((B * 48,), dtype=torch.uint8).pin_memory()
+    solve_host_buffers(a_h, u_h, s_h, v_h, i_h, m, n, opts, chunk=4)
+    torch.cuda.synchronize()
+    assert torch.equal(u_h, ref.u.cpu()) and torch.equal(s_h, ref.s.cpu()) and torch.equal(v_h, ref.v.cpu())
+    assert torch.equal(i_h, ref.info.cpu()), (dt, m, n)
+print("direct ok")
+"""
+    import os
+
+    env = dict(os.environ, BSVD_HOST_DIRECT="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "direct ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("kernel", [0, 17, 19, 20, 26])
 def test_problem_results_independent_of_warp_partner(kernel):
     """Two problems share a warp in the 32x32 register kernels; a problem's bits must not depend on its
