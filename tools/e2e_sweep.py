@@ -23,8 +23,10 @@ v_h = torch.empty((B, 32, 32), dtype=torch.float64, pin_memory=True)
 i_h = torch.empty((B * 48,), dtype=torch.uint8, pin_memory=True)
 opts = bs.JacobiOptions()
 dev = torch.device("cuda", 0)
-for nst in (2, 3, 4, 6):
-    for div in (4, 8, 16, 32):
+NST = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "2,3,4,6").split(",")]
+DIV = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "4,8,16,32").split(",")]
+for nst in NST:
+    for div in DIV:
         streams = [torch.cuda.current_stream()] + [torch.cuda.Stream(dev) for _ in range(nst - 1)]
         chunk = -(-B // div)
         ts = []
@@ -56,3 +58,16 @@ for _ in range(2):
     e1.record()
     torch.cuda.synchronize()
 print(f"H2D 82 MB: {e0.elapsed_time(e1):.2f} ms")
+s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+for _ in range(2):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    s1.wait_stream(torch.cuda.current_stream()); s2.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s1):
+        xh.copy_(x, non_blocking=True)
+    with torch.cuda.stream(s2):
+        y.copy_(yh, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s1); torch.cuda.current_stream().wait_stream(s2)
+    e1.record()
+    torch.cuda.synchronize()
+print(f"D2H 167 MB + H2D 82 MB concurrently: {e0.elapsed_time(e1):.2f} ms")
