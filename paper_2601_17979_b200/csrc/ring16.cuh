@@ -30,10 +30,10 @@ __host__ __device__ inline uint32_t pair_code(int t, int k) {
 }
 
 // ring move by SH positions; 15 = 3 x 5 is not prime, so follow every cycle of the permutation
-template <int SH>
-__device__ __forceinline__ void ring_shift(float (&x)[N]) {
+template <int SH, typename T>
+__device__ __forceinline__ void ring_shift(T (&x)[N]) {
     if constexpr (md(SH) != 0) {
-        float y[NIT];
+        T y[NIT];
 #pragma unroll
         for (int q = 0; q < NIT; ++q) y[q] = x[ring_slot(q)];
 #pragma unroll
@@ -64,25 +64,27 @@ __device__ __forceinline__ void rot_abs_core(float dabs, float g, float& s, floa
 }
 // |d|, |g| < 2^-50: the float32 squares of the chain above underflow (exactly rank-deficient inputs
 // leave rounding-noise columns that keep rotating among themselves and shrink towards the subnormal
-// range), so these parameters are formed in float64, as the reference forms all of them (F6)
+// range).  The parameters are ratios, so (|d|, g) are first normalised by an exact power of two taken
+// through float64 (2^-e itself overflows float32 for subnormal inputs) -- no IEEE division / square
+// root, whose slow paths would cost registers in the hot loop.
 __device__ __forceinline__ void rot_abs_tiny(float dabs, float g, float& s, float& cm1, float& tabs) {
-    const double dd = dabs, gd = g;
-    const double r = sqrt(fma(4.0 * gd, gd, dd * dd));
-    const double c = sqrt(0.5 + 0.5 * (dd / r));
-    const double sd = (gd / r) / c;
-    s = (float)sd;
-    cm1 = (float)(-(sd * sd) / (1.0 + c));
-    tabs = (float)(sd / c);
+    const double mx = (double)fmaxf(dabs, g);
+    const int e = (int)((__double_as_longlong(mx) >> 52) & 0x7ff) - 1023;
+    const double sc = __longlong_as_double((long long)(1023 - max(-1000, min(1000, e))) << 52);
+    rot_abs_core((float)((double)dabs * sc), (float)((double)g * sc), s, cm1, tabs);
 }
 __device__ __forceinline__ void rot_abs(float dabs, float g, float& s, float& cm1, float& tabs) {
     rot_abs_core(dabs, g, s, cm1, tabs);
     if (fmaxf(dabs, g) < 0x1p-50f) rot_abs_tiny(dabs, g, s, cm1, tabs);
 }
-// rotate iff |g| >= tol sqrt(g_ii g_jj) (src/_kernels_numba.py guard, F4): squared in float32, with the
-// exact form in float64 for |g| < 2^-60 where the float32 squares and products underflow
+// rotate iff |g| >= tol sqrt(g_ii g_jj) (src/_kernels_numba.py guard, F4): squared in float32, and
+// squared in float64 for |g| < 2^-60 where the float32 squares and products underflow
 __device__ __forceinline__ bool rot_guard(float absg, float gt, float gb, float tol2, float tol) {
     bool rot = !(absg * absg < tol2 * (gt * gb));
-    if (absg < 0x1p-60f && absg > 0.0f) rot = !((double)absg < (double)tol * sqrt((double)gt * (double)gb));
+    if (absg < 0x1p-60f && absg > 0.0f) {
+        const double ag = absg, td = tol;
+        rot = !(ag * ag < (td * td) * ((double)gt * (double)gb));
+    }
     return rot;
 }
 __device__ __forceinline__ float xor_signf(float x, bool neg) {

@@ -37,6 +37,7 @@ struct __align__(16) QSmem {  // one problem (quarter-warp)
     float nrm[N];             // maintained squared column norms
     float sig[N];             // finalisation: sigma by column
     int rk[N];                // finalisation: rank by column
+    int ex, bad, sweeps, last, rot;  // per-problem bookkeeping, kept here to free registers for the rows
 };
 
 // Transposing xor butterfly over the 8 lanes of a quarter: lane ql ends with the quarter's total
@@ -67,6 +68,16 @@ __device__ __forceinline__ uint32_t quarter_spread(uint32_t b) {
     return r;
 }
 
+// the two-FMA update (ring16::apply2) on rows l and l + 8 at once: packed FP32 FMAs (FFMA2, one issue
+// slot for two FMAs, the coefficient broadcast from one register); per half identical to apply2
+__device__ __forceinline__ void apply2x2(float2& x, float2& y, float cm1, float c) {
+    const float2 cc = make_float2(c, c), nc = make_float2(-c, -c), mm = make_float2(cm1, cm1);
+    const float2 tx = __ffma2_rn(cc, y, x);
+    const float2 ty = __ffma2_rn(nc, x, y);
+    x = __ffma2_rn(mm, x, tx);
+    y = __ffma2_rn(mm, y, ty);
+}
+
 struct St {
     int my_rot;
     bool full;       // some lane of the warp takes fresh norms this iteration
@@ -74,25 +85,34 @@ struct St {
 };
 
 template <int u, bool WANT_V>
-__device__ __forceinline__ void iter(float (&x0)[N], float (&x1)[N], float (&y0)[N], float (&y1)[N], QSmem& sm,
+__device__ __forceinline__ void iter(float2 (&X)[N], float2 (&Y)[N], QSmem& sm,
                                      const uint32_t* ctab, int t, int lane, int ql, bool done, float tol2,
                                      float tol, St& st) {
     float v[H];
 #pragma unroll
-    for (int q = 0; q < H; ++q) v[q] = __fadd_rn(__fmul_rn(x0[BS(q, u)], x0[TS(q, u)]), __fmul_rn(x1[BS(q, u)], x1[TS(q, u)]));
+    for (int q = 0; q < H; ++q) {
+        const float2 pr = __fmul2_rn(X[BS(q, u)], X[TS(q, u)]);
+        v[q] = __fadd_rn(pr.x, pr.y);
+    }
     const float g = reduce8q(v, ql);
     const uint32_t code = ctab[t * H + ql];
     const int ct = code & 0xff, cb = (code >> 8) & 0xff;
     const bool flip = (code >> 16) != 0;
     float gt = sm.nrm[ct], gb = sm.nrm[cb];
     if (st.full) {
-        float a[H], b[H];
+        float a[H];  // one set of partials at a time
 #pragma unroll
         for (int q = 0; q < H; ++q) {
-            a[q] = __fadd_rn(__fmul_rn(x0[TS(q, u)], x0[TS(q, u)]), __fmul_rn(x1[TS(q, u)], x1[TS(q, u)]));
-            b[q] = __fadd_rn(__fmul_rn(x0[BS(q, u)], x0[BS(q, u)]), __fmul_rn(x1[BS(q, u)], x1[BS(q, u)]));
+            const float2 pa = __fmul2_rn(X[TS(q, u)], X[TS(q, u)]);
+            a[q] = __fadd_rn(pa.x, pa.y);
         }
-        const float ft = reduce8q(a, ql), fb = reduce8q(b, ql);
+        const float ft = reduce8q(a, ql);
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            const float2 pb = __fmul2_rn(X[BS(q, u)], X[BS(q, u)]);
+            a[q] = __fadd_rn(pb.x, pb.y);
+        }
+        const float fb = reduce8q(a, ql);
         if ((st.fmask >> lane) & 1u) {
             gt = ft;
             gb = fb;
@@ -122,41 +142,32 @@ __device__ __forceinline__ void iter(float (&x0)[N], float (&x1)[N], float (&y0)
     }
     __syncwarp();
     if (mask) {
+        // two pairs' parameters per 16-byte load, fetched just before use (4 live registers, not 16)
         const float4* pp = reinterpret_cast<const float4*>(sm.pub);
-        float4 pr[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) pr[i] = pp[i];
-#pragma unroll
-        for (int q = 0; q < H; ++q) {
-            const float pc = (q & 1) ? pr[q >> 1].z : pr[q >> 1].x;
-            const float pcc = (q & 1) ? pr[q >> 1].w : pr[q >> 1].y;
-            apply2(x0[TS(q, u)], x0[BS(q, u)], pc, pcc);
-            apply2(x1[TS(q, u)], x1[BS(q, u)], pc, pcc);
-            if (WANT_V) {
-                apply2(y0[TS(q, u)], y0[BS(q, u)], pc, pcc);
-                apply2(y1[TS(q, u)], y1[BS(q, u)], pc, pcc);
-            }
+        for (int i = 0; i < 4; ++i) {
+            const float4 pr = pp[i];
+            apply2x2(X[TS(2 * i, u)], X[BS(2 * i, u)], pr.x, pr.y);
+            if (WANT_V) apply2x2(Y[TS(2 * i, u)], Y[BS(2 * i, u)], pr.x, pr.y);
+            apply2x2(X[TS(2 * i + 1, u)], X[BS(2 * i + 1, u)], pr.z, pr.w);
+            if (WANT_V) apply2x2(Y[TS(2 * i + 1, u)], Y[BS(2 * i + 1, u)], pr.z, pr.w);
         }
     }
 }
 
 template <int SH, bool WANT_V>
-__device__ __forceinline__ void shift_all(float (&x0)[N], float (&x1)[N], float (&y0)[N], float (&y1)[N]) {
-    ring_shift<SH>(x0);
-    ring_shift<SH>(x1);
-    if (WANT_V) {
-        ring_shift<SH>(y0);
-        ring_shift<SH>(y1);
-    }
+__device__ __forceinline__ void shift_all(float2 (&X)[N], float2 (&Y)[N]) {
+    ring_shift<SH>(X);
+    if (WANT_V) ring_shift<SH>(Y);
 }
 
 // iterations t0 + u .. t0 + U - 1 with compile-time register slots
 template <int U, int u, bool WANT_V>
-__device__ __forceinline__ void group(float (&x0)[N], float (&x1)[N], float (&y0)[N], float (&y1)[N], QSmem& sm,
+__device__ __forceinline__ void group(float2 (&X)[N], float2 (&Y)[N], QSmem& sm,
                                       const uint32_t* ctab, int t0, int lane, int ql, bool done, float tol2,
                                       float tol, St& st) {
-    iter<u, WANT_V>(x0, x1, y0, y1, sm, ctab, t0 + u, lane, ql, done, tol2, tol, st);
-    if constexpr (u + 1 < U) group<U, u + 1, WANT_V>(x0, x1, y0, y1, sm, ctab, t0, lane, ql, done, tol2, tol, st);
+    iter<u, WANT_V>(X, Y, sm, ctab, t0 + u, lane, ql, done, tol2, tol, st);
+    if constexpr (u + 1 < U) group<U, u + 1, WANT_V>(X, Y, sm, ctab, t0, lane, ql, done, tol2, tol, st);
 }
 
 template <int NW, int MINB, int U, bool WANT_V>
@@ -170,17 +181,17 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
     QSmem& sm = qsm[warp * 4 + qt];
     const int prob = (blockIdx.x * NW + warp) * 4 + qt;
     const bool live = prob < a.batch;
-    float x0[N], x1[N], y0[N], y1[N];
+    float2 X[N], Y[N];  // rows (l, l + 8) of W and V: packed pairs for the FFMA2 update
     int bad = 0;
     float amax = 0.0f;
     {
         const float* Ap = a.A + (size_t)(live ? prob : 0) * a.strideA;
 #pragma unroll
         for (int c = 0; c < N; ++c) {
-            x0[c] = live ? Ap[ql + (size_t)c * a.lda] : 0.0f;
-            x1[c] = live ? Ap[ql + 8 + (size_t)c * a.lda] : 0.0f;
-            bad |= !isfinite(x0[c]) || !isfinite(x1[c]);
-            amax = fmaxf(amax, fmaxf(fabsf(x0[c]), fabsf(x1[c])));
+            X[c].x = live ? Ap[ql + (size_t)c * a.lda] : 0.0f;
+            X[c].y = live ? Ap[ql + 8 + (size_t)c * a.lda] : 0.0f;
+            bad |= !isfinite(X[c].x) || !isfinite(X[c].y);
+            amax = fmaxf(amax, fmaxf(fabsf(X[c].x), fabsf(X[c].y)));
         }
     }
 #pragma unroll
@@ -189,18 +200,25 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
     if (!(amax > 0.0f) || !isfinite(amax)) ex = 0;
     ex = max(-100, min(100, ex));
     {
+        const unsigned bm = __ballot_sync(0xffffffffu, bad != 0);
+        if (ql == 0) {
+            sm.ex = ex;
+            sm.bad = ((bm >> (8 * qt)) & 0xFFu) ? 1 : 0;
+            sm.sweeps = 0;
+            sm.last = 0;
+            sm.rot = 0;
+        }
+    }
+    {
         const float sc = pow2f(-ex);
 #pragma unroll
         for (int c = 0; c < N; ++c) {
-            x0[c] *= sc;
-            x1[c] *= sc;
-            y0[c] = (c == ql) ? 1.0f : 0.0f;
-            y1[c] = (c == ql + 8) ? 1.0f : 0.0f;
+            X[c] = __fmul2_rn(X[c], make_float2(sc, sc));
+            Y[c] = make_float2((c == ql) ? 1.0f : 0.0f, (c == ql + 8) ? 1.0f : 0.0f);
         }
     }
     const float tol = (float)a.tol, tol2 = tol * tol;
-    int sweeps = 0, last = 0, done = live ? 0 : 1;
-    long long rot_total = 0;
+    int done = live ? 0 : 1;
 #pragma unroll 1
     for (int sw = 0; sw < a.max_sweeps; ++sw) {
         St st;
@@ -210,28 +228,30 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
         if constexpr (U == 2) {
 #pragma unroll 1
             for (int gi = 0; gi < 8; ++gi) {
-                iter<0, WANT_V>(x0, x1, y0, y1, sm, ctab, 2 * gi, lane, ql, done != 0, tol2, tol, st);
+                iter<0, WANT_V>(X, Y, sm, ctab, 2 * gi, lane, ql, done != 0, tol2, tol, st);
                 if (gi == 7) {
-                    shift_all<1, WANT_V>(x0, x1, y0, y1);
+                    shift_all<1, WANT_V>(X, Y);
                     break;
                 }
-                iter<1, WANT_V>(x0, x1, y0, y1, sm, ctab, 2 * gi + 1, lane, ql, done != 0, tol2, tol, st);
-                shift_all<2, WANT_V>(x0, x1, y0, y1);
+                iter<1, WANT_V>(X, Y, sm, ctab, 2 * gi + 1, lane, ql, done != 0, tol2, tol, st);
+                shift_all<2, WANT_V>(X, Y);
             }
         } else {  // U divides 15: the ring moves once per U iterations
 #pragma unroll 1
             for (int gi = 0; gi < NIT / U; ++gi) {
-                group<U, 0, WANT_V>(x0, x1, y0, y1, sm, ctab, U * gi, lane, ql, done != 0, tol2, tol, st);
-                shift_all<U, WANT_V>(x0, x1, y0, y1);
+                group<U, 0, WANT_V>(X, Y, sm, ctab, U * gi, lane, ql, done != 0, tol2, tol, st);
+                shift_all<U, WANT_V>(X, Y);
             }
         }
         int tot = st.my_rot;  // lane ql counts pair ql of its problem
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
         if (!done) {
-            sweeps = sw + 1;
-            last = tot;
-            rot_total += tot;
+            if (ql == 0) {
+                sm.sweeps = sw + 1;
+                sm.last = tot;
+                sm.rot += tot;
+            }
             if (tot == 0) done = 1;
         }
         if (__all_sync(0xffffffffu, done != 0)) break;
@@ -239,7 +259,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
     // ======== kernel (5) fused: sigma (float64 sums in finalize_block's order), order, U, V ========
     float* wsW = a.work + (size_t)(live ? prob : 0) * a.work_stride;
     float* wsV = wsW + N * N;
-    const float us = pow2f(ex);
+    __syncwarp();
+    const float us = pow2f(sm.ex);
     bool fused;
     {
         // per half of the columns: rows l, l + 8 pre-summed in-lane (finalize_block's xor-8 level; its
@@ -252,7 +273,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
             double v[8], a4[4], a2[2];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const double w0 = (double)(x0[8 * h + i] * us), w1 = (double)(x1[8 * h + i] * us);
+                const double w0 = (double)(X[8 * h + i].x * us), w1 = (double)(X[8 * h + i].y * us);
                 v[i] = w0 * w0 + w1 * w1;
             }
 #pragma unroll
@@ -295,46 +316,45 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
             for (int c = 0; c < N; ++c) {
                 const size_t col = (size_t)sm.rk[c] * o.ldu;
                 const float sc = sm.sig[c];
-                o.U[ql + col] = __fdiv_rn(x0[c] * us, sc);
-                o.U[ql + 8 + col] = __fdiv_rn(x1[c] * us, sc);
+                o.U[ql + col] = __fdiv_rn(X[c].x * us, sc);
+                o.U[ql + 8 + col] = __fdiv_rn(X[c].y * us, sc);
             }
             if (WANT_V && o.want_v && o.V) {
 #pragma unroll
                 for (int c = 0; c < N; ++c) {
                     const size_t col = (size_t)sm.rk[c] * o.ldv;
-                    o.V[ql + col] = y0[c];
-                    o.V[ql + 8 + col] = y1[c];
+                    o.V[ql + col] = Y[c].x;
+                    o.V[ql + 8 + col] = Y[c].y;
                 }
             }
         }
     }
-    const unsigned badm = __ballot_sync(0xffffffffu, bad != 0);
     if (live) {
         if (ql == 0) wsW[a.work_stride - 1] = fused ? 0.0f : 1.0f;  // flag for the standalone pass
         if (!fused) {
 #pragma unroll
             for (int c = 0; c < N; ++c) {
-                wsW[ql + c * N] = x0[c] * us;
-                wsW[ql + 8 + c * N] = x1[c] * us;
+                wsW[ql + c * N] = X[c].x * us;
+                wsW[ql + 8 + c * N] = X[c].y * us;
             }
             if (WANT_V) {
 #pragma unroll
                 for (int c = 0; c < N; ++c) {
-                    wsV[ql + c * N] = y0[c];
-                    wsV[ql + 8 + c * N] = y1[c];
+                    wsV[ql + c * N] = Y[c].x;
+                    wsV[ql + 8 + c * N] = Y[c].y;
                 }
             }
         }
         if (ql == 0 && a.info) {
             bsvd_info inf;
             inf.converged = done;
-            inf.outer_sweeps = sweeps;
-            inf.rotations = rot_total;
+            inf.outer_sweeps = sm.sweeps;
+            inf.rotations = sm.rot;
             inf.gram_calls = 0;
             inf.update_calls = 0;
-            inf.last_rotations = last;
+            inf.last_rotations = sm.last;
             inf.path = 1;
-            inf.status = ((badm >> (8 * qt)) & 0xFFu) ? 1 : 0;
+            inf.status = sm.bad;
             inf.kernel = a.kernel;
             a.info[prob] = inf;
         }
