@@ -82,6 +82,18 @@ BSVD_DEV double norm2d(float x) { double d = x; return d * d; }
 BSVD_DEV double norm2d(double x) { return x * x; }
 BSVD_DEV double norm2d(cx<float> z) { double a = z.re, b = z.im; return fma(a, a, b * b); }
 BSVD_DEV double norm2d(cx<double> z) { return fma(z.re, z.re, z.im * z.im); }
+// largest |component| and |x * sd|^2 (sd a power of two) for the FP64 column norms of finalize.cuh
+BSVD_DEV double abs_component(double x) { return fabs(x); }
+BSVD_DEV double abs_component(cx<double> z) { return fmax(fabs(z.re), fabs(z.im)); }
+BSVD_DEV double abs_component(float x) { return fabs((double)x); }
+BSVD_DEV double abs_component(cx<float> z) { return fmax(fabs((double)z.re), fabs((double)z.im)); }
+BSVD_DEV double norm2d_scaled(double x, double sd) { const double y = x * sd; return y * y; }
+BSVD_DEV double norm2d_scaled(cx<double> z, double sd) {
+    const double a = z.re * sd, b = z.im * sd;
+    return fma(a, a, b * b);
+}
+BSVD_DEV double norm2d_scaled(float x, double sd) { return norm2d(x) * (sd * sd); }
+BSVD_DEV double norm2d_scaled(cx<float> z, double sd) { return norm2d(z) * (sd * sd); }
 
 BSVD_DEV float conjT(float x) { return x; }
 BSVD_DEV double conjT(double x) { return x; }

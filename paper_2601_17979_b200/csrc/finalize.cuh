@@ -59,13 +59,32 @@ __device__ void finalize_block(T* W, int ldw, int bm, int bn, T* Vw, int ldvw,
     using Wt = typename tr<T>::W;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-    // 1. column norms in float64
+    // 1. column norms in float64.  FP64 columns are first scaled by a power of two from their largest
+    // component (the reference's np.linalg.norm is underflow/overflow-safe; plain squares of a column
+    // at 1e-200 vanish): exact, so the bits are those of the plain sum wherever its squares are
+    // representable -- and those of the register kernels' fused finalisation, which sums the squares
+    // of the problem-scaled W.  FP32 squares are exact and in range in float64.
     for (int c = warp; c < bn; c += nw) {
         double acc = 0.0;
-        for (int r = lane; r < bm; r += 32) acc += norm2d(W[r + (size_t)c * ldw]);
+        if constexpr (sizeof(R) == 8) {
+            double mx = 0.0;
+            for (int r = lane; r < bm; r += 32) mx = fmax(mx, abs_component(W[r + (size_t)c * ldw]));
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (lane == 0) sig[c] = (R)sqrt(acc);
+            for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            int e = (int)((__double_as_longlong(mx) >> 52) & 0x7ff) - 1023;
+            if (!(mx > 0.0) || !isfinite(mx)) e = 0;
+            e = max(-1021, min(1021, e));
+            const double sd = __longlong_as_double((long long)(1023 - e) << 52);
+            for (int r = lane; r < bm; r += 32) acc += norm2d_scaled(W[r + (size_t)c * ldw], sd);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane == 0) sig[c] = (R)(sqrt(acc) * __longlong_as_double((long long)(1023 + e) << 52));
+        } else {
+            for (int r = lane; r < bm; r += 32) acc += norm2d(W[r + (size_t)c * ldw]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane == 0) sig[c] = (R)sqrt(acc);
+        }
     }
     if (tid == 0) *flag = 0;
     __syncthreads();

@@ -586,9 +586,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         const double ssa = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl) * RSTR + 16 * half));
         const double ssb = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl + 1) * RSTR + 16 * half));
         const double sa = ssa * unscale, sb = ssb * unscale;
-        // holes (sigma < tiny/u) and scaled sigmas outside the reciprocal's safe range take the
+        // holes (sigma < tiny/u), scaled sigmas outside the reciprocal's safe range, and columns whose
+        // scaled squares may have left the normal range (sigma < 2^-480 of the problem's scale: the
+        // standalone pass rescales per column, like the reference's underflow-safe norms) take the
         // standalone pass
-        const bool tiny = !(sa >= dtiny<double>() && sb >= dtiny<double>() && ssa >= 0x1p-960 && ssb >= 0x1p-960 &&
+        const bool tiny = !(sa >= dtiny<double>() && sb >= dtiny<double>() && ssa >= 0x1p-480 && ssb >= 0x1p-480 &&
                             ssa <= 0x1p+960 && ssb <= 0x1p+960);
         const unsigned tm = __ballot_sync(0xffffffffu, tiny);
         fused = ((tm >> (16 * half)) & 0xFFFFu) == 0u;

