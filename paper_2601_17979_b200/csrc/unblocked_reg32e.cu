@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(2 * NP * 32, MINB) k_reg32e(SolveArgs<double> 
         PairSmem& ps = reinterpret_cast<PairSmem*>(smem_raw)[threadIdx.x / RING];
         mbar_init(&ps.full[threadIdx.x % RING], 32);
         mbar_init(&ps.empty[threadIdx.x % RING], 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // init visible before first use
     }
     __syncthreads();
 
