@@ -5,8 +5,11 @@
 
 A step solves one whole batch (default C1-10k: 10,000 x 32x32 FP64, arith
 spectrum kappa=1e10, full U/S/V) with inputs resident in HBM.  Multi-GPU is
-weak scaling by plain batch splitting: every rank solves its own batch of the
-same size; no collective on the data path.  The L2 (126 MB) is
+STRONG scaling by plain batch splitting (north star): the one
+global batch is cut into contiguous slices of ceil(B/N) problems, rank r
+solving slice r (parallel.solve_rank_slice); no collective on the data path,
+the optional gather of the factors is timed separately.  ``--batch B``
+overrides the global batch (``--batch 1250`` on one GPU = one 8-way slice).  The L2 (126 MB) is
 flushed with a 512 MiB write between timed steps; each step is timed with
 CUDA events on the launching stream; the job time is the max over ranks.
 
@@ -213,7 +216,7 @@ def run_reference(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": count / value * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_tag(cfg),
         "data": "synthetic (device-generated, same generator and seed as the b200 arm)",
-        "config": config_block(cfg, args),
+        "config": config_block(cfg, args, 1),
         "gflops": statistics.median(fl) / 1e9,
         "cpu_baseline": {"value": value, "unit": "matrices/s", "cores": nthreads, "kind": "port",
                          "sample": f"{count} of {cfg['batch']} problems per step (oracle/ C++ restatement, "
@@ -227,11 +230,15 @@ def dtype_tag(cfg):
     return {"float64": "f64", "float32": "f32", "complex128": "c128", "complex64": "c64"}[cfg["dtype"]]
 
 
-def config_block(cfg, args):
-    return {"workload": cfg["desc"], "config_id": args.config, "batch_per_gpu": cfg["batch"], "m": cfg["m"],
-            "n": cfg["n"], "dtype": cfg["dtype"], "want_v": cfg["want_v"],
+def config_block(cfg, args, world=1):
+    from paper_2601_17979_b200.parallel import shard
+
+    per = max(b - a for a, b in (shard(cfg["batch"], r, world) for r in range(world)))
+    return {"workload": cfg["desc"], "config_id": args.config, "global_batch": cfg["batch"], "batch_per_gpu": per,
+            "m": cfg["m"], "n": cfg["n"], "dtype": cfg["dtype"], "want_v": cfg["want_v"],
             "route": (cfg["route"] or "dispatch") + ("+use_qr_preprocess" if cfg.get("use_qr") else ""),
-            "parallelism": f"batch split x{args.gpus} (no collective)",
+            "parallelism": f"one batch split x{world}: contiguous slices of <= {per} problems per GPU, "
+                           "no collective on the data path",
             "l2": "flushed between timed steps (512 MiB write); inputs device-resident"}
 
 
@@ -299,13 +306,18 @@ def run_b200(args, cfg):
     dev = torch.device("cuda", torch.cuda.current_device())
     dt = np.dtype(cfg["dtype"])
     cplx = dt.kind == "c"
-    m, n, B = cfg["m"], cfg["n"], cfg["batch"]
+    from paper_2601_17979_b200.parallel import gather_slices, shard, solve_rank_slice
+
+    m, n, BG = cfg["m"], cfg["n"], cfg["batch"]
     k = min(m, n)
     opts = bs.JacobiOptions(compute_right_vectors=cfg["want_v"], use_qr_preprocess=cfg.get("use_qr", False))
     route = {None: _lib.DISPATCH, "blocked": _lib.FORCE_BLOCKED, "unblocked": _lib.FORCE_UNBLOCKED}[cfg["route"]]
-    # each rank its own problems (weak scaling): seed offset by rank
-    a = gen_batch_device(cfg["family"], m, n, B, dt, kappa=cfg["kappa"], seed=1000 * rank, rank=cfg.get("rank"),
-                         device=dev)
+    # one global batch (same seed on every rank, identical to the 1-GPU run); this rank solves slice r
+    a_global = gen_batch_device(cfg["family"], m, n, BG, dt, kappa=cfg["kappa"], seed=0, rank=cfg.get("rank"),
+                                device=dev)
+    s0, s1 = shard(BG, rank, world)
+    a = a_global[s0:s1]
+    B = s1 - s0
     es = dt.itemsize
     rs = np.dtype(bs.real_dtype(dt)).itemsize
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -324,8 +336,11 @@ def run_b200(args, cfg):
     sampler = ClockSampler(phys)
     sampler.start()
     time.sleep(0.3)
+    def step():
+        return solve_rank_slice(a_global, m, n, opts, rank, world, route=route, out=out)[2]
+
     for _ in range(args.warmup):
-        res = solve_tensor(a, m, n, opts, route, out=out)
+        res = step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -337,7 +352,7 @@ def run_b200(args, cfg):
         flush.fill_(1.0)  # L2 flush, outside the timed events
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        res = solve_tensor(a, m, n, opts, route, out=out)
+        res = step()
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize()
@@ -354,7 +369,16 @@ def run_b200(args, cfg):
     info = np.frombuffer(res.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
     kernel_id = int(info["kernel"][0])
     # our kernel launches per step, counted by the CUDA activity trace of one more (untimed) step
-    launches_per_step = count_launches(lambda: solve_tensor(a, m, n, opts, route, out=out))
+    launches_per_step = count_launches(step)
+    # optional gather of the factors to rank 0 (NCCL all_gather over NVLink), timed apart from the solve
+    gather_ms = None
+    if dist:
+        torch.cuda.synchronize()
+        dist.barrier()
+        tg = time.perf_counter()
+        gather_slices((res.u, res.s, res.v, res.info), BG)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - tg) * 1e3
     # accuracy of the whole timed batch on the device (bsvd_verify_batched; outside the timed region)
     from paper_2601_17979_b200.verify import verify_tensor
 
@@ -392,8 +416,8 @@ def run_b200(args, cfg):
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    h2d = B * m * n * es
-    d2h = B * m * k * es + B * k * rs + (B * n * k * es if v_t is not None else 0) + B * _lib.INFO_BYTES
+    h2d = BG * m * n * es  # whole job (every rank's slice) per step
+    d2h = BG * m * k * es + BG * k * rs + (BG * n * k * es if v_t is not None else 0) + BG * _lib.INFO_BYTES
     sampler.stop()
     clocks = sampler.summary(t_wall0, t_wall1)
 
@@ -417,18 +441,19 @@ def run_b200(args, cfg):
     f_mat = float(np.mean([flops_per_problem(i, m, n, cplx, cfg["want_v"]) for i in cinfos]))
     o_sweeps = float(np.mean([i["outer_sweeps"] for i in cinfos]))
     peak = measure_fma_peak(0 if rs == 4 else 1)
-    steps_total = args.steps * world
-    value = B * steps_total / dev_s
+    steps_total = args.steps
+    value = BG * steps_total / dev_s  # the whole job: every rank's slice of the one global batch
     ms_per_step = dev_s / args.steps * 1e3
     launch_s = (sum(step_ms) / len(step_ms)) / 1e3  # rank-0 average launch duration
     achieved = f_mat * B / launch_s / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "matrices/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": dtype_tag(cfg),
         "data": f"synthetic ({cfg['family']} spectrum, device-generated; A = U diag(s) V^H for prescribed spectra)",
-        "config": config_block(cfg, args),
-        "gflops": f_mat * B * steps_total / dev_s / 1e9,
+        "config": dict(config_block(cfg, args, world), gather_ms=gather_ms),
+        "gflops": f_mat * BG * steps_total / dev_s / 1e9,
         "roofline": {"bound": "fp64-fma" if rs == 8 else "fp32-fma", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": load_traffic(args.config),
                      "peak_source": "measured on this box by bsvd_bench_fma_peak (MEASURED_PEAKS.json has no "
@@ -440,7 +465,7 @@ def run_b200(args, cfg):
                      "sweep/rotation counts for the same inputs (bitwise equal to the reference's)",
                      "hbm_bytes_per_matrix": compulsory_bytes(m, n, es, rs, cfg["want_v"])},
         "cpu_baseline": cpu_line,
-        "e2e": {"value": B * steps_total / e2e_s, "unit": "matrices/s", "h2d_bytes_per_step": h2d,
+        "e2e": {"value": BG * steps_total / e2e_s, "unit": "matrices/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "path": "bsvd_gesvj_batched_host: pinned host buffers, H2D / solve / D2H "
                 f"pipelined in chunks of {e2e_chunk} over 4 streams"},
         "clocks": clocks,
@@ -465,8 +490,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c1-10k")
+    ap.add_argument("--batch", type=int, default=0, help="override the config's global batch")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.batch > 0:
+        cfg["batch"] = args.batch
+        cfg["desc"] = cfg["desc"] + f" [global batch overridden to {args.batch}]"
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:
             return

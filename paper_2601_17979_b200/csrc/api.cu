@@ -94,6 +94,7 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         if (o->kernel != 0) return p;
     }
     if (is_reg32e(o->kernel)) return plan_unblocked_reg32e(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
+    if (is_reg32f(o->kernel)) return plan_unblocked_reg32f(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
     if (is_reg32c(o->kernel)) return plan_unblocked_reg32c(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
     if (is_reg32b(o->kernel)) {
         Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel, o->max_sweeps);
@@ -195,6 +196,12 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_UNBLOCKED_REG32C_LAST:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32c(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
+        case KV_UNBLOCKED_REG32F:
+        case KV_UNBLOCKED_REG32F + 1:
+        case KV_UNBLOCKED_REG32F + 2:
+        case KV_UNBLOCKED_REG32F_LAST:
+            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32f(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
         case KV_CREG32:
             if constexpr (sizeof(T) == 16 && tr<T>::cplx) return launch_creg32(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
@@ -211,6 +218,10 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_UNBLOCKED_REG32B + 5:
         case KV_UNBLOCKED_REG32B + 6:
         case KV_UNBLOCKED_REG32B_LAST:
+        case KV_UNBLOCKED_REG32G:
+        case KV_UNBLOCKED_REG32G + 1:
+        case KV_UNBLOCKED_REG32G + 2:
+        case KV_UNBLOCKED_REG32G_LAST:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32b(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG32E:

@@ -62,6 +62,10 @@ enum {
     KV_BLOCKED_REG_U4 = 33,     // KV_BLOCKED_REG with the ring unrolled by 4
     KV_UNBLOCKED_REG16C = 34,   // 16x16 FP32 third generation: 4 problems per warp, 2 rows per lane
     KV_UNBLOCKED_REG16C_LAST = 37,  // 35, 36: ring unrolled by 3 / 5; 37: 2-warp CTAs
+    KV_UNBLOCKED_REG32F = 38,   // 32x32 FP64 fourth generation: one problem per warp, W and V rows in registers
+    KV_UNBLOCKED_REG32F_LAST = 41,  // 39: per-pair skip; 40: 168-register cap; 41: 2-warp CTAs
+    KV_UNBLOCKED_REG32G = 42,   // KV_UNBLOCKED_REG32B with scaled (fast) rotations: one FMA per updated element
+    KV_UNBLOCKED_REG32G_LAST = 45,  // 43: rotation prefetch 8; 44: 168-register cap
 };
 
 template <class T>

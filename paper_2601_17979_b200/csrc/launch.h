@@ -91,6 +91,9 @@ int launch_unblocked_reg16c(SolveArgs<float> a, const Plan& p, cudaStream_t st);
 bool is_reg32c(int kv);
 Plan plan_unblocked_reg32c(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
 int launch_unblocked_reg32c(SolveArgs<double> a, const Plan& p, cudaStream_t st);
+bool is_reg32f(int kv);
+Plan plan_unblocked_reg32f(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
+int launch_unblocked_reg32f(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blocked, int nb);
 int launch_creg32(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st);
 

@@ -59,6 +59,9 @@ struct WarpSmem {
     Par pub[2][H];             // this iteration's rotations, [half][pair]
     Par stage[2][2][H];        // V replay: double-buffered log rows [buf][half][pair]
     double nrm[2][N];          // maintained squared column norms [half][column]
+    double dsc[2][N];          // FG: column scale factors d (true column = d * stored column) [half][column]
+    double rds[2][N];          // FG: 1 / d
+    double dv[2][N];           // FG: d at the end of the W sweep, applied to V after its replay
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -91,6 +94,21 @@ __device__ __forceinline__ void apply2(double& x, double& y, double cm1, double 
     const double ty = fma(-c, x, y);
     x = fma(cm1, x, tx);
     y = fma(cm1, y, ty);
+}
+
+// Scaled (fast) rotation on stored columns (FG): with a_x = d_x p_x and a_y = d_y p_y the rotation
+//   a_x' = c a_x + S a_y,  a_y' = c a_y - S a_x        (S = +-s, the reference's update)
+// is p_x' = p_x + alpha p_y,  p_y' = p_y + beta p_x   with alpha = T d_y / d_x, beta = -T d_x / d_y,
+// T = S / c (the signed tangent), and d_x' = c d_x, d_y' = c d_y: one FMA per element instead of two.
+__device__ __forceinline__ void apply_fg(double& x, double& y, double alpha, double beta) {
+    const double xo = x;
+    x = fma(alpha, y, x);
+    y = fma(beta, xo, y);
+}
+template <bool FG>
+__device__ __forceinline__ void apply_any(double& x, double& y, double p0, double p1) {
+    if constexpr (FG) apply_fg(x, y, p0, p1);
+    else apply2(x, y, p0, p1);
 }
 
 __device__ __forceinline__ double sum16(const double* p) {  // 16 consecutive doubles, fixed tree
@@ -208,6 +226,20 @@ __device__ __forceinline__ void rot_abs(double dabs, double g, double& s, double
     rot_abs_core(dabs, g, s, cm1, tabs);
     if (fmax(dabs, g) < 0x1p-500) rot_abs_core(dabs * 0x1p+600, g * 0x1p+600, s, cm1, tabs);
 }
+// FG: |t|, c and 1/c of the same half-angle chain (no 1 / (1 + c): c - 1 is not needed)
+__device__ __forceinline__ void rot_fg_core(double dabs, double g, double& tabs, double& c, double& ic) {
+    const double q = fma(4.0 * g, g, dabs * dabs);
+    const double ir = rsqrt_cubic(q);
+    const double gi = g * ir;
+    const double c2 = fma(0.5 * dabs, ir, 0.5);
+    ic = rsqrt_cubic(c2);
+    c = c2 * ic;
+    tabs = (gi * ic) * ic;
+}
+__device__ __forceinline__ void rot_fg(double dabs, double g, double& tabs, double& c, double& ic) {
+    rot_fg_core(dabs, g, tabs, c, ic);
+    if (fmax(dabs, g) < 0x1p-500) rot_fg_core(dabs * 0x1p+600, g * 0x1p+600, tabs, c, ic);
+}
 
 // g_ji partial product of next pair k (offset u) from this lane's two rows
 template <int u>
@@ -263,7 +295,7 @@ __device__ __forceinline__ double reduce16_half(double (&v)[H], int hl) {
     return keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
-template <int u, int PD, bool SH = false>
+template <int u, int PD, bool SH = false, bool FG = false>
 __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab, int t,
                                        int lane, int half, int hl, bool done, double tol, double tol2,
                                        Par* logl, IterState& st) {
@@ -283,14 +315,26 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     const int ct = code & 0xff, cb = (code >> 8) & 0xff;
     const bool flip = (code >> 16) != 0;
     double gt, gb;
+    double sct = 1.0, scb = 1.0, rst = 1.0, rsb = 1.0;  // FG: scale factors of the pair's columns
+    if constexpr (FG) {
+        sct = sm.dsc[half][ct];
+        scb = sm.dsc[half][cb];
+        rst = sm.rds[half][ct];
+        rsb = sm.rds[half][cb];
+    }
     if (st.full && ((st.fmask >> lane) & 1u)) {
         gt = sum16(sm.red + (H + 2 * k) * RSTR + 16 * half);
         gb = sum16(sm.red + (H + 2 * k + 1) * RSTR + 16 * half);
+        if constexpr (FG) {
+            gt *= sct * sct;
+            gb *= scb * scb;
+        }
     } else {
         gt = sm.nrm[half][ct];
         gb = sm.nrm[half][cb];
     }
-    const double g = SH ? gsh : sum16(sm.red + k * RSTR + 16 * half);
+    double g = SH ? gsh : sum16(sm.red + k * RSTR + 16 * half);
+    if constexpr (FG) g *= sct * scb;  // dot product of the true columns
     const double absg = fabs(g);
     R32P(1, g);
     // guard (F4): rotate unless |g| <= 0 or |g| < tol sqrt(gii gjj); squared
@@ -300,14 +344,21 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     if (absg < 0x1p-400 && absg > 0.0) rot = !(absg < tol * fsqrt(p));
     rot = rot && !done && absg > 0.0;
     const double d = gt - gb;
-    double s, cm1, tabs;
-    rot_abs(fabs(d), absg, s, cm1, tabs);
+    double s, cm1, tabs, cc = 1.0, icc = 1.0;
+    if constexpr (FG) rot_fg(fabs(d), absg, tabs, cc, icc);
+    else rot_abs(fabs(d), absg, s, cm1, tabs);
     // sign of tau in slot orientation: sgn(d), and for d == 0 the reference's
     // sgn(0) = +1 taken in (i, j) orientation
     const bool eneg = d < 0.0 || (d == 0.0 && flip);
     Par par;
-    par.cm1 = rot ? cm1 : 0.0;
-    par.c = rot ? xor_sign(s, (g < 0.0) != eneg) : 0.0;  // x = top slot, y = bot slot
+    if constexpr (FG) {
+        const double T = xor_sign(tabs, (g < 0.0) != eneg);  // signed tangent S / c
+        par.cm1 = rot ? T * (scb * rst) : 0.0;                // alpha (x = top slot)
+        par.c = rot ? -T * (sct * rsb) : 0.0;                 // beta (y = bottom slot)
+    } else {
+        par.cm1 = rot ? cm1 : 0.0;
+        par.c = rot ? xor_sign(s, (g < 0.0) != eneg) : 0.0;  // x = top slot, y = bot slot
+    }
     R32P(2, par.cm1);
     sm.pub[half][k] = par;
     const unsigned mask = __ballot_sync(0xffffffffu, rot);
@@ -318,6 +369,12 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     const double nt = gt + dtg, nb = gb - dtg;
     sm.nrm[half][ct] = nt;
     sm.nrm[half][cb] = nb;
+    if (FG && rot) {
+        sm.dsc[half][ct] = cc * sct;
+        sm.dsc[half][cb] = cc * scb;
+        sm.rds[half][ct] = icc * rst;
+        sm.rds[half][cb] = icc * rsb;
+    }
     const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
     st.my_rot += rot ? 1 : 0;
     {  // a >4x shrink in a problem makes that problem's next iteration recompute its norms
@@ -336,8 +393,8 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
         for (int q = 0; q < H; ++q) {
             const Par cur = pq[q % PD];
             if (q + PD < H) pq[q % PD] = sm.pub[half][q + PD];
-            apply2(x0[TS(q, u)], x0[BS(q, u)], cur.cm1, cur.c);
-            apply2(x1[TS(q, u)], x1[BS(q, u)], cur.cm1, cur.c);
+            apply_any<FG>(x0[TS(q, u)], x0[BS(q, u)], cur.cm1, cur.c);
+            apply_any<FG>(x1[TS(q, u)], x1[BS(q, u)], cur.cm1, cur.c);
             if (!SH && q >= 1) cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs pairs q-2, q
         }
         if (!SH) cross_partial<un>(x0, x1, sm.red, lane, H - 1);
@@ -350,7 +407,7 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
 }
 
 // One V replay iteration at offset u (log row t is staged in sm.stage[t & 1]).
-template <int u, int PD, bool ZCHECK = false>
+template <int u, int PD, bool ZCHECK = false, bool FG = false>
 __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int t, int half, int hl,
                                        const Par* logl, uint32_t itbits, long long& tl) {
     R32PT(7, x0[TS(0, u)], tl);
@@ -375,15 +432,15 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
         for (int q = 0; q < H; ++q) {
             const Par pq = pr[q % PD];
             if (q + PD < H) pr[q % PD] = stp[q + PD];
-            apply2(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
-            apply2(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
+            apply_any<FG>(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
+            apply_any<FG>(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
         }
     }
     R32PT(9, x1[BS(H - 1, u)], tl);
     __syncwarp();
 }
 
-template <int U, int PD, bool SH = false>
+template <int U, int PD, bool SH = false, bool FG = false>
 __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab,
                                         int lane, int half, int hl, bool done, double tol, double tol2, Par* logl,
                                         IterState& st) {
@@ -394,25 +451,25 @@ __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSm
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
         const bool last = gi == NG - 1;
-        w_iter<0, PD, SH>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
+        w_iter<0, PD, SH, FG>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
         if constexpr (U >= 2) {
             if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            w_iter<1 % U, PD, SH>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<1 % U, PD, SH, FG>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
         }
         if constexpr (U >= 3) {
             if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            w_iter<2 % U, PD, SH>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<2 % U, PD, SH, FG>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
         }
         if constexpr (U >= 4) {
             if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            w_iter<3 % U, PD, SH>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<3 % U, PD, SH, FG>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
         }
         ring_shift<U>(x0);
         ring_shift<U>(x1);
     }
 }
 
-template <int U, int PD, bool ZCHECK = false>
+template <int U, int PD, bool ZCHECK = false, bool FG = false>
 __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int half, int hl,
                                         const Par* logl, uint32_t itbits, long long& tl) {
     constexpr int NG = (NIT + U - 1) / U;
@@ -421,25 +478,26 @@ __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSm
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
         const bool last = gi == NG - 1;
-        v_iter<0, PD, ZCHECK>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
+        v_iter<0, PD, ZCHECK, FG>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
         if constexpr (U >= 2) {
             if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            v_iter<1 % U, PD, ZCHECK>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
+            v_iter<1 % U, PD, ZCHECK, FG>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 3) {
             if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            v_iter<2 % U, PD, ZCHECK>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
+            v_iter<2 % U, PD, ZCHECK, FG>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 4) {
             if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            v_iter<3 % U, PD, ZCHECK>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
+            v_iter<3 % U, PD, ZCHECK, FG>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
         }
         ring_shift<U>(x0);
         ring_shift<U>(x1);
     }
 }
 
-template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true, bool SH = false>
+template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true, bool SH = false,
+          bool FG = false>
 __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -465,6 +523,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     }
     uint32_t* ctab = reinterpret_cast<uint32_t*>(smem_raw + NW * sizeof(WarpSmem));
     for (int e = threadIdx.x; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
+    if constexpr (FG) {  // unit scales (the warp's own slots; lane hl: columns 2 hl, 2 hl + 1)
+        sm.dsc[half][2 * hl] = sm.dsc[half][2 * hl + 1] = 1.0;
+        sm.rds[half][2 * hl] = sm.rds[half][2 * hl + 1] = 1.0;
+    }
     __syncthreads();
 
     double x0[N], x1[N];
@@ -506,8 +568,27 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         st.itbits = 0;
         st.full = true;  // fresh norms at the start of every sweep
         st.fmask = 0xffffffffu;
-        w_sweep<U, PD, SH>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2,
-                       (SPLIT && logw) ? logw + (size_t)sw * NIT * H : logw, st);
+        w_sweep<U, PD, SH, FG>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2,
+                           (SPLIT && logw) ? logw + (size_t)sw * NIT * H : logw, st);
+        if constexpr (FG) {
+            // back to true columns at the sweep end (the ring is back in place: slot c = column c), so
+            // every sweep starts from unit scales and the finalisation sees W and V themselves
+            __syncwarp();
+            if (st.itbits) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    const double dc = sm.dsc[half][c];
+                    x0[c] *= dc;
+                    x1[c] *= dc;
+                }
+            }
+            __syncwarp();
+            sm.dv[half][2 * hl] = sm.dsc[half][2 * hl];
+            sm.dv[half][2 * hl + 1] = sm.dsc[half][2 * hl + 1];
+            sm.dsc[half][2 * hl] = sm.dsc[half][2 * hl + 1] = 1.0;
+            sm.rds[half][2 * hl] = sm.rds[half][2 * hl + 1] = 1.0;
+            __syncwarp();
+        }
         // ---- sweep end: per-problem rotation count over the half warp ----
         int tot = st.my_rot;
 #pragma unroll
@@ -553,8 +634,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
             __syncwarp();  // this warp's log writes are visible to all its lanes
             cp_async16(&sm.stage[0][half][hl], logl);
             cp_commit();
-            v_sweep<UV, PD>(x0, x1, sm, half, hl, logl, st.itbits, st.tl);
+            v_sweep<UV, PD, false, FG>(x0, x1, sm, half, hl, logl, st.itbits, st.tl);
             cp_wait<0>();
+            if constexpr (FG) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    const double dc = sm.dv[half][c];
+                    x0[c] *= dc;
+                    x1[c] *= dc;
+                }
+            }
             if (live) {
 #pragma unroll
                 for (int c = 0; c < N; ++c) {  // park V
@@ -774,7 +863,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_vreplay(SolveArgs<double> a) 
 }  // namespace r32b
 
 // variants: (warps per CTA, min CTAs per SM, unroll, per-pair skip)
-bool is_reg32b(int kv) { return kv >= KV_UNBLOCKED_REG32B && kv <= KV_UNBLOCKED_REG32B_LAST; }
+bool is_reg32b(int kv) {
+    return (kv >= KV_UNBLOCKED_REG32B && kv <= KV_UNBLOCKED_REG32B_LAST) ||
+           (kv >= KV_UNBLOCKED_REG32G && kv <= KV_UNBLOCKED_REG32G_LAST);
+}
 
 size_t reg32b_work_elems(int kv, int max_sweeps);
 
@@ -799,12 +891,13 @@ size_t reg32b_work_elems(int kv, int max_sweeps) {
                             : 2 * 32 * 32 + r32b::LOG_ELEMS;
 }
 
-template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true, bool SH = false>
+template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true, bool SH = false,
+          bool FG = false>
 static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
     const int per_cta = 2 * NW;
     const int grid = (a.batch + per_cta - 1) / per_cta;
     const size_t smem = NW * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
-    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD, SPLIT, FF, SH>;
+    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD, SPLIT, FF, SH, FG>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<grid, NW * 32, smem, st>>>(a);
@@ -841,6 +934,9 @@ int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st)
         case KV_UNBLOCKED_REG32B + 3: rc = launch_r32b<4, 2, 2, 2, 16, false, true, true>(a, st); break;  // shuffle g
         case KV_UNBLOCKED_REG32B + 4: rc = launch_r32b<4, 3, 2, 2, 2>(a, st); break;   // 168 regs, depth 2
         case KV_UNBLOCKED_REG32B + 7: rc = launch_r32b<4, 2, 2, 2, 16, false, false>(a, st); break;  // unfused finalize
+        case KV_UNBLOCKED_REG32G: rc = launch_r32b<4, 2, 2, 2, 16, false, true, false, true>(a, st); break;  // scaled rotations
+        case KV_UNBLOCKED_REG32G + 1: rc = launch_r32b<4, 2, 2, 2, 8, false, true, false, true>(a, st); break;
+        case KV_UNBLOCKED_REG32G + 2: rc = launch_r32b<4, 3, 2, 2, 4, false, true, false, true>(a, st); break;  // 168 regs
         default: rc = launch_r32b<4, 2, 2, 2, 16>(a, st); break;                       // 255 regs, 8 warps/SM
     }
     if (rc) return rc;
