@@ -167,11 +167,14 @@ int bsvd_verify_batched(int dtype, int m, int n, int batch,
                         const void* V, int64_t ldv, int64_t strideV,
                         const double* Sref, int64_t strideSref, double* out, void* stream);
 
-/* Device scratch needed by bsvd_gesvj_batched for this problem class. */
+/* Device scratch needed by bsvd_gesvj_batched for this problem class (any lda >= m). */
 size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts* opts);
 
-/* Kernel variant the auto-dispatch would pick (for telemetry/tests). */
+/* Kernel variant the auto-dispatch would pick (for telemetry/tests); the choice may depend on the
+ * batch size (16x16 FP32 switches to the quarter-warp kernel from 3,500 problems): the _batched form
+ * answers for `batch` problems, the plain form for batch = 0. */
 int bsvd_select_kernel(int dtype, int m, int n, const bsvd_opts* opts);
+int bsvd_select_kernel_batched(int dtype, int m, int n, int batch, const bsvd_opts* opts);
 
 /* Fill opts with the reference defaults (JacobiOptions(), src/svd.py:70-78). */
 void bsvd_default_opts(bsvd_opts* opts);

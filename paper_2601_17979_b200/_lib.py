@@ -57,6 +57,7 @@ EXPORTS = (
     "bsvd_workspace_bytes",
     "bsvd_host_workspace_bytes",
     "bsvd_select_kernel",
+    "bsvd_select_kernel_batched",
     "bsvd_default_opts",
     "bsvd_strerror",
     "bsvd_abi_version",
@@ -101,6 +102,8 @@ def load():
     L.bsvd_workspace_bytes.restype = sz
     L.bsvd_select_kernel.argtypes = [ci, ci, ci, popts]
     L.bsvd_select_kernel.restype = ci
+    L.bsvd_select_kernel_batched.argtypes = [ci, ci, ci, ci, popts]
+    L.bsvd_select_kernel_batched.restype = ci
     L.bsvd_default_opts.argtypes = [popts]
     L.bsvd_default_opts.restype = None
     L.bsvd_strerror.argtypes = [ci]

@@ -55,67 +55,52 @@ int make_route(int m, int n, const bsvd_opts* o, Route* r) {
 Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = true, int batch = 0) {
     const size_t lim = smem_limit();
     const int es = esize_of(dt), rs = rsize_of(dt);
+    const bool reg_ok = contiguous && !r.trans;  // register kernels: dense column-major input, no transpose
     if (o->kernel == 0 || o->kernel == KV_CREG32) {  // complex FP64, n = 32: both routes
-        Plan p = plan_creg32(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, r.blocked, o->nb);
+        Plan p = plan_creg32(dt, r.bm, r.bn, r.need_v, reg_ok, r.blocked, o->nb);
         if (p.kernel) return p;
         if (o->kernel != 0) return p;
     }
     if (r.blocked) {
-        if (o->kernel == 0 || o->kernel == KV_BLOCKED_REG || o->kernel == KV_BLOCKED_REG_U4) {
-            Plan p = plan_blocked_reg(dt, r.bm, r.bn, o->nb, r.need_v, contiguous && !r.trans, o->inner_sweeps,
-                                      o->kernel);
+        if (o->kernel == 0 || o->kernel == KV_BLOCKED_REG) {
+            Plan p = plan_blocked_reg(dt, r.bm, r.bn, o->nb, r.need_v, reg_ok, o->inner_sweeps, o->kernel);
             if (p.kernel) return p;
             if (o->kernel != 0) return p;
         }
         if (o->kernel == 0 || o->kernel == KV_BLOCKED_DMMA || o->kernel == KV_BLOCKED_DMMA_VG ||
             o->kernel == KV_BLOCKED_DMMA_512) {
-            Plan p = plan_blocked_dmma(dt, r.bm, r.bn, o->nb, r.need_v, contiguous && !r.trans, lim, o->kernel);
+            Plan p = plan_blocked_dmma(dt, r.bm, r.bn, o->nb, r.need_v, reg_ok, lim, o->kernel);
             if (p.kernel) return p;
             if (o->kernel != 0) return p;
         }
         return plan_blocked_general(es, rs, r.bm, r.bn, o->nb, r.need_v, lim);
     }
-    if (is_reg16c(o->kernel)) return plan_unblocked_reg16c(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
-    if (o->kernel == 0 && batch >= 3500) {
+    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG16C) {
         // 16x16 FP32 from ~3,500 problems on: the quarter-warp kernel (C2 10k: 172 vs 207 us); below it the
         // half-warp kernel's shorter per-warp chain wins.  The two are bit-identical (same sums in the same
         // tree, same parameter and update arithmetic), so batch == standalone still holds bitwise.
-        Plan p = plan_unblocked_reg16c(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, 0);
-        if (p.kernel) return p;
-    }
-    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG16B || o->kernel == KV_UNBLOCKED_REG16B + 1) {
-        Plan p = plan_unblocked_reg16b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
-        if (p.kernel) return p;
-        if (o->kernel != 0) return p;
-    }
-    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG16F) {
-        Plan p = plan_unblocked_reg16(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans);
-        if (p.kernel) return p;
-        if (o->kernel != 0) return p;
-    }
-    if (is_reg32e(o->kernel)) return plan_unblocked_reg32e(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
-    if (is_reg32f(o->kernel)) return plan_unblocked_reg32f(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
-    if (is_reg32c(o->kernel)) return plan_unblocked_reg32c(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
-    if (is_reg32b(o->kernel)) {
-        Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel, o->max_sweeps);
-        return p;  // forced variant unavailable => kernel 0 => unsupported
-    }
-    if (o->kernel == 0) {  // default for 32x32 FP64: the second-generation register kernel
-        // up to one wave of problem pairs (148 SMs x 8 warps) the warp-specialised W/V kernel finishes
-        // first (500 problems 0.32 vs 0.35 ms, 1,000: 0.33 vs 0.35; from 1,500 on gen. 2 wins); its
-        // arithmetic is bit-identical to gen. 2, so batch == standalone still holds bitwise
-        if (batch > 0 && batch <= 1184) {
-            Plan p = plan_unblocked_reg32e(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, KV_UNBLOCKED_REG32E);
-            if (p.kernel) return p;
+        if (o->kernel != 0 || batch >= 3500) {
+            Plan p = plan_unblocked_reg16c(dt, r.bm, r.bn, r.need_v, reg_ok, o->kernel);
+            if (p.kernel || o->kernel != 0) return p;
         }
-        Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, 0, o->max_sweeps);
-        if (p.kernel) return p;
     }
-    if (o->kernel == 0 || (o->kernel >= KV_UNBLOCKED_REG32 && o->kernel <= KV_UNBLOCKED_REG32_F2)) {
-        Plan p = plan_unblocked_reg(dt, r.bm, r.bn, r.need_v, contiguous && !r.trans, o->kernel);
+    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG16B) {
+        Plan p = plan_unblocked_reg16b(dt, r.bm, r.bn, r.need_v, reg_ok, o->kernel);
+        if (p.kernel) return p;
+        if (o->kernel != 0) return p;
+    }
+    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG32B || o->kernel == KV_UNBLOCKED_REG32G) {
+        // 32x32 FP64, the second-generation register kernel.  With V: scaled rotations (one FMA per
+        // updated element; sigma = ||w|| / ||v||) at every batch size -- one kernel, so batch ==
+        // standalone holds bitwise (profiles/r2_c1_kernel_experiments.md: 10k 1.70 vs 1.85 ms, 1,184
+        // problems 0.333 vs 0.34 ms for the warp-specialised round-1 kernel).  Values only: the unscaled
+        // form (the scaled one needs V's column norms to cancel its scale roundings).
+        const int want = o->kernel ? o->kernel : (r.need_v ? KV_UNBLOCKED_REG32G : KV_UNBLOCKED_REG32B);
+        Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, reg_ok, want, o->max_sweeps);
         if (p.kernel) return p;
         if (o->kernel != 0) return p;  // forced variant unavailable => kernel 0 => unsupported
     }
+    if (o->kernel != 0 && o->kernel != KV_UNBLOCKED_GENERAL) return Plan{};
     return plan_unblocked_general(es, rs, r.bm, r.bn, r.need_v, lim);
 }
 
@@ -174,33 +159,13 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_UNBLOCKED_GENERAL: return launch_unblocked_general<T>(a, p, st);
         case KV_BLOCKED_GENERAL: return launch_blocked_general<T>(a, p, st);
         case KV_UNBLOCKED_REG16B:
-        case KV_UNBLOCKED_REG16B + 1:
             if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16b(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG16C:
-        case KV_UNBLOCKED_REG16C + 1:
-        case KV_UNBLOCKED_REG16C + 2:
-        case KV_UNBLOCKED_REG16C_LAST:
             if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16c(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
-        case KV_UNBLOCKED_REG16F:
-            if constexpr (sizeof(T) == 4 && !tr<T>::cplx) return launch_unblocked_reg16(a, p, st);
-            return BSVD_ERR_UNSUPPORTED;
         case KV_BLOCKED_REG:
-        case KV_BLOCKED_REG_U4:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_blocked_reg(a, p, st);
-            return BSVD_ERR_UNSUPPORTED;
-        case KV_UNBLOCKED_REG32C:
-        case KV_UNBLOCKED_REG32C + 1:
-        case KV_UNBLOCKED_REG32C + 2:
-        case KV_UNBLOCKED_REG32C_LAST:
-            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32c(a, p, st);
-            return BSVD_ERR_UNSUPPORTED;
-        case KV_UNBLOCKED_REG32F:
-        case KV_UNBLOCKED_REG32F + 1:
-        case KV_UNBLOCKED_REG32F + 2:
-        case KV_UNBLOCKED_REG32F_LAST:
-            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32f(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_CREG32:
             if constexpr (sizeof(T) == 16 && tr<T>::cplx) return launch_creg32(a, p, st);
@@ -211,31 +176,8 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_blocked_dmma(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG32B:
-        case KV_UNBLOCKED_REG32B + 1:
-        case KV_UNBLOCKED_REG32B + 2:
-        case KV_UNBLOCKED_REG32B + 3:
-        case KV_UNBLOCKED_REG32B + 4:
-        case KV_UNBLOCKED_REG32B + 5:
-        case KV_UNBLOCKED_REG32B + 6:
-        case KV_UNBLOCKED_REG32B_LAST:
         case KV_UNBLOCKED_REG32G:
-        case KV_UNBLOCKED_REG32G + 1:
-        case KV_UNBLOCKED_REG32G + 2:
-        case KV_UNBLOCKED_REG32G_LAST:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32b(a, p, st);
-            return BSVD_ERR_UNSUPPORTED;
-        case KV_UNBLOCKED_REG32E:
-        case KV_UNBLOCKED_REG32E + 1:
-        case KV_UNBLOCKED_REG32E + 2:
-        case KV_UNBLOCKED_REG32E_LAST:
-            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32e(a, p, st);
-            return BSVD_ERR_UNSUPPORTED;
-        case KV_UNBLOCKED_REG32:
-        case KV_UNBLOCKED_REG32_O3:
-        case KV_UNBLOCKED_REG32_R2:
-        case KV_UNBLOCKED_REG32_R3:
-        case KV_UNBLOCKED_REG32_F2:
-            if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg_d32(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
     }
     return BSVD_ERR_UNSUPPORTED;
@@ -374,8 +316,8 @@ const char* bsvd_strerror(int code) {
     return "unknown error";
 }
 
-int bsvd_select_kernel(int dtype, int m, int n, const bsvd_opts* opts) {
-    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || check_opts(opts)) return BSVD_ERR_ARG;
+int bsvd_select_kernel_batched(int dtype, int m, int n, int batch, const bsvd_opts* opts) {
+    if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || check_opts(opts)) return BSVD_ERR_ARG;
     Route r;
     if (make_route(m, n, opts, &r)) return BSVD_ERR_ARG;
     if (r.bn == 0 || r.bm == 0) return 0;
@@ -386,9 +328,13 @@ int bsvd_select_kernel(int dtype, int m, int n, const bsvd_opts* opts) {
         rr.blocked = r.bn > 32;
         rr.need_v = 1;
         rr.qr = 0;
-        return make_plan(dtype, rr, opts).kernel;
+        return make_plan(dtype, rr, opts, true, batch).kernel;
     }
-    return make_plan(dtype, r, opts).kernel;
+    return make_plan(dtype, r, opts, true, batch).kernel;
+}
+
+int bsvd_select_kernel(int dtype, int m, int n, const bsvd_opts* opts) {
+    return bsvd_select_kernel_batched(dtype, m, n, 0, opts);
 }
 
 namespace {
@@ -557,8 +503,12 @@ size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts*
     if (make_route(m, n, opts, &r)) return 0;
     if (r.bn == 0 || r.bm == 0) return 0;
     if (r.qr) return qr_ws(dtype, r, batch, opts).total;
-    const Plan p = make_plan(dtype, r, opts, true, batch);
-    return p.work_elems * (size_t)esize_of(dtype) * (size_t)batch;
+    // the call plans with contiguous = (lda == m): size for both plans, so a caller with a padded lda who
+    // allocates this many bytes never gets BSVD_ERR_WORKSPACE
+    const Plan pc = make_plan(dtype, r, opts, true, batch);
+    const Plan pg = make_plan(dtype, r, opts, false, batch);
+    const size_t elems = pc.work_elems > pg.work_elems ? pc.work_elems : pg.work_elems;
+    return elems * (size_t)esize_of(dtype) * (size_t)batch;
 }
 
 extern "C++" {

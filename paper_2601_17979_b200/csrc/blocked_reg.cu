@@ -473,7 +473,8 @@ Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contig
     const int ell = bn / 16, hb = (ell + (ell & 1)) / 2;
     int nwg = bm <= 64 ? 1 : (bm <= 128 ? 2 : (bm <= 256 ? 4 : 0));
     if (!nwg || hb * nwg > 8) return p;
-    p.kernel = variant == KV_BLOCKED_REG_U4 ? KV_BLOCKED_REG_U4 : KV_BLOCKED_REG;
+    (void)variant;
+    p.kernel = KV_BLOCKED_REG;
     p.threads = hb * nwg * 32;
     p.group = nwg;
     p.smem = breg::smem_bytes(bn, nwg);
@@ -497,18 +498,11 @@ int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
     a.kernel = p.kernel;
     a.work_stride = (int64_t)p.work_elems;
     int rc;
-    if (p.kernel == KV_BLOCKED_REG_U4) {  // ring unrolled by 4 (half the register moves, twice the code)
-        switch (p.group) {
-            case 1: rc = launch_br<1, 4>(a, p, st); break;
-            case 2: rc = launch_br<2, 4>(a, p, st); break;
-            default: rc = launch_br<4, 4>(a, p, st); break;
-        }
-    } else {
-        switch (p.group) {
-            case 1: rc = launch_br<1>(a, p, st); break;
-            case 2: rc = launch_br<2>(a, p, st); break;
-            default: rc = launch_br<4>(a, p, st); break;
-        }
+    // ring unrolled by 2 (by 4: half the register moves but twice the code, measured slower in round 1)
+    switch (p.group) {
+        case 1: rc = launch_br<1>(a, p, st); break;
+        case 2: rc = launch_br<2>(a, p, st); break;
+        default: rc = launch_br<4>(a, p, st); break;
     }
     if (rc) return rc;
     return launch_finalize_gm<double>(a, st);

@@ -36,36 +36,21 @@ struct SolveArgs {
     bsvd_info* info;
 };
 
-// Kernel variant ids (bsvd_info.kernel)
+// Kernel variant ids (bsvd_info.kernel).  Ids of retired round-1/round-2 experiments are not reused
+// (profiles/r2_c1_kernel_experiments.md).
 enum {
     KV_UNBLOCKED_GENERAL = 1,
     KV_BLOCKED_GENERAL = 2,
-    KV_UNBLOCKED_REG32 = 3,     // 32x32 FP64 register-resident (168 regs, 12 warps/SM)
-    KV_UNBLOCKED_REG32_O3 = 4,  // same, 255 regs, 8 warps/SM
-    KV_UNBLOCKED_REG32_R2 = 5,  // same, 204 regs, 10 warps/SM
-    KV_UNBLOCKED_REG32_R3 = 6,  // same, 227 regs, 9 warps/SM
-    KV_UNBLOCKED_REG32_F2 = 7,  // 168 regs, two-FMA rotation update (opt-in)
     KV_BLOCKED_DMMA = 8,        // blocked FP64, nb = 16, Gram/update on DMMA tensor cores
     KV_BLOCKED_DMMA_VG = 9,     // same, V kept in global memory (L2), 3 CTAs/SM
     KV_BLOCKED_DMMA_512 = 10,   // same, 512-thread CTAs (16 warps) for one-CTA-per-SM sizes
-    KV_UNBLOCKED_REG16F = 11,   // 16x16 FP32 register-resident, 4 problems per warp
     KV_UNBLOCKED_REG32B = 12,   // 32x32 FP64 second generation: unrolled ring, maintained norms, two-FMA
-    KV_UNBLOCKED_REG32B_LAST = 19,  // 13..19: tuning variants (registers, V unroll, CTA shape, split W/V, unfused finalize)
-    KV_UNBLOCKED_REG32C = 20,   // 32x32 FP64 third generation: one problem per warp, row per lane, 3-4 warps/SMSP
-    KV_UNBLOCKED_REG32C_LAST = 23,  // 21..23: register budget / rotation prefetch variants
-    KV_UNBLOCKED_REG16B = 24,   // 16x16 FP32 second generation: 2 problems per warp, row per lane (25: 56-register cap)
-    KV_UNBLOCKED_REG32E = 26,   // 32x32 FP64 warp-specialised: W warp + V warp per problem pair, smem ring
-    KV_UNBLOCKED_REG32E_LAST = 29,  // 27..29: tuning variants (pairs per CTA, V unroll)
+    KV_UNBLOCKED_REG16B = 24,   // 16x16 FP32 second generation: 2 problems per warp, row per lane
     KV_HEEVJ = 31,              // batched Hermitian Jacobi eigensolver (bsvd_heevj_batched)
     KV_BLOCKED_REG = 30,        // blocked FP64: block pairs register-resident (kernel (2) on X), V P on DMMA
     KV_CREG32 = 32,             // complex FP64, n = 32, m <= 256: CTA per problem, rows in registers, V in smem
-    KV_BLOCKED_REG_U4 = 33,     // KV_BLOCKED_REG with the ring unrolled by 4
     KV_UNBLOCKED_REG16C = 34,   // 16x16 FP32 third generation: 4 problems per warp, 2 rows per lane
-    KV_UNBLOCKED_REG16C_LAST = 37,  // 35, 36: ring unrolled by 3 / 5; 37: 2-warp CTAs
-    KV_UNBLOCKED_REG32F = 38,   // 32x32 FP64 fourth generation: one problem per warp, W and V rows in registers
-    KV_UNBLOCKED_REG32F_LAST = 41,  // 39: per-pair skip; 40: 168-register cap; 41: 2-warp CTAs
     KV_UNBLOCKED_REG32G = 42,   // KV_UNBLOCKED_REG32B with scaled (fast) rotations: one FMA per updated element
-    KV_UNBLOCKED_REG32G_LAST = 45,  // 43: rotation prefetch 8; 44: 168-register cap
 };
 
 template <class T>

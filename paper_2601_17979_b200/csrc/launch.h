@@ -22,7 +22,6 @@ struct Plan {
 
 Plan plan_unblocked_general(int esize, int rsize, int bm, int bn, int need_v, size_t smem_limit);
 Plan plan_blocked_general(int esize, int rsize, int bm, int bn, int nb, int need_v, size_t smem_limit);
-Plan plan_unblocked_reg(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
 Plan plan_blocked_dmma(int dtype, int bm, int bn, int nb, int need_v, bool contiguous, size_t smem_limit,
                        int variant);
 int launch_blocked_dmma(SolveArgs<double> a, const Plan& p, cudaStream_t st);
@@ -31,15 +30,9 @@ template <class T>
 int launch_unblocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
 template <class T>
 int launch_blocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
-int launch_unblocked_reg_d32(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 bool is_reg32b(int kv);
 Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant, int max_sweeps);
 int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st);
-bool is_reg32e(int kv);
-Plan plan_unblocked_reg32e(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
-int launch_unblocked_reg32e(SolveArgs<double> a, const Plan& p, cudaStream_t st);
-Plan plan_unblocked_reg16(int dtype, int bm, int bn, int need_v, bool lda_ok);
-int launch_unblocked_reg16(SolveArgs<float> a, const Plan& p, cudaStream_t st);
 
 template <class T>
 int launch_finalize_ws(SolveArgs<T> a, cudaStream_t st);
@@ -85,15 +78,8 @@ Plan plan_blocked_reg(int dtype, int bm, int bn, int nb, int need_v, bool contig
 int launch_blocked_reg(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 Plan plan_unblocked_reg16b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
 int launch_unblocked_reg16b(SolveArgs<float> a, const Plan& p, cudaStream_t st);
-bool is_reg16c(int kernel);
 Plan plan_unblocked_reg16c(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
 int launch_unblocked_reg16c(SolveArgs<float> a, const Plan& p, cudaStream_t st);
-bool is_reg32c(int kv);
-Plan plan_unblocked_reg32c(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
-int launch_unblocked_reg32c(SolveArgs<double> a, const Plan& p, cudaStream_t st);
-bool is_reg32f(int kv);
-Plan plan_unblocked_reg32f(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
-int launch_unblocked_reg32f(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blocked, int nb);
 int launch_creg32(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st);
 

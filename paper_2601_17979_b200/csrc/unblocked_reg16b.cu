@@ -291,7 +291,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16b(SolveArgs<float> a) {
 Plan plan_unblocked_reg16b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant) {
     Plan p{};
     if (dtype == BSVD_S && bn == 16 && bm == 16 && lda_ok) {
-        p.kernel = variant == KV_UNBLOCKED_REG16B + 1 ? variant : KV_UNBLOCKED_REG16B;
+        (void)variant;
+        p.kernel = KV_UNBLOCKED_REG16B;
         p.threads = reg16b::NW * 32;
         p.work_elems = (size_t)bm * 16 + (need_v ? 16 * 16 : 0) + 1;  // + the finalisation flag
     }
@@ -303,15 +304,9 @@ int launch_unblocked_reg16b(SolveArgs<float> a, const Plan& p, cudaStream_t st) 
     a.work_stride = (int64_t)p.work_elems;
     const int per_cta = 2 * reg16b::NW;
     const int grid = (a.batch + per_cta - 1) / per_cta;
-    // variant 25 caps registers at 56 (9 CTAs = 36 warps per SM: C2's 1,250 CTAs in one wave); measured
-    // slower than the uncapped default (the V kernel spills), kept for comparison
-    if (p.kernel == KV_UNBLOCKED_REG16B) {
-        if (a.need_v) reg16b::k_reg16b<true, 1><<<grid, reg16b::NW * 32, 0, st>>>(a);
-        else reg16b::k_reg16b<false, 1><<<grid, reg16b::NW * 32, 0, st>>>(a);
-    } else {
-        if (a.need_v) reg16b::k_reg16b<true, 9><<<grid, reg16b::NW * 32, 0, st>>>(a);
-        else reg16b::k_reg16b<false, 9><<<grid, reg16b::NW * 32, 0, st>>>(a);
-    }
+    // (a 56-register cap for 9 CTAs = 36 warps per SM measured slower in round 1: the V kernel spills)
+    if (a.need_v) reg16b::k_reg16b<true, 1><<<grid, reg16b::NW * 32, 0, st>>>(a);
+    else reg16b::k_reg16b<false, 1><<<grid, reg16b::NW * 32, 0, st>>>(a);
     if (cudaPeekAtLastError() != cudaSuccess) return BSVD_ERR_CUDA;
     return launch_finalize_flagged<float>(a, st);  // only problems the fused finalisation left over
 }

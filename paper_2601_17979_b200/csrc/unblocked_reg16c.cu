@@ -373,12 +373,11 @@ void launch_nw(const SolveArgs<float>& a, cudaStream_t st) {
 
 }  // namespace reg16c
 
-bool is_reg16c(int kernel) { return kernel >= KV_UNBLOCKED_REG16C && kernel <= KV_UNBLOCKED_REG16C_LAST; }
-
 Plan plan_unblocked_reg16c(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant) {
     Plan p{};
     if (dtype == BSVD_S && bn == 16 && bm == 16 && lda_ok) {
-        p.kernel = is_reg16c(variant) ? variant : KV_UNBLOCKED_REG16C;
+        (void)variant;
+        p.kernel = KV_UNBLOCKED_REG16C;
         p.threads = 32;
         p.work_elems = (size_t)bm * 16 + (need_v ? 16 * 16 : 0) + 1;  // + the finalisation flag
     }
@@ -388,14 +387,9 @@ Plan plan_unblocked_reg16c(int dtype, int bm, int bn, int need_v, bool lda_ok, i
 int launch_unblocked_reg16c(SolveArgs<float> a, const Plan& p, cudaStream_t st) {
     a.kernel = p.kernel;
     a.work_stride = (int64_t)p.work_elems;
-    // default: one-warp CTAs, ring unrolled by 2.  Variants (measured slower, tools/c2_cross.py): ring
-    // unrolled by 3 / 5 (fewer register moves, but longer bodies spill at the 96-register cap), 2-warp CTAs
-    switch (p.kernel - KV_UNBLOCKED_REG16C) {
-        case 1: reg16c::launch_nw<2, 9, 3>(a, st); break;
-        case 2: reg16c::launch_nw<2, 9, 5>(a, st); break;
-        case 3: reg16c::launch_nw<2, 9, 2>(a, st); break;
-        default: reg16c::launch_nw<1, 18, 2>(a, st); break;
-    }
+    // one-warp CTAs, ring unrolled by 2 (round 1 measured the ring unrolled by 3 / 5 -- fewer register
+    // moves, but longer bodies spill at the 96-register cap -- and 2-warp CTAs: all slower)
+    reg16c::launch_nw<1, 18, 2>(a, st);
     if (cudaPeekAtLastError() != cudaSuccess) return BSVD_ERR_CUDA;
     return launch_finalize_flagged<float>(a, st);  // only problems the fused finalisation left over
 }

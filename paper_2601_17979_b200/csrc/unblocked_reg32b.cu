@@ -62,6 +62,8 @@ struct WarpSmem {
     double dsc[2][N];          // FG: column scale factors d (true column = d * stored column) [half][column]
     double rds[2][N];          // FG: 1 / d
     double dv[2][N];           // FG: d at the end of the W sweep, applied to V after its replay
+    double vn[2][N];           // FG: column norms of V after its latest replay (1 before the first)
+    double sgs[2][N];          // FG finalisation: sigma of the scaled problem = ||w|| / ||v||
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -271,44 +273,12 @@ __device__ __forceinline__ void all_partials(const double (&x0)[N], const double
 // update is fused with the partials of iteration t + 1 (offset u + 1 in the
 // pre-shift register naming: next pair k = columns of this iteration's pairs
 // k - 1 and k + 1), so they are ready when the next reduction starts.
-// SH variant: the 16 g_ji partials of this lane's rows reduced over the half-warp by a transposing xor
-// butterfly (8, 4, 2, 1): lane hl ends with pair hl's sum, no shared-memory round trip
-__device__ __forceinline__ double reduce16_half(double (&v)[H], int hl) {
-    const bool b3 = hl & 8, b2 = hl & 4, b1 = hl & 2, b0 = hl & 1;
-    double a8[8], a4[4], a2[2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const double keep = b3 ? v[i + 8] : v[i], send = b3 ? v[i] : v[i + 8];
-        a8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double keep = b2 ? a8[i + 4] : a8[i], send = b2 ? a8[i] : a8[i + 4];
-        a4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const double keep = b1 ? a4[i + 2] : a4[i], send = b1 ? a4[i] : a4[i + 2];
-        a2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-    const double keep = b0 ? a2[1] : a2[0], send = b0 ? a2[0] : a2[1];
-    return keep + __shfl_xor_sync(0xffffffffu, send, 1);
-}
-
-template <int u, int PD, bool SH = false, bool FG = false>
+template <int u, int PD, bool FG = false>
 __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab, int t,
                                        int lane, int half, int hl, bool done, double tol, double tol2,
                                        Par* logl, IterState& st) {
     R32P(0, x0[TS(0, u)]);
     const uint32_t code = ctab[t * H + hl];
-    double gsh = 0.0;
-    if constexpr (SH) {
-        double v[H];
-#pragma unroll
-        for (int q = 0; q < H; ++q) v[q] = fma(x1[BS(q, u)], x1[TS(q, u)], x0[BS(q, u)] * x0[TS(q, u)]);
-        gsh = reduce16_half(v, hl);
-        if (st.full) norm_partials<u>(x0, x1, sm.red, lane);
-    }
     __syncwarp();
     // ---- lane hl owns pair k = hl of its half's problem ----
     const int k = hl;
@@ -333,7 +303,7 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
         gt = sm.nrm[half][ct];
         gb = sm.nrm[half][cb];
     }
-    double g = SH ? gsh : sum16(sm.red + k * RSTR + 16 * half);
+    double g = sum16(sm.red + k * RSTR + 16 * half);
     if constexpr (FG) g *= sct * scb;  // dot product of the true columns
     const double absg = fabs(g);
     R32P(1, g);
@@ -395,19 +365,19 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
             if (q + PD < H) pq[q % PD] = sm.pub[half][q + PD];
             apply_any<FG>(x0[TS(q, u)], x0[BS(q, u)], cur.cm1, cur.c);
             apply_any<FG>(x1[TS(q, u)], x1[BS(q, u)], cur.cm1, cur.c);
-            if (!SH && q >= 1) cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs pairs q-2, q
+            if (q >= 1) cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs pairs q-2, q
         }
-        if (!SH) cross_partial<un>(x0, x1, sm.red, lane, H - 1);
-    } else if (!SH) {
+        cross_partial<un>(x0, x1, sm.red, lane, H - 1);
+    } else {
 #pragma unroll
         for (int q = 0; q < H; ++q) cross_partial<un>(x0, x1, sm.red, lane, q);
     }
-    if (!SH && st.full) norm_partials<un>(x0, x1, sm.red, lane);
+    if (st.full) norm_partials<un>(x0, x1, sm.red, lane);
     R32P(3, x1[BS(H - 1, u)]);
 }
 
 // One V replay iteration at offset u (log row t is staged in sm.stage[t & 1]).
-template <int u, int PD, bool ZCHECK = false, bool FG = false>
+template <int u, int PD, bool FG = false>
 __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int t, int half, int hl,
                                        const Par* logl, uint32_t itbits, long long& tl) {
     R32PT(7, x0[TS(0, u)], tl);
@@ -416,13 +386,7 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
     cp_wait<1>();
     __syncwarp();
     R32PT(8, sm.stage[t & 1][half][0].c, tl);
-    bool go;
-    if constexpr (ZCHECK) {  // split replay: skip an iteration whose 32 rotations are all the identity
-        const Par own = sm.stage[t & 1][half][hl];
-        go = __ballot_sync(0xffffffffu, own.cm1 != 0.0 || own.c != 0.0) != 0u;
-    } else {
-        go = (itbits >> t) & 1u;
-    }
+    const bool go = (itbits >> t) & 1u;
     if (go) {
         const Par* stp = sm.stage[t & 1][half];
         Par pr[PD];  // rotations PD ahead, then independent FMAs
@@ -440,36 +404,36 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
     __syncwarp();
 }
 
-template <int U, int PD, bool SH = false, bool FG = false>
+template <int U, int PD, bool FG = false>
 __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab,
                                         int lane, int half, int hl, bool done, double tol, double tol2, Par* logl,
                                         IterState& st) {
     constexpr int NG = (NIT + U - 1) / U;
     constexpr int R = NIT - (NG - 1) * U;  // iterations in the last group
-    if (!SH) all_partials<0>(x0, x1, sm.red, lane, true);  // first iteration of a sweep: fresh norms
+    all_partials<0>(x0, x1, sm.red, lane, true);  // first iteration of a sweep: fresh norms
 #pragma unroll 1
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
         const bool last = gi == NG - 1;
-        w_iter<0, PD, SH, FG>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
+        w_iter<0, PD, FG>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
         if constexpr (U >= 2) {
             if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            w_iter<1 % U, PD, SH, FG>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<1 % U, PD, FG>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
         }
         if constexpr (U >= 3) {
             if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            w_iter<2 % U, PD, SH, FG>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<2 % U, PD, FG>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
         }
         if constexpr (U >= 4) {
             if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            w_iter<3 % U, PD, SH, FG>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
+            w_iter<3 % U, PD, FG>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
         }
         ring_shift<U>(x0);
         ring_shift<U>(x1);
     }
 }
 
-template <int U, int PD, bool ZCHECK = false, bool FG = false>
+template <int U, int PD, bool FG = false>
 __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int half, int hl,
                                         const Par* logl, uint32_t itbits, long long& tl) {
     constexpr int NG = (NIT + U - 1) / U;
@@ -478,26 +442,25 @@ __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSm
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
         const bool last = gi == NG - 1;
-        v_iter<0, PD, ZCHECK, FG>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
+        v_iter<0, PD, FG>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
         if constexpr (U >= 2) {
             if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            v_iter<1 % U, PD, ZCHECK, FG>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
+            v_iter<1 % U, PD, FG>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 3) {
             if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            v_iter<2 % U, PD, ZCHECK, FG>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
+            v_iter<2 % U, PD, FG>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
         }
         if constexpr (U >= 4) {
             if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            v_iter<3 % U, PD, ZCHECK, FG>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
+            v_iter<3 % U, PD, FG>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
         }
         ring_shift<U>(x0);
         ring_shift<U>(x1);
     }
 }
 
-template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true, bool SH = false,
-          bool FG = false>
+template <int NW, int MINB, int U, int UV, int PD, bool FG = false>
 __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -515,17 +478,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     // aliases problem 0's workspace) but may read
     Par* logl = want_v ? logp + hl : nullptr;
     Par* logw = live ? logl : nullptr;
-    // SPLIT: every sweep logged ([sweep][31][16] after a 2-double header), V replayed by k_vreplay
-    double* hdr = wsW + 2 * N * N;
-    if (SPLIT) {
-        logl = want_v ? reinterpret_cast<Par*>(hdr + 2) + hl : nullptr;
-        logw = live ? logl : nullptr;
-    }
     uint32_t* ctab = reinterpret_cast<uint32_t*>(smem_raw + NW * sizeof(WarpSmem));
     for (int e = threadIdx.x; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
     if constexpr (FG) {  // unit scales (the warp's own slots; lane hl: columns 2 hl, 2 hl + 1)
         sm.dsc[half][2 * hl] = sm.dsc[half][2 * hl + 1] = 1.0;
         sm.rds[half][2 * hl] = sm.rds[half][2 * hl + 1] = 1.0;
+        sm.vn[half][2 * hl] = sm.vn[half][2 * hl + 1] = 1.0;
     }
     __syncthreads();
 
@@ -568,8 +526,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         st.itbits = 0;
         st.full = true;  // fresh norms at the start of every sweep
         st.fmask = 0xffffffffu;
-        w_sweep<U, PD, SH, FG>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2,
-                           (SPLIT && logw) ? logw + (size_t)sw * NIT * H : logw, st);
+        w_sweep<U, PD, FG>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, logw, st);
         if constexpr (FG) {
             // back to true columns at the sweep end (the ring is back in place: slot c = column c), so
             // every sweep starts from unit scales and the finalisation sees W and V themselves
@@ -601,13 +558,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         }
         const int partner_done = __shfl_xor_sync(0xffffffffu, done, 16);
         const bool both_done = done && partner_done;
-        if (SPLIT) {
-            if (both_done || sw + 1 == a.max_sweeps) {
-                if (live && hl == 0) hdr[0] = (double)(sw + 1);  // sweeps k_vreplay replays
-                break;
-            }
-            continue;
-        }
         // ======================= V phase: replay the sweep =======================
         if (want_v && st.itbits) {
             if (live) {
@@ -634,7 +584,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
             __syncwarp();  // this warp's log writes are visible to all its lanes
             cp_async16(&sm.stage[0][half][hl], logl);
             cp_commit();
-            v_sweep<UV, PD, false, FG>(x0, x1, sm, half, hl, logl, st.itbits, st.tl);
+            v_sweep<UV, PD, FG>(x0, x1, sm, half, hl, logl, st.itbits, st.tl);
             cp_wait<0>();
             if constexpr (FG) {
 #pragma unroll
@@ -643,6 +593,15 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
                     x0[c] *= dc;
                     x1[c] *= dc;
                 }
+                // column norms of V (the scale roundings W and V share; the finalisation divides them out)
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < N; ++c)
+                    sm.red[c * RSTR + lane] = __dadd_rn(__dmul_rn(x0[c], x0[c]), __dmul_rn(x1[c], x1[c]));
+                __syncwarp();
+                sm.vn[half][2 * hl] = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl) * RSTR + 16 * half));
+                sm.vn[half][2 * hl + 1] = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl + 1) * RSTR + 16 * half));
+                __syncwarp();
             }
             if (live) {
 #pragma unroll
@@ -665,35 +624,48 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     // the standalone finalisation pass: W and V go to the workspace with its flag set.
     double* flagp = wsW + pstride - 1;  // last double of the problem's workspace (log padding)
     bool fused = false;
-    if (!SPLIT && FF) {
+    {
         const double unscale = pow2(ex);
 #pragma unroll
         for (int c = 0; c < N; ++c) sm.red[c * RSTR + lane] = __dadd_rn(__dmul_rn(x0[c], x0[c]), __dmul_rn(x1[c], x1[c]));
         __syncwarp();
         // lane hl: columns 2 hl, 2 hl + 1.  Sigma of the scaled W (ssa); the power-of-two scale is
         // exact, so sa = ssa * 2^ex and x / ssa are the unscaled sigma and quotient.
-        const double ssa = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl) * RSTR + 16 * half));
-        const double ssb = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl + 1) * RSTR + 16 * half));
+        const double wna = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl) * RSTR + 16 * half));
+        const double wnb = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl + 1) * RSTR + 16 * half));
+        // FG: sigma = ||w|| / ||v|| (the column-scale roundings W and V share cancel); U = W / ||w||
+        double ssa = wna, ssb = wnb;
+        bool vok = true;
+        if constexpr (FG) {
+            const double va = sm.vn[half][2 * hl], vb = sm.vn[half][2 * hl + 1];
+            ssa = div_by_sigma(wna, va, rcp_refined(va));
+            ssb = div_by_sigma(wnb, vb, rcp_refined(vb));
+            vok = va >= 0.5 && va <= 2.0 && vb >= 0.5 && vb <= 2.0;
+        }
         const double sa = ssa * unscale, sb = ssb * unscale;
         // holes (sigma < tiny/u), scaled sigmas outside the reciprocal's safe range, and columns whose
         // scaled squares may have left the normal range (sigma < 2^-480 of the problem's scale: the
         // standalone pass rescales per column, like the reference's underflow-safe norms) take the
         // standalone pass
-        const bool tiny = !(sa >= dtiny<double>() && sb >= dtiny<double>() && ssa >= 0x1p-480 && ssb >= 0x1p-480 &&
-                            ssa <= 0x1p+960 && ssb <= 0x1p+960);
+        const bool tiny = !(sa >= dtiny<double>() && sb >= dtiny<double>() && wna >= 0x1p-480 && wnb >= 0x1p-480 &&
+                            wna <= 0x1p+960 && wnb <= 0x1p+960 && vok);
         const unsigned tm = __ballot_sync(0xffffffffu, tiny);
         fused = ((tm >> (16 * half)) & 0xFFFFu) == 0u;
         __syncwarp();
         // [half][32] (scaled sigma, reciprocal) and rank by column, in rows 32.. of red
         double2* sr = reinterpret_cast<double2*>(sm.red + 32 * RSTR) + 32 * half;
         int* rk = reinterpret_cast<int*>(sm.red + 32 * RSTR + 128) + 32 * half;
-        sr[2 * hl] = make_double2(ssa, rcp_refined(ssa));
-        sr[2 * hl + 1] = make_double2(ssb, rcp_refined(ssb));
+        sr[2 * hl] = make_double2(wna, rcp_refined(wna));
+        sr[2 * hl + 1] = make_double2(wnb, rcp_refined(wnb));
+        if constexpr (FG) {
+            sm.sgs[half][2 * hl] = ssa;
+            sm.sgs[half][2 * hl + 1] = ssb;
+        }
         __syncwarp();
         int ra = 0, rb = 0;  // stable descending ranks (finalize.cuh step 4)
 #pragma unroll 8
         for (int c2 = 0; c2 < N; ++c2) {
-            const double s2 = sr[c2].x;
+            const double s2 = FG ? sm.sgs[half][c2] : sr[c2].x;
             ra += sig_before(s2, ssa) || (c2 < 2 * hl && sig_tie(s2, ssa));
             rb += sig_before(s2, ssb) || (c2 < 2 * hl + 1 && sig_tie(s2, ssb));
         }
@@ -732,23 +704,49 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
 #pragma unroll
                 for (int c = 0; c < N; ++c) {
                     const int rc = rk[c];
-                    o.V[r0 + (size_t)rc * o.ldv] = x0[c];
-                    o.V[r1 + (size_t)rc * o.ldv] = x1[c];
+                    double y0 = x0[c], y1 = x1[c];
+                    if constexpr (FG) {
+                        const double vv = sm.vn[half][c], rv = rcp_refined(vv);
+                        y0 = div_by_sigma(y0, vv, rv);
+                        y1 = div_by_sigma(y1, vv, rv);
+                    }
+                    o.V[r0 + (size_t)rc * o.ldv] = y0;
+                    o.V[r1 + (size_t)rc * o.ldv] = y1;
                 }
             }
         }
         if (live && hl == 0) *flagp = fused ? 0.0 : 1.0;
-    } else {
-        (void)flagp;
     }
     if (live && !fused) {
         const double unscale = pow2(ex);
+        if constexpr (FG) {  // W / ||v||, V / ||v|| by column for the standalone pass
 #pragma unroll
-        for (int c = 0; c < N; ++c) {
-            wsW[r0 + c * N] = x0[c] * unscale;
-            wsW[r1 + c * N] = x1[c] * unscale;
+            for (int c = 0; c < N; ++c) {
+                const double vv = sm.vn[half][c], rv = rcp_refined(vv);
+                wsW[r0 + c * N] = div_by_sigma(x0[c], vv, rv) * unscale;
+                wsW[r1 + c * N] = div_by_sigma(x1[c], vv, rv) * unscale;
+            }
+            if (want_v && v_started) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    x0[c] = wsV[r0 + c * N];
+                    x1[c] = wsV[r1 + c * N];
+                }
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    const double vv = sm.vn[half][c], rv = rcp_refined(vv);
+                    wsV[r0 + c * N] = div_by_sigma(x0[c], vv, rv);
+                    wsV[r1 + c * N] = div_by_sigma(x1[c], vv, rv);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                wsW[r0 + c * N] = x0[c] * unscale;
+                wsW[r1 + c * N] = x1[c] * unscale;
+            }
         }
-        if (want_v && !v_started && !SPLIT) {
+        if (want_v && !v_started) {
 #pragma unroll
             for (int c = 0; c < N; ++c) {
                 wsV[r0 + c * N] = (c == r0) ? 1.0 : 0.0;
@@ -772,111 +770,18 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     }
 }
 
-// Split design, second kernel: replay every logged sweep onto V = I (pure FP64 throughput: no
-// dependency chain) and leave V in the workspace.  The log streams from HBM, so it is staged DEPTH
-// iterations ahead with cp.async (one 16-byte rotation per lane per iteration).
-constexpr int VDEPTH = 8;
-struct VSmem {
-    Par stage[VDEPTH][2][H];
-};
-
-template <int u, int PD>
-__device__ __forceinline__ void vr_iter(double (&x0)[N], double (&x1)[N], VSmem& sm, int g, int half, int hl,
-                                        const Par* src, int total) {
-    // issue iteration g + VDEPTH - 1, then wait until iteration g has landed
-    const int gl = g + VDEPTH - 1;
-    if (gl < total) cp_async16(&sm.stage[gl % VDEPTH][half][hl], src + (size_t)gl * H);
-    cp_commit();
-    cp_wait<VDEPTH - 1>();
-    __syncwarp();
-    const Par* stp = sm.stage[g % VDEPTH][half];
-    const Par own = stp[hl];
-    if (__ballot_sync(0xffffffffu, own.cm1 != 0.0 || own.c != 0.0)) {  // all-identity iterations skipped
-        Par pr[PD];
-#pragma unroll
-        for (int q = 0; q < PD; ++q) pr[q] = stp[q];
-#pragma unroll
-        for (int q = 0; q < H; ++q) {
-            const Par pq = pr[q % PD];
-            if (q + PD < H) pr[q % PD] = stp[q + PD];
-            apply2(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
-            apply2(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
-        }
-    }
-    __syncwarp();  // the slot is refilled VDEPTH - 1 iterations later
-}
-
-template <int NW, int MINB, int PD>
-__global__ void __launch_bounds__(NW * 32, MINB) k_vreplay(SolveArgs<double> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    VSmem& sm = reinterpret_cast<VSmem*>(smem_raw)[warp];
-    const int half = lane >> 4, hl = lane & 15;
-    const int prob = (blockIdx.x * NW + warp) * 2 + half;
-    const bool live = prob < a.batch;
-    const int r0 = hl, r1 = hl + 16;
-    const int pair0 = (blockIdx.x * NW + warp) * 2;  // the warp's first problem (always live)
-    double* wsW = a.work + (size_t)(live ? prob : pair0) * (size_t)a.work_stride;
-    double* wsV = wsW + N * N;
-    const double* hdr0 = a.work + (size_t)pair0 * (size_t)a.work_stride + 2 * N * N;
-    const int nsw = (int)hdr0[0];  // both problems of the warp ran the same sweeps in the W kernel
-    const Par* src = reinterpret_cast<const Par*>(wsW + 2 * N * N + 2) + hl;  // [sweep][31][16]
-    const int total = nsw * NIT;
-    double x0[N], x1[N];
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-        x0[c] = (c == r0) ? 1.0 : 0.0;
-        x1[c] = (c == r1) ? 1.0 : 0.0;
-    }
-#pragma unroll
-    for (int d = 0; d < VDEPTH - 1; ++d) {
-        if (d < total) cp_async16(&sm.stage[d][half][hl], src + (size_t)d * H);
-        cp_commit();
-    }
-    int g = 0;
-#pragma unroll 1
-    for (int sw = 0; sw < nsw; ++sw) {
-        // one sweep: 15 pairs of iterations (ring moved by two) and a last one (moved by one)
-#pragma unroll 1
-        for (int gi = 0; gi < 15; ++gi) {
-            vr_iter<0, PD>(x0, x1, sm, g, half, hl, src, total);
-            vr_iter<1, PD>(x0, x1, sm, g + 1, half, hl, src, total);
-            g += 2;
-            ring_shift<2>(x0);
-            ring_shift<2>(x1);
-        }
-        vr_iter<0, PD>(x0, x1, sm, g, half, hl, src, total);
-        g += 1;
-        ring_shift<1>(x0);
-        ring_shift<1>(x1);
-    }
-    cp_wait<0>();
-    if (live) {
-#pragma unroll
-        for (int c = 0; c < N; ++c) {
-            wsV[r0 + c * N] = x0[c];
-            wsV[r1 + c * N] = x1[c];
-        }
-    }
-}
-
 }  // namespace r32b
 
-// variants: (warps per CTA, min CTAs per SM, unroll, per-pair skip)
-bool is_reg32b(int kv) {
-    return (kv >= KV_UNBLOCKED_REG32B && kv <= KV_UNBLOCKED_REG32B_LAST) ||
-           (kv >= KV_UNBLOCKED_REG32G && kv <= KV_UNBLOCKED_REG32G_LAST);
-}
-
-size_t reg32b_work_elems(int kv, int max_sweeps);
+bool is_reg32b(int kv) { return kv == KV_UNBLOCKED_REG32B || kv == KV_UNBLOCKED_REG32G; }
 
 Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant, int max_sweeps) {
     Plan p{};
+    (void)max_sweeps;
     if (dtype == BSVD_D && bm == 32 && bn == 32 && lda_ok) {
         p.kernel = is_reg32b(variant) ? variant : KV_UNBLOCKED_REG32B;
         p.threads = 128;
         p.smem = 4 * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
-        p.work_elems = reg32b_work_elems(p.kernel, max_sweeps);
+        p.work_elems = 2 * 32 * 32 + r32b::LOG_ELEMS;  // W, V, one sweep's rotation log, flag
         p.grid = 0;
         p.resident = 0;
         (void)need_v;
@@ -884,63 +789,27 @@ Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, i
     return p;
 }
 
-// split variants log every sweep: W, V, a 2-double header, max_sweeps x 31 x 16 rotations
-bool reg32b_split(int kv) { return kv == KV_UNBLOCKED_REG32B + 5 || kv == KV_UNBLOCKED_REG32B + 6; }
-size_t reg32b_work_elems(int kv, int max_sweeps) {
-    return reg32b_split(kv) ? 2 * 32 * 32 + 2 + (size_t)max_sweeps * r32b::NIT * r32b::H * 2
-                            : 2 * 32 * 32 + r32b::LOG_ELEMS;
-}
-
-template <int NW, int MINB, int U, int UV, int PD, bool SPLIT = false, bool FF = true, bool SH = false,
-          bool FG = false>
+template <int NW, int MINB, int U, int UV, int PD, bool FG>
 static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
     const int per_cta = 2 * NW;
     const int grid = (a.batch + per_cta - 1) / per_cta;
     const size_t smem = NW * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
-    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD, SPLIT, FF, SH, FG>;
+    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD, FG>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<grid, NW * 32, smem, st>>>(a);
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 
-template <int NW, int MINB, int PD>
-static int launch_vreplay(SolveArgs<double> a, cudaStream_t st) {
-    const int per_cta = 2 * NW;
-    const int grid = (a.batch + per_cta - 1) / per_cta;
-    const size_t smem = NW * sizeof(r32b::VSmem);
-    auto k = r32b::k_vreplay<NW, MINB, PD>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return BSVD_ERR_CUDA;
-    k<<<grid, NW * 32, smem, st>>>(a);
-    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
-}
-
+// 4 warps per CTA, 2 CTAs per SM (255 registers: 8 warps, 16 problems per SM), ring unrolled by 2.
+// Round-1 variants measured slower and retired: a 168-register cap (12 warps/SM, spills), the V ring
+// unrolled by 4, a shuffle-butterfly g_ji reduction, a split W kernel + V replay kernel.
 int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
     a.kernel = p.kernel;
-    a.work_stride = (int64_t)reg32b_work_elems(p.kernel, a.max_sweeps);
-    int rc;
-    switch (p.kernel) {
-        case KV_UNBLOCKED_REG32B + 5:  // split: W kernel (255 regs) + V replay (168 regs, 12 warps/SM)
-            rc = launch_r32b<4, 2, 2, 2, 16, true>(a, st);
-            if (!rc && a.need_v) rc = launch_vreplay<4, 3, 4>(a, st);
-            break;
-        case KV_UNBLOCKED_REG32B + 6:  // split, V replay at 255 registers (8 warps/SM), all rotations ahead
-            rc = launch_r32b<4, 2, 2, 2, 16, true>(a, st);
-            if (!rc && a.need_v) rc = launch_vreplay<4, 2, 16>(a, st);
-            break;
-        case KV_UNBLOCKED_REG32B + 1: rc = launch_r32b<4, 3, 2, 2, 4>(a, st); break;   // 168 regs, 12 warps/SM
-        case KV_UNBLOCKED_REG32B + 2: rc = launch_r32b<4, 2, 2, 4, 16>(a, st); break;  // V unroll 4
-        case KV_UNBLOCKED_REG32B + 3: rc = launch_r32b<4, 2, 2, 2, 16, false, true, true>(a, st); break;  // shuffle g
-        case KV_UNBLOCKED_REG32B + 4: rc = launch_r32b<4, 3, 2, 2, 2>(a, st); break;   // 168 regs, depth 2
-        case KV_UNBLOCKED_REG32B + 7: rc = launch_r32b<4, 2, 2, 2, 16, false, false>(a, st); break;  // unfused finalize
-        case KV_UNBLOCKED_REG32G: rc = launch_r32b<4, 2, 2, 2, 16, false, true, false, true>(a, st); break;  // scaled rotations
-        case KV_UNBLOCKED_REG32G + 1: rc = launch_r32b<4, 2, 2, 2, 8, false, true, false, true>(a, st); break;
-        case KV_UNBLOCKED_REG32G + 2: rc = launch_r32b<4, 3, 2, 2, 4, false, true, false, true>(a, st); break;  // 168 regs
-        default: rc = launch_r32b<4, 2, 2, 2, 16>(a, st); break;                       // 255 regs, 8 warps/SM
-    }
+    a.work_stride = (int64_t)p.work_elems;
+    const int rc = p.kernel == KV_UNBLOCKED_REG32G ? launch_r32b<4, 2, 2, 2, 8, true>(a, st)    // scaled rotations
+                                                   : launch_r32b<4, 2, 2, 2, 16, false>(a, st);
     if (rc) return rc;
-    if (reg32b_split(p.kernel) || p.kernel == KV_UNBLOCKED_REG32B + 7) return launch_finalize_ws<double>(a, st);
     return launch_finalize_flagged<double>(a, st);  // only problems the fused finalisation left over
 }
 

@@ -12,6 +12,7 @@ transpose view of A_b.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -165,7 +166,7 @@ def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: 
         ctypes.byref(o), info.data_ptr(),
         ws.data_ptr() if ws is not None else None, ws_bytes, stream)
     _lib.check(rc, f"bsvd_gesvj_batched({dt.name}, {m}x{n}, batch={B})")
-    kern = L.bsvd_select_kernel(code, m, n, ctypes.byref(o))
+    kern = L.bsvd_select_kernel_batched(code, m, n, B, ctypes.byref(o))  # the batch size can pick the kernel
     return DeviceResult(u=u, s=s, v=v, info=info, kernel=int(kern))
 
 
@@ -203,7 +204,7 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
         info_h.data_ptr() if info_h is not None else None, chunk,
         ws.data_ptr() if ws is not None else None, ws_bytes, arr, len(streams))
     _lib.check(rc, f"bsvd_gesvj_batched_host({dt.name}, {m}x{n}, batch={B})")
-    return int(L.bsvd_select_kernel(code, m, n, ctypes.byref(o)))
+    return int(L.bsvd_select_kernel_batched(code, m, n, min(B, chunk), ctypes.byref(o)))
 
 
 def default_chunk(batch: int, bytes_per_problem: int) -> int:
@@ -226,7 +227,7 @@ def _side_streams(dev, count):
     return lst[:count]
 
 
-_PINNED: dict = {}
+_TLS = threading.local()  # per-thread pinned staging: concurrent batch_svd calls never share buffers
 _POOL = None
 
 
@@ -253,13 +254,17 @@ def _parallel_slices(total: int, fn, min_per: int = 256) -> None:
 
 
 def _pinned(key, shape, tdt):
-    """Pinned staging reused across calls (pinned allocation is slow; results are copied out)."""
+    """Pinned staging reused across calls of the same host thread (pinned allocation is slow; results are
+    copied out before the call returns), so two threads calling batch_svd at once never share it."""
     torch = _torch()
-    buf = _PINNED.get(key)
+    pinned = getattr(_TLS, "pinned", None)
+    if pinned is None:
+        pinned = _TLS.pinned = {}
+    buf = pinned.get(key)
     n = int(np.prod(shape))
     if buf is None or buf.numel() < n or buf.dtype != tdt:
         buf = torch.empty(max(n, 1), dtype=tdt, pin_memory=True)
-        _PINNED[key] = buf
+        pinned[key] = buf
     return buf[:n].view(shape)
 
 

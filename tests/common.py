@@ -84,15 +84,18 @@ def e3(v) -> float:
     return one_norm(np.eye(r, dtype=v.dtype) - v.conj().T @ v) / n if n else 0.0
 
 
-def check_sigma_parity(s, s_ref, n, u, c=2.0):
-    """max |s - s_ref| <= c * n * u * s1_ref (normwise-relative), c = 2."""
+def check_sigma_parity(s, s_ref, n, u, c=1.0):
+    """max |s - s_ref| <= c * n * u * s1_ref (normwise-relative), c = 1, n = min(m, n).
+
+    n is floored at 4: below it the bound is under two ulps of s1, finer than the rounding of the
+    column norm itself (a 2x2 complex problem differs from the reference by 2 ulps of s1)."""
     s = np.asarray(s, dtype=np.float64)
     s_ref = np.asarray(s_ref, dtype=np.float64)
     assert s.shape == s_ref.shape
     if s.size == 0:
         return 0.0
     err = float(np.max(np.abs(s - s_ref)))
-    bound = c * max(n, 1) * u * max(float(s_ref[0]), np.finfo(np.float64).tiny)
+    bound = c * max(n, 4) * u * max(float(s_ref[0]), np.finfo(np.float64).tiny)
     assert err <= bound, f"sigma parity {err:.3e} > {bound:.3e}"
     return err
 
@@ -130,3 +133,14 @@ class Opts:
         self.row_block = 64
         for key, val in kw.items():
             setattr(self, key, val)
+
+
+def check_sigma_vs_reference_or_truth(s, a, s_ref, ref_converged, n, u):
+    """Parity against the reference where it converged; where it stopped at the sweep cap (exactly
+    rank-deficient inputs whose noise columns keep rotating) its own sigma can be tens of u off
+    (oracle vs LAPACK: 36 u sigma_1 on 1e-20 * ones(96, 20) through QR), so there the same bound is
+    taken against float64 LAPACK."""
+    if ref_converged:
+        return check_sigma_parity(s, s_ref, n, u)
+    a64 = np.asarray(a, dtype=np.complex128 if np.iscomplexobj(a) else np.float64)
+    return check_sigma_parity(s, np.linalg.svd(a64, compute_uv=False), n, u)

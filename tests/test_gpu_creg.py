@@ -42,9 +42,9 @@ def test_creg32_vs_oracle(m, route):
     assert (info["kernel"] == 32).all() and info["converged"].all()
     for b in range(B):
         _, s_ref, _, oi = O.solve(A[b], Opts(), route)
-        check_sigma_parity(S[b], s_ref, m, U64)
+        check_sigma_parity(S[b], s_ref, 32, U64)
         check_factors(A[b], U[b], S[b], V[b])
-        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 2
+        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 1
     if route == "blocked":
         assert (info["gram_calls"] == info["outer_sweeps"]).all() and (info["update_calls"] >= 1).all()
     else:
@@ -58,7 +58,7 @@ def test_creg32_public_api_paths(route):
     r = fn(a, bs.JacobiOptions())
     _, s_ref, _, oi = O.solve(a, Opts(), route)
     assert r.info.path == oi["path"] and r.info.converged
-    check_sigma_parity(r.sigma, s_ref, 256, U64)
+    check_sigma_parity(r.sigma, s_ref, 32, U64)
     check_factors(a, r.u, r.sigma, r.v)
 
 
@@ -86,7 +86,7 @@ def test_creg32_rank_deficient_and_edge_inputs():
     assert info["converged"].all() and (info["status"] == 0).all()
     for b in range(B):
         _, s_ref, _, _ = O.solve(A[b], Opts(), None)
-        check_sigma_parity(S[b], s_ref, 256, U64)
+        check_sigma_parity(S[b], s_ref, 32, U64)
         check_factors(A[b], U[b], S[b], V[b])
 
 
@@ -112,7 +112,7 @@ def test_qr_route_uses_creg32_for_r():
     r = bs.svd_qr_preprocessed(a, bs.JacobiOptions())
     assert r.info.path.startswith("qr+")
     _, s_ref, _, _ = O.solve(a, Opts(), None)
-    check_sigma_parity(r.sigma, s_ref, 256, U64)
+    check_sigma_parity(r.sigma, s_ref, 32, U64)
     check_factors(a, r.u, r.sigma, r.v)
     import ctypes
 

@@ -64,3 +64,33 @@ def test_solve_multi_device_gathers_in_global_order(cfg):
     for f in ("converged", "outer_sweeps", "rotations", "last_rotations", "path", "status"):
         assert np.array_equal(gi[f], fi[f]), f  # the kernel id may differ with the slice size, the bits not
     assert out["wall_s"] > 0 and len(out["device_ms"]) == 3
+
+
+def test_concurrent_batch_svd_threads_match_standalone():
+    """Two host threads calling batch_svd at once (the reference's batch_svd is pure numpy and safe to
+    call concurrently): per-thread pinned staging, so each gets exactly its standalone results."""
+    import threading
+
+    from common import random_matrix
+
+    sets = [[random_matrix(32, 32, np.float64, seed=6000 + 100 * t + b) for b in range(300)] for t in range(2)]
+    solo = [bs.batch_svd(ms) for ms in sets]
+    out = [None, None]
+    errs = []
+
+    def work(t):
+        try:
+            for _ in range(3):
+                out[t] = bs.batch_svd(sets[t])
+        except Exception as exc:  # pragma: no cover
+            errs.append(exc)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs
+    for t in range(2):
+        for r, s in zip(out[t], solo[t]):
+            assert np.array_equal(r.sigma, s.sigma) and np.array_equal(r.u, s.u) and np.array_equal(r.v, s.v)

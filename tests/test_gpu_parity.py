@@ -2,7 +2,7 @@
 reference's golden vectors and the CPU restatement on identical inputs.
 
 Tolerances (north star): singular values normwise-relative
-max|s - s_ref| <= n u s1_ref; e1, e2, e3 < 30u (e3 < 100u for double
+max|s - s_ref| <= n u s1_ref with n = min(m, n) (c = 1); e1, e2, e3 < 30u (e3 < 100u for double
 geometric spectra, src/cli.py:209); sorted, converged; outer sweeps within
 one of the reference (guard decisions near threshold can flip with the
 reduction order).
@@ -12,7 +12,8 @@ import numpy as np
 import pytest
 
 import paper_2601_17979_b200 as bs
-from common import ALL_DTYPES, Opts, check_factors, check_sigma_parity, e2, random_matrix, unit_roundoff
+from common import (ALL_DTYPES, Opts, check_factors, check_sigma_parity, check_sigma_vs_reference_or_truth, e2,
+                    random_matrix, unit_roundoff)
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -43,7 +44,7 @@ def test_golden_cases(golden):
         assert res.sigma.dtype == bs.real_dtype(a.dtype)
         assert (res.v is None) == (not c["has_v"])
         if a.size and c["converged"]:  # an unconverged (sweep-capped) solve has no accuracy contract
-            check_sigma_parity(res.sigma, golden.get(cid, "s"), max(m, n), unit_roundoff(a.dtype))
+            check_sigma_parity(res.sigma, golden.get(cid, "s"), min(m, n), unit_roundoff(a.dtype))
             e3k = 100.0 if cid.startswith("c3_") else None
             check_factors(a, res.u, res.sigma, res.v, e3_k=e3k)
         checked += 1
@@ -63,10 +64,9 @@ def test_random_batches_vs_oracle(dt, shape):
         _, s_ref, _, info = O.solve(a, None, None)
         assert r.info.path == info["path"]
         assert r.info.converged
-        # reduction order can flip a guard decision near the threshold: a
-        # flipped late rotation can cost or save a sweep on either side
-        assert abs(r.info.outer_sweeps - info["outer_sweeps"]) <= 2
-        check_sigma_parity(r.sigma, s_ref, max(m, n), uu)
+        # reduction order can flip a guard decision near the threshold: within one sweep
+        assert abs(r.info.outer_sweeps - info["outer_sweeps"]) <= 1
+        check_sigma_parity(r.sigma, s_ref, min(m, n), uu)
         check_factors(a, r.u, r.sigma, r.v)
     assert not st.active.any()
 
@@ -82,8 +82,8 @@ def test_forced_blocked_vs_oracle(dt, nb, shape):
         r = bs.svd_blocked(a, opts)
         _, s_ref, _, info = O.solve(a, Opts(nb=nb), "blocked")
         assert r.info.path == "blocked" and r.info.converged
-        assert abs(r.info.outer_sweeps - info["outer_sweeps"]) <= 2
-        check_sigma_parity(r.sigma, s_ref, max(m, n), unit_roundoff(dt))
+        assert abs(r.info.outer_sweeps - info["outer_sweeps"]) <= 1
+        check_sigma_parity(r.sigma, s_ref, min(m, n), unit_roundoff(dt))
         check_factors(a, r.u, r.sigma, r.v)
         assert r.info.counters.gram_calls == r.info.counters.eig_calls > 0
 
@@ -251,7 +251,7 @@ def test_full_size_c1_properties():
         check_factors(ab, U[b].T, s[b], V[b].T)
         _, s_ref, _, oi = O.solve(ab, None, None)
         check_sigma_parity(s[b], s_ref, n, 2.0 ** -53)
-        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 2
+        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 1
 
 
 @pytest.mark.parametrize("batch", [1, 3, 7, 9, 17])
@@ -261,12 +261,12 @@ def test_reg32_partial_ctas(batch):
     res = bs.batch_svd(mats, bs.JacobiOptions())
     for a, r in zip(mats, res):
         _, s_ref, _, info = O.solve(a, None, None)
-        assert r.info.converged and abs(r.info.outer_sweeps - info["outer_sweeps"]) <= 2
+        assert r.info.converged and abs(r.info.outer_sweeps - info["outer_sweeps"]) <= 1
         check_sigma_parity(r.sigma, s_ref, 32, 2.0 ** -53)
         check_factors(a, r.u, r.sigma, r.v)
 
 
-@pytest.mark.parametrize("kernel", [1, 3, 4, 5, 6, 7, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 26, 27, 28, 29])
+@pytest.mark.parametrize("kernel", [1, 12, 42])
 def test_c1_kernel_variants_agree(kernel):
     """Every 32x32 FP64 kernel variant meets the parity contract on the same inputs."""
     import torch
@@ -283,16 +283,19 @@ def test_c1_kernel_variants_agree(kernel):
     U, S, V = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy(), np.swapaxes(r.v.cpu().numpy(), 1, 2)
     for b in range(0, B, 9):
         _, s_ref, _, oi = O.solve(A[b], None, None)
-        check_sigma_parity(S[b], s_ref, 32, 2.0 ** -53, c=4.0 if kernel == 7 else 2.0)
+        check_sigma_parity(S[b], s_ref, 32, 2.0 ** -53)
+        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 1
         check_factors(A[b], U[b], S[b], V[b])
 
 
 @pytest.mark.parametrize("want_v", [True, False])
 def test_c1_fused_finalize_with_holes(want_v):
-    """The default 32x32 kernel finalises in-kernel; problems with sigma < tiny/u columns (orthogonal
+    """The default 32x32 kernels finalise in-kernel; problems with sigma < tiny/u columns (orthogonal
     completion, src/svd.py:224-240) are flagged to the standalone pass.  Mixed batch: both paths agree
-    with the oracle, and sigma is bitwise equal to the unfused variant (19, same norm order)."""
+    with the oracle (values only: the unscaled kernel 12; with V: scaled rotations, kernel 42)."""
     import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
 
     B = 40
     A = np.stack([random_matrix(32, 32, np.float64, seed=1700 + b) for b in range(B)])
@@ -303,13 +306,10 @@ def test_c1_fused_finalize_with_holes(want_v):
     A[25][:, ::2] = 0.0                   # half the columns zero
     a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
     opts = bs.JacobiOptions(compute_right_vectors=want_v)
-    r = bs.solve_tensor(a, 32, 32, opts, kernel=12)
-    r19 = bs.solve_tensor(a, 32, 32, opts, kernel=19)
+    r = bs.solve_tensor(a, 32, 32, opts)
     torch.cuda.synchronize()
-    assert torch.equal(r.s, r19.s)
-    assert torch.equal(r.u, r19.u)  # fused and standalone finalisation: same sigma, same U formula
-    if want_v:
-        assert torch.equal(r.v, r19.v)
+    info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (info["kernel"] == (42 if want_v else 12)).all()
     U, S = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy()
     V = np.swapaxes(r.v.cpu().numpy(), 1, 2) if want_v else None
     for b in [0, 1, 6, 11, 12, 25, 39]:
@@ -318,7 +318,7 @@ def test_c1_fused_finalize_with_holes(want_v):
         check_factors(A[b], U[b], S[b], V[b] if want_v else None)
 
 
-@pytest.mark.parametrize("kernel", [0, 11, 24, 25, 34, 35, 36])
+@pytest.mark.parametrize("kernel", [0, 24, 34])
 @pytest.mark.parametrize("want_v", [True, False])
 def test_c2_fp32_register_kernel(want_v, kernel):
     """BASELINE C2 shape (16x16 FP32, values-only and full) through the FP32 register kernel."""
@@ -340,7 +340,7 @@ def test_c2_fp32_register_kernel(want_v, kernel):
         _, s_ref, _, oi = O.solve(A[b], Opts(compute_right_vectors=want_v), None)
         check_sigma_parity(S[b], s_ref, 16, u)
         check_factors(A[b], U[b], S[b], V[b] if want_v else None)
-        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 2
+        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 1
 
 
 @pytest.mark.gpu
@@ -413,7 +413,7 @@ print("direct ok")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kernel", [0, 17, 19, 20, 26])
+@pytest.mark.parametrize("kernel", [0, 12, 42])
 def test_problem_results_independent_of_warp_partner(kernel):
     """Two problems share a warp in the 32x32 register kernels; a problem's bits must not depend on its
     partner (the reference's batch == standalone guarantee, tests/test_batch.py:19-28)."""
@@ -434,7 +434,7 @@ def test_problem_results_independent_of_warp_partner(kernel):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kernel", [11, 24, 25, 34, 35, 36])
+@pytest.mark.parametrize("kernel", [24, 34])
 def test_fp32_16x16_results_independent_of_warp_partner(kernel):
     """Several problems share a warp in the 16x16 FP32 register kernels; batch == standalone bitwise
     (tests/test_batch.py:19-28), including a problem whose norms shrink >4x (fresh-norm iterations)."""
@@ -454,7 +454,7 @@ def test_fp32_16x16_results_independent_of_warp_partner(kernel):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kernel", [2, 8, 9, 10, 30, 33])
+@pytest.mark.parametrize("kernel", [2, 8, 9, 10, 30])
 @pytest.mark.parametrize("m,n", [(64, 64), (128, 128), (96, 48)])
 def test_blocked_fp64_kernel_variants(kernel, m, n):
     """Every blocked FP64 kernel variant meets the parity contract against the blocked restatement."""
@@ -472,9 +472,9 @@ def test_blocked_fp64_kernel_variants(kernel, m, n):
     U, S, V = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy(), np.swapaxes(r.v.cpu().numpy(), 1, 2)
     for b in range(B):
         _, s_ref, _, oi = O.solve(A[b], Opts(), "blocked")
-        check_sigma_parity(S[b], s_ref, max(m, n), 2.0 ** -53)
+        check_sigma_parity(S[b], s_ref, min(m, n), 2.0 ** -53)
         check_factors(A[b], U[b], S[b], V[b])
-        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 2
+        assert abs(int(info["outer_sweeps"][b]) - oi["outer_sweeps"]) <= 1
 
 
 
@@ -519,7 +519,7 @@ def test_eig_sweeps_operator_full_solve(dt):
     assert np.max(np.abs(m.conj().T @ m - np.eye(n))) <= 60 * n * u
 
 
-_DEFAULT_KERNEL_SHAPES = [(np.float64, 32, 32, 26),  # small batches: the warp-specialised 32x32 kernel (np.float32, 16, 16, 24), (np.float64, 64, 64, 30),
+_DEFAULT_KERNEL_SHAPES = [(np.float64, 32, 32, 42), (np.float32, 16, 16, 24), (np.float64, 64, 64, 30),
                           (np.complex128, 256, 32, 32), (np.complex128, 40, 24, 1), (np.float32, 48, 48, 2)]
 
 
@@ -547,7 +547,7 @@ def test_every_default_kernel_isolates_nonfinite_problems(dt, m, n, kid):
     S = r.s.cpu().numpy()
     for b in good:
         _, s_ref, _, _ = O.solve(A[b], None, None)
-        check_sigma_parity(S[b], s_ref, max(m, n), unit_roundoff(dt))
+        check_sigma_parity(S[b], s_ref, min(m, n), unit_roundoff(dt))
     # like the reference (no finiteness check on the path), the poisoned problems still return a result
     # record -- NaN-valued -- and never disturb the others
     res = bs.batch_svd(list(A), bs.JacobiOptions())
@@ -593,7 +593,7 @@ def _exactly_rank_deficient(n, dt):
     return np.stack(out).astype(dt)
 
 
-@pytest.mark.parametrize("kernel", [0, 11, 24, 25, 34, 35])
+@pytest.mark.parametrize("kernel", [0, 24, 34])
 def test_fp32_16x16_exactly_rank_deficient(kernel):
     """Exactly rank-deficient 16x16 FP32 inputs: sigma matches the oracle (which, like the reference,
     keeps rotating the noise columns), factors valid, no NaN."""
@@ -611,7 +611,7 @@ def test_fp32_16x16_exactly_rank_deficient(kernel):
         check_factors(A[b], U[b], S[b], V[b])
 
 
-@pytest.mark.parametrize("dt,kernel", [(np.float64, 0), (np.float64, 12), (np.float64, 26), (np.float32, 0)])
+@pytest.mark.parametrize("dt,kernel", [(np.float64, 0), (np.float64, 12), (np.float32, 0)])
 def test_32x32_exactly_rank_deficient(dt, kernel):
     """Same inputs at 32x32 (FP64 register kernels; FP32 general kernel)."""
     import torch
@@ -623,14 +623,18 @@ def test_32x32_exactly_rank_deficient(dt, kernel):
     U, S, V = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy(), np.swapaxes(r.v.cpu().numpy(), 1, 2)
     assert np.isfinite(U).all() and np.isfinite(S).all() and np.isfinite(V).all()
     for b in range(A.shape[0]):
-        _, s_ref, _, _ = O.solve(A[b], Opts(), None)
-        check_sigma_parity(S[b], s_ref, 32, unit_roundoff(dt))
+        _, s_ref, _, oi = O.solve(A[b], Opts(), None)
         if dt == np.float32 and b == 5:
             # all entries 1e-20: the reference's unscaled FP32 dot products underflow once the null
             # columns are noise (its own U has e2 ~ 0.4 here, oracle-checked); the FP32 general kernel
             # follows it, only sigma is comparable
+            check_sigma_parity(S[b], s_ref, 32, unit_roundoff(dt))
             continue
-        check_factors(A[b], U[b], S[b], V[b])
+        check_sigma_vs_reference_or_truth(S[b], A[b], s_ref, oi["converged"], 32, unit_roundoff(dt))
+        if oi["converged"]:
+            check_factors(A[b], U[b], S[b], V[b])
+        # else (outer product, all-ones): the reference stops at the sweep cap with noise columns still
+        # rotating, its own U is not orthonormal; an unconverged solve has no contract beyond sigma
 
 
 def _rank_deficient_mn(m, n, dt):
@@ -672,7 +676,7 @@ def test_exactly_rank_deficient_every_route(dt, m, n, qr):
         o = Opts()
         o.use_qr_preprocess = qr
         u_ref, s_ref, _, oi = O.solve(A[b], o, None)
-        check_sigma_parity(S[b], s_ref, max(m, n), unit_roundoff(dt))
+        check_sigma_vs_reference_or_truth(S[b], A[b], s_ref, oi["converged"], min(m, n), unit_roundoff(dt))
         if oi["converged"]:
             check_factors(A[b], U[b], S[b], V[b])
         # else: the reference itself stops at the sweep cap with noise columns still rotating (outer
@@ -711,7 +715,7 @@ def test_extreme_scales_and_graded_columns(dt, m, n, kernel, qr):
         o = Opts()
         o.use_qr_preprocess = qr
         u_ref, s_ref, _, oi = O.solve(A[b], o, None)
-        check_sigma_parity(S[b], s_ref, max(m, n), unit_roundoff(dt))
+        check_sigma_parity(S[b], s_ref, min(m, n), unit_roundoff(dt))
         if oi["converged"]:
             check_factors(A[b], U[b], S[b], V[b], e3_k=100.0)
 
@@ -740,7 +744,7 @@ def test_register_kernels_beyond_reference_range(dt, m, n, kernel):
     assert np.isfinite(U).all() and np.isfinite(S).all() and np.isfinite(V).all()
     for b in range(A.shape[0]):
         st = np.linalg.svd(A[b].astype(np.complex128 if np.iscomplexobj(A[b]) else np.float64), compute_uv=False)
-        check_sigma_parity(S[b], st, max(m, n), unit_roundoff(dt))
+        check_sigma_parity(S[b], st, min(m, n), unit_roundoff(dt))
         if b < 2:
             check_factors(A[b], U[b], S[b], V[b])
 
@@ -784,10 +788,10 @@ def test_c2_batch_size_kernel_choice_is_bitwise_invisible():
 
 
 @pytest.mark.gpu
-def test_c1_batch_size_kernel_choice_is_bitwise_invisible():
-    """Up to 1,184 32x32 FP64 problems run the warp-specialised kernel (26), more the gen. 2 kernel (12);
-    their arithmetic is bit-identical, so batch == standalone holds across the switch
-    (tests/test_batch.py:19-28), holes and fresh-norm iterations included."""
+def test_c1_one_kernel_at_every_batch_size():
+    """The 32x32 FP64 default (scaled rotations, 42) runs at every batch size, so batch == standalone
+    holds bitwise (tests/test_batch.py:19-28) between a 1,300-problem batch (more than one wave) and a
+    9-problem one, holes, fresh-norm iterations and extreme scales included."""
     import torch
 
     from paper_2601_17979_b200.solver import INFO_DTYPE
@@ -808,9 +812,9 @@ def test_c1_batch_size_kernel_choice_is_bitwise_invisible():
     torch.cuda.synchronize()
     kb = np.frombuffer(big.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"]
     ks = np.frombuffer(small.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"]
-    assert (kb == 12).all() and (ks == 26).all()
+    assert (kb == 42).all() and (ks == 42).all()
     p = torch.tensor(pick).cuda()
     assert torch.equal(big.s[p], small.s) and torch.equal(big.u[p], small.u) and torch.equal(big.v[p], small.v)
     for b in (7, 11, 13, 15):  # and the extreme ones are right (underflow-safe norms, like the reference's)
         st = np.linalg.svd(A[b], compute_uv=False)
-        assert np.max(np.abs(big.s[b].cpu().numpy() - st)) <= 64 * 2.0 ** -53 * st[0]
+        assert np.max(np.abs(big.s[b].cpu().numpy() - st)) <= 32 * 2.0 ** -53 * st[0]

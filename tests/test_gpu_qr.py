@@ -34,7 +34,7 @@ def test_c07_qr_path_equivalence():
         check_factors(a, rq.u, rq.sigma, rq.v)
         assert float(np.max(np.abs(rq.sigma - rd.sigma))) <= 30.0 * u * float(rd.sigma[0])
         _, s_ref, _, _ = O.solve(a, None, "unblocked")
-        check_sigma_parity(rq.sigma, s_ref, 512, u)
+        check_sigma_parity(rq.sigma, s_ref, min(a.shape), u)
 
 
 @pytest.mark.parametrize("dt", ALL_DTYPES)
@@ -54,7 +54,7 @@ def test_qr_route_all_dtypes(dt, shape, want_v):
         assert r.info.path == ("transpose+" if m < n else "") + "qr+" + mode
         assert r.info.converged and r.u.shape == (m, k) and r.sigma.shape == (k,)
         _, s_ref, _, _ = O.solve(a, None, None)  # dispatch without QR: same singular values
-        check_sigma_parity(r.sigma, s_ref, bm, uu)
+        check_sigma_parity(r.sigma, s_ref, min(bm, bn), uu)
         if want_v:
             assert r.v.shape == (n, k)
             check_factors(a, r.u, r.sigma, r.v)

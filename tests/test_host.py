@@ -113,7 +113,10 @@ def test_kernel_selection_routes():
     assert L.bsvd_select_kernel(1, 64, 64, ctypes.byref(o)) == 30     # blocked FP64: register block pairs
     assert L.bsvd_select_kernel(3, 64, 64, ctypes.byref(o)) == 2      # blocked complex: general kernel
     assert L.bsvd_select_kernel(0, 16, 16, ctypes.byref(o)) == 24     # 16x16 FP32 register kernel (2nd gen)
-    assert L.bsvd_select_kernel(1, 32, 32, ctypes.byref(o)) == 12     # 32x32 FP64 register kernel (2nd gen)
+    assert L.bsvd_select_kernel(1, 32, 32, ctypes.byref(o)) == 42     # 32x32 FP64: 2nd gen, scaled rotations
+    o.want_v = 0
+    assert L.bsvd_select_kernel(1, 32, 32, ctypes.byref(o)) == 12     # values only: unscaled 2nd gen
+    o.want_v = 1
     assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) == 32    # c128 n = 32: complex register kernel
     assert L.bsvd_select_kernel(3, 300, 32, ctypes.byref(o)) == 1     # m > 256: general unblocked kernel
     assert L.bsvd_select_kernel(2, 256, 32, ctypes.byref(o)) == 1     # c64: general unblocked kernel

@@ -10,6 +10,7 @@ cfgs = [("C1-10k", "arith", 32, 32, 10000, np.float64, 1e10, True),
         ("C1-1k", "arith", 32, 32, 1000, np.float64, 1e10, True),
         ("C1-3k", "arith", 32, 32, 3000, np.float64, 1e10, True),
         ("C1-1.5k", "arith", 32, 32, 1500, np.float64, 1e10, True),
+        ("C1-1250", "arith", 32, 32, 1250, np.float64, 1e10, True),
         ("C1-2k", "arith", 32, 32, 2000, np.float64, 1e10, True),
         ("C1-2.5k", "arith", 32, 32, 2500, np.float64, 1e10, True),
         ("C1-500", "arith", 32, 32, 500, np.float64, 1e10, True),
