@@ -214,7 +214,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "matrices/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": count / value * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_tag(cfg),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype_tag(cfg),
         "data": "synthetic (device-generated, same generator and seed as the b200 arm)",
         "config": config_block(cfg, args, 1),
         "gflops": statistics.median(fl) / 1e9,
@@ -449,7 +449,7 @@ def run_b200(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": "matrices/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak",
+        "scaling": "strong",
         "vs_baseline": None, "dtype": dtype_tag(cfg),
         "data": f"synthetic ({cfg['family']} spectrum, device-generated; A = U diag(s) V^H for prescribed spectra)",
         "config": dict(config_block(cfg, args, world), gather_ms=gather_ms),

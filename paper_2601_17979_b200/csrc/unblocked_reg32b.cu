@@ -46,6 +46,11 @@ __host__ __device__ constexpr int ring_slot(int q) {  // ring position -> regist
     return q == 0 ? 1 : (q <= H - 1 ? 2 * q : 2 * (2 * H - 1 - q) + 1);
 }
 __host__ __device__ constexpr int md(int a) { return ((a % NIT) + NIT) % NIT; }
+__host__ __device__ constexpr int ring_pos(int s) {  // inverse of ring_slot (s >= 1)
+    return s == 1 ? 0 : ((s & 1) == 0 ? s / 2 : 2 * H - 1 - (s - 1) / 2);
+}
+// slot that register slot s moves to under a ring shift by SH (the fixed column, slot 0, stays)
+__host__ __device__ constexpr int dst_slot(int s, int SH) { return s == 0 ? 0 : ring_slot(md(ring_pos(s) + SH)); }
 // register slot of pair k's top / bottom column at offset u inside an unrolled group
 __host__ __device__ constexpr int TS(int k, int u) { return k == 0 ? 0 : ring_slot(md(k - u)); }
 __host__ __device__ constexpr int BS(int k, int u) { return ring_slot(md((k == 0 ? 0 : NIT - k) - u)); }
@@ -111,6 +116,20 @@ template <bool FG>
 __device__ __forceinline__ void apply_any(double& x, double& y, double p0, double p1) {
     if constexpr (FG) apply_fg(x, y, p0, p1);
     else apply2(x, y, p0, p1);
+}
+// the same update with the ring shift folded in: results go straight to their post-shift registers
+// (nx, ny are slots of a second array), so the loop back-edge needs no register moves
+template <bool FG>
+__device__ __forceinline__ void apply_to(double x, double y, double& nx, double& ny, double p0, double p1) {
+    if constexpr (FG) {
+        nx = fma(p0, y, x);
+        ny = fma(p1, x, y);
+    } else {
+        const double tx = fma(p1, y, x);
+        const double ty = fma(-p1, x, y);
+        nx = fma(p0, x, tx);
+        ny = fma(p0, y, ty);
+    }
 }
 
 __device__ __forceinline__ double sum16(const double* p) {  // 16 consecutive doubles, fixed tree
@@ -273,7 +292,7 @@ __device__ __forceinline__ void all_partials(const double (&x0)[N], const double
 // update is fused with the partials of iteration t + 1 (offset u + 1 in the
 // pre-shift register naming: next pair k = columns of this iteration's pairs
 // k - 1 and k + 1), so they are ready when the next reduction starts.
-template <int u, int PD, bool FG = false>
+template <int u, int PD, bool FG = false, int SH = 0>
 __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab, int t,
                                        int lane, int half, int hl, bool done, double tol, double tol2,
                                        Par* logl, IterState& st) {
@@ -354,30 +373,57 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     }
     st.itbits |= (mask != 0u ? 1u : 0u) << t;
     constexpr int un = u + 1;  // offset of iteration t + 1 (pre-shift naming)
-    if (mask) {
+    if (SH != 0 || mask) {
         // rotations PD ahead (PD = 16: all first) -- the loop interleaves stores to red[]
         Par pq[PD];
 #pragma unroll
         for (int q = 0; q < PD; ++q) pq[q] = sm.pub[half][q];
+        if constexpr (SH == 0) {
 #pragma unroll
-        for (int q = 0; q < H; ++q) {
-            const Par cur = pq[q % PD];
-            if (q + PD < H) pq[q % PD] = sm.pub[half][q + PD];
-            apply_any<FG>(x0[TS(q, u)], x0[BS(q, u)], cur.cm1, cur.c);
-            apply_any<FG>(x1[TS(q, u)], x1[BS(q, u)], cur.cm1, cur.c);
-            if (q >= 1) cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs pairs q-2, q
+            for (int q = 0; q < H; ++q) {
+                const Par cur = pq[q % PD];
+                if (q + PD < H) pq[q % PD] = sm.pub[half][q + PD];
+                apply_any<FG>(x0[TS(q, u)], x0[BS(q, u)], cur.cm1, cur.c);
+                apply_any<FG>(x1[TS(q, u)], x1[BS(q, u)], cur.cm1, cur.c);
+                if (q >= 1) cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs pairs q-2, q
+            }
+            cross_partial<un>(x0, x1, sm.red, lane, H - 1);
+            if (st.full) norm_partials<un>(x0, x1, sm.red, lane);
+        } else {
+            // last iteration of an unrolled group, branch-free: the ring shift by SH = un is folded into
+            // the update (every slot belongs to one pair, so every post-shift register is written by an
+            // FMA; a pair that does not rotate has zero parameters and its FMAs copy exactly), so the
+            // loop back-edge needs no register moves; iteration t + 1 is at offset 0 of the new naming
+            static_assert(SH == un, "the folded shift must bring the next iteration to offset 0");
+            double y0[N], y1[N];
+#pragma unroll
+            for (int q = 0; q < H; ++q) {
+                const Par cur = pq[q % PD];
+                if (q + PD < H) pq[q % PD] = sm.pub[half][q + PD];
+                apply_to<FG>(x0[TS(q, u)], x0[BS(q, u)], y0[dst_slot(TS(q, u), SH)], y0[dst_slot(BS(q, u), SH)],
+                             cur.cm1, cur.c);
+                apply_to<FG>(x1[TS(q, u)], x1[BS(q, u)], y1[dst_slot(TS(q, u), SH)], y1[dst_slot(BS(q, u), SH)],
+                             cur.cm1, cur.c);
+                if (q >= 1) cross_partial<0>(y0, y1, sm.red, lane, q - 1);
+            }
+            cross_partial<0>(y0, y1, sm.red, lane, H - 1);
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                x0[c] = y0[c];
+                x1[c] = y1[c];
+            }
+            if (st.full) norm_partials<0>(x0, x1, sm.red, lane);
         }
-        cross_partial<un>(x0, x1, sm.red, lane, H - 1);
     } else {
 #pragma unroll
         for (int q = 0; q < H; ++q) cross_partial<un>(x0, x1, sm.red, lane, q);
+        if (st.full) norm_partials<un>(x0, x1, sm.red, lane);
     }
-    if (st.full) norm_partials<un>(x0, x1, sm.red, lane);
     R32P(3, x1[BS(H - 1, u)]);
 }
 
 // One V replay iteration at offset u (log row t is staged in sm.stage[t & 1]).
-template <int u, int PD, bool FG = false>
+template <int u, int PD, bool FG = false, int SH = 0>
 __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, int t, int half, int hl,
                                        const Par* logl, uint32_t itbits, long long& tl) {
     R32PT(7, x0[TS(0, u)], tl);
@@ -387,17 +433,35 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
     __syncwarp();
     R32PT(8, sm.stage[t & 1][half][0].c, tl);
     const bool go = (itbits >> t) & 1u;
-    if (go) {
+    if (SH != 0 || go) {  // (the log holds zero parameters for pairs that did not rotate)
         const Par* stp = sm.stage[t & 1][half];
         Par pr[PD];  // rotations PD ahead, then independent FMAs
 #pragma unroll
         for (int q = 0; q < PD; ++q) pr[q] = stp[q];
+        if constexpr (SH == 0) {
 #pragma unroll
-        for (int q = 0; q < H; ++q) {
-            const Par pq = pr[q % PD];
-            if (q + PD < H) pr[q % PD] = stp[q + PD];
-            apply_any<FG>(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
-            apply_any<FG>(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
+            for (int q = 0; q < H; ++q) {
+                const Par pq = pr[q % PD];
+                if (q + PD < H) pr[q % PD] = stp[q + PD];
+                apply_any<FG>(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
+                apply_any<FG>(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
+            }
+        } else {  // ring shift folded into the update (see w_iter)
+            double y0[N], y1[N];
+#pragma unroll
+            for (int q = 0; q < H; ++q) {
+                const Par pq = pr[q % PD];
+                if (q + PD < H) pr[q % PD] = stp[q + PD];
+                apply_to<FG>(x0[TS(q, u)], x0[BS(q, u)], y0[dst_slot(TS(q, u), SH)], y0[dst_slot(BS(q, u), SH)],
+                             pq.cm1, pq.c);
+                apply_to<FG>(x1[TS(q, u)], x1[BS(q, u)], y1[dst_slot(TS(q, u), SH)], y1[dst_slot(BS(q, u), SH)],
+                             pq.cm1, pq.c);
+            }
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                x0[c] = y0[c];
+                x1[c] = y1[c];
+            }
         }
     }
     R32PT(9, x1[BS(H - 1, u)], tl);
@@ -410,26 +474,19 @@ __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSm
                                         IterState& st) {
     constexpr int NG = (NIT + U - 1) / U;
     constexpr int R = NIT - (NG - 1) * U;  // iterations in the last group
+    static_assert(U == 2 && R == 1, "ring unrolled by 2: 15 groups of two iterations and one single");
     all_partials<0>(x0, x1, sm.red, lane, true);  // first iteration of a sweep: fresh norms
 #pragma unroll 1
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
-        const bool last = gi == NG - 1;
         w_iter<0, PD, FG>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
-        if constexpr (U >= 2) {
-            if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            w_iter<1 % U, PD, FG>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
+        if (gi == NG - 1) {  // once per sweep: the shift by one that closes the ring
+            ring_shift<1>(x0);
+            ring_shift<1>(x1);
+            break;
         }
-        if constexpr (U >= 3) {
-            if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            w_iter<2 % U, PD, FG>(x0, x1, sm, ctab, t0 + 2, lane, half, hl, done, tol, tol2, logl, st);
-        }
-        if constexpr (U >= 4) {
-            if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            w_iter<3 % U, PD, FG>(x0, x1, sm, ctab, t0 + 3, lane, half, hl, done, tol, tol2, logl, st);
-        }
-        ring_shift<U>(x0);
-        ring_shift<U>(x1);
+        // the second iteration of the group writes its results straight into the shifted registers
+        w_iter<1, PD, FG, 2>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
     }
 }
 
@@ -438,25 +495,17 @@ __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSm
                                         const Par* logl, uint32_t itbits, long long& tl) {
     constexpr int NG = (NIT + U - 1) / U;
     constexpr int R = NIT - (NG - 1) * U;
+    static_assert(U == 2 && R == 1, "ring unrolled by 2");
 #pragma unroll 1
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
-        const bool last = gi == NG - 1;
         v_iter<0, PD, FG>(x0, x1, sm, t0, half, hl, logl, itbits, tl);
-        if constexpr (U >= 2) {
-            if (R == 1 && last) { ring_shift<1>(x0); ring_shift<1>(x1); break; }
-            v_iter<1 % U, PD, FG>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
+        if (gi == NG - 1) {
+            ring_shift<1>(x0);
+            ring_shift<1>(x1);
+            break;
         }
-        if constexpr (U >= 3) {
-            if (R == 2 && last) { ring_shift<2>(x0); ring_shift<2>(x1); break; }
-            v_iter<2 % U, PD, FG>(x0, x1, sm, t0 + 2, half, hl, logl, itbits, tl);
-        }
-        if constexpr (U >= 4) {
-            if (R == 3 && last) { ring_shift<3>(x0); ring_shift<3>(x1); break; }
-            v_iter<3 % U, PD, FG>(x0, x1, sm, t0 + 3, half, hl, logl, itbits, tl);
-        }
-        ring_shift<U>(x0);
-        ring_shift<U>(x1);
+        v_iter<1, PD, FG, 2>(x0, x1, sm, t0 + 1, half, hl, logl, itbits, tl);
     }
 }
 

@@ -24,14 +24,11 @@ def run(dt, m, n, route=0, kernel=0, B=3, **kw):
     print(dt.__name__, m, n, route, kernel, "ok", float(r.s[0, 0]), flush=True)
 
 
-run(np.float64, 32, 32)                       # r32b + fused finalise
-run(np.float64, 32, 32, kernel=19)            # unfused
-run(np.float64, 32, 32, kernel=20)            # r32c
-run(np.float64, 32, 32, kernel=26)            # reg32e
+run(np.float64, 32, 32)                       # r32b scaled rotations (42) + fused finalise
+run(np.float64, 32, 32, compute_right_vectors=False)  # r32b values only (12)
 run(np.float32, 16, 16)                       # reg16b
-run(np.float32, 16, 16, kernel=11)            # reg16
 run(np.float32, 16, 16, kernel=34, B=9)       # reg16c (quarter-warp)
-run(np.float32, 16, 16, kernel=35, B=5, compute_right_vectors=False)
+run(np.float32, 16, 16, kernel=34, B=5, compute_right_vectors=False)
 run(np.float64, 64, 64)                       # blocked_reg
 run(np.float64, 128, 128, B=2)                # blocked_reg NWG 2
 run(np.complex128, 256, 32, B=2)              # creg32 SP
