@@ -41,6 +41,13 @@ constexpr int H = 16;      // column pairs per iteration
 constexpr int NIT = 31;    // iterations per sweep (ring length)
 constexpr int RSTR = 34;   // doubles per row of the dot-product transpose buffer (bank padding)
 constexpr int LOG_ELEMS = NIT * H * 2 + 32;  // doubles per problem: rotation log (31 x 16 Par) + masks
+constexpr int SB = H + 2;  // slot-state offset of the bottom columns (bank padding)
+constexpr int SLS = 40;    // slot-state doubles per half
+// slot that pair k's top / bottom column occupies in the next iteration: tops move right (the top of
+// pair 15 becomes its bottom), bottoms move left (the bottom of pair 1 becomes pair 0's bottom, whose
+// previous bottom becomes the top of pair 1), the fixed column stays the top of pair 0
+__host__ __device__ constexpr int next_top(int k) { return k == 0 ? 0 : (k == H - 1 ? SB + H - 1 : k + 1); }
+__host__ __device__ constexpr int next_bot(int k) { return k == 0 ? 1 : (k == 1 ? SB : SB + k - 1); }
 
 __host__ __device__ constexpr int ring_slot(int q) {  // ring position -> register slot at t = 0
     return q == 0 ? 1 : (q <= H - 1 ? 2 * q : 2 * (2 * H - 1 - q) + 1);
@@ -63,9 +70,12 @@ struct WarpSmem {
     double red[3 * H * RSTR];  // dot-product transpose
     Par pub[2][H];             // this iteration's rotations, [half][pair]
     Par stage[2][2][H];        // V replay: double-buffered log rows [buf][half][pair]
-    double nrm[2][N];          // maintained squared column norms [half][column]
-    double dsc[2][N];          // FG: column scale factors d (true column = d * stored column) [half][column]
-    double rds[2][N];          // FG: 1 / d
+    // per-column state indexed by pair slot (top of pair k: k, bottom: SB + k) and moved along the
+    // tournament each iteration, so that lane k's reads and writes are bank-conflict free (indexed by
+    // column id they were 3.9 wavefronts per access instead of 2, profiles/r2_ncu_c1_k42.txt)
+    double nrm[2][SLS];        // maintained squared column norms [half][slot]
+    double dsc[2][SLS];        // FG: column scale factors d (true column = d * stored column) [half][slot]
+    double rds[2][SLS];        // FG: 1 / d
     double dv[2][N];           // FG: d at the end of the W sweep, applied to V after its replay
     double vn[2][N];           // FG: column norms of V after its latest replay (1 before the first)
     double sgs[2][N];          // FG finalisation: sigma of the scaled problem = ||w|| / ||v||
@@ -304,12 +314,14 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     const int ct = code & 0xff, cb = (code >> 8) & 0xff;
     const bool flip = (code >> 16) != 0;
     double gt, gb;
+    (void)ct;
+    (void)cb;
     double sct = 1.0, scb = 1.0, rst = 1.0, rsb = 1.0;  // FG: scale factors of the pair's columns
     if constexpr (FG) {
-        sct = sm.dsc[half][ct];
-        scb = sm.dsc[half][cb];
-        rst = sm.rds[half][ct];
-        rsb = sm.rds[half][cb];
+        sct = sm.dsc[half][k];
+        scb = sm.dsc[half][SB + k];
+        rst = sm.rds[half][k];
+        rsb = sm.rds[half][SB + k];
     }
     if (st.full && ((st.fmask >> lane) & 1u)) {
         gt = sum16(sm.red + (H + 2 * k) * RSTR + 16 * half);
@@ -319,8 +331,8 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
             gb *= scb * scb;
         }
     } else {
-        gt = sm.nrm[half][ct];
-        gb = sm.nrm[half][cb];
+        gt = sm.nrm[half][k];
+        gb = sm.nrm[half][SB + k];
     }
     double g = sum16(sm.red + k * RSTR + 16 * half);
     if constexpr (FG) g *= sct * scb;  // dot product of the true columns
@@ -356,13 +368,16 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     R32P(6, sm.pub[half][0].c);
     const double dtg = rot ? xor_sign(tabs * absg, eneg) : 0.0;
     const double nt = gt + dtg, nb = gb - dtg;
-    sm.nrm[half][ct] = nt;
-    sm.nrm[half][cb] = nb;
-    if (FG && rot) {
-        sm.dsc[half][ct] = cc * sct;
-        sm.dsc[half][cb] = cc * scb;
-        sm.rds[half][ct] = icc * rst;
-        sm.rds[half][cb] = icc * rsb;
+    {  // the pair's column state moves to the columns' slots of iteration t + 1
+        const int dt = next_top(k), db = next_bot(k);
+        sm.nrm[half][dt] = nt;
+        sm.nrm[half][db] = nb;
+        if constexpr (FG) {
+            sm.dsc[half][dt] = rot ? cc * sct : sct;
+            sm.dsc[half][db] = rot ? cc * scb : scb;
+            sm.rds[half][dt] = rot ? icc * rst : rst;
+            sm.rds[half][db] = rot ? icc * rsb : rsb;
+        }
     }
     const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
     st.my_rot += rot ? 1 : 0;
@@ -529,9 +544,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     Par* logw = live ? logl : nullptr;
     uint32_t* ctab = reinterpret_cast<uint32_t*>(smem_raw + NW * sizeof(WarpSmem));
     for (int e = threadIdx.x; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
-    if constexpr (FG) {  // unit scales (the warp's own slots; lane hl: columns 2 hl, 2 hl + 1)
-        sm.dsc[half][2 * hl] = sm.dsc[half][2 * hl + 1] = 1.0;
-        sm.rds[half][2 * hl] = sm.rds[half][2 * hl + 1] = 1.0;
+    if constexpr (FG) {  // unit scales (the warp's own slots; lane hl: pair hl's two slots, columns 2 hl, 2 hl + 1)
+        sm.dsc[half][hl] = sm.dsc[half][SB + hl] = 1.0;
+        sm.rds[half][hl] = sm.rds[half][SB + hl] = 1.0;
         sm.vn[half][2 * hl] = sm.vn[half][2 * hl + 1] = 1.0;
     }
     __syncthreads();
@@ -579,20 +594,25 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         if constexpr (FG) {
             // back to true columns at the sweep end (the ring is back in place: slot c = column c), so
             // every sweep starts from unit scales and the finalisation sees W and V themselves
+            // the state is in the slots of iteration 0 again: lane hl holds the scales of columns
+            // code(0, hl); d by column id into dv, then unit scales for the next sweep
+            __syncwarp();
+            {
+                const uint32_t c0 = ctab[hl];
+                sm.dv[half][c0 & 0xff] = sm.dsc[half][hl];
+                sm.dv[half][(c0 >> 8) & 0xff] = sm.dsc[half][SB + hl];
+                sm.dsc[half][hl] = sm.dsc[half][SB + hl] = 1.0;
+                sm.rds[half][hl] = sm.rds[half][SB + hl] = 1.0;
+            }
             __syncwarp();
             if (st.itbits) {
 #pragma unroll
                 for (int c = 0; c < N; ++c) {
-                    const double dc = sm.dsc[half][c];
+                    const double dc = sm.dv[half][c];
                     x0[c] *= dc;
                     x1[c] *= dc;
                 }
             }
-            __syncwarp();
-            sm.dv[half][2 * hl] = sm.dsc[half][2 * hl];
-            sm.dv[half][2 * hl + 1] = sm.dsc[half][2 * hl + 1];
-            sm.dsc[half][2 * hl] = sm.dsc[half][2 * hl + 1] = 1.0;
-            sm.rds[half][2 * hl] = sm.rds[half][2 * hl + 1] = 1.0;
             __syncwarp();
         }
         // ---- sweep end: per-problem rotation count over the half warp ----
