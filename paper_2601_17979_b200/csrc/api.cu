@@ -56,8 +56,8 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
     const size_t lim = smem_limit();
     const int es = esize_of(dt), rs = rsize_of(dt);
     const bool reg_ok = contiguous && !r.trans;  // register kernels: dense column-major input, no transpose
-    if (o->kernel == 0 || o->kernel == KV_CREG32) {  // complex FP64, n = 32: both routes
-        Plan p = plan_creg32(dt, r.bm, r.bn, r.need_v, reg_ok, r.blocked, o->nb);
+    if (o->kernel == 0 || o->kernel == KV_CREG32 || o->kernel == KV_CREG32_TMA) {  // complex FP64, n = 32: both routes
+        Plan p = plan_creg32(dt, r.bm, r.bn, r.need_v, reg_ok, r.blocked, o->nb, o->kernel, lim);
         if (p.kernel) return p;
         if (o->kernel != 0) return p;
     }
@@ -168,6 +168,7 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_blocked_reg(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_CREG32:
+        case KV_CREG32_TMA:
             if constexpr (sizeof(T) == 16 && tr<T>::cplx) return launch_creg32(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_BLOCKED_DMMA:

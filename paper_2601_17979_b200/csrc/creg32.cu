@@ -32,9 +32,12 @@
 // V never leaves shared memory: since V starts as I and only ever gets
 // right-multiplied by the rotations, V = P, the running product, updated
 // every iteration by all threads (one (row, pair) task each) in smem.
+#include <algorithm>
+
 #include "kernel_args.cuh"
 #include "launch.h"
 #include "rotation.cuh"
+#include "tma.cuh"
 
 namespace bsvd {
 namespace creg {
@@ -294,16 +297,31 @@ __device__ __forceinline__ void sweep(double (&xr)[N], double (&xi)[N], const Ct
     }
 }
 
-inline size_t smem_bytes(int nw, bool sp) {
+__host__ __device__ inline size_t smem_bytes(int nw, bool sp) {
     return (size_t)nw * sizeof(WarpSmem) + sizeof(CtaSmem) + (sp ? sizeof(PSmem) : 0) + NIT * H * 4;
+}
+// TMA loader: staging for one whole problem (m x 32 complex) plus its mbarrier, behind the rest
+__host__ __device__ inline size_t stage_offset(int nw, bool sp) { return (smem_bytes(nw, sp) + 127) & ~(size_t)127; }
+// columns staged: as many as fit beside the kernel's own shared memory (C4, 256 x 32 with V as P in
+// smem: 31 of 32; the last column is then read directly)
+inline int staged_cols(int nw, bool sp, int m, size_t limit) {
+    const size_t col = (size_t)m * sizeof(cx<double>);
+    const size_t base = stage_offset(nw, sp) + 16;
+    return limit <= base ? 0 : (int)std::min<size_t>(N, (limit - base) / col);
+}
+inline size_t smem_bytes_tma(int nw, bool sp, int m, int ncs) {
+    return stage_offset(nw, sp) + (size_t)m * ncs * sizeof(cx<double>) + 16;
 }
 
 // NW warps; SP: V as the smem product P (m > 224), else V rows ride along in registers below
 // W's rows (rows m .. m + 31 of the CTA, rotated like W, excluded from the dot products).
-template <int NW, bool SP>
-__global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_creg32(SolveArgs<cx<double>> a, int blocked) {
+// TMA: persistent CTAs; kernel (1) stages each problem into shared memory with 32 bulk copies (one
+// column each, cp.async.bulk -> UBLKCP) completing on an mbarrier, and the next problem of the CTA is
+// already in flight while this one is solved.  Without TMA: one CTA per problem, coalesced LDG.
+template <int NW, bool SP, bool TMA>
+__global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1)
+    k_creg32(SolveArgs<cx<double>> a, int blocked, int ncs) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int prob = blockIdx.x;
     const int m = a.bm;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem);
@@ -311,144 +329,180 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_creg32
     PSmem* ps = reinterpret_cast<PSmem*>(smem + NW * sizeof(WarpSmem) + sizeof(CtaSmem));
     uint32_t* ctab =
         reinterpret_cast<uint32_t*>(smem + NW * sizeof(WarpSmem) + sizeof(CtaSmem) + (SP ? sizeof(PSmem) : 0));
+    cx<double>* stg = reinterpret_cast<cx<double>*>(smem + stage_offset(NW, SP));
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(stg + (size_t)m * ncs);
     const bool want_p = a.need_v != 0;
     for (int e = tid; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
-    for (int e = lane; e < 2 * H * RSTR; e += 32) wsm[warp].red[e] = 0.0;  // V / padding lanes stay 0
-    if (tid < 4) cs->misc[tid] = 0;
-    if (SP && want_p)
-        for (int e = tid; e < N * N; e += NW * 32) {
-            const int r = e % N, col = e / N;
-            ps->P[col * N + r] = make_double2((r == col) ? 1.0 : 0.0, 0.0);
+    const uint32_t stage_bytes = (uint32_t)(m * sizeof(cx<double>));
+    // warp 0 puts problem q's first ncs columns in flight (lane = column)
+    auto issue = [&](int q) {
+        if (lane == 0) tma::mbar_arrive_expect(mbar, stage_bytes * ncs);
+        __syncwarp();
+        if (lane < ncs)
+            tma::bulk_g2s(stg + (size_t)lane * m, a.A + (size_t)q * a.strideA + (size_t)lane * a.lda, stage_bytes,
+                          mbar);
+    };
+    if constexpr (TMA) {
+        if (tid == 0) {
+            tma::mbar_init(mbar, 1);
+            tma::fence_mbar_init();
         }
-    // ---- kernel (1): this lane's row of A, exact power-of-two prescale ----
-    const int row = warp * 32 + lane;
-    const bool live = row < m;
-    const int vrow = (!SP && want_p && row >= m && row < m + N) ? row - m : -1;  // row of V this lane holds
-    const cx<double>* Ap = a.A + (size_t)prob * a.strideA;
-    double xr[N], xi[N];
-    double amax = 0.0;
-    int bad = 0;
-#pragma unroll
-    for (int col = 0; col < N; ++col) {
-        cx<double> z{0.0, 0.0};
-        if (live) z = Ap[row + (size_t)col * a.lda];
-        xr[col] = z.re;
-        xi[col] = z.im;
-        bad |= !(isfinite(z.re) && isfinite(z.im));
-        amax = fmax(amax, fmax(fabs(z.re), fabs(z.im)));
-    }
-    __syncthreads();
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-    }
-    if (lane == 0) {
-        if (bad) atomicOr(&cs->misc[0], 1);
-        atomicMax(reinterpret_cast<unsigned long long*>(&cs->misc[2]), (unsigned long long)__double_as_longlong(amax));
-    }
-    __syncthreads();
-    const int ex = prescale_exponent(__longlong_as_double(*reinterpret_cast<long long*>(&cs->misc[2])));
-    {
-        const double sc = pow2(-ex);
-#pragma unroll
-        for (int col = 0; col < N; ++col) {
-            xr[col] = vrow >= 0 ? (col == vrow ? 1.0 : 0.0) : xr[col] * sc;  // V = I
-            xi[col] *= sc;
-        }
-    }
-    Ctx c;
-    c.sm = &wsm[warp];
-    c.cs = cs;
-    c.ctab = ctab;
-    c.lane = lane;
-    c.half = lane >> 4;
-    c.k = lane & 15;
-    c.warp = warp;
-    c.ps = ps;
-    c.nww = (m + 31) / 32;
-    c.wrow = live;
-    c.tol = a.tol;
-    c.tol2 = a.tol * a.tol;
-    c.want_p = want_p;
-    const int budget = blocked ? a.inner_budget : 1;
-    int sweeps = 0, last = 0, conv = 0;
-    long long rot_total = 0, grams = 0, updates = 0;
-    IState st;
-    st.par = 0;
-#pragma unroll 1
-    for (int sw = 0; sw < a.max_sweeps; ++sw) {
-        int bp_rot = 0;
-#pragma unroll 1
-        for (int isw = 0; isw < budget; ++isw) {
-            st.my_rot = 0;
-            sweep<NW, SP>(xr, xi, c, st);
-            int r = st.my_rot;  // lanes 0..15: counts of pairs 0..15 (identical in every warp)
-#pragma unroll
-            for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-            r = __shfl_sync(0xffffffffu, r, 0);
-            bp_rot += r;
-            if (r == 0) break;
-        }
-        ++grams;
-        updates += bp_rot ? 1 : 0;
-        sweeps = sw + 1;
-        last = bp_rot;
-        rot_total += bp_rot;
-        if (bp_rot == 0) {
-            conv = 1;
-            break;
-        }
-    }
-    // ---- raw W (unscaled) and V = P to the workspace for the finalisation pass ----
-    cx<double>* W = a.work + (size_t)prob * (size_t)a.work_stride;
-    if (live) {
-        const double us = pow2(ex);
-#pragma unroll
-        for (int col = 0; col < N; ++col) W[row + (size_t)col * m] = cx<double>{xr[col] * us, xi[col] * us};
-    }
-    if (SP && want_p) {
         __syncthreads();
-        cx<double>* V = W + (size_t)m * N;
-        for (int e = tid; e < N * N; e += NW * 32) {
-            const int r = e % N, col = e / N;
-            const double2 z = ps->P[col * N + r];
-            V[e] = cx<double>{z.x, z.y};
+        if (warp == 0 && blockIdx.x < a.batch) issue(blockIdx.x);
+    }
+    uint32_t phase = 0;
+#pragma unroll 1
+    for (int prob = blockIdx.x; prob < a.batch; prob = a.batch) {  // one problem per CTA
+        for (int e = lane; e < 2 * H * RSTR; e += 32) wsm[warp].red[e] = 0.0;  // V / padding lanes stay 0
+        if (tid < 4) cs->misc[tid] = 0;
+        if (SP && want_p)
+            for (int e = tid; e < N * N; e += NW * 32) {
+                const int r = e % N, col = e / N;
+                ps->P[col * N + r] = make_double2((r == col) ? 1.0 : 0.0, 0.0);
+            }
+        // ---- kernel (1): this lane's row of A, exact power-of-two prescale ----
+        const int row = warp * 32 + lane;
+        const bool live = row < m;
+        const int vrow = (!SP && want_p && row >= m && row < m + N) ? row - m : -1;  // row of V this lane holds
+        double xr[N], xi[N];
+        double amax = 0.0;
+        int bad = 0;
+        if constexpr (TMA) {
+            tma::mbar_wait(mbar, phase);
+            phase ^= 1u;
         }
-    }
-    if (vrow >= 0) {
-        cx<double>* V = W + (size_t)m * N;
+        {
+            const cx<double>* Ap = a.A + (size_t)prob * a.strideA;
 #pragma unroll
-        for (int col = 0; col < N; ++col) V[vrow + (size_t)col * N] = cx<double>{xr[col], xi[col]};
-    }
-    if (tid == 0 && a.info) {
-        bsvd_info inf;
-        inf.converged = conv;
-        inf.outer_sweeps = sweeps;
-        inf.rotations = rot_total;
-        inf.gram_calls = blocked ? grams : 0;
-        inf.update_calls = blocked ? updates : 0;
-        inf.last_rotations = last;
-        inf.path = blocked ? 2 : 1;
-        inf.status = cs->misc[0] ? 1 : 0;
-        inf.kernel = a.kernel;
-        a.info[prob] = inf;
+            for (int col = 0; col < N; ++col) {
+                cx<double> z{0.0, 0.0};
+                if (live) z = (TMA && col < ncs) ? stg[row + (size_t)col * m] : Ap[row + (size_t)col * a.lda];
+                xr[col] = z.re;
+                xi[col] = z.im;
+                bad |= !(isfinite(z.re) && isfinite(z.im));
+                amax = fmax(amax, fmax(fabs(z.re), fabs(z.im)));
+            }
+        }
+        __syncthreads();  // (TMA) every lane has its row: the staging buffer is free
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        }
+        if (lane == 0) {
+            if (bad) atomicOr(&cs->misc[0], 1);
+            atomicMax(reinterpret_cast<unsigned long long*>(&cs->misc[2]),
+                      (unsigned long long)__double_as_longlong(amax));
+        }
+        __syncthreads();
+        const int ex = prescale_exponent(__longlong_as_double(*reinterpret_cast<long long*>(&cs->misc[2])));
+        {
+            const double sc = pow2(-ex);
+#pragma unroll
+            for (int col = 0; col < N; ++col) {
+                xr[col] = vrow >= 0 ? (col == vrow ? 1.0 : 0.0) : xr[col] * sc;  // V = I
+                xi[col] *= sc;
+            }
+        }
+        Ctx c;
+        c.sm = &wsm[warp];
+        c.cs = cs;
+        c.ctab = ctab;
+        c.lane = lane;
+        c.half = lane >> 4;
+        c.k = lane & 15;
+        c.warp = warp;
+        c.ps = ps;
+        c.nww = (m + 31) / 32;
+        c.wrow = live;
+        c.tol = a.tol;
+        c.tol2 = a.tol * a.tol;
+        c.want_p = want_p;
+        const int budget = blocked ? a.inner_budget : 1;
+        int sweeps = 0, last = 0, conv = 0;
+        long long rot_total = 0, grams = 0, updates = 0;
+        IState st;
+        st.par = 0;
+#pragma unroll 1
+        for (int sw = 0; sw < a.max_sweeps; ++sw) {
+            int bp_rot = 0;
+#pragma unroll 1
+            for (int isw = 0; isw < budget; ++isw) {
+                st.my_rot = 0;
+                sweep<NW, SP>(xr, xi, c, st);
+                int r = st.my_rot;  // lanes 0..15: counts of pairs 0..15 (identical in every warp)
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+                r = __shfl_sync(0xffffffffu, r, 0);
+                bp_rot += r;
+                if (r == 0) break;
+            }
+            ++grams;
+            updates += bp_rot ? 1 : 0;
+            sweeps = sw + 1;
+            last = bp_rot;
+            rot_total += bp_rot;
+            if (bp_rot == 0) {
+                conv = 1;
+                break;
+            }
+        }
+        // ---- raw W (unscaled) and V = P to the workspace for the finalisation pass ----
+        cx<double>* W = a.work + (size_t)prob * (size_t)a.work_stride;
+        if (live) {
+            const double us = pow2(ex);
+#pragma unroll
+            for (int col = 0; col < N; ++col) W[row + (size_t)col * m] = cx<double>{xr[col] * us, xi[col] * us};
+        }
+        if (SP && want_p) {
+            __syncthreads();
+            cx<double>* V = W + (size_t)m * N;
+            for (int e = tid; e < N * N; e += NW * 32) {
+                const int r = e % N, col = e / N;
+                const double2 z = ps->P[col * N + r];
+                V[e] = cx<double>{z.x, z.y};
+            }
+        }
+        if (vrow >= 0) {
+            cx<double>* V = W + (size_t)m * N;
+#pragma unroll
+            for (int col = 0; col < N; ++col) V[vrow + (size_t)col * N] = cx<double>{xr[col], xi[col]};
+        }
+        if (tid == 0 && a.info) {
+            bsvd_info inf;
+            inf.converged = conv;
+            inf.outer_sweeps = sweeps;
+            inf.rotations = rot_total;
+            inf.gram_calls = blocked ? grams : 0;
+            inf.update_calls = blocked ? updates : 0;
+            inf.last_rotations = last;
+            inf.path = blocked ? 2 : 1;
+            inf.status = cs->misc[0] ? 1 : 0;
+            inf.kernel = a.kernel;
+            a.info[prob] = inf;
+        }
+        __syncthreads();  // shared state (red, misc, P, gsum) is re-initialised for the next problem
     }
 }
 
 }  // namespace creg
 
-Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blocked, int nb) {
+Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blocked, int nb, int variant,
+                 size_t smem_limit) {
     Plan p{};
     if (dtype != BSVD_Z || bn != 32 || bm < 32 || bm > 256 || !contiguous) return p;
     if (blocked && nb != 16) return p;  // one block pair = the whole matrix only when nb = 16
     const int rows = bm + (need_v ? 32 : 0);  // V rows ride in registers when they fit
     const bool sp = rows > 256;
     const int nw = ((sp ? bm : rows) + 31) / 32;
-    p.kernel = KV_CREG32;
+    p.kernel = variant == KV_CREG32_TMA ? KV_CREG32_TMA : KV_CREG32;
     p.threads = nw * 32;
     p.group = nw | (sp ? 0x100 : 0);
     p.smem = creg::smem_bytes(nw, sp);
+    if (p.kernel == KV_CREG32_TMA) {
+        p.aux = creg::staged_cols(nw, sp, bm, smem_limit);
+        p.smem = creg::smem_bytes_tma(nw, sp, bm, p.aux);
+    }
     p.work_elems = (size_t)bm * bn + (need_v ? (size_t)bn * bn : 0);
     p.grid = 0;
     p.resident = blocked ? 1 : 0;  // route flag for the launcher
@@ -457,10 +511,10 @@ Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blo
 
 template <int NW, bool SP>
 static int launch_c(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st) {
-    auto k = creg::k_creg32<NW, SP>;
+    auto k = p.kernel == KV_CREG32_TMA ? creg::k_creg32<NW, SP, true> : creg::k_creg32<NW, SP, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
-    k<<<a.batch, NW * 32, p.smem, st>>>(a, p.resident);
+    k<<<a.batch, NW * 32, p.smem, st>>>(a, p.resident, p.aux);
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 

@@ -18,6 +18,7 @@ struct Plan {
     int threads;        // CTA size
     int group;          // lanes per pair (general unblocked)
     int grid;           // CTAs (0 = one per problem)
+    int aux;            // kernel-specific (creg32: columns staged by the bulk-copy loader)
 };
 
 Plan plan_unblocked_general(int esize, int rsize, int bm, int bn, int need_v, size_t smem_limit);
@@ -80,7 +81,8 @@ Plan plan_unblocked_reg16b(int dtype, int bm, int bn, int need_v, bool lda_ok, i
 int launch_unblocked_reg16b(SolveArgs<float> a, const Plan& p, cudaStream_t st);
 Plan plan_unblocked_reg16c(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant);
 int launch_unblocked_reg16c(SolveArgs<float> a, const Plan& p, cudaStream_t st);
-Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blocked, int nb);
+Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blocked, int nb, int variant,
+                 size_t smem_limit);
 int launch_creg32(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st);
 
 int group_for_rows(int bm);

@@ -121,3 +121,21 @@ def test_qr_route_uses_creg32_for_r():
 
     o = make_opts(bs.JacobiOptions(use_qr_preprocess=True))
     assert _lib.load().bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) == 32
+
+
+@pytest.mark.parametrize("m", [32, 100, 256])
+@pytest.mark.parametrize("route", [None, "blocked"])
+def test_creg32_tma_loader_bitwise(m, route):
+    """Kernel (1) through bulk copies (cp.async.bulk into shared memory, KV_CREG32_TMA = 45) loads the
+    same bits as the LDG loader: every output identical to the default kernel's."""
+    import torch
+
+    B = 5
+    A = np.stack([random_matrix(m, 32, np.complex128, seed=4500 + 3 * b + m) for b in range(B)])
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r0 = bs.solve_tensor(a, m, 32, bs.JacobiOptions(), route=ROUTE[route])
+    r1 = bs.solve_tensor(a, m, 32, bs.JacobiOptions(), route=ROUTE[route], kernel=45)
+    torch.cuda.synchronize()
+    assert torch.equal(r0.u, r1.u) and torch.equal(r0.s, r1.s) and torch.equal(r0.v, r1.v)
+    _, s_ref, _, _ = O.solve(A[0], Opts(), route)
+    check_sigma_parity(r1.s[0].cpu().numpy(), s_ref, 32, U64)
