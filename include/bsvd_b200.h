@@ -119,6 +119,22 @@ int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch,
                             int chunk, void* work, size_t work_bytes,
                             void* const* streams, int nstreams);
 
+/*
+ * bsvd_gesvj_batched_host for a LIST of host matrices (the reference's batch_svd input, a list of
+ * column-major m x n problems, src/batch.py:85-157): A_ptrs[b] points at problem b (m*n contiguous
+ * column-major elements, any host memory); A_stage is page-locked host memory of batch*m*n elements
+ * that receives the packed batch.  `pack_threads` host threads pack chunk after chunk while the
+ * pipeline transfers and solves the chunks already packed, so packing overlaps the device work.
+ * Outputs, streams and workspace as for bsvd_gesvj_batched_host; returns after every chunk is packed
+ * and enqueued (A_ptrs may be released then; A_stage only after streams[0] completes).
+ */
+int bsvd_gesvj_batched_host_gather(int dtype, int m, int n, int batch,
+                                   const void* const* A_ptrs, void* A_stage, int pack_threads,
+                                   void* U, void* S, void* V,
+                                   const bsvd_opts* opts, bsvd_info* info,
+                                   int chunk, void* work, size_t work_bytes,
+                                   void* const* streams, int nstreams);
+
 /* Device scratch needed by bsvd_gesvj_batched_host for (chunk, nstreams). */
 size_t bsvd_host_workspace_bytes(int dtype, int m, int n, int chunk, int nstreams, const bsvd_opts* opts);
 

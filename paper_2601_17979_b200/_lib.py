@@ -70,6 +70,7 @@ EXPORTS = (
     "bsvd_verify_batched",
     "bsvd_finalize_batched",
     "bsvd_pack_host",
+    "bsvd_gesvj_batched_host_gather",
     "bsvd_eig_sweeps_batched",
     "bsvd_householder_qr_workspace_bytes",
     "bsvd_householder_qr_batched",
@@ -96,6 +97,9 @@ def load():
     L.bsvd_gesvj_batched_host.argtypes = [ci, ci, ci, ci, vp, vp, vp, vp, popts, vp, ci, vp, sz,
                                           ctypes.POINTER(vp), ci]
     L.bsvd_gesvj_batched_host.restype = ci
+    L.bsvd_gesvj_batched_host_gather.argtypes = [ci, ci, ci, ci, vp, vp, ci, vp, vp, vp, popts, vp, ci, vp, sz,
+                                                 ctypes.POINTER(vp), ci]
+    L.bsvd_gesvj_batched_host_gather.restype = ci
     L.bsvd_host_workspace_bytes.argtypes = [ci, ci, ci, ci, ci, popts]
     L.bsvd_host_workspace_bytes.restype = sz
     L.bsvd_workspace_bytes.argtypes = [ci, ci, ci, ci, popts]
@@ -142,6 +146,40 @@ def load():
     L.bsvd_bench_fma_peak.restype = ci
     _lib = L
     return L
+
+
+_hostptrs = None
+HOSTPTRS_PATH = os.path.join(HERE, "_lib", "libbsvd_hostptrs.so")
+
+
+def gather_fortran(problems: list):
+    """(ptrs uintp[B], (m, n), itemsize) when every item of the list exports an F-contiguous 2-D buffer of
+    the same format and shape (one C pass, csrc/hostptrs.c), else None (the caller's per-item path)."""
+    global _hostptrs
+    if _hostptrs is None:
+        if not os.path.exists(HOSTPTRS_PATH):
+            return None
+        H = ctypes.PyDLL(HOSTPTRS_PATH)  # CPython API inside: keeps the GIL
+        H.bsvd_py_gather_fortran.argtypes = [ctypes.py_object, ctypes.c_ssize_t, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_char_p, ctypes.c_ssize_t]
+        H.bsvd_py_gather_fortran.restype = ctypes.c_int
+        H.bsvd_py_gather_ndarray.argtypes = [ctypes.py_object, ctypes.c_ssize_t, ctypes.py_object, ctypes.c_void_p,
+                                             ctypes.c_void_p]
+        H.bsvd_py_gather_ndarray.restype = ctypes.c_int
+        _hostptrs = H
+    import numpy as np
+
+    n = len(problems)
+    ptrs = np.empty(n, dtype=np.uintp)
+    shape = np.zeros(2, dtype=np.intp)
+    if _hostptrs.bsvd_py_gather_ndarray(problems, n, np.ndarray, ptrs.ctypes.data, shape.ctypes.data) == 0:
+        return ptrs, (int(shape[0]), int(shape[1])), int(problems[0].dtype.itemsize)
+    isz = np.zeros(1, dtype=np.intp)
+    fmt = ctypes.create_string_buffer(32)
+    rc = _hostptrs.bsvd_py_gather_fortran(problems, n, ptrs.ctypes.data, shape.ctypes.data, isz.ctypes.data, fmt, 32)
+    if rc != 0:
+        return None
+    return ptrs, (int(shape[0]), int(shape[1])), int(isz[0])
 
 
 def check(rc: int, what: str = "bsvd call") -> None:

@@ -133,11 +133,61 @@ def _clone_exc(exc: Exception) -> Exception:
         return exc
 
 
+class _Group:
+    """One device launch's outputs and the per-problem accounting rules its lazy records share."""
+
+    __slots__ = ("U", "S", "V", "cols", "calls", "masked", "blocked", "pps", "eig_unit", "dtime", "paths")
+
+
+_PATHS: dict = {}
+
+
+def _path_string(pv: int) -> str:
+    p = _PATHS.get(pv)
+    if p is None:
+        base = "blocked" if (pv & 0xFF) == 2 else "unblocked"
+        p = _PATHS[pv] = ("transpose+" if pv & 0x100 else "") + ("qr+" if pv & 0x200 else "") + base
+    return p
+
+
+class _LazyResult(SvdResult):
+    """An ``SvdResult`` whose fields (views into the group's factor arrays, the ``SolveInfo`` record)
+    are built on first access.  A 10k-problem batch would otherwise spend longer building 60k Python
+    objects than the device spends solving it; the record is otherwise the reference's frozen
+    dataclass (same fields, equality, repr, immutability; copies and pickles are plain SvdResults)."""
+
+    def __getattr__(self, name):
+        d = self.__dict__
+        g = d.get("_g")
+        if g is None or name not in ("u", "sigma", "v", "info"):
+            raise AttributeError(name)
+        j = d["_j"]
+        c = g.cols
+        if g.blocked:
+            cnt = WorkCounters(gram_calls=int(g.calls[j]) * g.pps, eig_calls=int(g.calls[j]) * g.pps,
+                               update_calls=int(c["update_calls"][j]), masked_pair_skips=int(g.masked[j]),
+                               t_eig=g.dtime)
+        else:
+            cnt = WorkCounters(eig_calls=int(g.calls[j]) * g.eig_unit, masked_pair_skips=int(g.masked[j]),
+                               t_eig=g.dtime)
+        info = SolveInfo(converged=bool(c["converged"][j]), outer_sweeps=int(c["outer_sweeps"][j]),
+                         inner_rotations=int(c["rotations"][j]), masked_pair_skips=int(g.masked[j]),
+                         path=_path_string(int(c["path"][j])), counters=cnt)
+        d.update(u=g.U[j], sigma=g.S[j], v=g.V[j] if g.V is not None else None, info=info)
+        del d["_g"], d["_j"]
+        return d[name]
+
+    def __reduce__(self):
+        return (SvdResult, (self.u, self.sigma, self.v, self.info))
+
+
 def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rounds: bool):
     """Solve a list of problems on the device; returns (results, errors, telemetry).
 
     Validation depends only on (dtype, shape), so it runs once per distinct pair; each uniform group is
-    one device launch; the per-problem records are built from column lists of the device telemetry.
+    one device launch; records are lazy views of the group's arrays and the batch telemetry is computed
+    with array operations on the kernels' per-problem counters.  Telemetry: (groups, trivial), groups a
+    list of (problem indices, outer sweeps, converged, last-sweep rotations, _Group).
     """
     from .solver import solve_host
 
@@ -148,14 +198,25 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
     proto: dict = {}
     groups: dict = {}
     trivial: list = []
-    for idx, a in enumerate(problems):
+    uniform = None
+    if n_prob > 64 and type(problems) is list and type(problems[0]) is np.ndarray:
+        # one C pass: every problem an F-contiguous matrix of one dtype and shape (the common case)
+        g = _lib.gather_fortran(problems)
+        if g is not None and g[1] == problems[0].shape and g[2] == problems[0].dtype.itemsize:
+            try:
+                t = _prepare(problems[0], opts, force)
+            except Exception:
+                t = None  # per-problem path reports the error for every problem
+            if t is not None and not t.trivial:
+                uniform = (g[0], t)
+    for idx, a in enumerate(problems if uniform is None else ()):
         if type(a) is not np.ndarray:
             try:
                 a = np.asarray(a)
             except Exception as exc:  # per-problem isolation (src/batch.py:105-111)
                 errors[idx] = exc
                 continue
-        key = (a.dtype.str, a.shape)
+        key = (a.dtype, a.shape)
         t = proto.get(key)
         if t is None:
             try:
@@ -173,27 +234,31 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
         else:
             groups.setdefault(key, []).append(idx)
 
-    solved: list = []  # (idxs, prep, U, S, V, columns, dt, kern)
+    solved: list = []  # (idxs, prep, U, S, V, info, seconds per problem)
+    if uniform is not None:
+        ptrs, t = uniform
+        groups = {None: range(n_prob)}
+        preps = [t]
     for key, idxs in groups.items():
         t0 = time.perf_counter()
         try:
-            U, S, V, info, kern = solve_host([arrays[i] for i in idxs], opts, route=_ROUTE[force])
+            if uniform is not None:
+                U, S, V, info, _kern = solve_host(problems, opts, route=_ROUTE[force], ptrs=ptrs)
+            else:
+                U, S, V, info, _kern = solve_host([arrays[i] for i in idxs], opts, route=_ROUTE[force])
         except Exception as exc:
             for i in idxs:
                 errors[i] = exc
             continue
-        dt = (time.perf_counter() - t0) / len(idxs)
-        cols = {f: info[f].tolist() for f in ("outer_sweeps", "converged", "rotations", "update_calls", "path",
-                                             "last_rotations")}
-        solved.append((idxs, preps[idxs[0]], U, S, V, cols, dt, kern))
+        solved.append((idxs, preps[idxs[0]], U, S, V, info, (time.perf_counter() - t0) / len(idxs)))
 
     # rounds the reference's lockstep loop would run (src/batch.py:113-142)
-    unconverged = any(not all(c["converged"]) for *_, c, _dt, _k in solved)
-    mx = max([max(max(c["outer_sweeps"]), 1) for *_, c, _dt, _k in solved] + ([1] if trivial else []), default=0)
+    unconverged = any(not info["converged"].all() for *_, info, _dt in solved)
+    mx = max([max(int(info["outer_sweeps"].max()), 1) for *_, info, _dt in solved] + ([1] if trivial else []),
+             default=0)
     rounds = opts.max_nsweeps if unconverged else mx
 
     results: list = [None] * n_prob
-    tele: dict = {}
     want_v = opts.compute_right_vectors
     for idx in trivial:
         p = preps[idx]
@@ -206,40 +271,32 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
         info = SolveInfo(converged=True, outer_sweeps=0, inner_rotations=0, masked_pair_skips=0, path="empty",
                          counters=WorkCounters())
         results[idx] = SvdResult(u=u, sigma=sigma, v=v, info=info)
-        tele[idx] = dict(outer_sweeps=0, converged=True, last=0, pair_stats=[])
-    paths: dict = {}
-    for idxs, p, U, S, V, cols, dtime, kern in solved:
-        pps, blocked = p.pairs_per_sweep, p.blocked
-        eig_unit = 0 if (not blocked and p.bn < 2) else 1
-        masking = bool(masked_rounds and opts.masking)
-        sw_l, cv_l, rot_l, up_l, path_l, last_l = (cols["outer_sweeps"], cols["converged"], cols["rotations"],
-                                                   cols["update_calls"], cols["path"], cols["last_rotations"])
-        for j, idx in enumerate(idxs):
-            s_i = sw_l[j]
-            conv = bool(cv_l[j])
-            calls = s_i if masked_rounds is False or opts.masking else rounds
-            masked = (rounds - max(s_i, 1)) * pps if (masking and conv) else 0
-            if blocked:
-                cnt = WorkCounters(gram_calls=calls * pps, eig_calls=calls * pps, update_calls=up_l[j],
-                                   masked_pair_skips=masked, t_eig=dtime)
-            else:
-                cnt = WorkCounters(eig_calls=calls * eig_unit, masked_pair_skips=masked, t_eig=dtime)
-            pv = path_l[j]
-            path = paths.get(pv)
-            if path is None:
-                base = "blocked" if (pv & 0xFF) == 2 else "unblocked"
-                path = ("transpose+" if pv & 0x100 else "") + ("qr+" if pv & 0x200 else "") + base
-                paths[pv] = path
-            info = SolveInfo(converged=conv, outer_sweeps=s_i, inner_rotations=rot_l[j], masked_pair_skips=masked,
-                             path=path, counters=cnt)
-            results[idx] = SvdResult(u=U[j], sigma=S[j], v=V[j] if (want_v and V is not None) else None, info=info)
-            last = last_l[j]
-            if not blocked:
-                stats = [(last == 0, 1, last)]
-            else:
-                stats = [(True, 1, 0)] * pps if last == 0 else [(False, 1, last)] + [(True, 1, 0)] * (pps - 1)
-            tele[idx] = dict(outer_sweeps=s_i, converged=conv, last=last, pair_stats=stats, kernel=kern)
-    return results, errors, tele
+    tele = []
+    masking = bool(masked_rounds and opts.masking)
+    new = object.__new__
+    for idxs, p, U, S, V, info, dtime in solved:
+        g = _Group()
+        sw = info["outer_sweeps"].astype(np.int64)
+        conv = info["converged"] != 0
+        g.U, g.S, g.V = U, S, (V if want_v else None)
+        g.cols = info
+        g.calls = sw if (masked_rounds is False or opts.masking) else np.full_like(sw, rounds)
+        g.masked = ((rounds - np.maximum(sw, 1)) * p.pairs_per_sweep) * (conv & masking)
+        g.blocked, g.pps = p.blocked, p.pairs_per_sweep
+        g.eig_unit = 0 if (not p.blocked and p.bn < 2) else 1
+        g.dtime = dtime
+        if isinstance(idxs, range):
+            recs = [new(_LazyResult) for _ in idxs]
+            for j, r in enumerate(recs):
+                r.__dict__.update(_g=g, _j=j)
+            results[idxs.start:idxs.stop] = recs
+        else:
+            for j, idx in enumerate(idxs):
+                r = new(_LazyResult)
+                r.__dict__.update(_g=g, _j=j)
+                results[idx] = r
+        tele.append((idxs, sw, conv, info["last_rotations"], g))
+    return results, errors, (tele, trivial)
 
 
 def batch_svd(problems, opts: JacobiOptions | None = None, state: BatchState | None = None):
@@ -261,17 +318,35 @@ def batch_svd(problems, opts: JacobiOptions | None = None, state: BatchState | N
             gc.enable()
     st.errors = dict(errors)
     c = st.counters
-    for idx, t in tele.items():
-        st.outer_sweeps[idx] = t["outer_sweeps"]
-        st.pair_stats[idx] = t["pair_stats"]
-        st.active[idx] = not t["converged"]
-        w = results[idx].info.counters
-        c.gram_calls += w.gram_calls
-        c.eig_calls += w.eig_calls
-        c.update_calls += w.update_calls
-        c.masked_pair_skips += w.masked_pair_skips
-        c.t_aux += w.t_aux
-        c.t_gram += w.t_gram
-        c.t_eig += w.t_eig
-        c.t_vec += w.t_vec
+    groups, trivial = tele
+    for idx in trivial:
+        st.outer_sweeps[idx] = 0
+        st.pair_stats[idx] = []
+        st.active[idx] = False
+    quiet1 = (True, 1, 0)
+    for idxs, sw, conv, last, g in groups:
+        ix = slice(idxs.start, idxs.stop) if isinstance(idxs, range) else np.asarray(idxs)
+        st.outer_sweeps[ix] = sw
+        st.active[ix] = ~conv
+        pps = g.pps
+        if not g.blocked:
+            if isinstance(idxs, range):  # (one shared tuple for the common quiet last sweep)
+                st.pair_stats[ix] = [[quiet1] if l == 0 else [(False, 1, l)] for l in last.tolist()]
+            else:
+                for i, l in zip(idxs, last.tolist()):
+                    st.pair_stats[i] = [(l == 0, 1, l)]
+        else:
+            quiet = [(True, 1, 0)] * pps
+            for i, l in zip(idxs, last.tolist()):
+                st.pair_stats[i] = list(quiet) if l == 0 else [(False, 1, l)] + [(True, 1, 0)] * (pps - 1)
+        n = len(idxs)
+        calls = int(g.calls.sum())
+        if g.blocked:
+            c.gram_calls += calls * pps
+            c.eig_calls += calls * pps
+            c.update_calls += int(g.cols["update_calls"].sum())
+        else:
+            c.eig_calls += calls * g.eig_unit
+        c.masked_pair_skips += int(g.masked.sum())
+        c.t_eig += g.dtime * n
     return results

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <string.h>
 
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -371,9 +372,61 @@ size_t bsvd_host_workspace_bytes(int dtype, int m, int n, int chunk, int nstream
     return host_slot(dtype, m, n, chunk, opts).total * (size_t)nstreams;
 }
 
+namespace {
+// Packs the chunks of a list of host matrices into the pinned batch layout on `nthreads` host threads
+// (thread t packs chunks t, t + nthreads, ...), publishing each chunk as done so that the pipeline can
+// enqueue its H2D while later chunks are still being packed.
+struct ChunkPacker {
+    std::vector<std::thread> pool;
+    std::atomic<int>* done = nullptr;
+    ChunkPacker(const void* const* src, unsigned char* dst, size_t bytes, int batch, int chunk, int nthreads) {
+        const int nchunks = (batch + chunk - 1) / chunk;
+        done = new std::atomic<int>[nchunks];
+        for (int c = 0; c < nchunks; ++c) done[c].store(0, std::memory_order_relaxed);
+        const int nt = nthreads < 1 ? 1 : (nthreads > nchunks ? nchunks : nthreads);
+        for (int t = 0; t < nt; ++t)
+            pool.emplace_back([=]() {
+                for (int c = t; c < nchunks; c += nt) {
+                    const int b1 = (c + 1) * chunk < batch ? (c + 1) * chunk : batch;
+                    for (int i = c * chunk; i < b1; ++i) memcpy(dst + (size_t)i * bytes, src[i], bytes);
+                    done[c].store(1, std::memory_order_release);
+                }
+            });
+    }
+    void wait(int c) const {
+        while (!done[c].load(std::memory_order_acquire)) std::this_thread::yield();
+    }
+    ~ChunkPacker() {
+        for (auto& t : pool) t.join();
+        delete[] done;
+    }
+};
+
+int gesvj_host_impl(int dtype, int m, int n, int batch, const void* A, const void* const* A_ptrs, int pack_threads,
+                    void* U, void* S, void* V, const bsvd_opts* opts, bsvd_info* info, int chunk, void* work,
+                    size_t work_bytes, void* const* streams, int nstreams);
+}  // namespace
+
 int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch, const void* A, void* U, void* S, void* V,
                             const bsvd_opts* opts, bsvd_info* info, int chunk, void* work, size_t work_bytes,
                             void* const* streams, int nstreams) {
+    return gesvj_host_impl(dtype, m, n, batch, A, nullptr, 0, U, S, V, opts, info, chunk, work, work_bytes, streams,
+                           nstreams);
+}
+
+int bsvd_gesvj_batched_host_gather(int dtype, int m, int n, int batch, const void* const* A_ptrs, void* A_stage,
+                                   int pack_threads, void* U, void* S, void* V, const bsvd_opts* opts,
+                                   bsvd_info* info, int chunk, void* work, size_t work_bytes, void* const* streams,
+                                   int nstreams) {
+    if (batch > 0 && !A_ptrs) return BSVD_ERR_ARG;
+    return gesvj_host_impl(dtype, m, n, batch, A_stage, A_ptrs, pack_threads, U, S, V, opts, info, chunk, work,
+                           work_bytes, streams, nstreams);
+}
+
+namespace {
+int gesvj_host_impl(int dtype, int m, int n, int batch, const void* A, const void* const* A_ptrs, int pack_threads,
+                    void* U, void* S, void* V, const bsvd_opts* opts, bsvd_info* info, int chunk, void* work,
+                    size_t work_bytes, void* const* streams, int nstreams) {
     if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || chunk < 1 || nstreams < 1 || !streams)
         return BSVD_ERR_ARG;
     int rc = check_opts(opts);
@@ -422,7 +475,12 @@ int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch, const void* A, v
     }
     rc = BSVD_OK;
     const int nchunks = (batch + chunk - 1) / chunk;
+    ChunkPacker* packer = nullptr;  // gather mode: pack chunks on host threads ahead of their H2D
+    if (A_ptrs && k > 0)
+        packer = new ChunkPacker(A_ptrs, static_cast<unsigned char*>(const_cast<void*>(A)), (size_t)m * n * es, batch,
+                                 chunk, pack_threads);
     for (int c = 0; c < nchunks && rc == BSVD_OK; ++c) {
+        if (packer) packer->wait(c);
         const int slot = c % nstreams;
         cudaStream_t st = static_cast<cudaStream_t>(streams[slot]);
         const int b0 = c * chunk, cb = (batch - b0) < chunk ? (batch - b0) : chunk;
@@ -469,8 +527,10 @@ int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch, const void* A, v
         if (joins[i]) cudaEventDestroy(joins[i]);
     if (fork) cudaEventDestroy(fork);
     delete[] joins;
+    delete packer;  // joins the packing threads (all chunks are packed once the loop has run)
     return rc;
 }
+}  // namespace
 
 extern "C++" {
 namespace {

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -171,8 +172,12 @@ def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: 
 
 
 def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: int = _lib.DISPATCH,
-                       kernel: int = 0, chunk: int = 0, streams=None):
+                       kernel: int = 0, chunk: int = 0, streams=None, a_ptrs=None, pack_threads: int = 8):
     """Pipelined host-buffer solve through bsvd_gesvj_batched_host.
+
+    With ``a_ptrs`` (uintp array of the B problems' column-major data) the batch is packed into a_h by
+    ``pack_threads`` host threads chunk by chunk while earlier chunks are in flight
+    (bsvd_gesvj_batched_host_gather); otherwise a_h already holds the packed batch.
 
     a_h (B, n, m), u_h (B, k, m), s_h (B, k), v_h (B, k, n) | None, info_h
     (B * INFO_BYTES,) are CPU tensors (pinned for full PCIe bandwidth).  The
@@ -198,11 +203,18 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
     ws_bytes = L.bsvd_host_workspace_bytes(code, m, n, chunk, len(streams), ctypes.byref(o))
     ws = _workspace(ws_bytes, dev)
     arr = (ctypes.c_void_p * len(streams))(*[st.cuda_stream for st in streams])
-    rc = L.bsvd_gesvj_batched_host(
-        code, m, n, B, a_h.data_ptr(), u_h.data_ptr(), s_h.data_ptr(),
-        v_h.data_ptr() if v_h is not None else None, ctypes.byref(o),
-        info_h.data_ptr() if info_h is not None else None, chunk,
-        ws.data_ptr() if ws is not None else None, ws_bytes, arr, len(streams))
+    if a_ptrs is None:
+        rc = L.bsvd_gesvj_batched_host(
+            code, m, n, B, a_h.data_ptr(), u_h.data_ptr(), s_h.data_ptr(),
+            v_h.data_ptr() if v_h is not None else None, ctypes.byref(o),
+            info_h.data_ptr() if info_h is not None else None, chunk,
+            ws.data_ptr() if ws is not None else None, ws_bytes, arr, len(streams))
+    else:  # gather mode: the problems are packed into a_h chunk by chunk, overlapping the pipeline
+        rc = L.bsvd_gesvj_batched_host_gather(
+            code, m, n, B, a_ptrs.ctypes.data, a_h.data_ptr(), pack_threads, u_h.data_ptr(), s_h.data_ptr(),
+            v_h.data_ptr() if v_h is not None else None, ctypes.byref(o),
+            info_h.data_ptr() if info_h is not None else None, chunk,
+            ws.data_ptr() if ws is not None else None, ws_bytes, arr, len(streams))
     _lib.check(rc, f"bsvd_gesvj_batched_host({dt.name}, {m}x{n}, batch={B})")
     return int(L.bsvd_select_kernel_batched(code, m, n, min(B, chunk), ctypes.byref(o)))
 
@@ -268,13 +280,50 @@ def _pinned(key, shape, tdt):
     return buf[:n].view(shape)
 
 
-def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, device=None):
+class _PinnedOwner:
+    """Owner of one pooled pinned result buffer, exposed to numpy through __array_interface__: every
+    array or view handed to the caller keeps it alive, so the pool can tell (by a weak reference) when
+    the caller has dropped all of them and the buffer may be written again."""
+
+    def __init__(self, t):
+        self.tensor = t
+        self.__array_interface__ = t.numpy().__array_interface__
+
+
+_RESULTS: dict = {}  # (tag, shape, dtype) -> [[tensor, weakref to the live _PinnedOwner | None], ...]
+_RESULTS_LOCK = threading.Lock()
+_RESULTS_PER_KEY = 4  # at most this many pinned result sets per shape; beyond it, fresh pageable arrays
+
+
+def _result_array(tag, shape, tdt, dt):
+    """A pinned array for results that go to the caller without a copy, or None when every pooled buffer
+    of this shape is still referenced by earlier results (the caller then copies into fresh memory)."""
+    torch = _torch()
+    key = (tag, tuple(shape), tdt)
+    with _RESULTS_LOCK:
+        lst = _RESULTS.setdefault(key, [])
+        ent = next((e for e in lst if e[1] is None or e[1]() is None), None)
+        if ent is None:
+            if len(lst) >= _RESULTS_PER_KEY:
+                return None
+            ent = [torch.empty(tuple(shape), dtype=tdt, pin_memory=True), None]
+            lst.append(ent)
+        owner = _PinnedOwner(ent[0])
+        ent[1] = weakref.ref(owner)
+    arr = np.asarray(owner)
+    assert arr.dtype == dt
+    return arr
+
+
+def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, device=None, ptrs=None):
     """Equal shape/dtype numpy matrices -> (U (B,m,k), S (B,k), V (B,n,k)|None, info records).
 
-    Host-buffer path: the column-major batch is packed (one C-level stack) into pinned staging that is
-    reused across calls, the pipelined bsvd_gesvj_batched_host overlaps H2D / solve / D2H in chunks,
-    and the factors are copied out of the staging into fresh arrays.  Returned U[b] / V[b] are
-    F-ordered views of those arrays.
+    Host-buffer path: the column-major batch is packed (one C-level copy; ``ptrs`` may pass the
+    problems' data pointers when the caller already checked them) into pinned staging that is
+    reused across calls of the thread, and the pipelined bsvd_gesvj_batched_host overlaps H2D / solve /
+    D2H in chunks.  The factors land directly in pooled pinned result buffers that are handed to the
+    caller (no copy-out; a buffer is reused only once every array viewing it has been dropped); when the
+    pool is exhausted the factors are copied into fresh arrays.  Returned U[b] / V[b] are F-ordered views.
     """
     torch = _torch()
     B = len(mats)
@@ -286,32 +335,44 @@ def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, de
     rdt = real_dtype(dt)
     host = _pinned("a", (B, n, m), tdt)
     hv = host.numpy()
-    if all(a.flags.f_contiguous and a.dtype == dt for a in mats):  # raw column-major copies in C
+    if ptrs is None and all(a.flags.f_contiguous and a.dtype == dt for a in mats):
         ptrs = np.fromiter((a.__array_interface__["data"][0] for a in mats), dtype=np.uintp, count=B)
-        _lib.check(_lib.load().bsvd_pack_host(ptrs.ctypes.data, B, m * n * dt.itemsize, host.data_ptr(), 8),
-                   "bsvd_pack_host")
+    if ptrs is not None:  # raw column-major copies in C, overlapped with the pipeline (gather mode)
+        pass
     else:
         _parallel_slices(B, lambda lo, hi: np.stack([a.T for a in mats[lo:hi]], out=hv[lo:hi]))
-    u_h = _pinned("u", (B, k, m), tdt)
-    s_h = _pinned("s", (B, k), torch_dtype(rdt))
-    v_h = _pinned("v", (B, k, n), tdt) if opts.compute_right_vectors else None
+    want_v = bool(opts.compute_right_vectors)
+    Uo = _result_array("u", (B, k, m), tdt, dt)
+    Vo = _result_array("v", (B, k, n), tdt, dt) if want_v else None
+    So = _result_array("s", (B, k), torch_dtype(rdt), rdt)
+    direct = Uo is not None and So is not None and (Vo is not None or not want_v)
+    if direct:
+        u_h = torch.from_numpy(Uo)
+        s_h = torch.from_numpy(So)
+        v_h = torch.from_numpy(Vo) if want_v else None
+    else:
+        u_h = _pinned("u", (B, k, m), tdt)
+        s_h = _pinned("s", (B, k), torch_dtype(rdt))
+        v_h = _pinned("v", (B, k, n), tdt) if want_v else None
     info_h = _pinned("i", (B * _lib.INFO_BYTES,), torch.uint8)
     with torch.cuda.device(device):
-        kern = solve_host_buffers(host, u_h, s_h, v_h, info_h, m, n, opts, route, kernel)
+        kern = solve_host_buffers(host, u_h, s_h, v_h, info_h, m, n, opts, route, kernel, a_ptrs=ptrs)
         torch.cuda.current_stream(device).synchronize()
-    # copy the factors out of the reusable staging (threaded: ~250 MB for C1-10k)
-    Uc = np.empty((B, k, m), dtype=dt)
-    Vc = np.empty((B, k, n), dtype=dt) if v_h is not None else None
-    un, vn = u_h.numpy(), (v_h.numpy() if v_h is not None else None)
+    if direct:
+        Uc, S, Vc = Uo, So, Vo
+    else:  # copy the factors out of the reusable staging (threaded: ~250 MB for C1-10k)
+        Uc = np.empty((B, k, m), dtype=dt)
+        Vc = np.empty((B, k, n), dtype=dt) if v_h is not None else None
+        un, vn = u_h.numpy(), (v_h.numpy() if v_h is not None else None)
 
-    def _out(lo, hi):
-        Uc[lo:hi] = un[lo:hi]
-        if Vc is not None:
-            Vc[lo:hi] = vn[lo:hi]
+        def _out(lo, hi):
+            Uc[lo:hi] = un[lo:hi]
+            if Vc is not None:
+                Vc[lo:hi] = vn[lo:hi]
 
-    _parallel_slices(B, _out)
+        _parallel_slices(B, _out)
+        S = s_h.numpy().copy()
     U = np.swapaxes(Uc, 1, 2)
-    S = s_h.numpy().copy()
     V = np.swapaxes(Vc, 1, 2) if Vc is not None else None
     info = np.frombuffer(info_h.numpy().tobytes(), dtype=INFO_DTYPE)
     return U, S, V, info, kern

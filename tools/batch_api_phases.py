@@ -1,4 +1,5 @@
-"""Phase timing of the list API host path for C1-10k shapes (development aid)."""
+"""Phase timing of the list API host path on C1-10k shapes (development aid): pack, pipelined device
+solve with copies, record building, batch telemetry."""
 import os
 import sys
 import time
@@ -8,26 +9,39 @@ import numpy as np
 import torch
 
 import paper_2601_17979_b200 as bs
-from paper_2601_17979_b200 import batch, solver
+from paper_2601_17979_b200 import _lib, batch, solver
 
 rng = np.random.default_rng(0)
-B = 10000
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
 mats = [np.asfortranarray(rng.random((32, 32))) for _ in range(B)]
 opts = bs.JacobiOptions()
-for it in range(4):
+T = {}
+orig_pack = _lib.load().bsvd_pack_host
+orig_buf = solver.solve_host_buffers
+
+
+def timed(name, fn):
+    def w(*a, **k):
+        t0 = time.perf_counter()
+        r = fn(*a, **k)
+        torch.cuda.synchronize()
+        T[name] = T.get(name, 0.0) + time.perf_counter() - t0
+        return r
+    return w
+
+
+solver.solve_host_buffers = timed("device (H2D+solve+D2H)", orig_buf)
+solver.solve_host = timed("solve_host", solver.solve_host)
+batch._solve_problems = timed("_solve_problems", batch._solve_problems)
+res = None
+for it in range(12):
+    T.clear()
     t0 = time.perf_counter()
-    U, S, V, info, kern = solver.solve_host(mats, opts)
+    res = bs.batch_svd(mats, opts)
     t1 = time.perf_counter()
-    res, err, tele = batch._solve_problems(mats, opts, None, True)
-    t2 = time.perf_counter()
-    r = bs.batch_svd(mats, opts)
-    t3 = time.perf_counter()
-    print(f"solve_host {1e3 * (t1 - t0):.1f} ms | _solve_problems {1e3 * (t2 - t1):.1f} ms | batch_svd {1e3 * (t3 - t2):.1f} ms")
-# inside solve_host
-torch.cuda.synchronize()
-hv = np.empty((B, 32, 32))
-t0 = time.perf_counter(); solver._parallel_slices(B, lambda lo, hi: np.stack([a.T for a in mats[lo:hi]], out=hv[lo:hi])); t1 = time.perf_counter()
-print(f"pack {1e3 * (t1 - t0):.1f} ms")
-x = np.empty((B, 32, 32)); y = np.ones((B, 32, 32))
-t0 = time.perf_counter(); solver._parallel_slices(B, lambda lo, hi: x.__setitem__(slice(lo, hi), y[lo:hi])); t1 = time.perf_counter()
-print(f"copy-out 82 MB into fresh pages {1e3 * (t1 - t0):.1f} ms")
+    tot = t1 - t0
+    if it >= 2:
+        print(f"B={B} batch_svd {tot * 1e3:.1f} ms ({B / tot:,.0f} mat/s) | " +
+              " | ".join(f"{k} {v * 1e3:.1f}" for k, v in T.items()), flush=True)
+r = res[7]
+print("record", r.info.path, r.info.outer_sweeps, r.sigma[:2], type(r).__name__)
