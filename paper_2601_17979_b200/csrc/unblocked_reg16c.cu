@@ -84,7 +84,16 @@ struct St {
     uint32_t fmask;  // lanes whose problem takes them
 };
 
-template <int u, bool WANT_V>
+// the same update written to other registers (the ring shift folded into it, see iter)
+__device__ __forceinline__ void apply2x2_to(float2 x, float2 y, float2& nx, float2& ny, float cm1, float c) {
+    const float2 cc = make_float2(c, c), nc = make_float2(-c, -c), mm = make_float2(cm1, cm1);
+    const float2 tx = __ffma2_rn(cc, y, x);
+    const float2 ty = __ffma2_rn(nc, x, y);
+    nx = __ffma2_rn(mm, x, tx);
+    ny = __ffma2_rn(mm, y, ty);
+}
+
+template <int u, bool WANT_V, int SH = 0>
 __device__ __forceinline__ void iter(float2 (&X)[N], float2 (&Y)[N], QSmem& sm,
                                      const uint32_t* ctab, int t, int lane, int ql, bool done, float tol2,
                                      float tol, St& st) {
@@ -141,16 +150,42 @@ __device__ __forceinline__ void iter(float2 (&X)[N], float2 (&Y)[N], QSmem& sm,
         st.full = sb != 0u;
     }
     __syncwarp();
-    if (mask) {
-        // two pairs' parameters per 16-byte load, fetched just before use (4 live registers, not 16)
+    if constexpr (SH == 0) {
+        if (mask) {
+            // two pairs' parameters per 16-byte load, fetched just before use (4 live registers, not 16)
+            const float4* pp = reinterpret_cast<const float4*>(sm.pub);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float4 pr = pp[i];
+                apply2x2(X[TS(2 * i, u)], X[BS(2 * i, u)], pr.x, pr.y);
+                if (WANT_V) apply2x2(Y[TS(2 * i, u)], Y[BS(2 * i, u)], pr.x, pr.y);
+                apply2x2(X[TS(2 * i + 1, u)], X[BS(2 * i + 1, u)], pr.z, pr.w);
+                if (WANT_V) apply2x2(Y[TS(2 * i + 1, u)], Y[BS(2 * i + 1, u)], pr.z, pr.w);
+            }
+        }
+    } else {
+        // last iteration of an unrolled group, branch-free: the ring shift by SH is folded into the
+        // update (every slot is in one pair; pairs that do not rotate have zero parameters and copy
+        // exactly), so the loop back-edge moves no registers
         const float4* pp = reinterpret_cast<const float4*>(sm.pub);
+        float2 X2[N], Y2[N];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const float4 pr = pp[i];
-            apply2x2(X[TS(2 * i, u)], X[BS(2 * i, u)], pr.x, pr.y);
-            if (WANT_V) apply2x2(Y[TS(2 * i, u)], Y[BS(2 * i, u)], pr.x, pr.y);
-            apply2x2(X[TS(2 * i + 1, u)], X[BS(2 * i + 1, u)], pr.z, pr.w);
-            if (WANT_V) apply2x2(Y[TS(2 * i + 1, u)], Y[BS(2 * i + 1, u)], pr.z, pr.w);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int q = 2 * i + h;
+                const float pc = h ? pr.z : pr.x, ps = h ? pr.w : pr.y;
+                apply2x2_to(X[TS(q, u)], X[BS(q, u)], X2[dst_slot(TS(q, u), SH)], X2[dst_slot(BS(q, u), SH)], pc, ps);
+                if (WANT_V)
+                    apply2x2_to(Y[TS(q, u)], Y[BS(q, u)], Y2[dst_slot(TS(q, u), SH)], Y2[dst_slot(BS(q, u), SH)], pc,
+                                ps);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            X[c] = X2[c];
+            if (WANT_V) Y[c] = Y2[c];
         }
     }
 }
@@ -233,8 +268,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
                     shift_all<1, WANT_V>(X, Y);
                     break;
                 }
-                iter<1, WANT_V>(X, Y, sm, ctab, 2 * gi + 1, lane, ql, done != 0, tol2, tol, st);
-                shift_all<2, WANT_V>(X, Y);
+                iter<1, WANT_V, 2>(X, Y, sm, ctab, 2 * gi + 1, lane, ql, done != 0, tol2, tol, st);
             }
         } else {  // U divides 15: the ring moves once per U iterations
 #pragma unroll 1
