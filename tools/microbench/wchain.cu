@@ -32,7 +32,7 @@ int main(int argc, char** argv) {
     a.tol = 30 * 0x1p-53; a.max_sweeps = 30; a.batch = B; a.work = W; a.work_stride = 2048 + r32b::LOG_ELEMS;
     a.info = info;
     const size_t smem = 4 * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
-    auto k = r32b::k_reg32b<4, 2, 2, 2, 16>;
+    auto k = r32b::k_reg32b<4, 2, 2, 2, 8, true>;  // the default (scaled rotations)
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int rep = 0; rep < 2; ++rep) {
         unsigned long long z[16] = {0};
