@@ -136,7 +136,7 @@ def _clone_exc(exc: Exception) -> Exception:
 class _Group:
     """One device launch's outputs and the per-problem accounting rules its lazy records share."""
 
-    __slots__ = ("U", "S", "V", "cols", "calls", "masked", "blocked", "pps", "eig_unit", "dtime", "paths")
+    __slots__ = ("U", "S", "V", "cols", "calls", "masked", "blocked", "pps", "eig_unit", "dtime", "atime", "paths")
 
 
 _PATHS: dict = {}
@@ -166,10 +166,10 @@ class _LazyResult(SvdResult):
         if g.blocked:
             cnt = WorkCounters(gram_calls=int(g.calls[j]) * g.pps, eig_calls=int(g.calls[j]) * g.pps,
                                update_calls=int(c["update_calls"][j]), masked_pair_skips=int(g.masked[j]),
-                               t_eig=g.dtime)
+                               t_eig=g.dtime, t_aux=g.atime)
         else:
             cnt = WorkCounters(eig_calls=int(g.calls[j]) * g.eig_unit, masked_pair_skips=int(g.masked[j]),
-                               t_eig=g.dtime)
+                               t_eig=g.dtime, t_aux=g.atime)
         info = SolveInfo(converged=bool(c["converged"][j]), outer_sweeps=int(c["outer_sweeps"][j]),
                          inner_rotations=int(c["rotations"][j]), masked_pair_skips=int(g.masked[j]),
                          path=_path_string(int(c["path"][j])), counters=cnt)
@@ -234,7 +234,9 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
         else:
             groups.setdefault(key, []).append(idx)
 
-    solved: list = []  # (idxs, prep, U, S, V, info, seconds per problem)
+    from .solver import last_device_seconds
+
+    solved: list = []  # (idxs, prep, U, S, V, info, (device, host) seconds per problem)
     if uniform is not None:
         ptrs, t = uniform
         groups = {None: range(n_prob)}
@@ -250,7 +252,8 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
             for i in idxs:
                 errors[i] = exc
             continue
-        solved.append((idxs, preps[idxs[0]], U, S, V, info, (time.perf_counter() - t0) / len(idxs)))
+        wall, dev = time.perf_counter() - t0, last_device_seconds()
+        solved.append((idxs, preps[idxs[0]], U, S, V, info, (dev / len(idxs), max(0.0, wall - dev) / len(idxs))))
 
     # rounds the reference's lockstep loop would run (src/batch.py:113-142)
     unconverged = any(not info["converged"].all() for *_, info, _dt in solved)
@@ -284,7 +287,7 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
         g.masked = ((rounds - np.maximum(sw, 1)) * p.pairs_per_sweep) * (conv & masking)
         g.blocked, g.pps = p.blocked, p.pairs_per_sweep
         g.eig_unit = 0 if (not p.blocked and p.bn < 2) else 1
-        g.dtime = dtime
+        g.dtime, g.atime = dtime
         if isinstance(idxs, range):
             recs = [new(_LazyResult) for _ in idxs]
             for j, r in enumerate(recs):
@@ -349,4 +352,5 @@ def batch_svd(problems, opts: JacobiOptions | None = None, state: BatchState | N
             c.eig_calls += calls * g.eig_unit
         c.masked_pair_skips += int(g.masked.sum())
         c.t_eig += g.dtime * n
+        c.t_aux += g.atime * n
     return results

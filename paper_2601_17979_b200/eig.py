@@ -114,8 +114,6 @@ def batch_hermitian_eig(mats, k: float = 30.0, max_sweeps: int = 30, eigvecs=Non
                 raise ShapeError("eigvecs must be 2-d with n columns and matching dtype")
             if not m.flags.f_contiguous:
                 raise ShapeError("eigvecs must be F-contiguous")
-            if m.shape[0] != n:
-                raise ShapeError("eigvecs must be n x n on the device path")
     if n < 2:  # src/eig.py:136-137
         out = []
         for b, g in enumerate(mats):
@@ -132,7 +130,10 @@ def batch_hermitian_eig(mats, k: float = 30.0, max_sweeps: int = 30, eigvecs=Non
     for b, g in enumerate(mats):
         gv[b] = g.T  # column-major per matrix
     m_h = torch.empty((B, n, n), dtype=tdt, pin_memory=True)
-    if eigvecs is not None:
+    # n x n accumulators are rotated in place on the device; any other row count (the reference accepts
+    # any n-column matrix, src/eig.py:128-133) gets the device's rotation product Q: eigvecs <- eigvecs Q
+    square = eigvecs is not None and all(m.shape[0] == n for m in eigvecs)
+    if square:
         mv = m_h.numpy()
         for b, m in enumerate(eigvecs):
             mv[b] = m.T
@@ -145,7 +146,7 @@ def batch_hermitian_eig(mats, k: float = 30.0, max_sweeps: int = 30, eigvecs=Non
     ws = _workspace(ws_bytes, dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
     rc = L.bsvd_heevj_batched(code, n, B, g_d.data_ptr(), n, n * n, d_d.data_ptr(), n, m_d.data_ptr(), n, n * n,
-                              1 if eigvecs is not None else 0, float(k), int(max_sweeps), info_d.data_ptr(),
+                              1 if square else 0, float(k), int(max_sweeps), info_d.data_ptr(),
                               ws.data_ptr() if ws is not None else None, ws_bytes, stream)
     _lib.check(rc, f"bsvd_heevj_batched({dt.name}, n={n}, batch={B})")
     d_h = d_d.cpu().numpy()
@@ -153,8 +154,11 @@ def batch_hermitian_eig(mats, k: float = 30.0, max_sweeps: int = 30, eigvecs=Non
     info = np.frombuffer(info_d.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
     out = []
     for b in range(B):
-        if eigvecs is not None:
+        if square:
             eigvecs[b][...] = m_out[b]
+            m = eigvecs[b]
+        elif eigvecs is not None:
+            eigvecs[b][...] = eigvecs[b] @ m_out[b]
             m = eigvecs[b]
         else:
             m = np.asfortranarray(m_out[b])

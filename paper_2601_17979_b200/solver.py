@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+import time
 import weakref
 from dataclasses import dataclass
 
@@ -315,6 +316,11 @@ def _result_array(tag, shape, tdt, dt):
     return arr
 
 
+def last_device_seconds() -> float:
+    """Wall time of this thread's latest solve_host device pipeline (H2D, kernels, D2H; synchronised)."""
+    return getattr(_TLS, "device_seconds", 0.0)
+
+
 def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, device=None, ptrs=None):
     """Equal shape/dtype numpy matrices -> (U (B,m,k), S (B,k), V (B,n,k)|None, info records).
 
@@ -355,9 +361,11 @@ def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, de
         s_h = _pinned("s", (B, k), torch_dtype(rdt))
         v_h = _pinned("v", (B, k, n), tdt) if want_v else None
     info_h = _pinned("i", (B * _lib.INFO_BYTES,), torch.uint8)
+    t_dev0 = time.perf_counter()
     with torch.cuda.device(device):
         kern = solve_host_buffers(host, u_h, s_h, v_h, info_h, m, n, opts, route, kernel, a_ptrs=ptrs)
         torch.cuda.current_stream(device).synchronize()
+    _TLS.device_seconds = time.perf_counter() - t_dev0  # the pipelined H2D / solve / D2H, for WorkCounters
     if direct:
         Uc, S, Vc = Uo, So, Vo
     else:  # copy the factors out of the reusable staging (threaded: ~250 MB for C1-10k)

@@ -52,10 +52,11 @@ class JacobiOptions:
 class WorkCounters:
     """Work and stage-time accounting (src/svd.py:93-124).
 
-    Call counts follow the reference's own bookkeeping.  Times: the device
-    solve of a group is timed with CUDA events and shared evenly by its
-    problems; the B200 kernels fuse Gram, eigensolve and update, so the
-    device time is booked under ``t_eig`` and host staging under ``t_aux``.
+    Call counts follow the reference's own bookkeeping.  Times, per problem: ``t_eig`` is the device
+    stage -- the pipelined host-to-device copy, solve and device-to-host copy of the problem's group
+    (wall time, synchronised) shared evenly by its problems; ``t_aux`` the host stage (validation,
+    pointer gathering, result handling).  The B200 kernels fuse the Gram, eigensolve and update stages
+    of the blocked path into one launch, so ``t_gram`` and ``t_vec`` stay 0 (their work is in t_eig).
     """
 
     gram_calls: int = 0

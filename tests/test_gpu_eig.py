@@ -106,3 +106,22 @@ def test_eigvecs_accumulate_in_place_and_validation():
         bs.jacobi_hermitian_eig(g4, eigvecs=np.asfortranarray(np.eye(3)))
     with pytest.raises(bs.DomainError):
         bs.jacobi_hermitian_eig(np.asfortranarray([[1.0, 2.0], [5.0, 1.0]]))
+
+
+@pytest.mark.parametrize("rows", [3, 9])
+def test_eigvecs_any_row_count(rows):
+    """The reference accepts any F-contiguous n-column accumulator (src/eig.py:128-133) and rotates its
+    columns in place: the result is eigvecs @ Q for the rotation product Q (the square run's m)."""
+    g = random_hermitian(6, seed=8)
+    rng = np.random.default_rng(rows)
+    pre = np.asfortranarray(rng.random((rows, 6)))
+    want = pre.copy()
+    d0, q, _ = bs.jacobi_hermitian_eig(g)
+    d1, m1, i1 = bs.jacobi_hermitian_eig(g, eigvecs=pre)
+    assert m1 is pre and np.array_equal(d0, d1) and i1.converged
+    np.testing.assert_allclose(m1, want @ q, rtol=0, atol=64 * 2.0 ** -53 * np.abs(want).sum())
+    # and batched, rows differing per problem
+    pres = [np.asfortranarray(rng.random((r, 6))) for r in (rows, 6, 2)]
+    outs = bs.batch_hermitian_eig([g, g, g], eigvecs=[p.copy(order="F") for p in pres])
+    for p, (d, m, _) in zip(pres, outs):
+        np.testing.assert_allclose(m, p @ q, rtol=0, atol=64 * 2.0 ** -53 * np.abs(p).sum())
