@@ -7,7 +7,7 @@ run() {  # name, kernel regex, quick_time args
   timeout 600 ncu --metrics $M --clock-control none -k regex:"$2" -c 1 --csv --log-file "$out/ncu_$1.csv" python tools/quick_time.py $3 > /dev/null 2>&1
 }
 run c1-10k k_reg32b "C1-10k"
-run c2-full k_reg16b "C2-full"
+run c2-full k_reg16c "C2-full"
 run c3 k_blocked_reg "C3"
 run c4 k_creg32 "C4"
 run c5 k_blocked_reg "C5"
