@@ -166,6 +166,12 @@ def gather_fortran(problems: list):
         H.bsvd_py_gather_ndarray.argtypes = [ctypes.py_object, ctypes.c_ssize_t, ctypes.py_object, ctypes.c_void_p,
                                              ctypes.c_void_p]
         H.bsvd_py_gather_ndarray.restype = ctypes.c_int
+        H.bsvd_py_fill_lazy.argtypes = [ctypes.py_object, ctypes.c_ssize_t, ctypes.c_ssize_t, ctypes.py_object,
+                                        ctypes.py_object]
+        H.bsvd_py_fill_lazy.restype = ctypes.c_int
+        H.bsvd_py_fill_pair_stats.argtypes = [ctypes.py_object, ctypes.c_ssize_t, ctypes.c_ssize_t,
+                                              ctypes.c_void_p, ctypes.py_object]
+        H.bsvd_py_fill_pair_stats.restype = ctypes.c_int
         _hostptrs = H
     import numpy as np
 
@@ -180,6 +186,13 @@ def gather_fortran(problems: list):
     if rc != 0:
         return None
     return ptrs, (int(shape[0]), int(shape[1])), int(isz[0])
+
+
+def hostptrs():
+    """The CPython helper library (csrc/hostptrs.c) or None when it was not built."""
+    if _hostptrs is None and os.path.exists(HOSTPTRS_PATH):
+        gather_fortran([])  # loads and declares it
+    return _hostptrs
 
 
 def check(rc: int, what: str = "bsvd call") -> None:

@@ -288,7 +288,10 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
         g.blocked, g.pps = p.blocked, p.pairs_per_sweep
         g.eig_unit = 0 if (not p.blocked and p.bn < 2) else 1
         g.dtime, g.atime = dtime
-        if isinstance(idxs, range):
+        H = _lib.hostptrs() if isinstance(idxs, range) else None
+        if H is not None:  # one C pass (csrc/hostptrs.c): allocate the records, set (_g, _j)
+            H.bsvd_py_fill_lazy(results, idxs.start, len(idxs), _LazyResult, g)
+        elif isinstance(idxs, range):
             recs = [new(_LazyResult) for _ in idxs]
             for j, r in enumerate(recs):
                 r.__dict__.update(_g=g, _j=j)
@@ -333,7 +336,11 @@ def batch_svd(problems, opts: JacobiOptions | None = None, state: BatchState | N
         st.active[ix] = ~conv
         pps = g.pps
         if not g.blocked:
-            if isinstance(idxs, range):  # (one shared tuple for the common quiet last sweep)
+            H = _lib.hostptrs() if isinstance(idxs, range) else None
+            if H is not None:  # one C pass; one shared tuple for the common quiet last sweep
+                lc = np.ascontiguousarray(last, dtype=np.int32)
+                H.bsvd_py_fill_pair_stats(st.pair_stats, idxs.start, len(idxs), lc.ctypes.data, quiet1)
+            elif isinstance(idxs, range):
                 st.pair_stats[ix] = [[quiet1] if l == 0 else [(False, 1, l)] for l in last.tolist()]
             else:
                 for i, l in zip(idxs, last.tolist()):

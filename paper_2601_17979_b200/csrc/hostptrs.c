@@ -82,3 +82,61 @@ int bsvd_py_gather_ndarray(PyObject* list, Py_ssize_t n, PyObject* ndarray_type,
     shape[1] = a0->dimensions[1];
     return 0;
 }
+
+/* list[start + j] = a fresh instance of `type` (allocated without __init__, like object.__new__) whose
+ * instance dict is {"_g": group, "_j": j}, for j < n: the lazy SvdResult records of one device launch
+ * (batch.py _LazyResult).  Returns 0, or -1 with a Python error set. */
+int bsvd_py_fill_lazy(PyObject* list, Py_ssize_t start, Py_ssize_t n, PyObject* type, PyObject* group) {
+    static PyObject *key_g = NULL, *key_j = NULL;
+    if (!key_g) key_g = PyUnicode_InternFromString("_g");
+    if (!key_j) key_j = PyUnicode_InternFromString("_j");
+    if (!key_g || !key_j) return -1;
+    if (!PyList_Check(list) || !PyType_Check(type) || start < 0 || start + n > PyList_GET_SIZE(list)) {
+        PyErr_SetString(PyExc_ValueError, "bsvd_py_fill_lazy: bad arguments");
+        return -1;
+    }
+    PyTypeObject* tp = (PyTypeObject*)type;
+    for (Py_ssize_t j = 0; j < n; ++j) {
+        PyObject* obj = tp->tp_alloc(tp, 0);
+        if (!obj) return -1;
+        PyObject* d = PyObject_GenericGetDict(obj, NULL);
+        PyObject* jj = PyLong_FromSsize_t(j);
+        if (!d || !jj || PyDict_SetItem(d, key_g, group) < 0 || PyDict_SetItem(d, key_j, jj) < 0) {
+            Py_XDECREF(d);
+            Py_XDECREF(jj);
+            Py_DECREF(obj);
+            return -1;
+        }
+        Py_DECREF(d);
+        Py_DECREF(jj);
+        PyList_SetItem(list, start + j, obj); /* steals obj, releases the old item */
+    }
+    return 0;
+}
+
+/* list[start + j] = [quiet] if last[j] == 0 else [(False, 1, last[j])] for j < n (the reference's
+ * per-problem pair_stats of an unblocked problem's last sweep, src/batch.py:113-142); last: int32[n]. */
+int bsvd_py_fill_pair_stats(PyObject* list, Py_ssize_t start, Py_ssize_t n, const int32_t* last, PyObject* quiet) {
+    if (!PyList_Check(list) || start < 0 || start + n > PyList_GET_SIZE(list) || !last) {
+        PyErr_SetString(PyExc_ValueError, "bsvd_py_fill_pair_stats: bad arguments");
+        return -1;
+    }
+    for (Py_ssize_t j = 0; j < n; ++j) {
+        PyObject* inner = PyList_New(1);
+        if (!inner) return -1;
+        PyObject* item;
+        if (last[j] == 0) {
+            Py_INCREF(quiet);
+            item = quiet;
+        } else {
+            item = Py_BuildValue("(Oii)", Py_False, 1, (int)last[j]);
+            if (!item) {
+                Py_DECREF(inner);
+                return -1;
+            }
+        }
+        PyList_SET_ITEM(inner, 0, item);
+        PyList_SetItem(list, start + j, inner);
+    }
+    return 0;
+}

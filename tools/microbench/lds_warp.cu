@@ -31,9 +31,20 @@ __global__ void k(double* out, long long* cyc, int iters) {
         } else if (MODE == 2) {  // STS.64 distinct (the transpose writes)
 #pragma unroll
             for (int q = 0; q < 16; ++q) buf[2048 + 34 * q + lane] = acc[q] + it;
-        } else {  // LDS.64 broadcast-pair
+        } else if (MODE == 3) {  // LDS.64 broadcast-pair
 #pragma unroll
             for (int q = 0; q < 16; ++q) acc[q] += buf[o + q + 32 * half];
+        } else if (MODE == 4) {  // SHFL.IDX of a double (2 x SHFL32) from lane q of the half
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] += __shfl_sync(0xffffffffu, acc[(q + 1) & 15] + it, q + 16 * half);
+        } else {  // mixed: 8 LDS.128 + 8 double shuffles
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double2 v = *reinterpret_cast<const double2*>(&buf[o + 2 * q + 32 * half]);
+                acc[q] += v.x * v.y;
+            }
+#pragma unroll
+            for (int q = 8; q < 16; ++q) acc[q] += __shfl_sync(0xffffffffu, acc[(q + 1) & 15] + it, q + 16 * half);
         }
     }
     long long t1 = clock64();
@@ -61,6 +72,8 @@ int main() {
         run<1>("LDS.128 distinct", w);
         run<2>("STS.64 distinct", w);
         run<3>("LDS.64 half-warp broadcast", w);
+        run<4>("SHFL.IDX double (2 x 32-bit)", w);
+        run<5>("8 LDS.128 + 8 double SHFL", w);
     }
     return 0;
 }
