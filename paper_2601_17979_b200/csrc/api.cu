@@ -339,7 +339,10 @@ int bsvd_select_kernel_batched(int dtype, int m, int n, int batch, const bsvd_op
         rr.qr = 0;
         return make_plan(dtype, rr, opts, true, batch).kernel;
     }
-    if (promote_f32(dtype, r, opts)) return KV_BLOCKED_REG;  // FP32 on the FP64 register blocked kernel
+    if (promote_f32(dtype, r, opts)) {  // single precision on a double-precision register kernel
+        Route rd = r;
+        return make_plan(dtype == BSVD_C ? BSVD_Z : BSVD_D, rd, opts, true, batch).kernel;
+    }
     return make_plan(dtype, r, opts, true, batch).kernel;
 }
 
@@ -568,30 +571,38 @@ QrWs qr_ws(int dtype, const Route& r, int batch, const bsvd_opts* o) {
 
 extern "C++" {
 namespace {
-// FP32 blocked problems whose shape the FP64 register blocked kernel takes (n % 16 == 0, m <= 256, not
-// transposed): solved in float64 -- inputs widened, factors rounded to float32 -- with the FP32 tolerance
-// k u_32 (opts.k scaled by u_32 / u_64 = 2^29, exact).  At n = 128 this is ~8x faster than the general
-// FP32 blocked kernel (tools/general_time.py) and at least as accurate as the reference's FP32 path.
+// Single-precision problems whose shape a double-precision register kernel takes are solved in double
+// precision -- inputs widened, factors rounded back -- with the single-precision tolerance k u_32 (opts.k
+// scaled by u_32 / u_64 = 2^29, exact): FP32 blocked shapes (n % 16 == 0, m <= 256) and 32 x 32 on the
+// FP64 register kernels, complex64 with n = 32, m <= 256 on the complex128 one.  The general
+// single-precision kernels are 1.5-9.5x slower on these shapes (tools/general_time.py,
+// tools/promo_time.py); the double-precision solve is at least as accurate as the reference's.
 bool promote_f32(int dtype, const Route& r, const bsvd_opts* o) {
-    if (dtype != BSVD_S || r.qr || !r.blocked || r.trans || o->kernel != 0) return false;
-    return plan_blocked_reg(BSVD_D, r.bm, r.bn, o->nb, r.need_v, true, o->inner_sweeps, 0).kernel != 0;
+    if (r.qr || r.trans || o->kernel != 0) return false;
+    if (dtype == BSVD_S) {
+        if (r.blocked) return plan_blocked_reg(BSVD_D, r.bm, r.bn, o->nb, r.need_v, true, o->inner_sweeps, 0).kernel != 0;
+        return r.bm == 32 && r.bn == 32;
+    }
+    if (dtype == BSVD_C) return plan_creg32(BSVD_Z, r.bm, r.bn, r.need_v, true, r.blocked, o->nb, 0, smem_limit()).kernel != 0;
+    return false;
 }
 struct PromWs {
     size_t a, u, s, v, inner, total;
     bsvd_opts io;
 };
-PromWs prom_ws(int m, int n, int batch, const bsvd_opts* o) {
+PromWs prom_ws(int dtype, int m, int n, int batch, const bsvd_opts* o) {
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t B = (size_t)batch, k = (size_t)(m < n ? m : n);
+    const size_t es = dtype == BSVD_C ? 16 : 8, rs = 8;  // the double-precision element sizes
     PromWs w{};
     w.io = *o;
     w.io.k = o->k * 0x1p+29;
     w.a = 0;
-    w.u = al(B * m * n * 8);
-    w.s = w.u + al(B * m * k * 8);
-    w.v = w.s + al(B * k * 8);
-    w.inner = w.v + (o->want_v ? al(B * n * k * 8) : 0);
-    w.total = w.inner + bsvd_workspace_bytes(BSVD_D, m, n, batch, &w.io);
+    w.u = al(B * m * n * es);
+    w.s = w.u + al(B * m * k * es);
+    w.v = w.s + al(B * k * rs);
+    w.inner = w.v + (o->want_v ? al(B * n * k * es) : 0);
+    w.total = w.inner + bsvd_workspace_bytes(dtype == BSVD_C ? BSVD_Z : BSVD_D, m, n, batch, &w.io);
     return w;
 }
 __global__ void k_widen(const float* A, int64_t lda, int64_t sA, int m, int n, int batch, double* out) {
@@ -620,7 +631,7 @@ size_t bsvd_workspace_bytes(int dtype, int m, int n, int batch, const bsvd_opts*
     if (make_route(m, n, opts, &r)) return 0;
     if (r.bn == 0 || r.bm == 0) return 0;
     if (r.qr) return qr_ws(dtype, r, batch, opts).total;
-    if (promote_f32(dtype, r, opts)) return prom_ws(m, n, batch, opts).total;
+    if (promote_f32(dtype, r, opts)) return prom_ws(dtype, m, n, batch, opts).total;
     // the call plans with contiguous = (lda == m): size for both plans, so a caller with a padded lda who
     // allocates this many bytes never gets BSVD_ERR_WORKSPACE
     const Plan pc = make_plan(dtype, r, opts, true, batch);
@@ -714,26 +725,30 @@ int bsvd_gesvj_batched(int dtype, int m, int n, int batch, const void* A, int64_
                                           ldv, strideV, opts, info, work, work_bytes, st);
         }
     }
-    if (promote_f32(dtype, r, opts)) {  // FP32 on the FP64 register blocked kernel (see promote_f32)
-        const PromWs w = prom_ws(m, n, batch, opts);
+    if (promote_f32(dtype, r, opts)) {  // single precision on a double-precision register kernel
+        const PromWs w = prom_ws(dtype, m, n, batch, opts);
         if (w.total > work_bytes || !work) return BSVD_ERR_WORKSPACE;
+        const int c = dtype == BSVD_C ? 2 : 1;  // complex: interleaved (re, im) = twice the rows of floats
         unsigned char* wb = static_cast<unsigned char*>(work);
         double* A64 = reinterpret_cast<double*>(wb + w.a);
         double* U64 = reinterpret_cast<double*>(wb + w.u);
         double* S64 = reinterpret_cast<double*>(wb + w.s);
         double* V64 = opts->want_v ? reinterpret_cast<double*>(wb + w.v) : nullptr;
-        const int64_t tot_a = (int64_t)batch * m * n;
-        k_widen<<<grid_for(tot_a), 256, 0, st>>>(static_cast<const float*>(A), lda, strideA, m, n, batch, A64);
+        const int64_t tot_a = (int64_t)batch * c * m * n;
+        k_widen<<<grid_for(tot_a), 256, 0, st>>>(static_cast<const float*>(A), c * lda, c * strideA, c * m, n, batch,
+                                                 A64);
         if (cudaPeekAtLastError() != cudaSuccess) return BSVD_ERR_CUDA;
-        rc = bsvd_gesvj_batched(BSVD_D, m, n, batch, A64, m, (int64_t)m * n, U64, m, (int64_t)m * k, S64, k, V64, n,
-                                (int64_t)n * k, &w.io, info, wb + w.inner, work_bytes - w.inner, stream);
+        rc = bsvd_gesvj_batched(dtype == BSVD_C ? BSVD_Z : BSVD_D, m, n, batch, A64, m, (int64_t)m * n, U64, m,
+                                (int64_t)m * k, S64, k, V64, n, (int64_t)n * k, &w.io, info, wb + w.inner,
+                                work_bytes - w.inner, stream);
         if (rc) return rc;
-        k_narrow<<<grid_for((int64_t)batch * m * k), 256, 0, st>>>(U64, m, k, batch, static_cast<float*>(U), ldu,
-                                                                    strideU);
+        k_narrow<<<grid_for((int64_t)batch * c * m * k), 256, 0, st>>>(U64, c * m, k, batch, static_cast<float*>(U),
+                                                                        c * ldu, c * strideU);
         k_narrow<<<grid_for((int64_t)batch * k), 256, 0, st>>>(S64, k, 1, batch, static_cast<float*>(S), k, strideS);
         if (V64)
-            k_narrow<<<grid_for((int64_t)batch * n * k), 256, 0, st>>>(V64, n, k, batch, static_cast<float*>(V), ldv,
-                                                                        strideV);
+            k_narrow<<<grid_for((int64_t)batch * c * n * k), 256, 0, st>>>(V64, c * n, k, batch,
+                                                                            static_cast<float*>(V), c * ldv,
+                                                                            c * strideV);
         return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
     }
     const Plan p = make_plan(dtype, r, opts, lda == m, batch);

@@ -119,7 +119,10 @@ def test_kernel_selection_routes():
     o.want_v = 1
     assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) == 32    # c128 n = 32: complex register kernel
     assert L.bsvd_select_kernel(3, 300, 32, ctypes.byref(o)) == 1     # m > 256: general unblocked kernel
-    assert L.bsvd_select_kernel(2, 256, 32, ctypes.byref(o)) == 1     # c64: general unblocked kernel
+    assert L.bsvd_select_kernel(2, 256, 32, ctypes.byref(o)) == 32    # c64 n = 32: on the c128 register kernel
+    assert L.bsvd_select_kernel(2, 256, 24, ctypes.byref(o)) == 1     # c64, other n: general unblocked kernel
+    assert L.bsvd_select_kernel(0, 64, 64, ctypes.byref(o)) == 30     # FP32 blocked: on the FP64 register kernel
+    assert L.bsvd_select_kernel(0, 32, 32, ctypes.byref(o)) == 42     # FP32 32x32: on the FP64 register kernel
     o.route = _lib.FORCE_BLOCKED
     assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) == 32    # blocked route, ell = 2: same kernel
     o.nb = 8
