@@ -45,7 +45,6 @@ namespace creg {
 constexpr int N = 32;      // columns
 constexpr int H = 16;      // pairs per iteration
 constexpr int NIT = 31;    // iterations per sweep
-constexpr int RSTR = 34;   // transpose buffer row stride (doubles)
 constexpr int MAXW = 8;    // warps per CTA (m <= 256)
 
 __host__ __device__ constexpr int ring_slot(int q) {
@@ -68,9 +67,11 @@ struct __align__(16) Par {
     double cm1, ar, ai, pad;  // x_t += cm1 x_t + A x_b;  x_b += cm1 x_b - conj(A) x_t
 };
 
+constexpr int RS2 = 33;    // double2 transpose buffer row stride (conflict-free 16-byte reads)
+
 struct WarpSmem {
-    double red[2 * H * RSTR];  // transpose buffer (32 partial rows x 32 lanes)
-    Par pub[H];
+    double2 red[H * RS2];      // transpose buffer: pair q's (re, im) partials of the 32 lanes, row q
+    double pub[3 * H];         // this iteration's rotations, dense (cm1, ar, ai) triples: 2 pairs = 3 x 16 B
     double nrm[N];             // maintained squared column norms (identical in every warp)
 };
 
@@ -82,18 +83,23 @@ struct PSmem {
     double2 P[N * N];              // running rotation product (= V), column-major, (re, im) interleaved
 };
 
-__device__ __forceinline__ double sum16(const double* p) {
-    const double2* r = reinterpret_cast<const double2*>(p);
-    const double2 p0 = r[0], p1 = r[1], p2 = r[2], p3 = r[3], p4 = r[4], p5 = r[5], p6 = r[6], p7 = r[7];
-    const double s0 = (p0.x + p0.y) + (p1.x + p1.y), s1 = (p2.x + p2.y) + (p3.x + p3.y);
-    const double s2 = (p4.x + p4.y) + (p5.x + p5.y), s3 = (p6.x + p6.y) + (p7.x + p7.y);
-    return (s0 + s1) + (s2 + s3);
-}
-// total over the warp's 32 lanes of transpose row `row` (identical bits on both halves)
-__device__ __forceinline__ double sum32(const double* red, int row, int half) {
-    const double s = sum16(red + row * RSTR + 16 * half);
-    const double o = __shfl_xor_sync(0xffffffffu, s, 16);
-    return half ? o + s : s + o;
+// totals over the warp's 32 lanes of both components of transpose row `row` (identical bits on both
+// halves; each component summed in the tree of sum16 over consecutive lanes, then across the halves)
+__device__ __forceinline__ double2 sum32x2(const double2* red, int row, int half) {
+    const double2* r = red + row * RS2 + 16 * half;
+    double2 p[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) p[i] = r[i];
+    double sx[4], sy[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        sx[j] = (p[4 * j].x + p[4 * j + 1].x) + (p[4 * j + 2].x + p[4 * j + 3].x);
+        sy[j] = (p[4 * j].y + p[4 * j + 1].y) + (p[4 * j + 2].y + p[4 * j + 3].y);
+    }
+    const double tx = (sx[0] + sx[1]) + (sx[2] + sx[3]);
+    const double ty = (sy[0] + sy[1]) + (sy[2] + sy[3]);
+    const double ox = __shfl_xor_sync(0xffffffffu, tx, 16), oy = __shfl_xor_sync(0xffffffffu, ty, 16);
+    return half ? make_double2(ox + tx, oy + ty) : make_double2(tx + ox, ty + oy);
 }
 __device__ __forceinline__ void bar_named(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
@@ -178,15 +184,17 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
 #pragma unroll
         for (int q = 0; q < H; ++q) {
             const double tr = xr[TS(q, u)], ti = xi[TS(q, u)], br = xr[BS(q, u)], bi = xi[BS(q, u)];
-            sm.red[q * RSTR + c.lane] = fma(bi, ti, br * tr);
-            sm.red[(H + q) * RSTR + c.lane] = fma(-bi, tr, br * ti);
+            sm.red[q * RS2 + c.lane] = make_double2(fma(bi, ti, br * tr), fma(-bi, tr, br * ti));
         }
     }
     const uint32_t code = c.ctab[t * H + c.k];
     __syncwarp();
     double v[4];
-    v[0] = sum32(sm.red, c.k, c.half);
-    v[1] = sum32(sm.red, H + c.k, c.half);
+    {
+        const double2 g = sum32x2(sm.red, c.k, c.half);
+        v[0] = g.x;
+        v[1] = g.y;
+    }
     int nval = 2;
     if (st.full) {  // fresh squared norms through the same buffer (rare: sweep start, >4x shrink)
         __syncwarp();
@@ -194,13 +202,13 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
 #pragma unroll
             for (int q = 0; q < H; ++q) {
                 const double tr = xr[TS(q, u)], ti = xi[TS(q, u)], br = xr[BS(q, u)], bi = xi[BS(q, u)];
-                sm.red[q * RSTR + c.lane] = fma(ti, ti, tr * tr);
-                sm.red[(H + q) * RSTR + c.lane] = fma(bi, bi, br * br);
+                sm.red[q * RS2 + c.lane] = make_double2(fma(ti, ti, tr * tr), fma(bi, bi, br * br));
             }
         }
         __syncwarp();
-        v[2] = sum32(sm.red, c.k, c.half);
-        v[3] = sum32(sm.red, H + c.k, c.half);
+        const double2 gn = sum32x2(sm.red, c.k, c.half);
+        v[2] = gn.x;
+        v[3] = gn.y;
         nval = 4;
     }
     if constexpr (NW > 1) {  // sum over the CTA's warps: one barrier, fixed warp order
@@ -246,7 +254,9 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
     const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
     __syncwarp();  // every lane has read nrm[] and red[] of this iteration
     if (c.lane < H) {
-        sm.pub[c.k] = par;
+        sm.pub[3 * c.k] = par.cm1;
+        sm.pub[3 * c.k + 1] = par.ar;
+        sm.pub[3 * c.k + 2] = par.ai;
         sm.nrm[ct] = nt;
         sm.nrm[cb] = nb;
         st.my_rot += rot ? 1 : 0;
@@ -255,17 +265,29 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
     st.full = __ballot_sync(0xffffffffu, shrink) != 0u;
     __syncwarp();
     if (!mask) return;
-    // ---- W update in registers ----
+    // ---- W update in registers (two pairs' parameters per three 16-byte loads) ----
 #pragma unroll
-    for (int q = 0; q < H; ++q) {
-        const Par pq = sm.pub[q];
-        capply(xr[TS(q, u)], xi[TS(q, u)], xr[BS(q, u)], xi[BS(q, u)], pq);
+    for (int q = 0; q < H; q += 2) {
+        const double2* pp = reinterpret_cast<const double2*>(sm.pub + 3 * q);
+        const double2 a = pp[0], b = pp[1], d = pp[2];
+        Par p0, p1;
+        p0.cm1 = a.x;
+        p0.ar = a.y;
+        p0.ai = b.x;
+        p1.cm1 = b.y;
+        p1.ar = d.x;
+        p1.ai = d.y;
+        capply(xr[TS(q, u)], xi[TS(q, u)], xr[BS(q, u)], xi[BS(q, u)], p0);
+        capply(xr[TS(q + 1, u)], xi[TS(q + 1, u)], xr[BS(q + 1, u)], xi[BS(q + 1, u)], p1);
     }
     // ---- P (= V) update in smem: task (row = lane, pair q) for q = warp, warp + NW, ... ----
     if (SP && c.want_p) {
         double2* P = c.ps->P;
         for (int q = c.warp; q < H; q += NW) {
-            const Par pq = sm.pub[q];
+            Par pq;
+            pq.cm1 = sm.pub[3 * q];
+            pq.ar = sm.pub[3 * q + 1];
+            pq.ai = sm.pub[3 * q + 2];
             if (pq.cm1 == 0.0 && pq.ar == 0.0 && pq.ai == 0.0) continue;  // skipped pair (warp-uniform)
             const uint32_t cq = c.ctab[t * H + q];
             const int a0 = (cq & 0xff) * N + c.lane, b0 = ((cq >> 8) & 0xff) * N + c.lane;
@@ -353,7 +375,7 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1)
     uint32_t phase = 0;
 #pragma unroll 1
     for (int prob = blockIdx.x; prob < a.batch; prob = a.batch) {  // one problem per CTA
-        for (int e = lane; e < 2 * H * RSTR; e += 32) wsm[warp].red[e] = 0.0;  // V / padding lanes stay 0
+        for (int e = lane; e < H * RS2; e += 32) wsm[warp].red[e] = make_double2(0.0, 0.0);  // V / padding lanes stay 0
         if (tid < 4) cs->misc[tid] = 0;
         if (SP && want_p)
             for (int e = tid; e < N * N; e += NW * 32) {
