@@ -63,6 +63,11 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         if (p.kernel) return p;
         if (o->kernel != 0) return p;
     }
+    if (r.blocked && (o->kernel == 0 || o->kernel == KV_CREGB)) {  // complex FP64, n > 32
+        Plan p = plan_cregb(dt, r.bm, r.bn, r.need_v, r.trans, o->nb);
+        if (p.kernel) return p;
+        if (o->kernel != 0) return p;
+    }
     if (r.blocked) {
         if (o->kernel == 0 || o->kernel == KV_BLOCKED_REG) {
             Plan p = plan_blocked_reg(dt, r.bm, r.bn, o->nb, r.need_v, reg_ok, o->inner_sweeps, o->kernel);
@@ -172,6 +177,9 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
         case KV_CREG32:
         case KV_CREG32_TMA:
             if constexpr (sizeof(T) == 16 && tr<T>::cplx) return launch_creg32(a, p, st);
+            return BSVD_ERR_UNSUPPORTED;
+        case KV_CREGB:
+            if constexpr (sizeof(T) == 16 && tr<T>::cplx) return launch_cregb(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
         case KV_BLOCKED_DMMA:
         case KV_BLOCKED_DMMA_VG:
@@ -583,7 +591,9 @@ bool promote_f32(int dtype, const Route& r, const bsvd_opts* o) {
         if (r.blocked) return plan_blocked_reg(BSVD_D, r.bm, r.bn, o->nb, r.need_v, true, o->inner_sweeps, 0).kernel != 0;
         return r.bm == 32 && r.bn == 32;
     }
-    if (dtype == BSVD_C) return plan_creg32(BSVD_Z, r.bm, r.bn, r.need_v, true, r.blocked, o->nb, 0, smem_limit()).kernel != 0;
+    if (dtype == BSVD_C)
+        return plan_creg32(BSVD_Z, r.bm, r.bn, r.need_v, true, r.blocked, o->nb, 0, smem_limit()).kernel != 0 ||
+               (r.blocked && plan_cregb(BSVD_Z, r.bm, r.bn, r.need_v, r.trans, o->nb).kernel != 0);
     return false;
 }
 struct PromWs {

@@ -337,9 +337,9 @@ inline size_t smem_bytes_tma(int nw, bool sp, int m, int ncs) {
 
 // NW warps; SP: V as the smem product P (m > 224), else V rows ride along in registers below
 // W's rows (rows m .. m + 31 of the CTA, rotated like W, excluded from the dot products).
-// TMA: persistent CTAs; kernel (1) stages each problem into shared memory with 32 bulk copies (one
-// column each, cp.async.bulk -> UBLKCP) completing on an mbarrier, and the next problem of the CTA is
-// already in flight while this one is solved.  Without TMA: one CTA per problem, coalesced LDG.
+// TMA (variant 45): kernel (1) stages the problem into shared memory with one bulk copy per column
+// (cp.async.bulk -> UBLKCP) completing on an mbarrier; without TMA (default): coalesced LDG.  One CTA
+// per problem either way.
 template <int NW, bool SP, bool TMA>
 __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1)
     k_creg32(SolveArgs<cx<double>> a, int blocked, int ncs) {
@@ -507,6 +507,170 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1)
     }
 }
 
+// Blocked complex FP64, n > 32 (n % 16 == 0, m <= 256): the outer round-robin over the l = n / 16 column
+// blocks of _sweep_blocked (src/svd.py:481-522); each block pair X = [Wi Wj] (m x 32) is solved by this
+// file's register iteration in its P-in-shared-memory form (the inner eigensolve of the block pair's
+// Gram is one-sided Jacobi on X itself: the same rotations, G never formed), then X is written back and
+// [Vi Vj] <- [Vi Vj] P (the fused update of src/_kernels_numba.py:141-175) row by row from the
+// workspace.  One CTA per problem, block pairs of an outer iteration in turn; W and V live in the
+// (L2-resident) workspace, finalised by the standalone pass.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_cregb(SolveArgs<cx<double>> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int m = a.bm, n = a.bn, prob = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem);
+    CtaSmem* cs = reinterpret_cast<CtaSmem*>(smem + NW * sizeof(WarpSmem));
+    PSmem* ps = reinterpret_cast<PSmem*>(smem + NW * sizeof(WarpSmem) + sizeof(CtaSmem));
+    uint32_t* ctab = reinterpret_cast<uint32_t*>(smem + NW * sizeof(WarpSmem) + sizeof(CtaSmem) + sizeof(PSmem));
+    const bool want_p = a.need_v != 0;
+    const int ell = n / 16, Sb = ell + (ell & 1), nib = Sb - 1, hb = Sb / 2;
+    cx<double>* W = a.work + (size_t)prob * (size_t)a.work_stride;  // m x n, then V n x n
+    cx<double>* V = W + (size_t)m * n;
+    for (int e = tid; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
+    if (tid < 4) cs->misc[tid] = 0;
+    __syncthreads();
+    // ---- kernel (1): A -> W with an exact power-of-two prescale, V = I ----
+    {
+        const cx<double>* Ap = a.A + (size_t)prob * a.strideA;
+        double amax = 0.0;
+        int bad = 0;
+        for (int e = tid; e < m * n; e += NW * 32) {
+            const cx<double> z = Ap[(e % m) + (size_t)(e / m) * a.lda];
+            bad |= !(isfinite(z.re) && isfinite(z.im));
+            amax = fmax(amax, fmax(fabs(z.re), fabs(z.im)));
+        }
+        if (bad) atomicOr(&cs->misc[0], 1);
+        atomicMax(reinterpret_cast<unsigned long long*>(&cs->misc[2]), (unsigned long long)__double_as_longlong(amax));
+        __syncthreads();
+        const double sc = pow2(-prescale_exponent(__longlong_as_double(*reinterpret_cast<long long*>(&cs->misc[2]))));
+        for (int e = tid; e < m * n; e += NW * 32) {
+            const cx<double> z = Ap[(e % m) + (size_t)(e / m) * a.lda];
+            W[e] = cx<double>{z.re * sc, z.im * sc};
+        }
+        if (want_p)
+            for (int e = tid; e < n * n; e += NW * 32) V[e] = cx<double>{(e % n) == (e / n) ? 1.0 : 0.0, 0.0};
+        __syncthreads();
+    }
+    const int ex = prescale_exponent(__longlong_as_double(*reinterpret_cast<long long*>(&cs->misc[2])));
+    const int row = warp * 32 + lane;
+    const bool live = row < m;
+    Ctx c;
+    c.sm = &wsm[warp];
+    c.cs = cs;
+    c.ctab = ctab;
+    c.lane = lane;
+    c.half = lane >> 4;
+    c.k = lane & 15;
+    c.warp = warp;
+    c.ps = ps;
+    c.nww = (m + 31) / 32;
+    c.wrow = live;
+    c.tol = a.tol;
+    c.tol2 = a.tol * a.tol;
+    c.want_p = want_p;
+    const int budget = a.inner_budget;
+    int sweeps = 0, last = 0, conv = 0;
+    long long rot_total = 0, grams = 0, updates = 0;
+    double xr[N], xi[N];
+#pragma unroll 1
+    for (int sw = 0; sw < a.max_sweeps; ++sw) {
+        long long sweep_rot = 0;
+#pragma unroll 1
+        for (int tb = 0; tb < nib; ++tb) {
+#pragma unroll 1
+            for (int g = 0; g < hb; ++g) {
+                int bi = 0, bj = 0;
+                if (!rr_pair(tb, g, Sb, ell, bi, bj)) continue;  // phantom block (odd l)
+                auto col = [&](int x) { return x < 16 ? bi * 16 + x : bj * 16 + x - 16; };
+                // X = [Wi Wj]: this lane's row; P = I; transpose buffers cleared (padding lanes read 0)
+#pragma unroll
+                for (int x = 0; x < N; ++x) {
+                    const cx<double> z = live ? W[row + (size_t)col(x) * m] : cx<double>{0.0, 0.0};
+                    xr[x] = z.re;
+                    xi[x] = z.im;
+                }
+                for (int e = lane; e < H * RS2; e += 32) wsm[warp].red[e] = make_double2(0.0, 0.0);
+                if (want_p)
+                    for (int e = tid; e < N * N; e += NW * 32)
+                        ps->P[e] = make_double2((e % N) == (e / N) ? 1.0 : 0.0, 0.0);
+                __syncthreads();
+                IState st;
+                st.par = 0;
+                int bp_rot = 0;
+#pragma unroll 1
+                for (int isw = 0; isw < budget; ++isw) {
+                    st.my_rot = 0;
+                    sweep<NW, true>(xr, xi, c, st);
+                    int r = st.my_rot;  // lanes 0..15: counts of pairs 0..15 (identical in every warp)
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+                    r = __shfl_sync(0xffffffffu, r, 0);
+                    bp_rot += r;
+                    if (r == 0) break;
+                }
+                ++grams;
+                sweep_rot += bp_rot;
+                if (bp_rot) {
+                    ++updates;
+                    if (live) {
+#pragma unroll
+                        for (int x = 0; x < N; ++x) W[row + (size_t)col(x) * m] = cx<double>{xr[x], xi[x]};
+                    }
+                    if (want_p) {
+                        __syncthreads();  // P complete
+                        // [Vi Vj] <- [Vi Vj] P, one row of V per thread (the rows of X are free registers)
+                        for (int vr = tid; vr < n; vr += NW * 32) {
+#pragma unroll
+                            for (int x = 0; x < N; ++x) {
+                                const cx<double> z = V[vr + (size_t)col(x) * n];
+                                xr[x] = z.re;
+                                xi[x] = z.im;
+                            }
+#pragma unroll 4
+                            for (int y = 0; y < N; ++y) {
+                                double sr = 0.0, si = 0.0;
+#pragma unroll
+                                for (int x = 0; x < N; ++x) {
+                                    const double2 p = ps->P[y * N + x];  // P[x][y], column-major
+                                    sr = fma(xr[x], p.x, fma(-xi[x], p.y, sr));
+                                    si = fma(xr[x], p.y, fma(xi[x], p.x, si));
+                                }
+                                V[vr + (size_t)col(y) * n] = cx<double>{sr, si};
+                            }
+                        }
+                    }
+                }
+                __syncthreads();  // the next block pair reads the columns written here
+            }
+        }
+        sweeps = sw + 1;
+        last = (int)sweep_rot;
+        rot_total += sweep_rot;
+        if (sweep_rot == 0) {
+            conv = 1;
+            break;
+        }
+    }
+    {
+        const double us = pow2(ex);
+        for (int e = tid; e < m * n; e += NW * 32) W[e] = cx<double>{W[e].re * us, W[e].im * us};
+    }
+    if (tid == 0 && a.info) {
+        bsvd_info inf;
+        inf.converged = conv;
+        inf.outer_sweeps = sweeps;
+        inf.rotations = rot_total;
+        inf.gram_calls = grams;
+        inf.update_calls = updates;
+        inf.last_rotations = last;
+        inf.path = 2;
+        inf.status = cs->misc[0] ? 1 : 0;
+        inf.kernel = a.kernel;
+        a.info[prob] = inf;
+    }
+}
+
 }  // namespace creg
 
 Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blocked, int nb, int variant,
@@ -529,6 +693,45 @@ Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blo
     p.grid = 0;
     p.resident = blocked ? 1 : 0;  // route flag for the launcher
     return p;
+}
+
+Plan plan_cregb(int dtype, int bm, int bn, int need_v, bool trans, int nb) {
+    Plan p{};
+    if (dtype != BSVD_Z || trans || nb != 16 || bn <= 32 || bn % 16 != 0 || bm < bn || bm > 256) return p;
+    const int nw = (bm + 31) / 32;
+    p.kernel = KV_CREGB;
+    p.threads = nw * 32;
+    p.group = nw;
+    p.smem = creg::smem_bytes(nw, true);
+    p.work_elems = (size_t)bm * bn + (need_v ? (size_t)bn * bn : 0);
+    return p;
+}
+
+template <int NW>
+static int launch_cb(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st) {
+    auto k = creg::k_cregb<NW>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<a.batch, NW * 32, p.smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+int launch_cregb(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st) {
+    a.kernel = p.kernel;
+    a.work_stride = (int64_t)p.work_elems;
+    int rc;
+    switch (p.group) {
+        case 2: rc = launch_cb<2>(a, p, st); break;
+        case 3: rc = launch_cb<3>(a, p, st); break;
+        case 4: rc = launch_cb<4>(a, p, st); break;
+        case 5: rc = launch_cb<5>(a, p, st); break;
+        case 6: rc = launch_cb<6>(a, p, st); break;
+        case 7: rc = launch_cb<7>(a, p, st); break;
+        case 8: rc = launch_cb<8>(a, p, st); break;
+        default: return BSVD_ERR_UNSUPPORTED;
+    }
+    if (rc) return rc;
+    return launch_finalize_gm<cx<double>>(a, st);
 }
 
 template <int NW, bool SP>

@@ -50,6 +50,7 @@ enum {
     KV_BLOCKED_REG = 30,        // blocked FP64: block pairs register-resident (kernel (2) on X), V P on DMMA
     KV_CREG32 = 32,             // complex FP64, n = 32, m <= 256: CTA per problem, rows in registers, V in smem
     KV_UNBLOCKED_REG16C = 34,   // 16x16 FP32 third generation: 4 problems per warp, 2 rows per lane
+    KV_CREGB = 51,              // complex FP64 blocked (n > 32): block pairs through the complex register iteration
     KV_CREG32_TMA = 45,         // KV_CREG32 with the bulk-copy (TMA) loader: 1-3 % slower, opt-in
                                 //   (profiles/r2_tma_loader.md)
     KV_UNBLOCKED_REG32G = 42,   // KV_UNBLOCKED_REG32B with scaled (fast) rotations: one FMA per updated element

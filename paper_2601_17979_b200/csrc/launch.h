@@ -84,6 +84,8 @@ int launch_unblocked_reg16c(SolveArgs<float> a, const Plan& p, cudaStream_t st);
 Plan plan_creg32(int dtype, int bm, int bn, int need_v, bool contiguous, int blocked, int nb, int variant,
                  size_t smem_limit);
 int launch_creg32(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st);
+Plan plan_cregb(int dtype, int bm, int bn, int need_v, bool trans, int nb);
+int launch_cregb(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st);
 
 int group_for_rows(int bm);
 int threads_for(int bn, int G);

@@ -519,10 +519,12 @@ def test_eig_sweeps_operator_full_solve(dt):
     assert np.max(np.abs(m.conj().T @ m - np.eye(n))) <= 60 * n * u
 
 
-# (FP32 blocked shapes the FP64 register kernel takes are solved on it in float64: kernel 30)
+# (FP32 blocked shapes the FP64 register kernel takes are solved on it in float64: kernel 30; complex
+# blocked n % 16 == 0: the complex register blocked kernel 51, complex64 promoted to it)
 _DEFAULT_KERNEL_SHAPES = [(np.float64, 32, 32, 42), (np.float32, 16, 16, 24), (np.float64, 64, 64, 30),
                           (np.complex128, 256, 32, 32), (np.complex128, 40, 24, 1), (np.float32, 48, 48, 30),
-                          (np.complex64, 48, 48, 2), (np.float32, 40, 40, 2)]
+                          (np.complex64, 48, 48, 51), (np.complex128, 64, 64, 51), (np.float32, 40, 40, 2),
+                          (np.complex128, 40, 40, 2)]
 
 
 @pytest.mark.gpu

@@ -111,7 +111,8 @@ def test_kernel_selection_routes():
     o = _lib.BsvdOpts()
     L.bsvd_default_opts(ctypes.byref(o))
     assert L.bsvd_select_kernel(1, 64, 64, ctypes.byref(o)) == 30     # blocked FP64: register block pairs
-    assert L.bsvd_select_kernel(3, 64, 64, ctypes.byref(o)) == 2      # blocked complex: general kernel
+    assert L.bsvd_select_kernel(3, 64, 64, ctypes.byref(o)) == 51     # blocked complex: complex register blocked
+    assert L.bsvd_select_kernel(3, 40, 40, ctypes.byref(o)) == 2      # n % 16 != 0: general blocked kernel
     assert L.bsvd_select_kernel(0, 16, 16, ctypes.byref(o)) == 24     # 16x16 FP32 register kernel (2nd gen)
     assert L.bsvd_select_kernel(1, 32, 32, ctypes.byref(o)) == 42     # 32x32 FP64: 2nd gen, scaled rotations
     o.want_v = 0
