@@ -558,8 +558,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         const double* Ap = a.A + (size_t)(live ? prob : 0) * a.strideA;  // plan requires lda == 32
 #pragma unroll
         for (int c = 0; c < N; ++c) {
-            x0[c] = live ? Ap[r0 + c * N] : 0.0;
-            x1[c] = live ? Ap[r1 + c * N] : 0.0;
+            x0[c] = live ? __ldcs(Ap + r0 + c * N) : 0.0;  // read once: evict-first, keep L2 for the workspace
+            x1[c] = live ? __ldcs(Ap + r1 + c * N) : 0.0;
         }
 #pragma unroll
         for (int c = 0; c < N; ++c) {
@@ -751,8 +751,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
             for (int c = 0; c < N; ++c) {  // U = W / sigma: reciprocal, then one residual correction
                 const int rc = rk[c];
                 const double2 t = sr[c];
-                u0[(size_t)rc * o.ldu] = div_by_sigma(x0[c], t.x, t.y);
-                u1[(size_t)rc * o.ldu] = div_by_sigma(x1[c], t.x, t.y);
+                __stcs(u0 + (size_t)rc * o.ldu, div_by_sigma(x0[c], t.x, t.y));  // streaming: not re-read
+                __stcs(u1 + (size_t)rc * o.ldu, div_by_sigma(x1[c], t.x, t.y));
             }
             if (o.want_v && o.V) {
                 // all 64 loads ahead of the stores (the compiler cannot prove o.V and wsV disjoint,
@@ -779,8 +779,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
                         y0 = div_by_sigma(y0, vv, rv);
                         y1 = div_by_sigma(y1, vv, rv);
                     }
-                    o.V[r0 + (size_t)rc * o.ldv] = y0;
-                    o.V[r1 + (size_t)rc * o.ldv] = y1;
+                    __stcs(o.V + r0 + (size_t)rc * o.ldv, y0);
+                    __stcs(o.V + r1 + (size_t)rc * o.ldv, y1);
                 }
             }
         }
@@ -822,6 +822,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
                 wsV[r1 + c * N] = (c == r1) ? 1.0 : 0.0;
             }
         }
+    }
+    if (live && fused) {
+        // the problem is finished and its workspace (W / V parking, rotation log) is dead: drop its L2
+        // lines instead of letting them be written back to DRAM (they were ~60 % of the kernel's DRAM
+        // traffic); the line holding the finalisation flag, which the standalone pass reads, is kept
+        __syncwarp();
+        const uintptr_t lo = ((uintptr_t)wsW + 127) & ~(uintptr_t)127;
+        const uintptr_t hi = (uintptr_t)flagp & ~(uintptr_t)127;
+        for (uintptr_t l = lo + (uintptr_t)hl * 128; l < hi; l += 16 * 128)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");
     }
     const unsigned badm = __ballot_sync(0xffffffffu, bad != 0);
     if (live && hl == 0 && a.info) {
