@@ -10,8 +10,18 @@
 #include <vector>
 
 #include "launch.h"
+#include <nvtx3/nvToolsExt.h>
 
 using namespace bsvd;
+
+namespace {
+// NVTX range around every C-ABI entry point (tracing): the calls show up by name on an nsys /
+// Nsight timeline next to the kernels they launch; free when no tool is attached (nvtx3 is header-only)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -206,6 +216,7 @@ size_t bsvd_heevj_workspace_bytes(int dtype, int n, int batch) {
 int bsvd_heevj_batched(int dtype, int n, int batch, const void* G, int64_t ldg, int64_t strideG, void* D,
                        int64_t strideD, void* M, int64_t ldm, int64_t strideM, int m_init, double k, int max_sweeps,
                        bsvd_info* info, void* work, size_t work_bytes, void* stream) {
+    const NvtxRange nvtx_range("bsvd_heevj_batched");
     if (dtype < 0 || dtype > 3 || n < 0 || batch < 0 || !(k > 0) || max_sweeps < 1) return BSVD_ERR_ARG;
     if (batch == 0 || n == 0) return BSVD_OK;
     if (!G || !D || !M || ldg < n || ldm < n) return BSVD_ERR_ARG;
@@ -217,6 +228,7 @@ int bsvd_heevj_batched(int dtype, int n, int batch, const void* G, int64_t ldg, 
 int bsvd_eig_sweeps_batched(int dtype, int n, int batch, void* G, int64_t ldg, int64_t strideG, void* D,
                             int64_t strideD, void* M, int64_t ldm, int64_t strideM, double tol, int max_sweeps,
                             int delta, bsvd_info* info, void* work, size_t work_bytes, void* stream) {
+    const NvtxRange nvtx_range("bsvd_eig_sweeps_batched");
     if (dtype < 0 || dtype > 3 || n < 0 || batch < 0 || !(tol >= 0) || max_sweeps < 1) return BSVD_ERR_ARG;
     if (batch == 0 || n == 0) return BSVD_OK;
     if (!G || !D || !M || ldg < n || ldm < n) return BSVD_ERR_ARG;
@@ -230,6 +242,7 @@ int bsvd_verify_batched(int dtype, int m, int n, int batch, const void* A, int64
                         const void* U, int64_t ldu, int64_t strideU, const void* S, int64_t strideS, const void* V,
                         int64_t ldv, int64_t strideV, const double* Sref, int64_t strideSref, double* out,
                         void* stream) {
+    const NvtxRange nvtx_range("bsvd_verify_batched");
     if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0) return BSVD_ERR_ARG;
     if (batch == 0) return BSVD_OK;
     if (!A || !U || !S || !out || lda < m || ldu < m || (V && ldv < n)) return BSVD_ERR_ARG;
@@ -241,6 +254,7 @@ int bsvd_finalize_batched(int dtype, int m, int n, int batch, const void* W, int
                           int vrows, const void* V, int64_t ldv, int64_t strideV, void* U, int64_t ldu,
                           int64_t strideU, void* S, int64_t strideS, void* Vout, int64_t ldvo, int64_t strideVout,
                           void* stream) {
+    const NvtxRange nvtx_range("bsvd_finalize_batched");
     if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || vrows < 0) return BSVD_ERR_ARG;
     if (n > m) return BSVD_ERR_ARG;  // finalize expects m >= n (src/svd.py:246-247)
     if (batch == 0 || n == 0) return BSVD_OK;
@@ -265,6 +279,7 @@ size_t bsvd_householder_qr_workspace_bytes(int dtype, int m, int n, int batch) {
 int bsvd_householder_qr_batched(int dtype, int m, int n, int batch, const void* A, int64_t lda, int64_t strideA,
                                 void* Q, int64_t ldq, int64_t strideQ, void* R, int64_t ldr, int64_t strideR,
                                 void* work, size_t work_bytes, void* stream) {
+    const NvtxRange nvtx_range("bsvd_householder_qr_batched");
     if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0) return BSVD_ERR_ARG;
     if (m < n) return BSVD_ERR_ARG;  // householder_qr needs m >= n (src/core.py:125-126)
     if (batch == 0 || n == 0) return BSVD_OK;
@@ -429,6 +444,7 @@ int gesvj_host_impl(int dtype, int m, int n, int batch, const void* A, const voi
 int bsvd_gesvj_batched_host(int dtype, int m, int n, int batch, const void* A, void* U, void* S, void* V,
                             const bsvd_opts* opts, bsvd_info* info, int chunk, void* work, size_t work_bytes,
                             void* const* streams, int nstreams) {
+    const NvtxRange nvtx_range("bsvd_gesvj_batched_host");
     return gesvj_host_impl(dtype, m, n, batch, A, nullptr, 0, U, S, V, opts, info, chunk, work, work_bytes, streams,
                            nstreams);
 }
@@ -437,6 +453,7 @@ int bsvd_gesvj_batched_host_gather(int dtype, int m, int n, int batch, const voi
                                    int pack_threads, void* U, void* S, void* V, const bsvd_opts* opts,
                                    bsvd_info* info, int chunk, void* work, size_t work_bytes, void* const* streams,
                                    int nstreams) {
+    const NvtxRange nvtx_range("bsvd_gesvj_batched_host_gather");
     if (batch > 0 && !A_ptrs) return BSVD_ERR_ARG;
     return gesvj_host_impl(dtype, m, n, batch, A_stage, A_ptrs, pack_threads, U, S, V, opts, info, chunk, work,
                            work_bytes, streams, nstreams);
@@ -699,6 +716,7 @@ int bsvd_gesvj_batched(int dtype, int m, int n, int batch, const void* A, int64_
                        int64_t ldu, int64_t strideU, void* S, int64_t strideS, void* V, int64_t ldv,
                        int64_t strideV, const bsvd_opts* opts, bsvd_info* info, void* work, size_t work_bytes,
                        void* stream) {
+    const NvtxRange nvtx_range("bsvd_gesvj_batched");
     if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0) return BSVD_ERR_ARG;
     int rc = check_opts(opts);
     if (rc) return rc;
@@ -786,6 +804,7 @@ int bsvd_gesvj_batched(int dtype, int m, int n, int batch, const void* A, int64_
 int bsvd_onesided_sweeps_batched(int dtype, int m, int n, int batch, void* a, int64_t lda, int64_t stride_a,
                                  int vrows, void* v, int64_t ldv, int64_t stride_v, double tol, int max_sweeps,
                                  int64_t* rotations, int32_t* sweeps, void* stream) {
+    const NvtxRange nvtx_range("bsvd_onesided_sweeps_batched");
     if (dtype < 0 || dtype > 3 || m < 0 || n < 0 || batch < 0 || vrows < 0 || max_sweeps < 1) return BSVD_ERR_ARG;
     if (batch == 0) return BSVD_OK;
     if (!a || lda < m || (vrows > 0 && (!v || ldv < vrows))) return BSVD_ERR_ARG;
@@ -810,6 +829,7 @@ int bsvd_onesided_sweeps_batched(int dtype, int m, int n, int batch, void* a, in
 
 int bsvd_gram_batched(int dtype, int m, int wi, int wj, int batch, const void* a, int64_t lda, int64_t stride_a,
                       void* g, int64_t ldg, int64_t stride_g, void* stream) {
+    const NvtxRange nvtx_range("bsvd_gram_batched");
     if (dtype < 0 || dtype > 3 || m < 0 || wi < 1 || wj < 0 || batch < 0) return BSVD_ERR_ARG;
     if (batch == 0) return BSVD_OK;
     if (!a || !g || lda < m || ldg < wi + wj) return BSVD_ERR_ARG;
@@ -825,6 +845,7 @@ int bsvd_gram_batched(int dtype, int m, int wi, int wj, int batch, const void* a
 
 int bsvd_fused_pair_update_batched(int dtype, int m, int w, int batch, void* b, int64_t ldb, int64_t stride_b,
                                    const void* j, int64_t ldj, int64_t stride_j, int delta, void* stream) {
+    const NvtxRange nvtx_range("bsvd_fused_pair_update_batched");
     if (dtype < 0 || dtype > 3 || m < 0 || w < 1 || batch < 0) return BSVD_ERR_ARG;
     if (batch == 0 || m == 0) return BSVD_OK;
     if (!b || !j || ldb < m || ldj < w) return BSVD_ERR_ARG;
