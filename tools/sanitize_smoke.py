@@ -36,6 +36,12 @@ run(np.complex128, 64, 32)                    # creg32 register V
 run(np.complex128, 256, 32, B=2, use_qr_preprocess=True)  # qr_col + creg32 + applyq_col
 run(np.float64, 96, 20, use_qr_preprocess=True)
 run(np.complex64, 40, 24)                     # general unblocked
+run(np.complex128, 64, 64, B=2)               # complex register blocked (k_cregb)
+run(np.complex64, 48, 48, B=2)                # complex64 promoted to k_cregb
+run(np.float32, 64, 64, B=2)                  # FP32 blocked promoted to the FP64 register blocked kernel
+run(np.float32, 32, 32, B=3)                  # FP32 32x32 promoted to the FP64 32x32 kernel
+run(np.complex64, 256, 32, B=2)               # complex64 promoted to creg32
+run(np.complex128, 256, 32, B=2, kernel=45)   # creg32 with the TMA (bulk-copy) loader
 run(np.float32, 48, 48)                       # general blocked
 q, r = bs.householder_qr(rng.random((40, 12)))
 f = bs.finalize(rng.random((20, 7)), rng.random((7, 7)))
