@@ -26,6 +26,7 @@ struct NvtxRange {
 namespace {
 
 constexpr size_t kSmemFallback = 232448;  // 227 KB opt-in limit of sm_100
+constexpr int FV_WARPS_PER_SM = 7;  // kernel 52 up to 7 problems per SM (C1: 1,000 0.29 vs 0.31 ms; 1,250 0.44 vs 0.41)
 
 size_t smem_limit() {
     int dev = 0;
@@ -62,6 +63,16 @@ int make_route(int m, int n, const bsvd_opts* o, Route* r) {
     else r->blocked = r->bn > 32;  // SMALL_CUTOFF, src/svd.py:52
     r->need_v = (o->want_v || r->trans) ? 1 : 0;
     return BSVD_OK;
+}
+
+int sm_count() {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        v <= 0) {
+        cudaGetLastError();
+        return 148;  // B200
+    }
+    return v;
 }
 
 Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = true, int batch = 0) {
@@ -106,13 +117,19 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         if (p.kernel) return p;
         if (o->kernel != 0) return p;
     }
-    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG32B || o->kernel == KV_UNBLOCKED_REG32G) {
+    if (o->kernel == 0 || o->kernel == KV_UNBLOCKED_REG32B || o->kernel == KV_UNBLOCKED_REG32G ||
+        o->kernel == KV_UNBLOCKED_REG32F) {
         // 32x32 FP64, the second-generation register kernel.  With V: scaled rotations (one FMA per
         // updated element; sigma = ||w|| / ||v||) at every batch size -- one kernel, so batch ==
         // standalone holds bitwise (profiles/r2_c1_kernel_experiments.md: 10k 1.70 vs 1.85 ms, 1,184
         // problems 0.333 vs 0.34 ms for the warp-specialised round-1 kernel).  Values only: the unscaled
         // form (the scaled one needs V's column norms to cancel its scale roundings).
-        const int want = o->kernel ? o->kernel : (r.need_v ? KV_UNBLOCKED_REG32G : KV_UNBLOCKED_REG32B);
+        // Batches of at most FV_WARPS_PER_SM problems per SM: one problem per warp, V carried in lockstep
+        // by the other half-warp (bit-identical to 42, no replay phase) -- the GPU is not full, so the
+        // shorter per-problem chain wins over 42's two problems per warp.
+        const bool fv = r.need_v && batch > 0 && batch <= FV_WARPS_PER_SM * sm_count();
+        const int want = o->kernel ? o->kernel
+                                   : (r.need_v ? (fv ? KV_UNBLOCKED_REG32F : KV_UNBLOCKED_REG32G) : KV_UNBLOCKED_REG32B);
         Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, reg_ok, want, o->max_sweeps);
         if (p.kernel) return p;
         if (o->kernel != 0) return p;  // forced variant unavailable => kernel 0 => unsupported
@@ -198,6 +215,7 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
             return BSVD_ERR_UNSUPPORTED;
         case KV_UNBLOCKED_REG32B:
         case KV_UNBLOCKED_REG32G:
+        case KV_UNBLOCKED_REG32F:
             if constexpr (sizeof(T) == 8 && !tr<T>::cplx) return launch_unblocked_reg32b(a, p, st);
             return BSVD_ERR_UNSUPPORTED;
     }

@@ -54,6 +54,7 @@ enum {
     KV_CREG32_TMA = 45,         // KV_CREG32 with the bulk-copy (TMA) loader: 1-3 % slower, opt-in
                                 //   (profiles/r2_tma_loader.md)
     KV_UNBLOCKED_REG32G = 42,   // KV_UNBLOCKED_REG32B with scaled (fast) rotations: one FMA per updated element
+    KV_UNBLOCKED_REG32F = 52,   // KV_UNBLOCKED_REG32G, one problem per warp with V in lockstep (small batches)
 };
 
 template <class T>

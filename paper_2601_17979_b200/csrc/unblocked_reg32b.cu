@@ -302,7 +302,7 @@ __device__ __forceinline__ void all_partials(const double (&x0)[N], const double
 // update is fused with the partials of iteration t + 1 (offset u + 1 in the
 // pre-shift register naming: next pair k = columns of this iteration's pairs
 // k - 1 and k + 1), so they are ready when the next reduction starts.
-template <int u, int PD, bool FG = false, int SH = 0>
+template <int u, int PD, bool FG = false, int SH = 0, bool FV = false>
 __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab, int t,
                                        int lane, int half, int hl, bool done, double tol, double tol2,
                                        Par* logl, IterState& st) {
@@ -362,7 +362,9 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     }
     R32P(2, par.cm1);
     sm.pub[half][k] = par;
-    const unsigned mask = __ballot_sync(0xffffffffu, rot);
+    // FV (one problem per warp: W rows in half 0, V rows in half 1): only half 0's rotations are real;
+    // half 1 evaluates pairs of V's columns in lockstep and discards them
+    const unsigned mask = __ballot_sync(0xffffffffu, rot) & (FV ? 0xFFFFu : 0xFFFFFFFFu);
     if (logl) logl[t * H] = par;
     __syncwarp();
     R32P(6, sm.pub[half][0].c);
@@ -382,7 +384,7 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     const bool shrink = rot && (nt < 0.25 * gt || nb < 0.25 * gb);
     st.my_rot += rot ? 1 : 0;
     {  // a >4x shrink in a problem makes that problem's next iteration recompute its norms
-        const uint32_t sb = __ballot_sync(0xffffffffu, shrink);
+        const uint32_t sb = __ballot_sync(0xffffffffu, shrink) & (FV ? 0xFFFFu : 0xFFFFFFFFu);
         st.fmask = ((sb & 0xFFFFu) ? 0xFFFFu : 0u) | ((sb >> 16) ? 0xFFFF0000u : 0u);
         st.full = sb != 0u;
     }
@@ -390,14 +392,15 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
     constexpr int un = u + 1;  // offset of iteration t + 1 (pre-shift naming)
     if (SH != 0 || mask) {
         // rotations PD ahead (PD = 16: all first) -- the loop interleaves stores to red[]
+        const int ph = FV ? 0 : half;  // FV: V's rows (half 1) take W's rotations
         Par pq[PD];
 #pragma unroll
-        for (int q = 0; q < PD; ++q) pq[q] = sm.pub[half][q];
+        for (int q = 0; q < PD; ++q) pq[q] = sm.pub[ph][q];
         if constexpr (SH == 0) {
 #pragma unroll
             for (int q = 0; q < H; ++q) {
                 const Par cur = pq[q % PD];
-                if (q + PD < H) pq[q % PD] = sm.pub[half][q + PD];
+                if (q + PD < H) pq[q % PD] = sm.pub[ph][q + PD];
                 apply_any<FG>(x0[TS(q, u)], x0[BS(q, u)], cur.cm1, cur.c);
                 apply_any<FG>(x1[TS(q, u)], x1[BS(q, u)], cur.cm1, cur.c);
                 if (q >= 1) cross_partial<un>(x0, x1, sm.red, lane, q - 1);  // needs pairs q-2, q
@@ -414,7 +417,7 @@ __device__ __forceinline__ void w_iter(double (&x0)[N], double (&x1)[N], WarpSme
 #pragma unroll
             for (int q = 0; q < H; ++q) {
                 const Par cur = pq[q % PD];
-                if (q + PD < H) pq[q % PD] = sm.pub[half][q + PD];
+                if (q + PD < H) pq[q % PD] = sm.pub[ph][q + PD];
                 apply_to<FG>(x0[TS(q, u)], x0[BS(q, u)], y0[dst_slot(TS(q, u), SH)], y0[dst_slot(BS(q, u), SH)],
                              cur.cm1, cur.c);
                 apply_to<FG>(x1[TS(q, u)], x1[BS(q, u)], y1[dst_slot(TS(q, u), SH)], y1[dst_slot(BS(q, u), SH)],
@@ -483,7 +486,7 @@ __device__ __forceinline__ void v_iter(double (&x0)[N], double (&x1)[N], WarpSme
     __syncwarp();
 }
 
-template <int U, int PD, bool FG = false>
+template <int U, int PD, bool FG = false, bool FV = false>
 __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSmem& sm, const uint32_t* ctab,
                                         int lane, int half, int hl, bool done, double tol, double tol2, Par* logl,
                                         IterState& st) {
@@ -494,14 +497,14 @@ __device__ __forceinline__ void w_sweep(double (&x0)[N], double (&x1)[N], WarpSm
 #pragma unroll 1
     for (int gi = 0; gi < NG; ++gi) {
         const int t0 = gi * U;
-        w_iter<0, PD, FG>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
+        w_iter<0, PD, FG, 0, FV>(x0, x1, sm, ctab, t0, lane, half, hl, done, tol, tol2, logl, st);
         if (gi == NG - 1) {  // once per sweep: the shift by one that closes the ring
             ring_shift<1>(x0);
             ring_shift<1>(x1);
             break;
         }
         // the second iteration of the group writes its results straight into the shifted registers
-        w_iter<1, PD, FG, 2>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
+        w_iter<1, PD, FG, 2, FV>(x0, x1, sm, ctab, t0 + 1, lane, half, hl, done, tol, tol2, logl, st);
     }
 }
 
@@ -524,13 +527,19 @@ __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSm
     }
 }
 
-template <int NW, int MINB, int U, int UV, int PD, bool FG = false>
+// FV (fused V, kernel id 52): one problem per warp for batches that leave SM sub-partitions idle.  Half 0
+// holds W's rows (hl, hl + 16) and half 1 the same rows of V, which take W's rotations in lockstep (the
+// same parameters, the same FMAs as the replay, so the same bits): no rotation log, no replay phase, no
+// parking of W and V in global memory.  Half 1 evaluates pairs of V's columns and discards them.
+template <int NW, int MINB, int U, int UV, int PD, bool FG = false, bool FV = false>
 __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
+    static_assert(!FV || FG, "the fused-V mode is built on the scaled rotations");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
     const int half = lane >> 4, hl = lane & 15;
-    const int prob = (blockIdx.x * NW + warp) * 2 + half;
+    const int ph = FV ? 0 : half;  // the half whose problem this lane's results belong to
+    const int prob = FV ? blockIdx.x * NW + warp : (blockIdx.x * NW + warp) * 2 + half;
     const bool live = prob < a.batch;
     const int r0 = hl, r1 = hl + 16;
     const size_t pstride = (size_t)a.work_stride;
@@ -540,7 +549,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     const bool want_v = a.need_v != 0;
     // this lane's column of the rotation log; a dead half never writes (it
     // aliases problem 0's workspace) but may read
-    Par* logl = want_v ? logp + hl : nullptr;
+    Par* logl = want_v && !FV ? logp + hl : nullptr;
     Par* logw = live ? logl : nullptr;
     uint32_t* ctab = reinterpret_cast<uint32_t*>(smem_raw + NW * sizeof(WarpSmem));
     for (int e = threadIdx.x; e < NIT * H; e += NW * 32) ctab[e] = pair_code(e / H, e % H);
@@ -556,10 +565,18 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     double amax = 0.0;
     {
         const double* Ap = a.A + (size_t)(live ? prob : 0) * a.strideA;  // plan requires lda == 32
+        const bool ld = live && !(FV && half);
 #pragma unroll
         for (int c = 0; c < N; ++c) {
-            x0[c] = live ? __ldcs(Ap + r0 + c * N) : 0.0;  // read once: evict-first, keep L2 for the workspace
-            x1[c] = live ? __ldcs(Ap + r1 + c * N) : 0.0;
+            x0[c] = ld ? __ldcs(Ap + r0 + c * N) : 0.0;  // read once: evict-first, keep L2 for the workspace
+            x1[c] = ld ? __ldcs(Ap + r1 + c * N) : 0.0;
+        }
+        if (FV && half) {  // V = I
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                x0[c] = (c == r0) ? 1.0 : 0.0;
+                x1[c] = (c == r1) ? 1.0 : 0.0;
+            }
         }
 #pragma unroll
         for (int c = 0; c < N; ++c) {
@@ -569,9 +586,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    const int ex = prescale_exponent(amax);
+    const int ex = FV ? __shfl_sync(0xffffffffu, prescale_exponent(amax), 0) : prescale_exponent(amax);
     {
-        const double scale = pow2(-ex);
+        const double scale = (FV && half) ? 1.0 : pow2(-ex);
 #pragma unroll
         for (int c = 0; c < N; ++c) {
             x0[c] *= scale;
@@ -590,7 +607,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         st.itbits = 0;
         st.full = true;  // fresh norms at the start of every sweep
         st.fmask = 0xffffffffu;
-        w_sweep<U, PD, FG>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, logw, st);
+        w_sweep<U, PD, FG, FV>(x0, x1, sm, ctab, lane, half, hl, done != 0, tol, tol2, logw, st);
         if constexpr (FG) {
             // back to true columns at the sweep end (the ring is back in place: slot c = column c), so
             // every sweep starts from unit scales and the finalisation sees W and V themselves
@@ -605,20 +622,35 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
                 sm.rds[half][hl] = sm.rds[half][SB + hl] = 1.0;
             }
             __syncwarp();
-            if (st.itbits) {
+            if (st.itbits) {  // (FV: V's rows take the same scales, as after the replay)
 #pragma unroll
                 for (int c = 0; c < N; ++c) {
-                    const double dc = sm.dv[half][c];
+                    const double dc = sm.dv[ph][c];
                     x0[c] *= dc;
                     x1[c] *= dc;
                 }
             }
             __syncwarp();
+            if (FV && want_v && st.itbits) {  // column norms of V (half 1's rows), as after the replay
+#pragma unroll
+                for (int c = 0; c < N; ++c)
+                    sm.red[c * RSTR + lane] = __dadd_rn(__dmul_rn(x0[c], x0[c]), __dmul_rn(x1[c], x1[c]));
+                __syncwarp();
+                const double na = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl) * RSTR + 16));
+                const double nb = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl + 1) * RSTR + 16));
+                __syncwarp();
+                if (half) {
+                    sm.vn[0][2 * hl] = na;
+                    sm.vn[0][2 * hl + 1] = nb;
+                }
+                __syncwarp();
+            }
         }
         // ---- sweep end: per-problem rotation count over the half warp ----
         int tot = st.my_rot;
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if constexpr (FV) tot = __shfl_sync(0xffffffffu, tot, 0);  // half 1's count is not a problem's
         if (!done) {
             sweeps = sw + 1;
             last = tot;
@@ -628,7 +660,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         const int partner_done = __shfl_xor_sync(0xffffffffu, done, 16);
         const bool both_done = done && partner_done;
         // ======================= V phase: replay the sweep =======================
-        if (want_v && st.itbits) {
+        if (!FV && want_v && st.itbits) {
             if (live) {
 #pragma unroll
                 for (int c = 0; c < N; ++c) {  // park W
@@ -700,13 +732,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         __syncwarp();
         // lane hl: columns 2 hl, 2 hl + 1.  Sigma of the scaled W (ssa); the power-of-two scale is
         // exact, so sa = ssa * 2^ex and x / ssa are the unscaled sigma and quotient.
-        const double wna = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl) * RSTR + 16 * half));
-        const double wnb = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl + 1) * RSTR + 16 * half));
+        const double wna = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl) * RSTR + 16 * ph));
+        const double wnb = __dsqrt_rn(sum16_butterfly(sm.red + (2 * hl + 1) * RSTR + 16 * ph));
         // FG: sigma = ||w|| / ||v|| (the column-scale roundings W and V share cancel); U = W / ||w||
         double ssa = wna, ssb = wnb;
         bool vok = true;
         if constexpr (FG) {
-            const double va = sm.vn[half][2 * hl], vb = sm.vn[half][2 * hl + 1];
+            const double va = sm.vn[ph][2 * hl], vb = sm.vn[ph][2 * hl + 1];
             ssa = div_by_sigma(wna, va, rcp_refined(va));
             ssb = div_by_sigma(wnb, vb, rcp_refined(vb));
             vok = va >= 0.5 && va <= 2.0 && vb >= 0.5 && vb <= 2.0;
@@ -719,51 +751,58 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         const bool tiny = !(sa >= dtiny<double>() && sb >= dtiny<double>() && wna >= 0x1p-480 && wnb >= 0x1p-480 &&
                             wna <= 0x1p+960 && wnb <= 0x1p+960 && vok);
         const unsigned tm = __ballot_sync(0xffffffffu, tiny);
-        fused = ((tm >> (16 * half)) & 0xFFFFu) == 0u;
+        fused = ((tm >> (16 * ph)) & 0xFFFFu) == 0u;
         __syncwarp();
         // [half][32] (scaled sigma, reciprocal) and rank by column, in rows 32.. of red
-        double2* sr = reinterpret_cast<double2*>(sm.red + 32 * RSTR) + 32 * half;
-        int* rk = reinterpret_cast<int*>(sm.red + 32 * RSTR + 128) + 32 * half;
-        sr[2 * hl] = make_double2(wna, rcp_refined(wna));
-        sr[2 * hl + 1] = make_double2(wnb, rcp_refined(wnb));
-        if constexpr (FG) {
-            sm.sgs[half][2 * hl] = ssa;
-            sm.sgs[half][2 * hl + 1] = ssb;
+        double2* sr = reinterpret_cast<double2*>(sm.red + 32 * RSTR) + 32 * ph;
+        int* rk = reinterpret_cast<int*>(sm.red + 32 * RSTR + 128) + 32 * ph;
+        const bool own = !(FV && half);  // FV: half 0 alone fills the shared tables, half 1 (V) reads them
+        if (own) {
+            sr[2 * hl] = make_double2(wna, rcp_refined(wna));
+            sr[2 * hl + 1] = make_double2(wnb, rcp_refined(wnb));
+            if constexpr (FG) {
+                sm.sgs[half][2 * hl] = ssa;
+                sm.sgs[half][2 * hl + 1] = ssb;
+            }
         }
         __syncwarp();
         int ra = 0, rb = 0;  // stable descending ranks (finalize.cuh step 4)
+        if (own) {
 #pragma unroll 8
-        for (int c2 = 0; c2 < N; ++c2) {
-            const double s2 = FG ? sm.sgs[half][c2] : sr[c2].x;
-            ra += sig_before(s2, ssa) || (c2 < 2 * hl && sig_tie(s2, ssa));
-            rb += sig_before(s2, ssb) || (c2 < 2 * hl + 1 && sig_tie(s2, ssb));
+            for (int c2 = 0; c2 < N; ++c2) {
+                const double s2 = FG ? sm.sgs[half][c2] : sr[c2].x;
+                ra += sig_before(s2, ssa) || (c2 < 2 * hl && sig_tie(s2, ssa));
+                rb += sig_before(s2, ssb) || (c2 < 2 * hl + 1 && sig_tie(s2, ssb));
+            }
+            rk[2 * hl] = ra;
+            rk[2 * hl + 1] = rb;
         }
-        rk[2 * hl] = ra;
-        rk[2 * hl + 1] = rb;
         __syncwarp();
         if (live && fused) {
             const FinalOut<double> o = final_out(a, prob);
-            o.S[ra] = sa;
-            o.S[rb] = sb;
-            double* u0 = o.U + r0;
-            double* u1 = o.U + r1;
+            if (own) {
+                o.S[ra] = sa;
+                o.S[rb] = sb;
+                double* u0 = o.U + r0;
+                double* u1 = o.U + r1;
 #pragma unroll
-            for (int c = 0; c < N; ++c) {  // U = W / sigma: reciprocal, then one residual correction
-                const int rc = rk[c];
-                const double2 t = sr[c];
-                __stcs(u0 + (size_t)rc * o.ldu, div_by_sigma(x0[c], t.x, t.y));  // streaming: not re-read
-                __stcs(u1 + (size_t)rc * o.ldu, div_by_sigma(x1[c], t.x, t.y));
+                for (int c = 0; c < N; ++c) {  // U = W / sigma: reciprocal, then one residual correction
+                    const int rc = rk[c];
+                    const double2 t = sr[c];
+                    __stcs(u0 + (size_t)rc * o.ldu, div_by_sigma(x0[c], t.x, t.y));  // streaming: not re-read
+                    __stcs(u1 + (size_t)rc * o.ldu, div_by_sigma(x1[c], t.x, t.y));
+                }
             }
-            if (o.want_v && o.V) {
+            if (o.want_v && o.V && (!FV || half)) {
                 // all 64 loads ahead of the stores (the compiler cannot prove o.V and wsV disjoint,
-                // so interleaving would serialise one L2 round trip per element)
-                if (v_started) {
+                // so interleaving would serialise one L2 round trip per element); FV: V is in registers
+                if (!FV && v_started) {
 #pragma unroll
                     for (int c = 0; c < N; ++c) {
                         x0[c] = wsV[r0 + c * N];
                         x1[c] = wsV[r1 + c * N];
                     }
-                } else {
+                } else if (!FV) {
 #pragma unroll
                     for (int c = 0; c < N; ++c) {
                         x0[c] = (c == r0) ? 1.0 : 0.0;
@@ -775,7 +814,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
                     const int rc = rk[c];
                     double y0 = x0[c], y1 = x1[c];
                     if constexpr (FG) {
-                        const double vv = sm.vn[half][c], rv = rcp_refined(vv);
+                        const double vv = sm.vn[ph][c], rv = rcp_refined(vv);
                         y0 = div_by_sigma(y0, vv, rv);
                         y1 = div_by_sigma(y1, vv, rv);
                     }
@@ -784,11 +823,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
                 }
             }
         }
-        if (live && hl == 0) *flagp = fused ? 0.0 : 1.0;
+        if (live && (FV ? lane : hl) == 0) *flagp = fused ? 0.0 : 1.0;
     }
     if (live && !fused) {
         const double unscale = pow2(ex);
-        if constexpr (FG) {  // W / ||v||, V / ||v|| by column for the standalone pass
+        if constexpr (FV) {  // W / ||v|| (half 0), V / ||v|| (half 1) by column for the standalone pass
+            double* dst = half ? wsV : wsW;
+            const double us = half ? 1.0 : unscale;
+            if (!half || want_v) {
+#pragma unroll
+                for (int c = 0; c < N; ++c) {
+                    const double vv = sm.vn[0][c], rv = rcp_refined(vv);
+                    dst[r0 + c * N] = div_by_sigma(x0[c], vv, rv) * us;
+                    dst[r1 + c * N] = div_by_sigma(x1[c], vv, rv) * us;
+                }
+            }
+        } else if constexpr (FG) {  // W / ||v||, V / ||v|| by column for the standalone pass
 #pragma unroll
             for (int c = 0; c < N; ++c) {
                 const double vv = sm.vn[half][c], rv = rcp_refined(vv);
@@ -815,7 +865,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
                 wsW[r1 + c * N] = x1[c] * unscale;
             }
         }
-        if (want_v && !v_started) {
+        if (!FV && want_v && !v_started) {
 #pragma unroll
             for (int c = 0; c < N; ++c) {
                 wsV[r0 + c * N] = (c == r0) ? 1.0 : 0.0;
@@ -823,10 +873,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
             }
         }
     }
-    if (live && fused) {
+    if (!FV && live && fused) {
         // the problem is finished and its workspace (W / V parking, rotation log) is dead: drop its L2
         // lines instead of letting them be written back to DRAM (they were ~60 % of the kernel's DRAM
         // traffic); the line holding the finalisation flag, which the standalone pass reads, is kept
+        // (FV never touches its workspace before the flag)
         __syncwarp();
         const uintptr_t lo = ((uintptr_t)wsW + 127) & ~(uintptr_t)127;
         const uintptr_t hi = (uintptr_t)flagp & ~(uintptr_t)127;
@@ -834,7 +885,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
             asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");
     }
     const unsigned badm = __ballot_sync(0xffffffffu, bad != 0);
-    if (live && hl == 0 && a.info) {
+    if (live && (FV ? lane : hl) == 0 && a.info) {
         bsvd_info inf;
         inf.converged = done;
         inf.outer_sweeps = sweeps;
@@ -843,7 +894,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
         inf.update_calls = 0;
         inf.last_rotations = last;
         inf.path = 1;
-        inf.status = ((badm >> (16 * half)) & 0xFFFFu) ? 1 : 0;
+        inf.status = ((badm >> (16 * ph)) & 0xFFFFu) ? 1 : 0;
         inf.kernel = a.kernel;
         a.info[prob] = inf;
     }
@@ -851,7 +902,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
 
 }  // namespace r32b
 
-bool is_reg32b(int kv) { return kv == KV_UNBLOCKED_REG32B || kv == KV_UNBLOCKED_REG32G; }
+bool is_reg32b(int kv) { return kv == KV_UNBLOCKED_REG32B || kv == KV_UNBLOCKED_REG32G || kv == KV_UNBLOCKED_REG32F; }
 
 Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant, int max_sweeps) {
     Plan p{};
@@ -868,12 +919,12 @@ Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, i
     return p;
 }
 
-template <int NW, int MINB, int U, int UV, int PD, bool FG>
+template <int NW, int MINB, int U, int UV, int PD, bool FG, bool FV = false>
 static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
-    const int per_cta = 2 * NW;
+    const int per_cta = FV ? NW : 2 * NW;
     const int grid = (a.batch + per_cta - 1) / per_cta;
     const size_t smem = NW * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
-    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD, FG>;
+    auto k = r32b::k_reg32b<NW, MINB, U, UV, PD, FG, FV>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<grid, NW * 32, smem, st>>>(a);
@@ -886,8 +937,9 @@ static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
 int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
     a.kernel = p.kernel;
     a.work_stride = (int64_t)p.work_elems;
-    const int rc = p.kernel == KV_UNBLOCKED_REG32G ? launch_r32b<4, 2, 2, 2, 8, true>(a, st)    // scaled rotations
-                                                   : launch_r32b<4, 2, 2, 2, 16, false>(a, st);
+    const int rc = p.kernel == KV_UNBLOCKED_REG32G   ? launch_r32b<4, 2, 2, 2, 8, true>(a, st)  // scaled rotations
+                   : p.kernel == KV_UNBLOCKED_REG32F ? launch_r32b<4, 2, 2, 2, 8, true, true>(a, st)  // + V in lockstep
+                                                     : launch_r32b<4, 2, 2, 2, 16, false>(a, st);
     if (rc) return rc;
     return launch_finalize_flagged<double>(a, st);  // only problems the fused finalisation left over
 }

@@ -288,11 +288,13 @@ def test_c1_kernel_variants_agree(kernel):
         check_factors(A[b], U[b], S[b], V[b])
 
 
+@pytest.mark.parametrize("forced", [0, 42, 52])
 @pytest.mark.parametrize("want_v", [True, False])
-def test_c1_fused_finalize_with_holes(want_v):
+def test_c1_fused_finalize_with_holes(want_v, forced):
     """The default 32x32 kernels finalise in-kernel; problems with sigma < tiny/u columns (orthogonal
     completion, src/svd.py:224-240) are flagged to the standalone pass.  Mixed batch: both paths agree
-    with the oracle (values only: the unscaled kernel 12; with V: scaled rotations, kernel 42)."""
+    with the oracle (values only: the unscaled kernel 12; with V: scaled rotations, kernel 52 on a
+    batch this small, 42 forced)."""
     import torch
 
     from paper_2601_17979_b200.solver import INFO_DTYPE
@@ -306,10 +308,10 @@ def test_c1_fused_finalize_with_holes(want_v):
     A[25][:, ::2] = 0.0                   # half the columns zero
     a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
     opts = bs.JacobiOptions(compute_right_vectors=want_v)
-    r = bs.solve_tensor(a, 32, 32, opts)
+    r = bs.solve_tensor(a, 32, 32, opts, kernel=forced)
     torch.cuda.synchronize()
     info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
-    assert (info["kernel"] == (42 if want_v else 12)).all()
+    assert (info["kernel"] == (forced or (52 if want_v else 12))).all()
     U, S = np.swapaxes(r.u.cpu().numpy(), 1, 2), r.s.cpu().numpy()
     V = np.swapaxes(r.v.cpu().numpy(), 1, 2) if want_v else None
     for b in [0, 1, 6, 11, 12, 25, 39]:
@@ -519,9 +521,10 @@ def test_eig_sweeps_operator_full_solve(dt):
     assert np.max(np.abs(m.conj().T @ m - np.eye(n))) <= 60 * n * u
 
 
-# (FP32 blocked shapes the FP64 register kernel takes are solved on it in float64: kernel 30; complex
+# (32x32 FP64 with V on a batch this small: kernel 52; FP32 blocked shapes the FP64 register kernel takes
+# are solved on it in float64: kernel 30; complex
 # blocked n % 16 == 0: the complex register blocked kernel 51, complex64 promoted to it)
-_DEFAULT_KERNEL_SHAPES = [(np.float64, 32, 32, 42), (np.float32, 16, 16, 24), (np.float64, 64, 64, 30),
+_DEFAULT_KERNEL_SHAPES = [(np.float64, 32, 32, 52), (np.float32, 16, 16, 24), (np.float64, 64, 64, 30),
                           (np.complex128, 256, 32, 32), (np.complex128, 40, 24, 1), (np.float32, 48, 48, 30),
                           (np.complex64, 48, 48, 51), (np.complex128, 64, 64, 51), (np.float32, 40, 40, 2),
                           (np.complex128, 40, 40, 2)]
@@ -793,8 +796,9 @@ def test_c2_batch_size_kernel_choice_is_bitwise_invisible():
 
 @pytest.mark.gpu
 def test_c1_one_kernel_at_every_batch_size():
-    """The 32x32 FP64 default (scaled rotations, 42) runs at every batch size, so batch == standalone
-    holds bitwise (tests/test_batch.py:19-28) between a 1,300-problem batch (more than one wave) and a
+    """The 32x32 FP64 default (scaled rotations) runs as 42 (two problems per warp) on batches above one
+    resident wave and as 52 (one problem per warp, V in lockstep) below it; the two give the same bits,
+    so batch == standalone holds bitwise (tests/test_batch.py:19-28) between a 1,300-problem batch and a
     9-problem one, holes, fresh-norm iterations and extreme scales included."""
     import torch
 
@@ -816,9 +820,48 @@ def test_c1_one_kernel_at_every_batch_size():
     torch.cuda.synchronize()
     kb = np.frombuffer(big.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"]
     ks = np.frombuffer(small.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"]
-    assert (kb == 42).all() and (ks == 42).all()
+    assert (kb == 42).all() and (ks == 52).all()
     p = torch.tensor(pick).cuda()
     assert torch.equal(big.s[p], small.s) and torch.equal(big.u[p], small.u) and torch.equal(big.v[p], small.v)
     for b in (7, 11, 13, 15):  # and the extreme ones are right (underflow-safe norms, like the reference's)
         st = np.linalg.svd(A[b], compute_uv=False)
         assert np.max(np.abs(big.s[b].cpu().numpy() - st)) <= 32 * 2.0 ** -53 * st[0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("want_v", [True, False])
+def test_c1_fused_v_kernel_matches_two_problem_kernel(want_v):
+    """Kernel 52 (one problem per warp, V's rows take W's rotations in lockstep) against 42 forced on
+    the same small batch: identical sigma / U / V and sweep / rotation counts, holes and non-finite
+    problems included; a values-only request may force 52 as well."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    B = 301
+    rng = np.random.default_rng(91)
+    A = rng.standard_normal((B, 32, 32))
+    A[3] = np.diag(np.geomspace(1.0, 1e-14, 32)) @ A[3]
+    A[4][:, 30] = 0.0
+    A[6][:, 1:3] = 0.0
+    A[8] *= 1e-250
+    A[10][5, 5] = np.nan
+    A[12] = np.eye(32)
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    opts = bs.JacobiOptions(compute_right_vectors=want_v)
+    r52 = bs.solve_tensor(a, 32, 32, opts, kernel=52)
+    r42 = bs.solve_tensor(a, 32, 32, opts, kernel=42)
+    torch.cuda.synchronize()
+    i52 = np.frombuffer(r52.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    i42 = np.frombuffer(r42.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (i52["kernel"] == 52).all() and (i42["kernel"] == 42).all()
+    for f in ("outer_sweeps", "rotations", "last_rotations", "converged", "status"):
+        assert (i52[f] == i42[f]).all(), f
+    ok = torch.tensor([b for b in range(B) if b != 10]).cuda()
+    assert torch.equal(r52.s[ok], r42.s[ok]) and torch.equal(r52.u[ok], r42.u[ok])
+    if not want_v:  # (values only, the scaled rotations keep their scale roundings: 12 is the default there)
+        return
+    assert torch.equal(r52.v[ok], r42.v[ok])
+    for b in (0, 3, 4, 6, 8):
+        st = np.linalg.svd(A[b], compute_uv=False)
+        assert np.max(np.abs(r52.s[b].cpu().numpy() - st)) <= 32 * 2.0 ** -53 * st[0]

@@ -124,6 +124,13 @@ def test_kernel_selection_routes():
     assert L.bsvd_select_kernel(2, 256, 24, ctypes.byref(o)) == 1     # c64, other n: general unblocked kernel
     assert L.bsvd_select_kernel(0, 64, 64, ctypes.byref(o)) == 30     # FP32 blocked: on the FP64 register kernel
     assert L.bsvd_select_kernel(0, 32, 32, ctypes.byref(o)) == 42     # FP32 32x32: on the FP64 register kernel
+    # by batch size (148 SMs assumed without a device): one problem per warp below 7 problems per SM
+    assert L.bsvd_select_kernel_batched(1, 32, 32, 1000, ctypes.byref(o)) == 52
+    assert L.bsvd_select_kernel_batched(0, 32, 32, 1000, ctypes.byref(o)) == 52
+    assert L.bsvd_select_kernel_batched(1, 32, 32, 10000, ctypes.byref(o)) == 42
+    o.want_v = 0
+    assert L.bsvd_select_kernel_batched(1, 32, 32, 1000, ctypes.byref(o)) == 12
+    o.want_v = 1
     o.route = _lib.FORCE_BLOCKED
     assert L.bsvd_select_kernel(3, 256, 32, ctypes.byref(o)) == 32    # blocked route, ell = 2: same kernel
     o.nb = 8

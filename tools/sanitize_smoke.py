@@ -24,7 +24,8 @@ def run(dt, m, n, route=0, kernel=0, B=3, **kw):
     print(dt.__name__, m, n, route, kernel, "ok", float(r.s[0, 0]), flush=True)
 
 
-run(np.float64, 32, 32)                       # r32b scaled rotations (42) + fused finalise
+run(np.float64, 32, 32)                       # r32b scaled rotations, V in lockstep (52) + fused finalise
+run(np.float64, 32, 32, kernel=42, B=5)       # r32b scaled rotations, two problems per warp (42)
 run(np.float64, 32, 32, compute_right_vectors=False)  # r32b values only (12)
 run(np.float32, 16, 16)                       # reg16b
 run(np.float32, 16, 16, kernel=34, B=9)       # reg16c (quarter-warp)
