@@ -200,3 +200,15 @@ def test_pack_host_helper_packs_column_major_batches():
         out[...] = 0
         assert L.bsvd_pack_host(ptrs.ctypes.data, len(mats), 15 * 8, out.ctypes.data, nt) == 0
         assert np.array_equal(out, np.stack([a.T for a in mats]))
+
+
+def test_default_chunk_policy():
+    from paper_2601_17979_b200.solver import default_chunk
+
+    per32 = 3 * 32 * 32 * 8
+    assert default_chunk(1000, per32, 32 * 32, 4, 148) == 250      # latency-bound: one chunk per stream
+    assert default_chunk(1250, per32, 32 * 32, 4, 148) == 313
+    assert default_chunk(10000, per32, 32 * 32, 4, 148) == 625     # ~4 MB chunks, at most 16
+    assert default_chunk(10000, 3 * 16 * 16 * 4, 16 * 16, 4, 148) == 1366
+    assert default_chunk(2000, 3 * 128 * 128 * 8, 128 * 128, 4, 148) == 125  # large problems: 16 chunks
+    assert default_chunk(3, per32, 32 * 32, 4, 148) == 1

@@ -1,4 +1,4 @@
-"""Host-buffer pipeline sweep (streams x chunk) for C1-10k through bsvd_gesvj_batched_host, plus raw PCIe
+"""Host-buffer pipeline sweep (streams x chunk; argv: streams, divisors, batch) for C1-10k through bsvd_gesvj_batched_host, plus raw PCIe
 copies (development aid).  Measured on B200: 4 streams x B/16 best (4.02 ms vs 4.26 ms at 3 x B/8);
 raw D2H of the 167 MB of factors alone takes 2.93 ms, H2D of the 82 MB input 1.49 ms."""
 import os
@@ -13,7 +13,7 @@ from paper_2601_17979_b200.matgen import gen_batch_device
 from paper_2601_17979_b200.solver import solve_host_buffers
 
 m = n = 32
-B = 10000
+B = int(sys.argv[3]) if len(sys.argv) > 3 else 10000
 a = gen_batch_device("arith", m, n, B, np.float64, kappa=1e10, seed=0)
 a_h = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
 a_h.copy_(a)
@@ -40,6 +40,8 @@ for nst in NST:
                 ts.append(e0.elapsed_time(e1))
         t = min(ts)
         print(f"streams={nst} chunk=B/{div}: {t:.2f} ms  {B / t * 1e3 / 1e6:.2f} M mat/s", flush=True)
+if B != 10000:
+    sys.exit(0)
 x = torch.empty(167_000_000 // 8, dtype=torch.float64, device=dev)
 xh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
 for _ in range(2):
