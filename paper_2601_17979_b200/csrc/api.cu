@@ -26,7 +26,7 @@ struct NvtxRange {
 namespace {
 
 constexpr size_t kSmemFallback = 232448;  // 227 KB opt-in limit of sm_100
-constexpr int FV_WARPS_PER_SM = 7;  // kernel 52 up to 7 problems per SM (C1: 1,000 0.29 vs 0.31 ms; 1,250 0.44 vs 0.41)
+constexpr int FV_WARPS_PER_SM = 8;  // kernel 52 while it fits one resident wave (C1: 1,184 0.29 vs 0.32 ms; 1,250 0.45 vs 0.41)
 
 size_t smem_limit() {
     int dev = 0;

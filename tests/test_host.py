@@ -124,7 +124,7 @@ def test_kernel_selection_routes():
     assert L.bsvd_select_kernel(2, 256, 24, ctypes.byref(o)) == 1     # c64, other n: general unblocked kernel
     assert L.bsvd_select_kernel(0, 64, 64, ctypes.byref(o)) == 30     # FP32 blocked: on the FP64 register kernel
     assert L.bsvd_select_kernel(0, 32, 32, ctypes.byref(o)) == 42     # FP32 32x32: on the FP64 register kernel
-    # by batch size (148 SMs assumed without a device): one problem per warp below 7 problems per SM
+    # by batch size (148 SMs assumed without a device): one problem per warp up to one resident wave (8 per SM)
     assert L.bsvd_select_kernel_batched(1, 32, 32, 1000, ctypes.byref(o)) == 52
     assert L.bsvd_select_kernel_batched(0, 32, 32, 1000, ctypes.byref(o)) == 52
     assert L.bsvd_select_kernel_batched(1, 32, 32, 10000, ctypes.byref(o)) == 42

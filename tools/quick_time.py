@@ -14,6 +14,8 @@ cfgs = [("C1-10k", "arith", 32, 32, 10000, np.float64, 1e10, True),
         ("C1-2k", "arith", 32, 32, 2000, np.float64, 1e10, True),
         ("C1-2.5k", "arith", 32, 32, 2500, np.float64, 1e10, True),
         ("C1-500", "arith", 32, 32, 500, np.float64, 1e10, True),
+        ("C1-1100", "arith", 32, 32, 1100, np.float64, 1e10, True),
+        ("C1-1184", "arith", 32, 32, 1184, np.float64, 1e10, True),
         ("C2-full", "random", 16, 16, 10000, np.float32, 1, True),
         ("C2-vals", "random", 16, 16, 10000, np.float32, 1, False),
         ("C4", "random", 256, 32, 5000, np.complex128, 1, True),
