@@ -51,6 +51,11 @@ __host__ __device__ constexpr int ring_slot(int q) {
     return q == 0 ? 1 : (q <= H - 1 ? 2 * q : 2 * (2 * H - 1 - q) + 1);
 }
 __host__ __device__ constexpr int md(int a) { return ((a % NIT) + NIT) % NIT; }
+__host__ __device__ constexpr int ring_pos(int s) {  // inverse of ring_slot (s >= 1)
+    return s == 1 ? 0 : ((s & 1) == 0 ? s / 2 : 2 * H - 1 - (s - 1) / 2);
+}
+// slot that register slot s moves to under a ring shift by SH (the fixed column, slot 0, stays)
+__host__ __device__ constexpr int dst_slot(int s, int SH) { return s == 0 ? 0 : ring_slot(md(ring_pos(s) + SH)); }
 __host__ __device__ constexpr int TS(int k, int u) { return k == 0 ? 0 : ring_slot(md(k - u)); }
 __host__ __device__ constexpr int BS(int k, int u) { return ring_slot(md((k == 0 ? 0 : NIT - k) - u)); }
 
@@ -126,6 +131,14 @@ __device__ __forceinline__ void capply(double& tr, double& ti, double& br, doubl
     br = nbr;
     bi = nbi;
 }
+// the same update written to other registers (the ring shift folded into it, see iter)
+__device__ __forceinline__ void capply_to(double tr, double ti, double br, double bi, double& ntr, double& nti,
+                                          double& nbr, double& nbi, const Par& p) {
+    ntr = fma(p.cm1, tr, fma(p.ar, br, fma(-p.ai, bi, tr)));
+    nti = fma(p.cm1, ti, fma(p.ar, bi, fma(p.ai, br, ti)));
+    nbr = fma(p.cm1, br, fma(-p.ar, tr, fma(-p.ai, ti, br)));
+    nbi = fma(p.cm1, bi, fma(-p.ar, ti, fma(p.ai, tr, bi)));
+}
 
 // Half-angle rotation for (|d|, p = g_tb): kk = (1/r)(1/c) with r = sqrt(d^2 + 4|p|^2),
 // so that A = +-kk p, cm1 = -|s|^2 / (1 + c), dn = t |g| = |p|^2 kk / c.
@@ -176,7 +189,10 @@ struct IState {
     int par;     // cross-warp buffer parity
 };
 
-template <int u, int NW, bool SP>
+// SH != 0: the last iteration of an unrolled group with the ring shift by SH folded into the W update
+// (results go straight to their post-shift registers; branch-free: pairs that do not rotate have zero
+// parameters and copy exactly), so the loop back-edge moves no registers
+template <int u, int NW, bool SP, int SH = 0>
 __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx& c, int t, IState& st) {
     WarpSmem& sm = *c.sm;
     // ---- partial products of this lane's row: p_q = conj(x_b) x_t (V / padding lanes keep 0) ----
@@ -264,21 +280,48 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
     const unsigned mask = __ballot_sync(0xffffffffu, rot);
     st.full = __ballot_sync(0xffffffffu, shrink) != 0u;
     __syncwarp();
-    if (!mask) return;
+    if (SH == 0 && !mask) return;
     // ---- W update in registers (two pairs' parameters per three 16-byte loads) ----
+    if constexpr (SH == 0) {
 #pragma unroll
-    for (int q = 0; q < H; q += 2) {
-        const double2* pp = reinterpret_cast<const double2*>(sm.pub + 3 * q);
-        const double2 a = pp[0], b = pp[1], d = pp[2];
-        Par p0, p1;
-        p0.cm1 = a.x;
-        p0.ar = a.y;
-        p0.ai = b.x;
-        p1.cm1 = b.y;
-        p1.ar = d.x;
-        p1.ai = d.y;
-        capply(xr[TS(q, u)], xi[TS(q, u)], xr[BS(q, u)], xi[BS(q, u)], p0);
-        capply(xr[TS(q + 1, u)], xi[TS(q + 1, u)], xr[BS(q + 1, u)], xi[BS(q + 1, u)], p1);
+        for (int q = 0; q < H; q += 2) {
+            const double2* pp = reinterpret_cast<const double2*>(sm.pub + 3 * q);
+            const double2 a = pp[0], b = pp[1], d = pp[2];
+            Par p0, p1;
+            p0.cm1 = a.x;
+            p0.ar = a.y;
+            p0.ai = b.x;
+            p1.cm1 = b.y;
+            p1.ar = d.x;
+            p1.ai = d.y;
+            capply(xr[TS(q, u)], xi[TS(q, u)], xr[BS(q, u)], xi[BS(q, u)], p0);
+            capply(xr[TS(q + 1, u)], xi[TS(q + 1, u)], xr[BS(q + 1, u)], xi[BS(q + 1, u)], p1);
+        }
+    } else {
+        double yr[N], yi[N];
+#pragma unroll
+        for (int q = 0; q < H; q += 2) {
+            const double2* pp = reinterpret_cast<const double2*>(sm.pub + 3 * q);
+            const double2 a = pp[0], b = pp[1], d = pp[2];
+            Par p0, p1;
+            p0.cm1 = a.x;
+            p0.ar = a.y;
+            p0.ai = b.x;
+            p1.cm1 = b.y;
+            p1.ar = d.x;
+            p1.ai = d.y;
+            capply_to(xr[TS(q, u)], xi[TS(q, u)], xr[BS(q, u)], xi[BS(q, u)], yr[dst_slot(TS(q, u), SH)],
+                      yi[dst_slot(TS(q, u), SH)], yr[dst_slot(BS(q, u), SH)], yi[dst_slot(BS(q, u), SH)], p0);
+            capply_to(xr[TS(q + 1, u)], xi[TS(q + 1, u)], xr[BS(q + 1, u)], xi[BS(q + 1, u)],
+                      yr[dst_slot(TS(q + 1, u), SH)], yi[dst_slot(TS(q + 1, u), SH)], yr[dst_slot(BS(q + 1, u), SH)],
+                      yi[dst_slot(BS(q + 1, u), SH)], p1);
+        }
+#pragma unroll
+        for (int col = 0; col < N; ++col) {
+            xr[col] = yr[col];
+            xi[col] = yi[col];
+        }
+        if (!mask) return;
     }
     // ---- P (= V) update in smem: task (row = lane, pair q) for q = warp, warp + NW, ... ----
     if (SP && c.want_p) {
@@ -313,9 +356,7 @@ __device__ __forceinline__ void sweep(double (&xr)[N], double (&xi)[N], const Ct
             ring_shift<1>(xi);
             break;
         }
-        iter<1, NW, SP>(xr, xi, c, t0 + 1, st);
-        ring_shift<2>(xr);
-        ring_shift<2>(xi);
+        iter<1, NW, SP, 2>(xr, xi, c, t0 + 1, st);  // writes straight into the registers shifted by two
     }
 }
 
