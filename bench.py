@@ -339,8 +339,9 @@ def run_b200(args, cfg):
     def step():
         return solve_rank_slice(a_global, m, n, opts, rank, world, route=route, out=out)[2]
 
-    for _ in range(args.warmup):
-        res = step()
+    for _ in range(args.warmup):  # warm-up steps exactly like the timed ones (the flush kernel's module is
+        flush.fill_(1.0)           # loaded lazily at its first launch: ~5 ms of host time that left the
+        res = step()               # first timed step launching onto an idle GPU, 0.25 vs 0.15 ms on C2)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -348,19 +349,24 @@ def run_b200(args, cfg):
     t_wall0 = time.perf_counter()
     evs = []
     stream = torch.cuda.current_stream()
+    host_us = []
     for _ in range(args.steps):
+        h0 = time.perf_counter()
         flush.fill_(1.0)  # L2 flush, outside the timed events
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         res = step()
         e1.record(stream)
         evs.append((e0, e1))
+        host_us.append((time.perf_counter() - h0) * 1e6)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     t_wall1 = time.perf_counter()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    if os.environ.get("BSVD_BENCH_STEPS"):
+        log("step ms:", " ".join(f"{x:.4f}" for x in step_ms), "| host us:", " ".join(f"{x:.0f}" for x in host_us))
     dev_s = sum(step_ms) / 1e3
     if dist:
         tt = torch.tensor([dev_s], dtype=torch.float64, device=dev)
