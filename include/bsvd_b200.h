@@ -53,7 +53,7 @@ typedef struct {
     int row_block;      /* accepted for parity (tiling is the kernel's own)  */
     int kernel;         /* 0 = auto; >0 forces a kernel variant (tests/bench) */
     int use_qr;         /* use_qr_preprocess: dispatch takes the "qr+" route when m >= 3n (QR_RATIO) */
-    int reserved[2];
+    int reserved[2];    /* [0]: 32x32 FP64 tail as kernel 52 (0 = automatic, < 0 off; experimental); [1]: 0 */
 } bsvd_opts;
 
 /* Per-problem telemetry, written by the device (mirrors SolveInfo / BatchState). */

@@ -131,6 +131,9 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         const int want = o->kernel ? o->kernel
                                    : (r.need_v ? (fv ? KV_UNBLOCKED_REG32F : KV_UNBLOCKED_REG32G) : KV_UNBLOCKED_REG32B);
         Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, reg_ok, want, o->max_sweeps);
+        // above one resident wave of 52's warps: the last problems run as 52 in the same launch
+        if (p.kernel == KV_UNBLOCKED_REG32G && o->kernel == 0 && batch > 0)
+            p.aux = split_tail(batch, sm_count(), o->reserved[0]);
         if (p.kernel) return p;
         if (o->kernel != 0) return p;  // forced variant unavailable => kernel 0 => unsupported
     }
@@ -188,7 +191,6 @@ int run(const Route& r, const Plan& p, int m, int n, int batch, const void* A, i
     a.work = p.work_elems ? static_cast<T*>(work) : nullptr;
     a.work_stride = (int64_t)p.work_elems;
     a.info = info;
-    a.reserved_stagger = o->reserved[0];
     switch (p.kernel) {
         case KV_UNBLOCKED_GENERAL: return launch_unblocked_general<T>(a, p, st);
         case KV_BLOCKED_GENERAL: return launch_blocked_general<T>(a, p, st);

@@ -32,7 +32,6 @@ struct SolveArgs {
     int resident;        // bit0: W in smem, bit1: V in smem, bit2: scratch in smem
     int group;           // lanes per column pair (general unblocked kernel)
     int kernel;          // variant id for telemetry
-    int reserved_stagger;  // experimental: per-warp start stagger (ns)
     bsvd_info* info;
 };
 

@@ -33,6 +33,7 @@ template <class T>
 int launch_blocked_general(SolveArgs<T> a, const Plan& p, cudaStream_t st);
 bool is_reg32b(int kv);
 Plan plan_unblocked_reg32b(int dtype, int bm, int bn, int need_v, bool lda_ok, int variant, int max_sweeps);
+int split_tail(int batch, int sms, int override);  // 32x32 FP64: problems of a batch run as kernel 52's tail
 int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st);
 
 template <class T>

@@ -29,6 +29,8 @@
 // formula up to rounding); tools/acc_cmp.py and tests/test_gpu_parity.py hold
 // the kernel to the parity contract.  V is replayed from a per-sweep rotation
 // log exactly as in unblocked_reg.cu; finalize.cu forms sigma, U, the order.
+#include <algorithm>
+
 #include "kernel_args.cuh"
 #include "launch.h"
 #include "rotation.cuh"
@@ -532,14 +534,14 @@ __device__ __forceinline__ void v_sweep(double (&x0)[N], double (&x1)[N], WarpSm
 // same parameters, the same FMAs as the replay, so the same bits): no rotation log, no replay phase, no
 // parking of W and V in global memory.  Half 1 evaluates pairs of V's columns and discards them.
 template <int NW, int MINB, int U, int UV, int PD, bool FG = false, bool FV = false>
-__global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
+__device__ __forceinline__ void reg32b_body(const SolveArgs<double>& a, int cta) {
     static_assert(!FV || FG, "the fused-V mode is built on the scaled rotations");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
     const int half = lane >> 4, hl = lane & 15;
     const int ph = FV ? 0 : half;  // the half whose problem this lane's results belong to
-    const int prob = FV ? blockIdx.x * NW + warp : (blockIdx.x * NW + warp) * 2 + half;
+    const int prob = FV ? cta * NW + warp : (cta * NW + warp) * 2 + half;
     const bool live = prob < a.batch;
     const int r0 = hl, r1 = hl + 16;
     const size_t pstride = (size_t)a.work_stride;
@@ -900,6 +902,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
     }
 }
 
+template <int NW, int MINB, int U, int UV, int PD, bool FG = false, bool FV = false>
+__global__ void __launch_bounds__(NW * 32, MINB) k_reg32b(SolveArgs<double> a) {
+    reg32b_body<NW, MINB, U, UV, PD, FG, FV>(a, blockIdx.x);
+}
+
+// Batches above one resident wave: the head as 42 (two problems per warp) and a tail of whole problems
+// as 52 (one problem per warp, V in lockstep) in ONE launch, head CTAs first, so the last partial wave
+// runs the shorter single-problem chain instead of leaving SM sub-partitions idle (bit-identical: 42 and
+// 52 give the same bits).  `tail` is `head` with every per-problem pointer advanced past the head.
+template <int NW, int MINB, int U, int UV, int PD>
+__global__ void __launch_bounds__(NW * 32, MINB) k_reg32b_split(SolveArgs<double> head, SolveArgs<double> tail,
+                                                               int head_ctas) {
+    if ((int)blockIdx.x < head_ctas) reg32b_body<NW, MINB, U, UV, PD, true, false>(head, blockIdx.x);
+    else reg32b_body<NW, MINB, U, UV, PD, true, true>(tail, blockIdx.x - head_ctas);
+}
+
 }  // namespace r32b
 
 bool is_reg32b(int kv) { return kv == KV_UNBLOCKED_REG32B || kv == KV_UNBLOCKED_REG32G || kv == KV_UNBLOCKED_REG32F; }
@@ -931,12 +949,56 @@ static int launch_r32b(SolveArgs<double> a, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 
+// head (42) + tail (52) in one launch; tail problems = p.aux (make_plan: split_tail)
+static int launch_r32b_split(SolveArgs<double> a, int tail, cudaStream_t st) {
+    constexpr int NW = 4;
+    SolveArgs<double> h = a, t = a;
+    const int nh = a.batch - tail;
+    h.batch = nh;
+    h.kernel = KV_UNBLOCKED_REG32G;
+    t.batch = tail;
+    t.kernel = KV_UNBLOCKED_REG32F;
+    t.A = a.A + (size_t)nh * a.strideA;
+    t.U = a.U + (size_t)nh * a.strideU;
+    t.S = a.S + (size_t)nh * a.strideS;
+    if (a.V) t.V = a.V + (size_t)nh * a.strideV;
+    t.work = a.work + (size_t)nh * a.work_stride;
+    if (a.info) t.info = a.info + nh;
+    const int head_ctas = (nh + 2 * NW - 1) / (2 * NW), tail_ctas = (tail + NW - 1) / NW;
+    const size_t smem = NW * sizeof(r32b::WarpSmem) + r32b::NIT * r32b::H * 4;
+    auto k = r32b::k_reg32b_split<NW, 2, 2, 2, 8>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return BSVD_ERR_CUDA;
+    k<<<head_ctas + tail_ctas, NW * 32, smem, st>>>(h, t, head_ctas);
+    return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
+}
+
+// tail problems for a batch of `batch` on `sms` SMs (0: no split): above one resident wave of 42's warps
+// a tail of 4 problems per SM; between one wave of 52's warps and one of 42's, as many as keep every warp
+// resident (measured on B200, tools/tail_split.py: 1,250 0.43 -> 0.40 ms, 2,500 0.66 -> 0.58 ms, 5,000
+// 1.00 -> 0.97 ms, 10,000 1.69 -> 1.65 ms); `override` (bsvd_opts.reserved[0], experimental): > 0 forces
+// that tail, < 0 disables the split
+int split_tail(int batch, int sms, int override) {
+    if (override < 0) return 0;
+    if (override > 0) return override < batch ? override : 0;
+    if (batch <= 8 * sms) return 0;  // kernel 52 alone
+    int x = 4 * sms;
+    if (batch <= 16 * sms) x = std::min(x, 15 * sms - batch);  // keep head warps + tail warps resident
+    x &= ~3;
+    return x >= 2 * sms ? x : 0;
+}
+
 // 4 warps per CTA, 2 CTAs per SM (255 registers: 8 warps, 16 problems per SM), ring unrolled by 2.
 // Round-1 variants measured slower and retired: a 168-register cap (12 warps/SM, spills), the V ring
 // unrolled by 4, a shuffle-butterfly g_ji reduction, a split W kernel + V replay kernel.
 int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st) {
     a.kernel = p.kernel;
     a.work_stride = (int64_t)p.work_elems;
+    if (p.kernel == KV_UNBLOCKED_REG32G && p.aux > 0 && p.aux < a.batch) {
+        const int rc = launch_r32b_split(a, p.aux, st);
+        if (rc) return rc;
+        return launch_finalize_flagged<double>(a, st);
+    }
     const int rc = p.kernel == KV_UNBLOCKED_REG32G   ? launch_r32b<4, 2, 2, 2, 8, true>(a, st)  // scaled rotations
                    : p.kernel == KV_UNBLOCKED_REG32F ? launch_r32b<4, 2, 2, 2, 8, true, true>(a, st)  // + V in lockstep
                                                      : launch_r32b<4, 2, 2, 2, 16, false>(a, st);

@@ -75,17 +75,17 @@ _OPTS_CACHE: dict = {}
 _WSB_CACHE: dict = {}
 
 
-def _cached_opts(opts, route: int, kernel: int, stagger: int) -> _lib.BsvdOpts:
+def _cached_opts(opts, route: int, kernel: int, tail: int) -> _lib.BsvdOpts:
     """make_opts memoised on the (frozen, hashable) JacobiOptions: the C side only reads the struct."""
-    key = (opts, int(route), int(kernel), int(stagger))
+    key = (opts, int(route), int(kernel), int(tail))
     o = _OPTS_CACHE.get(key)
     if o is None:
-        o = make_opts(opts, route, kernel, stagger)
+        o = make_opts(opts, route, kernel, tail)
         _OPTS_CACHE[key] = o
     return o
 
 
-def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0, stagger: int = 0) -> _lib.BsvdOpts:
+def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0, tail: int = 0) -> _lib.BsvdOpts:
     """JacobiOptions -> POD bsvd_opts (src/svd.py:70-78 field by field)."""
     o = _lib.BsvdOpts()
     o.k = float(opts.k)
@@ -99,7 +99,7 @@ def make_opts(opts, route: int = _lib.DISPATCH, kernel: int = 0, stagger: int = 
     o.row_block = int(opts.row_block)
     o.kernel = int(kernel)
     o.use_qr = int(bool(opts.use_qr_preprocess))
-    o.reserved[0] = int(stagger)
+    o.reserved[0] = int(tail)  # experimental: 32x32 FP64 tail size (0 automatic, < 0 off)
     return o
 
 
@@ -130,7 +130,7 @@ class DeviceResult:
 
 
 def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: int = 0,
-                 out=None, stagger: int = 0) -> DeviceResult:
+                 out=None, tail: int = 0) -> DeviceResult:
     """Batched SVD of a device tensor a_t (B, n, m) (column-major matrices).
 
     Launches on torch's current stream; returns device tensors without
@@ -143,7 +143,7 @@ def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: 
     dt = np_dtype_of(a_t.dtype)
     code = DTYPE_CODE[dt]
     k = min(m, n)
-    o = _cached_opts(opts, route, kernel, stagger)
+    o = _cached_opts(opts, route, kernel, tail)
     dev = a_t.device
     if out is None:
         u = torch.empty((B, k, m), dtype=a_t.dtype, device=dev)

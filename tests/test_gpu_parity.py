@@ -797,9 +797,10 @@ def test_c2_batch_size_kernel_choice_is_bitwise_invisible():
 @pytest.mark.gpu
 def test_c1_one_kernel_at_every_batch_size():
     """The 32x32 FP64 default (scaled rotations) runs as 42 (two problems per warp) on batches above one
-    resident wave and as 52 (one problem per warp, V in lockstep) below it; the two give the same bits,
-    so batch == standalone holds bitwise (tests/test_batch.py:19-28) between a 1,300-problem batch and a
-    9-problem one, holes, fresh-norm iterations and extreme scales included."""
+    resident wave -- with the batch's last problems as 52 in the same launch -- and as 52 (one problem
+    per warp, V in lockstep) below it; the two give the same bits, so batch == standalone holds bitwise
+    (tests/test_batch.py:19-28) between a 1,300-problem batch and a 9-problem one, holes, fresh-norm
+    iterations and extreme scales included."""
     import torch
 
     from paper_2601_17979_b200.solver import INFO_DTYPE
@@ -820,7 +821,8 @@ def test_c1_one_kernel_at_every_batch_size():
     torch.cuda.synchronize()
     kb = np.frombuffer(big.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"]
     ks = np.frombuffer(small.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"]
-    assert (kb == 42).all() and (ks == 52).all()
+    tail = len(kb) - int((kb == 42).sum())  # the batch's last problems run as 52 in the same launch
+    assert set(kb.tolist()) <= {42, 52} and (kb[len(kb) - tail:] == 52).all() and (ks == 52).all()
     p = torch.tensor(pick).cuda()
     assert torch.equal(big.s[p], small.s) and torch.equal(big.u[p], small.u) and torch.equal(big.v[p], small.v)
     for b in (7, 11, 13, 15):  # and the extreme ones are right (underflow-safe norms, like the reference's)
@@ -865,3 +867,34 @@ def test_c1_fused_v_kernel_matches_two_problem_kernel(want_v):
     for b in (0, 3, 4, 6, 8):
         st = np.linalg.svd(A[b], compute_uv=False)
         assert np.max(np.abs(r52.s[b].cpu().numpy() - st)) <= 32 * 2.0 ** -53 * st[0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,tail", [(1300, 0), (3000, 0), (3000, 1000), (2000, 7)])
+def test_c1_head_tail_split_matches_unsplit(B, tail):
+    """A batch above one resident wave runs its head as 42 and a tail as 52 in one launch (automatic tail
+    for tail=0, forced otherwise): factors, sweeps and rotation counts identical to the unsplit launch
+    (bsvd_opts.reserved[0] < 0), the kernel ids recorded per problem."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    rng = np.random.default_rng(B + tail)
+    A = rng.standard_normal((B, 32, 32))
+    A[B - 3][:, 4] = 0.0
+    A[B - 5] *= 1e-200
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    opts = bs.JacobiOptions()
+    rs = bs.solve_tensor(a, 32, 32, opts, tail=tail)
+    r0 = bs.solve_tensor(a, 32, 32, opts, tail=-1)
+    torch.cuda.synchronize()
+    i_s = np.frombuffer(rs.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    i_0 = np.frombuffer(r0.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (i_0["kernel"] == 42).all()
+    nt = int((i_s["kernel"] == 52).sum())
+    assert nt > 0 and (i_s["kernel"][B - nt:] == 52).all() and (i_s["kernel"][:B - nt] == 42).all()
+    if tail:
+        assert nt == tail
+    for f in ("outer_sweeps", "rotations", "last_rotations", "converged", "status"):
+        assert (i_s[f] == i_0[f]).all(), f
+    assert torch.equal(rs.s, r0.s) and torch.equal(rs.u, r0.u) and torch.equal(rs.v, r0.v)

@@ -27,9 +27,9 @@ args = sys.argv[1:]
 kernels = [0]
 if "--kernels" in args:
     i = args.index("--kernels"); kernels = [int(x) for x in args[i+1].split(",")]; del args[i:i+2]
-stagger = 0
-if "--stagger" in args:
-    i = args.index("--stagger"); stagger = int(args[i+1]); del args[i:i+2]
+tail = 0
+if "--tail" in args:
+    i = args.index("--tail"); tail = int(args[i+1]); del args[i:i+2]
 only = args
 for name, fam, m, n, B, dt, kappa, wantv in cfgs:
     if only and name not in only: continue
@@ -37,13 +37,13 @@ for name, fam, m, n, B, dt, kappa, wantv in cfgs:
     opts = bs.JacobiOptions(compute_right_vectors=wantv)
     for kern in kernels:
       try:
-          r = bs.solve_tensor(a, m, n, opts, kernel=kern, stagger=stagger); torch.cuda.synchronize()
+          r = bs.solve_tensor(a, m, n, opts, kernel=kern, tail=tail); torch.cuda.synchronize()
       except RuntimeError as exc:
           print(f"{name:8s} kernel={kern}: {exc}"); continue
       ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
       ts = []
       for _ in range(3):
-        ev0.record(); r = bs.solve_tensor(a, m, n, opts, kernel=kern, stagger=stagger); ev1.record(); torch.cuda.synchronize()
+        ev0.record(); r = bs.solve_tensor(a, m, n, opts, kernel=kern, tail=tail); ev1.record(); torch.cuda.synchronize()
         ts.append(ev0.elapsed_time(ev1))
       info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
       t = min(ts)
