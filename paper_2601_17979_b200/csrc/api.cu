@@ -127,7 +127,7 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         // Batches of at most FV_WARPS_PER_SM problems per SM: one problem per warp, V carried in lockstep
         // by the other half-warp (bit-identical to 42, no replay phase) -- the GPU is not full, so the
         // shorter per-problem chain wins over 42's two problems per warp.
-        const bool fv = r.need_v && batch > 0 && batch <= FV_WARPS_PER_SM * sm_count();
+        const bool fv = r.need_v && batch > 0 && batch <= FV_WARPS_PER_SM * sm_count() && o->reserved[0] <= 0;
         const int want = o->kernel ? o->kernel
                                    : (r.need_v ? (fv ? KV_UNBLOCKED_REG32F : KV_UNBLOCKED_REG32G) : KV_UNBLOCKED_REG32B);
         Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, reg_ok, want, o->max_sweeps);
