@@ -173,7 +173,7 @@ def solve_tensor(a_t, m: int, n: int, opts, route: int = _lib.DISPATCH, kernel: 
 
 
 def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: int = _lib.DISPATCH,
-                       kernel: int = 0, chunk: int = 0, streams=None, a_ptrs=None, pack_threads: int = 8):
+                       kernel: int = 0, chunk: int = 0, streams=None, a_ptrs=None, pack_threads: int = 4):
     """Pipelined host-buffer solve through bsvd_gesvj_batched_host.
 
     With ``a_ptrs`` (uintp array of the B problems' column-major data) the batch is packed into a_h by
