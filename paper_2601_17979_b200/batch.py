@@ -236,32 +236,39 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
 
     from .solver import last_device_seconds
 
-    solved: list = []  # (idxs, prep, U, S, V, info, (device, host) seconds per problem)
+    solved: list = []  # (idxs, prep, U, S, V, info, (device, host) seconds per problem, group)
+    results: list = [None] * n_prob
     if uniform is not None:
         ptrs, t = uniform
         groups = {None: range(n_prob)}
         preps = [t]
+    H = _lib.hostptrs()
     for key, idxs in groups.items():
         t0 = time.perf_counter()
+        g = _Group()
         try:
             if uniform is not None:
-                U, S, V, info, _kern = solve_host(problems, opts, route=_ROUTE[force], ptrs=ptrs)
+                finish = solve_host(problems, opts, route=_ROUTE[force], ptrs=ptrs, defer=True)
+                if H is not None:  # the records (lazy views of g) are built while the device pipeline drains
+                    H.bsvd_py_fill_lazy(results, 0, n_prob, _LazyResult, g)
+                U, S, V, info, _kern = finish()
             else:
                 U, S, V, info, _kern = solve_host([arrays[i] for i in idxs], opts, route=_ROUTE[force])
         except Exception as exc:
             for i in idxs:
                 errors[i] = exc
+                results[i] = None
             continue
         wall, dev = time.perf_counter() - t0, last_device_seconds()
-        solved.append((idxs, preps[idxs[0]], U, S, V, info, (dev / len(idxs), max(0.0, wall - dev) / len(idxs))))
+        solved.append((idxs, preps[idxs[0]], U, S, V, info, (dev / len(idxs), max(0.0, wall - dev) / len(idxs)),
+                       g if (uniform is not None and H is not None) else None))
 
     # rounds the reference's lockstep loop would run (src/batch.py:113-142)
-    unconverged = any(not info["converged"].all() for *_, info, _dt in solved)
-    mx = max([max(int(info["outer_sweeps"].max()), 1) for *_, info, _dt in solved] + ([1] if trivial else []),
+    unconverged = any(not info["converged"].all() for *_, info, _dt, _g in solved)
+    mx = max([max(int(info["outer_sweeps"].max()), 1) for *_, info, _dt, _g in solved] + ([1] if trivial else []),
              default=0)
     rounds = opts.max_nsweeps if unconverged else mx
 
-    results: list = [None] * n_prob
     want_v = opts.compute_right_vectors
     for idx in trivial:
         p = preps[idx]
@@ -277,8 +284,8 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
     tele = []
     masking = bool(masked_rounds and opts.masking)
     new = object.__new__
-    for idxs, p, U, S, V, info, dtime in solved:
-        g = _Group()
+    for idxs, p, U, S, V, info, dtime, pre in solved:
+        g = pre if pre is not None else _Group()
         sw = info["outer_sweeps"].astype(np.int64)
         conv = info["converged"] != 0
         g.U, g.S, g.V = U, S, (V if want_v else None)
@@ -288,8 +295,9 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
         g.blocked, g.pps = p.blocked, p.pairs_per_sweep
         g.eig_unit = 0 if (not p.blocked and p.bn < 2) else 1
         g.dtime, g.atime = dtime
-        H = _lib.hostptrs() if isinstance(idxs, range) else None
-        if H is not None:  # one C pass (csrc/hostptrs.c): allocate the records, set (_g, _j)
+        if pre is not None:
+            pass  # records already built (during the device pipeline)
+        elif isinstance(idxs, range) and H is not None:  # one C pass (csrc/hostptrs.c): records with (_g, _j)
             H.bsvd_py_fill_lazy(results, idxs.start, len(idxs), _LazyResult, g)
         elif isinstance(idxs, range):
             recs = [new(_LazyResult) for _ in idxs]

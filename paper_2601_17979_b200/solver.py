@@ -331,7 +331,8 @@ def last_device_seconds() -> float:
     return getattr(_TLS, "device_seconds", 0.0)
 
 
-def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, device=None, ptrs=None):
+def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, device=None, ptrs=None,
+               defer: bool = False):
     """Equal shape/dtype numpy matrices -> (U (B,m,k), S (B,k), V (B,n,k)|None, info records).
 
     Host-buffer path: the column-major batch is packed (one C-level copy; ``ptrs`` may pass the
@@ -340,6 +341,8 @@ def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, de
     D2H in chunks.  The factors land directly in pooled pinned result buffers that are handed to the
     caller (no copy-out; a buffer is reused only once every array viewing it has been dropped); when the
     pool is exhausted the factors are copied into fresh arrays.  Returned U[b] / V[b] are F-ordered views.
+    ``defer``: return a callable instead, which waits for the device and returns the same tuple, so the
+    caller can do host work (building records) while the pipeline drains.
     """
     torch = _torch()
     B = len(mats)
@@ -374,8 +377,17 @@ def solve_host(mats: list, opts, route: int = _lib.DISPATCH, kernel: int = 0, de
     t_dev0 = time.perf_counter()
     with torch.cuda.device(device):
         kern = solve_host_buffers(host, u_h, s_h, v_h, info_h, m, n, opts, route, kernel, a_ptrs=ptrs)
-        torch.cuda.current_stream(device).synchronize()
-    _TLS.device_seconds = time.perf_counter() - t_dev0  # the pipelined H2D / solve / D2H, for WorkCounters
+        stream = torch.cuda.current_stream(device)
+
+    def finish():
+        stream.synchronize()
+        _TLS.device_seconds = time.perf_counter() - t_dev0  # the pipelined H2D / solve / D2H, for WorkCounters
+        return _host_outputs(direct, Uo, So, Vo, u_h, s_h, v_h, info_h, B, k, m, n, dt, kern)
+
+    return finish if defer else finish()
+
+
+def _host_outputs(direct, Uo, So, Vo, u_h, s_h, v_h, info_h, B, k, m, n, dt, kern):
     if direct:
         Uc, S, Vc = Uo, So, Vo
     else:  # copy the factors out of the reusable staging (threaded: ~250 MB for C1-10k)
