@@ -974,16 +974,16 @@ static int launch_r32b_split(SolveArgs<double> a, int tail, cudaStream_t st) {
 }
 
 // tail problems for a batch of `batch` on `sms` SMs (0: no split): above one resident wave of 42's warps
-// a tail of 4 problems per SM; between one wave of 52's warps and one of 42's, as many as keep every warp
-// resident (measured on B200, tools/tail_split.py: 1,250 0.43 -> 0.40 ms, 2,500 0.66 -> 0.58 ms, 5,000
+// a tail of 2 problems per SM (4 from 48 problems per SM on); between one wave of 52's warps and one of
+// 42's, up to 4 per SM as long as every warp of the launch stays resident (measured on B200, tools/tail_split.py: 1,250 0.43 -> 0.40 ms, 2,500 0.66 -> 0.58 ms, 5,000
 // 1.00 -> 0.97 ms, 10,000 1.69 -> 1.65 ms); `override` (bsvd_opts.reserved[0], experimental): > 0 forces
 // that tail, < 0 disables the split
 int split_tail(int batch, int sms, int override) {
     if (override < 0) return 0;
     if (override > 0) return override <= batch ? override : 0;
     if (batch <= 8 * sms) return 0;  // kernel 52 alone
-    int x = 4 * sms;
-    if (batch <= 16 * sms) x = std::min(x, 15 * sms - batch);  // keep head warps + tail warps resident
+    int x = batch < 48 * sms ? 2 * sms : 4 * sms;  // (tools/tail_split.py: 5,000 best at 296, 10,000 at 592)
+    if (batch <= 16 * sms) x = std::min(4 * sms, 15 * sms - batch);  // keep head warps + tail warps resident
     x &= ~3;
     return x >= 2 * sms ? x : 0;
 }
