@@ -33,7 +33,7 @@ BSVD_DEV T scale_by_sigma(T x, typename tr<T>::R s) {
     } else if constexpr (sizeof(T) == 8) {
         return div_by_sigma(x, s, rcp_refined(s));  // the fused finalisations' formula, bit for bit
     } else {
-        return x / s;
+        return div_by_sigma_f(x, s, __frcp_rn(s));  // the 16x16 kernels' fused formula, bit for bit
     }
 }
 

@@ -252,7 +252,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16b(SolveArgs<float> a) {
             const FinalOut<float> o = final_out(a, prob);
             o.S[r] = sg;
 #pragma unroll
-            for (int c = 0; c < N; ++c) o.U[hl + (size_t)sm.rk[half][c] * o.ldu] = __fdiv_rn(x[c] * us, sm.sig[half][c]);
+            for (int c = 0; c < N; ++c) {
+                const float sc = sm.sig[half][c];
+                o.U[hl + (size_t)sm.rk[half][c] * o.ldu] = div_by_sigma_f(x[c] * us, sc, __frcp_rn(sc));
+            }
             if (WANT_V && o.want_v && o.V) {
 #pragma unroll
                 for (int c = 0; c < N; ++c) o.V[hl + (size_t)sm.rk[half][c] * o.ldv] = y[c];

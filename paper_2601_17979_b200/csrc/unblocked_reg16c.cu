@@ -349,9 +349,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_reg16c(SolveArgs<float> a) {
 #pragma unroll
             for (int c = 0; c < N; ++c) {
                 const size_t col = (size_t)sm.rk[c] * o.ldu;
-                const float sc = sm.sig[c];
-                o.U[ql + col] = __fdiv_rn(X[c].x * us, sc);
-                o.U[ql + 8 + col] = __fdiv_rn(X[c].y * us, sc);
+                const float sc = sm.sig[c], rs = __frcp_rn(sc);
+                o.U[ql + col] = div_by_sigma_f(X[c].x * us, sc, rs);
+                o.U[ql + 8 + col] = div_by_sigma_f(X[c].y * us, sc, rs);
             }
             if (WANT_V && o.want_v && o.V) {
 #pragma unroll
