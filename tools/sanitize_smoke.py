@@ -14,18 +14,19 @@ import paper_2601_17979_b200 as bs
 rng = np.random.default_rng(1)
 
 
-def run(dt, m, n, route=0, kernel=0, B=3, **kw):
+def run(dt, m, n, route=0, kernel=0, B=3, tail=0, **kw):
     A = rng.random((B, n, m))
     if np.dtype(dt).kind == "c":
         A = A + 1j * rng.random((B, n, m))
     a = torch.from_numpy(A.astype(dt)).cuda()
-    r = bs.solve_tensor(a, m, n, bs.JacobiOptions(**kw), route=route, kernel=kernel)
+    r = bs.solve_tensor(a, m, n, bs.JacobiOptions(**kw), route=route, kernel=kernel, tail=tail)
     torch.cuda.synchronize()
     print(dt.__name__, m, n, route, kernel, "ok", float(r.s[0, 0]), flush=True)
 
 
 run(np.float64, 32, 32)                       # r32b scaled rotations, V in lockstep (52) + fused finalise
 run(np.float64, 32, 32, kernel=42, B=5)       # r32b scaled rotations, two problems per warp (42)
+run(np.float64, 32, 32, B=40, tail=13)        # r32b head (42) + tail (52) in one launch (k_reg32b_split)
 run(np.float64, 32, 32, compute_right_vectors=False)  # r32b values only (12)
 run(np.float32, 16, 16)                       # reg16b
 run(np.float32, 16, 16, kernel=34, B=9)       # reg16c (quarter-warp)
