@@ -898,3 +898,41 @@ def test_c1_head_tail_split_matches_unsplit(B, tail):
     for f in ("outer_sweeps", "rotations", "last_rotations", "converged", "status"):
         assert (i_s[f] == i_0[f]).all(), f
     assert torch.equal(rs.s, r0.s) and torch.equal(rs.u, r0.u) and torch.equal(rs.v, r0.v)
+
+
+@pytest.mark.gpu
+def test_c1_split_boundary_problems_and_fp32_promotion():
+    """Non-finite problems on either side of the head/tail boundary are flagged alone; FP32 32x32 (solved
+    on the FP64 kernels) keeps batch == standalone bitwise across the split."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    B, tail = 3000, 296
+    rng = np.random.default_rng(5150)
+    A = rng.standard_normal((B, 32, 32))
+    A[B - tail - 1][3, 3] = np.nan  # last head problem
+    A[B - tail][0, 7] = np.inf      # first tail problem
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, 32, 32, bs.JacobiOptions(), tail=tail)
+    torch.cuda.synchronize()
+    info = np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)
+    assert info["kernel"][B - tail - 1] == 42 and info["kernel"][B - tail] == 52
+    bad = {B - tail - 1, B - tail}
+    assert all(info["status"][i] != 0 for i in bad)
+    good = np.array([i for i in range(B) if i not in bad])
+    assert (info["status"][good] == 0).all() and info["converged"][good].all()
+    for b in (B - tail - 2, B - tail + 1, 0, B - 1):
+        st = np.linalg.svd(A[b], compute_uv=False)
+        assert np.max(np.abs(r.s[b].cpu().numpy() - st)) <= 32 * 2.0 ** -53 * st[0]
+    # FP32: promoted to the FP64 kernels, split at this size; a subset alone gives the same bits
+    A32 = A.astype(np.float32)
+    A32[B - tail - 1] = rng.standard_normal((32, 32))
+    A32[B - tail] = rng.standard_normal((32, 32))
+    a32 = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A32, 1, 2))).cuda()
+    big = bs.solve_tensor(a32, 32, 32, bs.JacobiOptions())
+    pick = [0, 17, B - tail - 1, B - tail, B - 1]
+    small = bs.solve_tensor(a32[pick].contiguous(), 32, 32, bs.JacobiOptions())
+    torch.cuda.synchronize()
+    p = torch.tensor(pick).cuda()
+    assert torch.equal(big.s[p], small.s) and torch.equal(big.u[p], small.u) and torch.equal(big.v[p], small.v)
