@@ -408,7 +408,7 @@ def run_b200(args, cfg):
     from paper_2601_17979_b200.solver import default_chunk
 
     e2e_chunk = default_chunk(B, h2d_per + d2h_per, m * n, len(e2e_streams),
-                              torch.cuda.get_device_properties(dev).multi_processor_count)  # ~4 MB, 4..16 chunks
+                              torch.cuda.get_device_properties(dev).multi_processor_count)  # ~8 MB, 4..16 chunks
     e2e_ms = []
     for it in range(args.warmup + args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
