@@ -320,8 +320,8 @@ def batch_svd(problems, opts: JacobiOptions | None = None, state: BatchState | N
     problems = list(problems)
     if not problems:
         raise DomainError("batch must contain at least one problem")
-    st = state if state is not None else BatchState.for_batch(len(problems))
-    st._reset(len(problems))
+    if state is not None:
+        state._reset(len(problems))
     # the records are tens of thousands of small objects: keep the cyclic collector out of the way
     gc_was = gc.isenabled()
     gc.disable()
@@ -330,6 +330,9 @@ def batch_svd(problems, opts: JacobiOptions | None = None, state: BatchState | N
     finally:
         if gc_was:
             gc.enable()
+    if state is None:  # no caller-visible state: the per-problem batch telemetry would only be discarded
+        return results
+    st = state
     st.errors = dict(errors)
     c = st.counters
     groups, trivial = tele
