@@ -142,6 +142,11 @@ class _Group:
 _PATHS: dict = {}
 
 
+def _set_ref(r, g, j):
+    object.__setattr__(r, "_g", g)
+    object.__setattr__(r, "_j", j)
+
+
 def _path_string(pv: int) -> str:
     p = _PATHS.get(pv)
     if p is None:
@@ -156,12 +161,19 @@ class _LazyResult(SvdResult):
     objects than the device spends solving it; the record is otherwise the reference's frozen
     dataclass (same fields, equality, repr, immutability; copies and pickles are plain SvdResults)."""
 
+    __slots__ = ("_g", "_j")  # set by the C helper straight into the slots (no per-record dict until first use)
+
     def __getattr__(self, name):
-        d = self.__dict__
-        g = d.get("_g")
-        if g is None or name not in ("u", "sigma", "v", "info"):
+        if name not in ("u", "sigma", "v", "info"):
             raise AttributeError(name)
-        j = d["_j"]
+        try:
+            g = object.__getattribute__(self, "_g")
+        except AttributeError:
+            raise AttributeError(name) from None
+        if g is None:
+            raise AttributeError(name)
+        j = object.__getattribute__(self, "_j")
+        d = self.__dict__
         c = g.cols
         if g.blocked:
             cnt = WorkCounters(gram_calls=int(g.calls[j]) * g.pps, eig_calls=int(g.calls[j]) * g.pps,
@@ -174,7 +186,7 @@ class _LazyResult(SvdResult):
                          inner_rotations=int(c["rotations"][j]), masked_pair_skips=int(g.masked[j]),
                          path=_path_string(int(c["path"][j])), counters=cnt)
         d.update(u=g.U[j], sigma=g.S[j], v=g.V[j] if g.V is not None else None, info=info)
-        del d["_g"], d["_j"]
+        object.__setattr__(self, "_g", None)  # materialised: the fields now live in the instance dict
         return d[name]
 
     def __reduce__(self):
@@ -302,12 +314,12 @@ def _solve_problems(problems, opts: JacobiOptions, force: str | None, masked_rou
         elif isinstance(idxs, range):
             recs = [new(_LazyResult) for _ in idxs]
             for j, r in enumerate(recs):
-                r.__dict__.update(_g=g, _j=j)
+                _set_ref(r, g, j)
             results[idxs.start:idxs.stop] = recs
         else:
             for j, idx in enumerate(idxs):
                 r = new(_LazyResult)
-                r.__dict__.update(_g=g, _j=j)
+                _set_ref(r, g, j)
                 results[idx] = r
         tele.append((idxs, sw, conv, info["last_rotations"], g))
     return results, errors, (tele, trivial)

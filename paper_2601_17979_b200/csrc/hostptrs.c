@@ -9,6 +9,7 @@
 
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#include <structmember.h>
 #include <stdint.h>
 #include <string.h>
 #define NPY_NO_DEPRECATED_API NPY_2_0_API_VERSION
@@ -83,11 +84,26 @@ int bsvd_py_gather_ndarray(PyObject* list, Py_ssize_t n, PyObject* ndarray_type,
     return 0;
 }
 
-/* list[start + j] = a fresh instance of `type` (allocated without __init__, like object.__new__) whose
- * instance dict is {"_g": group, "_j": j}, for j < n: the lazy SvdResult records of one device launch
- * (batch.py _LazyResult).  Returns 0, or -1 with a Python error set. */
+/* list[start + j] = a fresh instance of `type` (allocated without __init__, like object.__new__) with its
+ * slots _g = group, _j = j, for j < n: the lazy SvdResult records of one device launch (batch.py
+ * _LazyResult, __slots__ = ("_g", "_j")).  The slot offsets come from the type's member descriptors, so a
+ * record costs one allocation and two stores (no per-record instance dict until its first use).  Returns
+ * 0, or -1 with a Python error set. */
+static Py_ssize_t slot_offset(PyObject* type, const char* name) {
+    PyObject* d = PyObject_GetAttrString(type, name);
+    Py_ssize_t off = -1;
+    if (d && Py_TYPE(d) == &PyMemberDescr_Type) {
+        const PyMemberDef* mdef = ((PyMemberDescrObject*)d)->d_member;
+        if (mdef->type == Py_T_OBJECT_EX) off = mdef->offset;
+    }
+    Py_XDECREF(d);
+    PyErr_Clear();
+    return off;
+}
+
 int bsvd_py_fill_lazy(PyObject* list, Py_ssize_t start, Py_ssize_t n, PyObject* type, PyObject* group) {
-    static PyObject *key_g = NULL, *key_j = NULL;
+    static PyObject *key_g = NULL, *key_j = NULL, *cached = NULL;
+    static Py_ssize_t off_g = -1, off_j = -1;
     if (!key_g) key_g = PyUnicode_InternFromString("_g");
     if (!key_j) key_j = PyUnicode_InternFromString("_j");
     if (!key_g || !key_j) return -1;
@@ -95,20 +111,31 @@ int bsvd_py_fill_lazy(PyObject* list, Py_ssize_t start, Py_ssize_t n, PyObject* 
         PyErr_SetString(PyExc_ValueError, "bsvd_py_fill_lazy: bad arguments");
         return -1;
     }
+    if (cached != type) {
+        off_g = slot_offset(type, "_g");
+        off_j = slot_offset(type, "_j");
+        cached = type;  /* borrowed: the type lives as long as the module */
+    }
     PyTypeObject* tp = (PyTypeObject*)type;
     for (Py_ssize_t j = 0; j < n; ++j) {
         PyObject* obj = tp->tp_alloc(tp, 0);
-        if (!obj) return -1;
-        PyObject* d = PyObject_GenericGetDict(obj, NULL);
         PyObject* jj = PyLong_FromSsize_t(j);
-        if (!d || !jj || PyDict_SetItem(d, key_g, group) < 0 || PyDict_SetItem(d, key_j, jj) < 0) {
-            Py_XDECREF(d);
+        if (!obj || !jj) {
+            Py_XDECREF(obj);
             Py_XDECREF(jj);
-            Py_DECREF(obj);
             return -1;
         }
-        Py_DECREF(d);
-        Py_DECREF(jj);
+        if (off_g >= 0 && off_j >= 0) {  /* fresh object: the slots are NULL */
+            Py_INCREF(group);
+            *(PyObject**)((char*)obj + off_g) = group;
+            *(PyObject**)((char*)obj + off_j) = jj;
+        } else if (PyObject_GenericSetAttr(obj, key_g, group) < 0 || PyObject_GenericSetAttr(obj, key_j, jj) < 0) {
+            Py_DECREF(jj);
+            Py_DECREF(obj);
+            return -1;
+        } else {
+            Py_DECREF(jj);
+        }
         PyList_SetItem(list, start + j, obj); /* steals obj, releases the old item */
     }
     return 0;

@@ -212,3 +212,40 @@ def test_default_chunk_policy():
     assert default_chunk(10000, 3 * 16 * 16 * 4, 16 * 16, 4, 148) == 2500    # ~8 MB chunks, at least 4
     assert default_chunk(2000, 3 * 128 * 128 * 8, 128 * 128, 4, 148) == 125  # large problems: 16 chunks
     assert default_chunk(3, per32, 32 * 32, 4, 148) == 1
+
+
+def test_lazy_records_filled_by_c_helper():
+    """bsvd_py_fill_lazy writes the records' (_g, _j) slots directly; a record materialises its fields on
+    first use and otherwise behaves as the reference's frozen SvdResult (repr, copy, pickle, replace)."""
+    import copy
+    import dataclasses
+    import pickle
+
+    from paper_2601_17979_b200 import batch
+    from paper_2601_17979_b200.solver import INFO_DTYPE
+
+    H = _lib.hostptrs()
+    if H is None:
+        pytest.skip("CPython helper not built")
+    g = batch._Group()
+    g.U = np.arange(5 * 4, dtype=float).reshape(5, 2, 2)
+    g.S = np.ones((5, 2))
+    g.V = None
+    g.cols = np.zeros(5, dtype=INFO_DTYPE)
+    g.cols["converged"] = 1
+    g.cols["outer_sweeps"] = 3
+    g.calls = np.full(5, 3)
+    g.masked = np.zeros(5, dtype=int)
+    g.blocked, g.pps, g.eig_unit, g.dtime, g.atime = False, 1, 1, 1e-6, 1e-7
+    recs = [None] * 6
+    assert H.bsvd_py_fill_lazy(recs, 1, 5, batch._LazyResult, g) == 0
+    assert recs[0] is None and all(isinstance(r, bs.SvdResult) for r in recs[1:])
+    r = recs[4]
+    assert np.array_equal(r.u, g.U[3]) and np.array_equal(r.sigma, g.S[3]) and r.v is None
+    assert r.info.outer_sweeps == 3 and r.info.converged and "SvdResult" in repr(r) or "LazyResult" in repr(r)
+    for c in (copy.copy(r), copy.deepcopy(r), pickle.loads(pickle.dumps(r))):
+        assert type(c) is bs.SvdResult and np.array_equal(c.u, r.u) and c.info == r.info
+    r2 = dataclasses.replace(recs[2], sigma=np.zeros(2))
+    assert np.array_equal(r2.u, g.U[1]) and not r2.sigma.any()
+    with pytest.raises(dataclasses.FrozenInstanceError):
+        r.u = None
