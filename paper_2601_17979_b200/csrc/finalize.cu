@@ -8,19 +8,11 @@
 
 namespace bsvd {
 
-template <class T, bool FLAGGED = false>
-__global__ void __launch_bounds__(128) k_finalize_ws(SolveArgs<T> a) {
+template <class T>
+__device__ __forceinline__ void finalize_one_ws(const SolveArgs<T>& a, int prob, unsigned char* smem) {
     using R = typename tr<T>::R;
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int prob = blockIdx.x;
     const int bm = a.bm, bn = a.bn;
     const T* src = a.work + (size_t)prob * a.work_stride;
-    if constexpr (FLAGGED) {  // the solver finalised this problem itself unless its flag is set
-        const T f = src[a.work_stride - 1];
-        bool set;
-        if constexpr (tr<T>::cplx) set = f.re != 0; else set = f != 0;
-        if (!set) return;
-    }
     T* W = reinterpret_cast<T*>(smem);
     T* Vw = a.need_v ? W + (size_t)bm * bn : nullptr;
     size_t off = ((size_t)bm * bn + (a.need_v ? (size_t)bn * bn : 0)) * sizeof(T);
@@ -36,6 +28,37 @@ __global__ void __launch_bounds__(128) k_finalize_ws(SolveArgs<T> a) {
     finalize_block<T>(W, bm, bm, bn, Vw, bn, sig, perm, flag, final_out(a, prob));
 }
 
+template <class T>
+__device__ __forceinline__ bool flag_set(const SolveArgs<T>& a, int prob) {
+    const T f = a.work[(size_t)prob * a.work_stride + a.work_stride - 1];
+    if constexpr (tr<T>::cplx) return f.re != 0;
+    else return f != 0;
+}
+
+// FLAGGED: the pass after a solver that finalised most problems itself.  One thread per problem reads its
+// flag (CTA c covers problems 128 c .. 128 c + 127), and the CTA finalises the flagged ones in turn --
+// instead of one CTA per problem that mostly exits at once (C2: 7.3 us for 10,000 empty CTAs).
+template <class T, bool FLAGGED = false>
+__global__ void __launch_bounds__(128) k_finalize_ws(SolveArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if constexpr (FLAGGED) {
+        __shared__ int list[128];
+        __shared__ int cnt;
+        if (threadIdx.x == 0) cnt = 0;
+        __syncthreads();
+        const int p = blockIdx.x * 128 + threadIdx.x;
+        if (p < a.batch && flag_set(a, p)) list[atomicAdd(&cnt, 1)] = p;
+        __syncthreads();
+        const int nf = cnt;
+        for (int j = 0; j < nf; ++j) {
+            finalize_one_ws(a, list[j], smem);
+            __syncthreads();  // the staging buffer is reused for the next flagged problem
+        }
+    } else {
+        finalize_one_ws(a, blockIdx.x, smem);
+    }
+}
+
 template <class T, bool FLAGGED>
 static int launch_finalize_impl(SolveArgs<T> a, cudaStream_t st) {
     const size_t es = sizeof(T);
@@ -47,7 +70,7 @@ static int launch_finalize_impl(SolveArgs<T> a, cudaStream_t st) {
         if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return BSVD_ERR_CUDA;
     }
-    k<<<a.batch, 128, smem, st>>>(a);
+    k<<<FLAGGED ? (a.batch + 127) / 128 : a.batch, 128, smem, st>>>(a);
     return cudaPeekAtLastError() == cudaSuccess ? BSVD_OK : BSVD_ERR_CUDA;
 }
 

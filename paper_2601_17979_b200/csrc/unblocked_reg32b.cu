@@ -999,10 +999,10 @@ int launch_unblocked_reg32b(SolveArgs<double> a, const Plan& p, cudaStream_t st)
         if (rc) return rc;
         return launch_finalize_flagged<double>(a, st);
     }
-    // kernel 52 alone is the split launch with an empty head (the split kernel's instance of the
-    // one-problem-per-warp body spills 16 instead of 208 bytes: 1-2 % faster)
+    // (kernel 52 alone runs its own instantiation: 3-4 % faster below one wave than the split kernel's
+    // one-problem-per-warp body with an empty head, _abtest A/B on B200, although that one spills less)
     const int rc = p.kernel == KV_UNBLOCKED_REG32G   ? launch_r32b<4, 2, 2, 2, 8, true>(a, st)  // scaled rotations
-                   : p.kernel == KV_UNBLOCKED_REG32F ? launch_r32b_split(a, a.batch, st)     // + V in lockstep
+                   : p.kernel == KV_UNBLOCKED_REG32F ? launch_r32b<4, 2, 2, 2, 8, true, true>(a, st)  // + V in lockstep
                                                      : launch_r32b<4, 2, 2, 2, 16, false>(a, st);
     if (rc) return rc;
     return launch_finalize_flagged<double>(a, st);  // only problems the fused finalisation left over
