@@ -125,3 +125,38 @@ def test_eigvecs_any_row_count(rows):
     outs = bs.batch_hermitian_eig([g, g, g], eigvecs=[p.copy(order="F") for p in pres])
     for p, (d, m, _) in zip(pres, outs):
         np.testing.assert_allclose(m, p @ q, rtol=0, atol=64 * 2.0 ** -53 * np.abs(p).sum())
+
+
+def test_single_sweep_reduces_off_norm():  # reference tests/test_eig.py:133-136
+    g = random_hermitian(10, seed=5)
+    d, m, info = bs.jacobi_hermitian_eig(g, max_sweeps=1)
+    assert info.sweeps_run == 1 and off_norm(m.conj().T @ g @ m) < off_norm(g)
+
+
+def test_rejections_and_input_not_mutated():  # reference tests/test_eig.py:156-178
+    with pytest.raises(bs.DomainError):
+        bs.jacobi_hermitian_eig(np.asfortranarray([[1.0, 2.0], [5.0, 1.0]]))
+    with pytest.raises(bs.ShapeError):
+        bs.jacobi_hermitian_eig(np.zeros((2, 3), order="F"))
+    g = random_hermitian(4)
+    for kw in ({"k": 0.0}, {"max_sweeps": 0}):
+        with pytest.raises(bs.DomainError):
+            bs.jacobi_hermitian_eig(g, **kw)
+    g8 = random_hermitian(8, seed=8)
+    keep = g8.copy()
+    bs.jacobi_hermitian_eig(g8)
+    assert np.array_equal(g8, keep)
+
+
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=25, deadline=None)
+@given(n=st.integers(2, 24), seed=st.integers(0, 2 ** 16))
+def test_property_spectrum_matches_lapack(n, seed):  # reference tests/test_eig.py:180-187
+    g = random_hermitian(n, np.float64, seed=seed)
+    d, m, info = bs.jacobi_hermitian_eig(g)
+    assert info.converged
+    tol = 64 * n * 2.0 ** -53 * max(np.linalg.norm(g), 1.0)
+    assert np.allclose(np.sort(d), np.linalg.eigvalsh(g), atol=tol)
