@@ -48,3 +48,59 @@ def test_full_batch_on_device():
     u = 2.0 ** -53
     assert np.isnan(met[:, 3]).all()
     assert met[:, :3].max() < 30 * u, met[:, :3].max(axis=0) / u
+
+
+# ---- the reference's metric scenarios (pkg/tests/test_verify.py: TestThreshold, TestMetrics) ----
+from common import random_matrix  # noqa: E402
+
+
+def test_threshold_values():  # test_verify.py:26-31
+    assert bs.threshold(np.float32) == pytest.approx(30 * 2.0 ** -24)
+    assert bs.threshold(np.float64) == pytest.approx(30 * 2.0 ** -53)
+    assert bs.threshold(np.complex64) == bs.threshold(np.float32)
+    assert bs.threshold(np.complex128, k=100.0) == pytest.approx(100 * 2.0 ** -53)
+
+
+def test_exact_factorization_scores_zero():  # test_verify.py:34-39
+    a = np.asfortranarray(np.diag([3.0, 2.0]))
+    r = bs.svd_dispatch(a)
+    assert bs.residual_e1(a, r) == 0.0
+    e2, e3 = bs.orthogonality_e2_e3(r)
+    assert e2 == 0.0 and e3 == 0.0
+
+
+def test_e1_detects_wrong_factors_and_requires_v():  # test_verify.py:41-51
+    a = random_matrix(8, 8, seed=60)
+    r = bs.svd_dispatch(a)
+    wrong = bs.SvdResult(u=r.u, sigma=r.sigma * 2.0, v=r.v, info=r.info)
+    assert bs.residual_e1(a, wrong) > 0.01
+    b = random_matrix(8, 8, seed=61)
+    with pytest.raises(bs.DomainError):
+        bs.residual_e1(b, bs.svd_dispatch(b, bs.JacobiOptions(compute_right_vectors=False)))
+
+
+def test_e4_normalizes_by_min_dim():  # test_verify.py:53-57
+    assert bs.sigma_error_e4(np.array([3.0, 0.0]), np.array([0.0, 0.0]), 4, 2) == pytest.approx(1.5)
+    with pytest.raises(bs.ShapeError):
+        bs.sigma_error_e4(np.ones(3), np.ones(2), 3, 3)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64, np.complex64, np.complex128])
+def test_report_passes_on_good_solves(dt):  # test_verify.py:59-66 (arith spectrum, kappa 1e2)
+    from paper_2601_17979_b200.matgen import gen_batch_device
+
+    a = gen_batch_device("arith", 24, 24, 1, dt, kappa=1e2, seed=62)[0].cpu().numpy().T.copy(order="F")
+    r = bs.svd_dispatch(a)
+    sref = bs.make_sigma("arith", 24, 1e2)
+    rep = bs.error_report(a, r, sigma_ref=sref)
+    assert rep.all_pass and rep.threshold == pytest.approx(bs.threshold(dt)) and len(rep.passes) == 4
+
+
+def test_report_thresholds_and_missing_reference():  # test_verify.py:68-87
+    a = random_matrix(8, 8, seed=63)
+    r = bs.svd_dispatch(a)
+    assert bs.error_report(a, r, e3_threshold=100 * 2.0 ** -53).e3_threshold == pytest.approx(100 * 2.0 ** -53)
+    rep = bs.error_report(a, r)
+    assert rep.e4 is None and rep.all_pass
+    bad = bs.error_report(a, r, sigma_ref=np.linspace(5, 1, 8))
+    assert not bad.passes[3] and not bad.all_pass
