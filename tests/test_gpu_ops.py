@@ -63,3 +63,40 @@ def test_operator_shape_errors():
         bs.finalize(np.zeros((3, 5)))
     with pytest.raises(bs.ShapeError):
         bs.finalize(np.zeros((5, 3)), np.zeros((3, 4)))
+
+
+# ---- the reference's householder_qr scenarios (pkg/tests/test_core.py: TestHouseholderQR) ----
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+from common import ALL_DTYPES, random_matrix  # noqa: E402
+
+
+@pytest.mark.parametrize("dt", ALL_DTYPES)
+@pytest.mark.parametrize("shape", [(6, 6), (10, 4), (600, 16)])
+def test_householder_factorization_all_dtypes(dt, shape):  # test_core.py:116-132
+    m, n = shape
+    a = random_matrix(m, n, dt, seed=m + n)
+    q, r = bs.householder_qr(a)
+    u = unit_roundoff(dt)
+    one = lambda x: float(np.abs(x).sum(axis=0).max())  # noqa: E731
+    assert q.shape == (m, n) and r.shape == (n, n)
+    assert np.allclose(q @ r, a, atol=50 * u * one(a))
+    assert one(np.eye(n) - q.conj().T @ q) < 50 * n * u
+    assert np.allclose(np.tril(r, -1), 0.0)
+    d = np.diag(r)
+    assert np.all(np.real(d) >= 0)
+    if np.iscomplexobj(a):
+        assert np.max(np.abs(np.imag(d))) < 10 * u * one(a)
+
+
+@settings(max_examples=40, deadline=None)
+@given(m=st.integers(1, 30), n=st.integers(1, 30), seed=st.integers(0, 2 ** 16))
+def test_householder_property_reconstruction(m, n, seed):  # test_core.py:137-149
+    if m < n:
+        m, n = n, m
+    a = random_matrix(m, n, np.float64, seed=seed)
+    q, r = bs.householder_qr(a)
+    u = 2.0 ** -53
+    assert np.linalg.norm(a - q @ r) <= 100 * m * u * max(np.linalg.norm(a), 1e-300)
+    assert np.linalg.norm(np.eye(n) - q.T @ q) <= 100 * m * u
