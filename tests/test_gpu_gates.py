@@ -183,3 +183,62 @@ def test_full_batch_baseline_configs(cid, fam, m, n, B, dt, kappa, rank, route):
         assert np.abs(d).max() <= 3 and abs(d.mean()) <= 0.25, (np.abs(d).max(), d.mean())
     else:
         assert np.abs(d).max() <= 1
+
+
+# ---- acceptance c03, c06, c09 (/root/reference/pkg/tests/test_acceptance.py:141-331) ----
+def _design(name):  # src/cli.py:46-58 design presets (cumulative variants)
+    import dataclasses
+
+    base = bs.JacobiOptions()
+    return {"baseline": dataclasses.replace(base, inner_sweeps=0, fused_updates=False, masking=False),
+            "design2": dataclasses.replace(base, inner_sweeps=1, fused_updates=False, masking=False),
+            "design3": dataclasses.replace(base, inner_sweeps=1, fused_updates=True, masking=False),
+            "design4": dataclasses.replace(base, inner_sweeps=1, fused_updates=True, masking=True)}[name]
+
+
+def test_c03_design_variant_equivalence():
+    """sigma of every design variant within 30u of the baseline; design4 == design3 bitwise (batched: the
+    50 seeds of each n in one call per design)."""
+    u = 2.0 ** -53
+    for n in (16, 64, 128):
+        mats = [np.asfortranarray(np.random.default_rng(9000 * n + s).random((n, n))) for s in range(50)]
+        base = bs.batch_svd(mats, _design("baseline"))
+        res = {name: bs.batch_svd(mats, _design(name)) for name in ("design2", "design3", "design4")}
+        for name, rs in res.items():
+            for b, r in zip(base, rs):
+                assert float(np.max(np.abs(r.sigma - b.sigma))) < 30 * u * float(b.sigma[0]), (name, n)
+        for r3, r4 in zip(res["design3"], res["design4"]):
+            assert np.array_equal(r3.sigma, r4.sigma) and np.array_equal(r3.u, r4.u) and np.array_equal(r3.v, r4.v)
+
+
+def test_c06_masked_batch_work_saving():
+    rng = np.random.default_rng(606)
+    probs = [np.asfortranarray(np.diag(rng.uniform(0.5, 2.0, 64))) for _ in range(8)] + \
+            [np.asfortranarray(rng.random((64, 64))) for _ in range(8)]
+    st3, st4 = bs.BatchState.for_batch(len(probs)), bs.BatchState.for_batch(len(probs))
+    r3 = bs.batch_svd(probs, _design("design3"), st3)
+    r4 = bs.batch_svd(probs, _design("design4"), st4)
+    assert not st3.errors and not st4.errors
+    assert st4.counters.masked_pair_skips > 0 and st4.counters.eig_calls < st3.counters.eig_calls
+    for a3, a4 in zip(r3, r4):
+        assert np.array_equal(a3.sigma, a4.sigma) and np.array_equal(a3.u, a4.u) and np.array_equal(a3.v, a4.v)
+
+
+def test_c09_frobenius_mass_conservation():
+    """sum sigma^2 equals ||A||_F^2 within 30u, at most 30 outer sweeps (logrand spectra and random)."""
+    from paper_2601_17979_b200.matgen import gen_batch_device
+
+    rng = np.random.default_rng(909)
+    for n in (16, 64):
+        for dt in (np.float32, np.complex128):
+            a = gen_batch_device("logrand", n, n, 3, dt, kappa=1e3, seed=1).cpu().numpy()
+            mats = [np.asfortranarray(x.T) for x in a]
+            for m_, r in zip(mats, bs.batch_svd(mats, _design("design4"))):
+                u = unit_roundoff(dt)
+                fro2 = float(np.sum(np.abs(m_.astype(np.complex128)) ** 2))
+                ssq = float(np.sum(np.asarray(r.sigma, dtype=np.float64) ** 2))
+                assert r.info.outer_sweeps <= 30 and abs(ssq - fro2) < 30 * u * fro2
+        mats = [np.asfortranarray(rng.random((n, n))) for _ in range(5)]
+        for m_, r in zip(mats, bs.batch_svd(mats, _design("baseline"))):
+            fro2 = float(np.sum(m_ ** 2))
+            assert abs(float(np.sum(r.sigma ** 2)) - fro2) < 30 * 2.0 ** -53 * fro2
