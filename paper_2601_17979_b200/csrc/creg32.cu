@@ -192,7 +192,9 @@ struct IState {
 // SH != 0: the last iteration of an unrolled group with the ring shift by SH folded into the W update
 // (results go straight to their post-shift registers; branch-free: pairs that do not rotate have zero
 // parameters and copy exactly), so the loop back-edge moves no registers
-template <int u, int NW, bool SP, int SH = 0>
+// DELTA (k_cregb): the shared-memory P holds Delta = P - I, updated as Delta J + (J - I) (the reference's
+// delta mode), J - I = [[cm1, -conj(A)], [A, cm1]] on (top, bottom) for the task rows ct and cb
+template <int u, int NW, bool SP, int SH = 0, bool DELTA = false>
 __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx& c, int t, IState& st) {
     WarpSmem& sm = *c.sm;
     // ---- partial products of this lane's row: p_q = conj(x_b) x_t (V / padding lanes keep 0) ----
@@ -337,6 +339,18 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
             const double2 ta = P[a0], tb = P[b0];  // 16-byte accesses: 32 lanes, one column, conflict-free
             double tr = ta.x, ti = ta.y, br = tb.x, bi = tb.y;
             capply(tr, ti, br, bi, pq);
+            if (DELTA) {
+                const int ctq = cq & 0xff, cbq = (cq >> 8) & 0xff;
+                if (c.lane == ctq) {
+                    tr += pq.cm1;
+                    br -= pq.ar;
+                    bi += pq.ai;
+                } else if (c.lane == cbq) {
+                    tr += pq.ar;
+                    ti += pq.ai;
+                    br += pq.cm1;
+                }
+            }
             P[a0] = make_double2(tr, ti);
             P[b0] = make_double2(br, bi);
         }
@@ -344,19 +358,19 @@ __device__ __forceinline__ void iter(double (&xr)[N], double (&xi)[N], const Ctx
 }
 
 // one sweep (31 iterations, ring unrolled by 2); returns with the columns in natural order
-template <int NW, bool SP>
+template <int NW, bool SP, bool DELTA = false>
 __device__ __forceinline__ void sweep(double (&xr)[N], double (&xi)[N], const Ctx& c, IState& st) {
     st.full = true;
 #pragma unroll 1
     for (int gi = 0; gi < 16; ++gi) {
         const int t0 = 2 * gi;
-        iter<0, NW, SP>(xr, xi, c, t0, st);
+        iter<0, NW, SP, 0, DELTA>(xr, xi, c, t0, st);
         if (gi == 15) {
             ring_shift<1>(xr);
             ring_shift<1>(xi);
             break;
         }
-        iter<1, NW, SP, 2>(xr, xi, c, t0 + 1, st);  // writes straight into the registers shifted by two
+        iter<1, NW, SP, 2, DELTA>(xr, xi, c, t0 + 1, st);  // writes straight into the registers shifted by two
     }
 }
 
@@ -555,7 +569,10 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1)
 // [Vi Vj] <- [Vi Vj] P (the fused update of src/_kernels_numba.py:141-175) row by row from the
 // workspace.  One CTA per problem, block pairs of an outer iteration in turn; W and V live in the
 // (L2-resident) workspace, finalised by the standalone pass.
-template <int NW>
+// DELTA (more than 4 column blocks or inner sweeps != 1): P accumulates Delta = P - I and both W and V are
+// updated once per round as M + M Delta from the unrotated workspace copy (one rounding per round instead of
+// one per rotation on W; c128 128x128 Frobenius-mass drift 35.9u -> see profiles)
+template <int NW, bool DELTA = false>
 __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_cregb(SolveArgs<cx<double>> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int m = a.bm, n = a.bn, prob = blockIdx.x;
@@ -632,9 +649,9 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_cregb(
                     xi[x] = z.im;
                 }
                 for (int e = lane; e < H * RS2; e += 32) wsm[warp].red[e] = make_double2(0.0, 0.0);
-                if (want_p)
+                if (want_p || DELTA)
                     for (int e = tid; e < N * N; e += NW * 32)
-                        ps->P[e] = make_double2((e % N) == (e / N) ? 1.0 : 0.0, 0.0);
+                        ps->P[e] = make_double2((!DELTA && (e % N) == (e / N)) ? 1.0 : 0.0, 0.0);
                 __syncthreads();
                 IState st;
                 st.par = 0;
@@ -642,7 +659,7 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_cregb(
 #pragma unroll 1
                 for (int isw = 0; isw < budget; ++isw) {
                     st.my_rot = 0;
-                    sweep<NW, true>(xr, xi, c, st);
+                    sweep<NW, true, DELTA>(xr, xi, c, st);
                     int r = st.my_rot;  // lanes 0..15: counts of pairs 0..15 (identical in every warp)
 #pragma unroll
                     for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
@@ -654,17 +671,17 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_cregb(
                 sweep_rot += bp_rot;
                 if (bp_rot) {
                     ++updates;
-                    if (live) {
+                    if (!DELTA && live) {
 #pragma unroll
                         for (int x = 0; x < N; ++x) W[row + (size_t)col(x) * m] = cx<double>{xr[x], xi[x]};
                     }
-                    if (want_p) {
-                        __syncthreads();  // P complete
-                        // [Vi Vj] <- [Vi Vj] P, one row of V per thread (the rows of X are free registers)
-                        for (int vr = tid; vr < n; vr += NW * 32) {
+                    // [Mi Mj] <- [Mi Mj] P (V) or [Mi Mj] + [Mi Mj] Delta (DELTA: W and V), one row per thread
+                    // (the rows of X are free registers now)
+                    auto rows_update = [&](cx<double>* M, int ld, int nrows) {
+                        for (int vr = tid; vr < nrows; vr += NW * 32) {
 #pragma unroll
                             for (int x = 0; x < N; ++x) {
-                                const cx<double> z = V[vr + (size_t)col(x) * n];
+                                const cx<double> z = M[vr + (size_t)col(x) * ld];
                                 xr[x] = z.re;
                                 xi[x] = z.im;
                             }
@@ -677,10 +694,13 @@ __global__ void __launch_bounds__(NW * 32, (8 / NW) > 0 ? (8 / NW) : 1) k_cregb(
                                     sr = fma(xr[x], p.x, fma(-xi[x], p.y, sr));
                                     si = fma(xr[x], p.y, fma(xi[x], p.x, si));
                                 }
-                                V[vr + (size_t)col(y) * n] = cx<double>{sr, si};
+                                M[vr + (size_t)col(y) * ld] = DELTA ? cx<double>{xr[y] + sr, xi[y] + si} : cx<double>{sr, si};
                             }
                         }
-                    }
+                    };
+                    if (want_p || DELTA) __syncthreads();  // P complete
+                    if (DELTA) rows_update(W, m, m);
+                    if (want_p) rows_update(V, n, n);
                 }
                 __syncthreads();  // the next block pair reads the columns written here
             }
@@ -750,7 +770,8 @@ Plan plan_cregb(int dtype, int bm, int bn, int need_v, bool trans, int nb) {
 
 template <int NW>
 static int launch_cb(SolveArgs<cx<double>> a, const Plan& p, cudaStream_t st) {
-    auto k = creg::k_cregb<NW>;
+    // delta mode as in the real blocked kernel: more than 4 column blocks or inner sweeps other than one
+    auto k = (a.bn > 64 || a.inner_budget != 1) ? creg::k_cregb<NW, true> : creg::k_cregb<NW, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
         return BSVD_ERR_CUDA;
     k<<<a.batch, NW * 32, p.smem, st>>>(a);
