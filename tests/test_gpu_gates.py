@@ -242,3 +242,30 @@ def test_c09_frobenius_mass_conservation():
         for m_, r in zip(mats, bs.batch_svd(mats, _design("baseline"))):
             fro2 = float(np.sum(m_ ** 2))
             assert abs(float(np.sum(r.sigma ** 2)) - fro2) < 30 * 2.0 ** -53 * fro2
+
+
+@pytest.mark.parametrize("m,n,dt,B,inner", [(32, 32, np.float64, 200, 1), (16, 16, np.float32, 200, 1),
+                                            (64, 64, np.float64, 30, 1), (64, 64, np.float64, 30, 0),
+                                            (128, 128, np.float64, 12, 1), (128, 128, np.float64, 8, 0),
+                                            (256, 32, np.complex128, 30, 1), (128, 128, np.complex128, 8, 1)])
+def test_c09_mass_and_sigma_every_family(m, n, dt, B, inner):
+    """The c09 bar (sum sigma^2 = ||A||_F^2 within 30u) and sigma within 30u s1 of LAPACK on random batches of
+    every kernel family, the large blocked shapes and the inner-budget-100 design included (the blocked
+    kernels' delta mode; tools/mass_check.py)."""
+    import torch
+
+    rng = np.random.default_rng(m * 31 + n + inner)
+    A = rng.random((B, m, n))
+    if np.dtype(dt).kind == "c":
+        A = A + 1j * rng.random((B, m, n))
+    A = A.astype(dt)
+    r = bs.solve_tensor(torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda(), m, n,
+                        bs.JacobiOptions(inner_sweeps=inner))
+    torch.cuda.synchronize()
+    S = r.s.cpu().numpy().astype(np.float64)
+    u = unit_roundoff(dt)
+    A64 = A.astype(np.complex128) if np.dtype(dt).kind == "c" else A.astype(np.float64)
+    fro2 = np.sum(np.abs(A64) ** 2, axis=(1, 2))
+    assert np.max(np.abs(np.sum(S ** 2, axis=1) - fro2) / (u * fro2)) < 30
+    ref = np.stack([np.linalg.svd(x, compute_uv=False) for x in A64])
+    assert np.max(np.max(np.abs(S - ref), axis=1) / (u * ref[:, 0])) < 30
