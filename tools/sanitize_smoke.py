@@ -40,6 +40,8 @@ run(np.float64, 96, 20, use_qr_preprocess=True)
 run(np.complex64, 40, 24)                     # general unblocked
 run(np.complex128, 64, 64, B=2)               # complex register blocked (k_cregb)
 run(np.complex64, 48, 48, B=2)                # complex64 promoted to k_cregb
+run(np.complex128, 128, 128, B=1)             # k_cregb delta mode (n > 64)
+run(np.float64, 64, 64, B=2, inner_sweeps=0)  # blocked_reg delta mode (inner budget 100)
 run(np.float32, 64, 64, B=2)                  # FP32 blocked promoted to the FP64 register blocked kernel
 run(np.float32, 32, 32, B=3)                  # FP32 32x32 promoted to the FP64 32x32 kernel
 run(np.complex64, 256, 32, B=2)               # complex64 promoted to creg32
