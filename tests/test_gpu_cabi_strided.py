@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 CASES = [
     (np.float64, 32, 32), (np.float32, 32, 32), (np.float32, 64, 64), (np.float32, 16, 16),
     (np.complex64, 256, 32), (np.complex64, 40, 32), (np.complex128, 256, 32), (np.float64, 64, 64),
-    (np.float32, 48, 33),
+    (np.float32, 48, 33), (np.float64, 128, 128), (np.complex128, 128, 128),
 ]
 
 
