@@ -245,10 +245,9 @@ __device__ __forceinline__ void inner_iter(double (&x0)[N], double (&x1)[N], dou
                 apply2(x0[TS(q, u)], x0[BS(q, u)], pq.cm1, pq.c);
                 apply2(x1[TS(q, u)], x1[BS(q, u)], pq.cm1, pq.c);
                 apply2(p[TS(q, u)], p[BS(q, u)], pq.cm1, pq.c);
-                if (myq == q) {
-                    p[TS(q, u)] += at;
-                    p[BS(q, u)] += ab;
-                }
+                const double mq = myq == q ? 1.0 : 0.0;  // (exact: 0 * finite = 0, 1 * x = x)
+                p[TS(q, u)] = fma(mq, at, p[TS(q, u)]);
+                p[BS(q, u)] = fma(mq, ab, p[BS(q, u)]);
             }
         } else if (c.want_p) {
 #pragma unroll
