@@ -53,7 +53,8 @@ typedef struct {
     int row_block;      /* accepted for parity (tiling is the kernel's own)  */
     int kernel;         /* 0 = auto; >0 forces a kernel variant (tests/bench) */
     int use_qr;         /* use_qr_preprocess: dispatch takes the "qr+" route when m >= 3n (QR_RATIO) */
-    int reserved[2];    /* [0]: 32x32 FP64 tail as kernel 52 (0 = automatic, < 0 off; experimental); [1]: 0 */
+    int reserved[2];    /* [0]: 32x32 FP64 kernel 52 (0 = automatic: one-wave batches and the tail of larger ones; > 0 = that
+                           many tail problems; < 0 = off, kernel 42 alone; experimental); [1]: 0 */
 } bsvd_opts;
 
 /* Per-problem telemetry, written by the device (mirrors SolveInfo / BatchState). */
@@ -109,7 +110,10 @@ int bsvd_gesvj_batched(int dtype, int m, int n, int batch,
  * streams[0], and streams[0] is ordered after all of it on return, so the call
  * behaves like one stream-ordered operation on streams[0].  `work` is DEVICE
  * scratch of bsvd_host_workspace_bytes(...) bytes (staging for nstreams
- * chunks plus their solver workspace).  Asynchronous: synchronise streams[0]
+ * chunks plus their solver workspace).  Chunks on different streams solve
+ * concurrently, so above one wave of kernel 52 (8 problems per SM) a 32x32
+ * FP64 batch solves with kernel 42 alone (the throughput kernel; factors
+ * bitwise those of the one-call solve).  Asynchronous: synchronise streams[0]
  * before reading the outputs.  Replaces the reference's per-problem host loop
  * batch_svd -> _ProblemRun (src/batch.py:85-157) for host-resident batches.
  */

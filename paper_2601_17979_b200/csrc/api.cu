@@ -129,7 +129,7 @@ Plan make_plan(int dt, const Route& r, const bsvd_opts* o, bool contiguous = tru
         // Batches of at most FV_WARPS_PER_SM problems per SM: one problem per warp, V carried in lockstep
         // by the other half-warp (bit-identical to 42, no replay phase) -- the GPU is not full, so the
         // shorter per-problem chain wins over 42's two problems per warp.
-        const bool fv = r.need_v && batch > 0 && batch <= FV_WARPS_PER_SM * sm_count() && o->reserved[0] <= 0;
+        const bool fv = r.need_v && batch > 0 && batch <= FV_WARPS_PER_SM * sm_count() && o->reserved[0] == 0;
         const int want = o->kernel ? o->kernel
                                    : (r.need_v ? (fv ? KV_UNBLOCKED_REG32F : KV_UNBLOCKED_REG32G) : KV_UNBLOCKED_REG32B);
         Plan p = plan_unblocked_reg32b(dt, r.bm, r.bn, r.need_v, reg_ok, want, o->max_sweeps);
@@ -407,6 +407,17 @@ bool host_direct_enabled() {
 struct HostSlot {
     size_t a, u, v, s, info, ws, total;
 };
+// The options a chunk of a multi-chunk host pipeline solves with: chunks on different streams run
+// concurrently, so throughput beats single-problem latency -- the 32x32 FP64 problems use kernel 42 alone
+// (two problems per warp) rather than 52 (one problem per warp: the fastest single chunk, but half the
+// problems per resident warp).  C1-10k end to end, chunks of 1,250 on 4 streams, medians of 3 on one box:
+// 4.04 ms with 52 / 42 + 52 tail -> 3.86 ms (tools/ramp_probe.py).
+bsvd_opts pipeline_opts(const bsvd_opts& o) {
+    bsvd_opts p = o;
+    if (p.reserved[0] == 0) p.reserved[0] = -1;
+    return p;
+}
+
 HostSlot host_slot(int dtype, int m, int n, int chunk, const bsvd_opts* o) {
     const size_t es = (size_t)esize_of(dtype), rs = (size_t)rsize_of(dtype);
     const size_t k = (size_t)(m < n ? m : n);
@@ -417,7 +428,8 @@ HostSlot host_slot(int dtype, int m, int n, int chunk, const bsvd_opts* o) {
     h.v = o->want_v ? al((size_t)chunk * n * k * es) : 0;
     h.s = al((size_t)chunk * k * rs);
     h.info = al((size_t)chunk * sizeof(bsvd_info));
-    h.ws = al(bsvd_workspace_bytes(dtype, m, n, chunk, o));
+    const bsvd_opts po = pipeline_opts(*o);
+    h.ws = al(std::max(bsvd_workspace_bytes(dtype, m, n, chunk, o), bsvd_workspace_bytes(dtype, m, n, chunk, &po)));
     h.total = h.a + h.u + h.v + h.s + h.info + h.ws;
     return h;
 }
@@ -459,19 +471,27 @@ inline void stream_copy(unsigned char* dst, const void* src, size_t bytes) {
     }
 }
 
+// Chunk boundaries of the host pipeline: `chunk`-problem chunks, the last one ragged.
+struct ChunkPlan {
+    int batch, chunk;
+    int count() const { return (batch + chunk - 1) / chunk; }
+    int begin(int c) const { return c * chunk; }
+    int end(int c) const { return (c + 1) * chunk < batch ? (c + 1) * chunk : batch; }
+};
+
 struct ChunkPacker {
     std::vector<std::thread> pool;
     std::atomic<int>* done = nullptr;
-    ChunkPacker(const void* const* src, unsigned char* dst, size_t bytes, int batch, int chunk, int nthreads) {
-        const int nchunks = (batch + chunk - 1) / chunk;
+    ChunkPacker(const void* const* src, unsigned char* dst, size_t bytes, ChunkPlan plan, int nthreads) {
+        const int nchunks = plan.count();
         done = new std::atomic<int>[nchunks];
         for (int c = 0; c < nchunks; ++c) done[c].store(0, std::memory_order_relaxed);
         const int nt = nthreads < 1 ? 1 : (nthreads > nchunks ? nchunks : nthreads);
         for (int t = 0; t < nt; ++t)
             pool.emplace_back([=]() {
                 for (int c = t; c < nchunks; c += nt) {
-                    const int b1 = (c + 1) * chunk < batch ? (c + 1) * chunk : batch;
-                    for (int i = c * chunk; i < b1; ++i) stream_copy(dst + (size_t)i * bytes, src[i], bytes);
+                    const int b1 = plan.end(c);
+                    for (int i = plan.begin(c); i < b1; ++i) stream_copy(dst + (size_t)i * bytes, src[i], bytes);
                     _mm_sfence();  // the non-temporal stores are visible before the chunk is published
                     done[c].store(1, std::memory_order_release);
                 }
@@ -560,16 +580,19 @@ int gesvj_host_impl(int dtype, int m, int n, int batch, const void* A, const voi
         for (int i = 1; i < nstreams; ++i) cudaStreamWaitEvent(static_cast<cudaStream_t>(streams[i]), fork, 0);
     }
     rc = BSVD_OK;
-    const int nchunks = (batch + chunk - 1) / chunk;
+    const ChunkPlan plan{batch, chunk};
+    // one wave of kernel 52 takes the whole batch at once: keep its latency; above it, pipeline options
+    const bsvd_opts po = batch > FV_WARPS_PER_SM * sm_count() ? pipeline_opts(*opts) : *opts;
+    const int nchunks = plan.count();
     ChunkPacker* packer = nullptr;  // gather mode: pack chunks on host threads ahead of their H2D
     if (A_ptrs && k > 0)
-        packer = new ChunkPacker(A_ptrs, static_cast<unsigned char*>(const_cast<void*>(A)), (size_t)m * n * es, batch,
-                                 chunk, pack_threads);
+        packer = new ChunkPacker(A_ptrs, static_cast<unsigned char*>(const_cast<void*>(A)), (size_t)m * n * es, plan,
+                                 pack_threads);
     for (int c = 0; c < nchunks && rc == BSVD_OK; ++c) {
         if (packer) packer->wait(c);
         const int slot = c % nstreams;
         cudaStream_t st = static_cast<cudaStream_t>(streams[slot]);
-        const int b0 = c * chunk, cb = (batch - b0) < chunk ? (batch - b0) : chunk;
+        const int b0 = plan.begin(c), cb = plan.end(c) - b0;
         unsigned char* base = static_cast<unsigned char*>(work) + hs.total * (size_t)slot;
         void* Ad = base;
         void* Ud = base + hs.a;
@@ -584,12 +607,12 @@ int gesvj_host_impl(int dtype, int m, int n, int batch, const void* A, const voi
             rc = bsvd_gesvj_batched(dtype, m, n, cb, Ad, m > 0 ? m : 1, (int64_t)m * n, Uh + (size_t)b0 * m * k * es,
                                     m > 0 ? m : 1, (int64_t)m * k, Sh + (size_t)b0 * k * rs, k,
                                     opts->want_v ? Vh + (size_t)b0 * n * k * es : nullptr, n > 0 ? n : 1,
-                                    (int64_t)n * k, opts, Ih ? Ih + b0 : Id, Wd, hs.ws, st);
+                                    (int64_t)n * k, &po, Ih ? Ih + b0 : Id, Wd, hs.ws, st);
             if (rc) break;
             continue;
         }
         rc = bsvd_gesvj_batched(dtype, m, n, cb, Ad, m > 0 ? m : 1, (int64_t)m * n, Ud, m > 0 ? m : 1,
-                                (int64_t)m * k, Sd, k, Vd, n > 0 ? n : 1, (int64_t)n * k, opts, Id, Wd, hs.ws, st);
+                                (int64_t)m * k, Sd, k, Vd, n > 0 ? n : 1, (int64_t)n * k, &po, Id, Wd, hs.ws, st);
         if (rc) break;
         const size_t ub = (size_t)cb * m * k * es, vb = (size_t)cb * n * k * es, sb = (size_t)cb * k * rs;
         bool ok = true;

@@ -221,15 +221,16 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
 
 
 def default_chunk(batch: int, bytes_per_problem: int, elems: int = 0, nstreams: int = 4, sms: int = 148) -> int:
-    """Host-pipeline chunk: about 8 MB of copies per chunk, between 4 and 16 chunks (measured on B200,
-    tools/e2e_sweep.py, tools/e2e_sweep_c2.py: C1-10k best at B/16, C2 full at B/4 -- 0.635 vs 0.679 ms at
-    B/8 --, C4 at B/16).  Small problems (m n <= 1,024, a
-    problem per warp or half-warp) in batches of at most 16 per SM take one chunk per stream: their solve
-    is a single-problem latency whatever the chunk size, so more chunks than streams queue a second
-    latency behind the first (C1 1,000 problems: 0.65 ms at B/4 vs 0.75 ms at B/6)."""
+    """Host-pipeline chunk: about 8 MB of copies per chunk, between 4 and 16 chunks -- at most 8 for
+    problems of m n <= 1,024 (measured on B200, tools/e2e_sweep.py, tools/e2e_sweep_c2.py,
+    tools/ramp_probe.py: C1-10k best at B/8 with the pipeline's kernel 42, 3.86 vs 3.96 ms at B/16; C2 full
+    at B/4, 0.635 vs 0.679 ms at B/8; C4 at B/16).  Small problems (m n <= 1,024, a problem per warp or
+    half-warp) in batches of at most 16 per SM take one chunk per stream: their solve is a single-problem
+    latency whatever the chunk size, so more chunks than streams queue a second latency behind the first
+    (C1 1,000 problems: 0.65 ms at B/4 vs 0.75 ms at B/6)."""
     if 0 < elems <= 1024 and batch <= 16 * sms:
         return max(1, -(-batch // max(1, nstreams)))
-    lo, hi = -(-batch // 16), -(-batch // 4)
+    lo, hi = -(-batch // (8 if 0 < elems <= 1024 else 16)), -(-batch // 4)
     want = -(-(8 << 20) // max(1, bytes_per_problem))
     return max(1, min(max(want, lo), hi))
 

@@ -936,3 +936,34 @@ def test_c1_split_boundary_problems_and_fp32_promotion():
     torch.cuda.synchronize()
     p = torch.tensor(pick).cuda()
     assert torch.equal(big.s[p], small.s) and torch.equal(big.u[p], small.u) and torch.equal(big.v[p], small.v)
+
+
+@pytest.mark.gpu
+def test_c1_kernel52_off_and_host_pipeline_kernel():
+    """reserved[0] < 0 turns kernel 52 off for one-wave batches too (kernel 42 alone); the multi-chunk host
+    pipeline of a batch above one wave solves every chunk with 42, bitwise the one-call tail-off solve."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE, solve_host_buffers
+
+    rng = np.random.default_rng(4242)
+    A = rng.standard_normal((500, 32, 32))
+    a = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).cuda()
+    r = bs.solve_tensor(a, 32, 32, bs.JacobiOptions(), tail=-1)
+    torch.cuda.synchronize()
+    assert (np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"] == 42).all()
+
+    B = 2600
+    A = rng.standard_normal((B, 32, 32))
+    a_h = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).pin_memory()
+    u_h = torch.empty((B, 32, 32), dtype=torch.float64).pin_memory()
+    v_h = torch.empty((B, 32, 32), dtype=torch.float64).pin_memory()
+    s_h = torch.empty((B, 32), dtype=torch.float64).pin_memory()
+    i_h = torch.empty((B * INFO_DTYPE.itemsize,), dtype=torch.uint8).pin_memory()
+    solve_host_buffers(a_h, u_h, s_h, v_h, i_h, 32, 32, bs.JacobiOptions(), chunk=400)
+    torch.cuda.synchronize()
+    info = np.frombuffer(i_h.numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (info["kernel"] == 42).all() and info["converged"].all()
+    ref = bs.solve_tensor(a_h.cuda(), 32, 32, bs.JacobiOptions(), tail=-1)
+    torch.cuda.synchronize()
+    assert torch.equal(ref.s.cpu(), s_h) and torch.equal(ref.u.cpu(), u_h) and torch.equal(ref.v.cpu(), v_h)

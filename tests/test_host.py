@@ -208,7 +208,7 @@ def test_default_chunk_policy():
     per32 = 3 * 32 * 32 * 8
     assert default_chunk(1000, per32, 32 * 32, 4, 148) == 250      # latency-bound: one chunk per stream
     assert default_chunk(1250, per32, 32 * 32, 4, 148) == 313
-    assert default_chunk(10000, per32, 32 * 32, 4, 148) == 625     # at most 16 chunks
+    assert default_chunk(10000, per32, 32 * 32, 4, 148) == 1250    # small problems: at most 8 chunks
     assert default_chunk(10000, 3 * 16 * 16 * 4, 16 * 16, 4, 148) == 2500    # ~8 MB chunks, at least 4
     assert default_chunk(2000, 3 * 128 * 128 * 8, 128 * 128, 4, 148) == 125  # large problems: 16 chunks
     assert default_chunk(3, per32, 32 * 32, 4, 148) == 1
