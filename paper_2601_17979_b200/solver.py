@@ -200,7 +200,7 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
         k = min(m, n)
         es = np.dtype(dt).itemsize
         per = m * n * es + m * k * es + (n * k * es if opts.compute_right_vectors else 0)  # bytes in + out
-        chunk = default_chunk(B, per, m * n, len(streams), _sm_count(dev))
+        chunk = default_chunk(B, per, m * n, len(streams), _sm_count(dev), gather=a_ptrs is not None)
     ws_bytes = L.bsvd_host_workspace_bytes(code, m, n, chunk, len(streams), ctypes.byref(o))
     ws = _workspace(ws_bytes, dev)
     arr = (ctypes.c_void_p * len(streams))(*[st.cuda_stream for st in streams])
@@ -217,20 +217,27 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
             info_h.data_ptr() if info_h is not None else None, chunk,
             ws.data_ptr() if ws is not None else None, ws_bytes, arr, len(streams))
     _lib.check(rc, f"bsvd_gesvj_batched_host({dt.name}, {m}x{n}, batch={B})")
-    return int(L.bsvd_select_kernel_batched(code, m, n, min(B, chunk), ctypes.byref(o)))
+    # the kernel of a chunk: above one wave of kernel 52 the pipeline turns it off (csrc/api.cu pipeline_opts)
+    o_sel = make_opts(opts, route, kernel, -1) if B > 8 * _sm_count(dev) else o
+    return int(L.bsvd_select_kernel_batched(code, m, n, min(B, chunk), ctypes.byref(o_sel)))
 
 
-def default_chunk(batch: int, bytes_per_problem: int, elems: int = 0, nstreams: int = 4, sms: int = 148) -> int:
+def default_chunk(batch: int, bytes_per_problem: int, elems: int = 0, nstreams: int = 4, sms: int = 148,
+                  gather: bool = False) -> int:
     """Host-pipeline chunk: about 8 MB of copies per chunk, between 4 and 16 chunks -- at most 8 for
     problems of m n <= 1,024 (measured on B200, tools/e2e_sweep.py, tools/e2e_sweep_c2.py,
     tools/ramp_probe.py: C1-10k best at B/8 with the pipeline's kernel 42, 3.86 vs 3.96 ms at B/16; C2 full
     at B/4, 0.635 vs 0.679 ms at B/8; C4 at B/16).  Small problems (m n <= 1,024, a problem per warp or
     half-warp) in batches of at most 16 per SM take one chunk per stream: their solve is a single-problem
     latency whatever the chunk size, so more chunks than streams queue a second latency behind the first
-    (C1 1,000 problems: 0.65 ms at B/4 vs 0.75 ms at B/6)."""
-    if 0 < elems <= 1024 and batch <= 16 * sms:
+    (C1 1,000 problems: 0.65 ms at B/4 vs 0.75 ms at B/6).  ``gather``: the batch is packed on host threads
+    ahead of the pipeline, and the first H2D waits for its whole chunk, so small problems go down to B/24
+    (batch_svd C1-10k, tools/list_api_chunk_probe.py: 5.39 ms at B/24, 5.42-5.67 at B/16, 5.98-6.33 at B/8;
+    C2 unchanged at its ~8 MB chunks, 1.47-1.61 ms at B/4, 1.60 at B/16)."""
+    small = 0 < elems <= 1024
+    if small and batch <= 16 * sms:
         return max(1, -(-batch // max(1, nstreams)))
-    lo, hi = -(-batch // (8 if 0 < elems <= 1024 else 16)), -(-batch // 4)
+    lo, hi = -(-batch // (24 if small and gather else 8 if small else 16)), -(-batch // 4)
     want = -(-(8 << 20) // max(1, bytes_per_problem))
     return max(1, min(max(want, lo), hi))
 

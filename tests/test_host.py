@@ -212,6 +212,8 @@ def test_default_chunk_policy():
     assert default_chunk(10000, 3 * 16 * 16 * 4, 16 * 16, 4, 148) == 2500    # ~8 MB chunks, at least 4
     assert default_chunk(2000, 3 * 128 * 128 * 8, 128 * 128, 4, 148) == 125  # large problems: 16 chunks
     assert default_chunk(3, per32, 32 * 32, 4, 148) == 1
+    assert default_chunk(10000, per32, 32 * 32, 4, 148, gather=True) == 417         # packed ahead: B/24
+    assert default_chunk(10000, 3 * 16 * 16 * 4, 16 * 16, 4, 148, gather=True) == 2500
 
 
 def test_lazy_records_filled_by_c_helper():
