@@ -111,9 +111,10 @@ int bsvd_gesvj_batched(int dtype, int m, int n, int batch,
  * behaves like one stream-ordered operation on streams[0].  `work` is DEVICE
  * scratch of bsvd_host_workspace_bytes(...) bytes (staging for nstreams
  * chunks plus their solver workspace).  Chunks on different streams solve
- * concurrently, so above one wave of kernel 52 (8 problems per SM) a 32x32
- * FP64 batch solves with kernel 42 alone (the throughput kernel; factors
- * bitwise those of the one-call solve).  Asynchronous: synchronise streams[0]
+ * concurrently, so when the chunks in flight (one per stream) exceed two
+ * waves of kernel 52 (16 problems per SM) a 32x32 FP64 batch solves with
+ * kernel 42 alone (the throughput kernel; factors bitwise those of the
+ * one-call solve).  Asynchronous: synchronise streams[0]
  * before reading the outputs.  Replaces the reference's per-problem host loop
  * batch_svd -> _ProblemRun (src/batch.py:85-157) for host-resident batches.
  */

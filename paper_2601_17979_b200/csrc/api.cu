@@ -412,6 +412,13 @@ struct HostSlot {
 // (two problems per warp) rather than 52 (one problem per warp: the fastest single chunk, but half the
 // problems per resident warp).  C1-10k end to end, chunks of 1,250 on 4 streams, medians of 3 on one box:
 // 4.04 ms with 52 / 42 + 52 tail -> 3.86 ms (tools/ramp_probe.py).
+// ... when the chunks in flight (one per stream) hold more than two waves of kernel 52: below that, 52's
+// shorter chain wins (C1 slices: 1,250 problems in chunks of 313 1.57 M/s with 52 vs 1.38-1.50 with 42;
+// 2,500 in chunks of 342 1.96 vs 1.76-1.91)
+bool pipeline_throughput(int batch, int chunk, int nstreams) {
+    const long in_flight = (long)nstreams * (chunk < batch ? chunk : batch);
+    return in_flight > 2L * FV_WARPS_PER_SM * sm_count();
+}
 bsvd_opts pipeline_opts(const bsvd_opts& o) {
     bsvd_opts p = o;
     if (p.reserved[0] == 0) p.reserved[0] = -1;
@@ -581,8 +588,7 @@ int gesvj_host_impl(int dtype, int m, int n, int batch, const void* A, const voi
     }
     rc = BSVD_OK;
     const ChunkPlan plan{batch, chunk};
-    // one wave of kernel 52 takes the whole batch at once: keep its latency; above it, pipeline options
-    const bsvd_opts po = batch > FV_WARPS_PER_SM * sm_count() ? pipeline_opts(*opts) : *opts;
+    const bsvd_opts po = pipeline_throughput(batch, chunk, nstreams) ? pipeline_opts(*opts) : *opts;
     const int nchunks = plan.count();
     ChunkPacker* packer = nullptr;  // gather mode: pack chunks on host threads ahead of their H2D
     if (A_ptrs && k > 0)

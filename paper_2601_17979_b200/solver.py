@@ -217,8 +217,9 @@ def solve_host_buffers(a_h, u_h, s_h, v_h, info_h, m: int, n: int, opts, route: 
             info_h.data_ptr() if info_h is not None else None, chunk,
             ws.data_ptr() if ws is not None else None, ws_bytes, arr, len(streams))
     _lib.check(rc, f"bsvd_gesvj_batched_host({dt.name}, {m}x{n}, batch={B})")
-    # the kernel of a chunk: above one wave of kernel 52 the pipeline turns it off (csrc/api.cu pipeline_opts)
-    o_sel = make_opts(opts, route, kernel, -1) if B > 8 * _sm_count(dev) else o
+    # the kernel of a chunk: with more than two waves of kernel 52 in flight the pipeline turns it off
+    # (csrc/api.cu pipeline_throughput)
+    o_sel = make_opts(opts, route, kernel, -1) if len(streams) * min(chunk, B) > 16 * _sm_count(dev) else o
     return int(L.bsvd_select_kernel_batched(code, m, n, min(B, chunk), ctypes.byref(o_sel)))
 
 

@@ -940,8 +940,9 @@ def test_c1_split_boundary_problems_and_fp32_promotion():
 
 @pytest.mark.gpu
 def test_c1_kernel52_off_and_host_pipeline_kernel():
-    """reserved[0] < 0 turns kernel 52 off for one-wave batches too (kernel 42 alone); the multi-chunk host
-    pipeline of a batch above one wave solves every chunk with 42, bitwise the one-call tail-off solve."""
+    """reserved[0] < 0 turns kernel 52 off for one-wave batches too (kernel 42 alone); a host pipeline with
+    more than two waves of kernel 52 in flight solves every chunk with 42, bitwise the one-call tail-off
+    solve."""
     import torch
 
     from paper_2601_17979_b200.solver import INFO_DTYPE, solve_host_buffers
@@ -953,14 +954,14 @@ def test_c1_kernel52_off_and_host_pipeline_kernel():
     torch.cuda.synchronize()
     assert (np.frombuffer(r.info.cpu().numpy().tobytes(), dtype=INFO_DTYPE)["kernel"] == 42).all()
 
-    B = 2600
+    B = 4000
     A = rng.standard_normal((B, 32, 32))
     a_h = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).pin_memory()
     u_h = torch.empty((B, 32, 32), dtype=torch.float64).pin_memory()
     v_h = torch.empty((B, 32, 32), dtype=torch.float64).pin_memory()
     s_h = torch.empty((B, 32), dtype=torch.float64).pin_memory()
     i_h = torch.empty((B * INFO_DTYPE.itemsize,), dtype=torch.uint8).pin_memory()
-    solve_host_buffers(a_h, u_h, s_h, v_h, i_h, 32, 32, bs.JacobiOptions(), chunk=400)
+    solve_host_buffers(a_h, u_h, s_h, v_h, i_h, 32, 32, bs.JacobiOptions(), chunk=700)  # 4 x 700 > 2 x 1,184
     torch.cuda.synchronize()
     info = np.frombuffer(i_h.numpy().tobytes(), dtype=INFO_DTYPE)
     assert (info["kernel"] == 42).all() and info["converged"].all()
