@@ -968,3 +968,30 @@ def test_c1_kernel52_off_and_host_pipeline_kernel():
     ref = bs.solve_tensor(a_h.cuda(), 32, 32, bs.JacobiOptions(), tail=-1)
     torch.cuda.synchronize()
     assert torch.equal(ref.s.cpu(), s_h) and torch.equal(ref.u.cpu(), u_h) and torch.equal(ref.v.cpu(), v_h)
+
+
+@pytest.mark.gpu
+def test_c1_host_pipeline_slice_keeps_kernel52():
+    """A strong-scaling slice (1,250 problems in chunks of 313 on 4 streams: fewer than two waves of kernel
+    52 in flight) keeps 52 per chunk; factors bitwise those of standalone 313-problem solves."""
+    import torch
+
+    from paper_2601_17979_b200.solver import INFO_DTYPE, solve_host_buffers
+
+    B, chunk = 1250, 313
+    A = np.random.default_rng(1250).standard_normal((B, 32, 32))
+    a_h = torch.from_numpy(np.ascontiguousarray(np.swapaxes(A, 1, 2))).pin_memory()
+    u_h = torch.empty((B, 32, 32), dtype=torch.float64).pin_memory()
+    v_h = torch.empty((B, 32, 32), dtype=torch.float64).pin_memory()
+    s_h = torch.empty((B, 32), dtype=torch.float64).pin_memory()
+    i_h = torch.empty((B * INFO_DTYPE.itemsize,), dtype=torch.uint8).pin_memory()
+    solve_host_buffers(a_h, u_h, s_h, v_h, i_h, 32, 32, bs.JacobiOptions(), chunk=chunk)
+    torch.cuda.synchronize()
+    info = np.frombuffer(i_h.numpy().tobytes(), dtype=INFO_DTYPE)
+    assert (info["kernel"] == 52).all() and info["converged"].all()
+    for b0 in range(0, B, chunk):
+        ref = bs.solve_tensor(a_h[b0:b0 + chunk].cuda(), 32, 32, bs.JacobiOptions())
+        torch.cuda.synchronize()
+        b1 = min(B, b0 + chunk)
+        assert torch.equal(ref.s.cpu(), s_h[b0:b1]) and torch.equal(ref.u.cpu(), u_h[b0:b1])
+        assert torch.equal(ref.v.cpu(), v_h[b0:b1])
